@@ -1,0 +1,167 @@
+/*
+ * sfcdd_b200.h -- C ABI of the B200-native SFC two-level Schwarz PCG path.
+ *
+ * Drop-in boundary for the hot path of the reference package `sfcdd`
+ * (arXiv 2110.11211; /root/reference/pkg/src/sfcdd/).  Every entry point
+ * cites the reference interface it replaces (file:line).  The Python mirror
+ * in paper_2110_11211_b200/ binds these with ctypes exactly as a maintainer
+ * would from the reference side.
+ *
+ * Conventions
+ *   - Every function returns int status: 0 = OK, negative = error; the
+ *     message is available from sfcdd_last_error() (thread-local).
+ *   - *_dev pointers are device pointers owned by the caller; *_host
+ *     pointers are host memory.  Streams are cudaStream_t passed as void*.
+ *   - Vectors are fp64 in SFC-rank order (grid.py:1-8), length N.
+ *   - The operator never mutates caller inputs (schwarz.py:103-118).
+ */
+#ifndef SFCDD_B200_H
+#define SFCDD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes; the Python shim maps them to the reference's exceptions */
+#define SFCDD_OK 0
+#define SFCDD_EVALUE (-1)      /* ValueError          (partition.py:66, coarse.py:39) */
+#define SFCDD_EFACTOR (-2)     /* FactorizationError  (linalg.py:21)                 */
+#define SFCDD_EBREAKDOWN (-3)  /* BreakdownError      (krylov.py:21)                 */
+#define SFCDD_EOVERFLOW (-4)   /* OverflowError       (grid.py:55)                   */
+#define SFCDD_ECUDA (-5)       /* CUDA runtime failure / no device                   */
+#define SFCDD_EINTERNAL (-6)   /* internal invariant violated                        */
+
+/* variants / weightings (schwarz.py:27-28) */
+#define SFCDD_VARIANT_ONE_LEVEL 0
+#define SFCDD_VARIANT_ADDITIVE 1
+#define SFCDD_VARIANT_DEFLATED 2
+#define SFCDD_VARIANT_BALANCED 3
+#define SFCDD_WEIGHT_NONE 0
+#define SFCDD_WEIGHT_OMEGA 1
+#define SFCDD_WEIGHT_DMATRIX 2
+
+const char* sfcdd_last_error(void);
+int sfcdd_version(void);
+
+/* ------------------------------------------------------------------ SFC --
+ * Replaces sfc.encode (sfc.py:120-136) for a batch of n points.
+ * coords_dev: n*dim uint64 words, point-major; keys as (hi, lo) uint64 words.
+ * dim*bits <= 128 (sfc.py:36-39); coordinates must be < 2^bits.        */
+int sfcdd_sfc_encode(int dim, int bits, const uint64_t* coords_dev, int64_t n,
+                     uint64_t* keys_hi_dev, uint64_t* keys_lo_dev, void* stream);
+
+/* Replaces sfc.decode (sfc.py:139-147) for a batch of n keys. */
+int sfcdd_sfc_decode(int dim, int bits, const uint64_t* keys_hi_dev,
+                     const uint64_t* keys_lo_dev, int64_t n, uint64_t* coords_dev,
+                     void* stream);
+
+/* Replaces grid.sfc_permutation (grid.py:60-77): perm[s] = lex index of the
+ * interior point with the s-th smallest grid_point_key (sfc.py:150-169).
+ * rank_dev (optional, may be NULL) receives the inverse permutation.
+ * force_radix != 0 selects the general radix-sort path even when the dense
+ * key-space bitmap path applies (test hook).                              */
+int sfcdd_sfc_perm(int dim, const int32_t* levels_host, int64_t* perm_dev,
+                   int64_t* rank_dev, int force_radix, void* stream);
+
+/* -------------------------------------------------------------- operator --
+ * One handle = one grid, partition, coarse space and Schwarz configuration,
+ * bound to one CUDA device.  Replaces the composition
+ *   grid.assemble_laplacian + symmetrize_diag   (grid.py:91-130)
+ *   partition.build_partition/compute_weights   (partition.py:130-157)
+ *   coarse.build_coarse + deflation_ops         (coarse.py:38-88)
+ *   schwarz.setup / SchwarzOperator             (schwarz.py:48-130)     */
+typedef struct sfcdd_op sfcdd_op;
+
+typedef struct sfcdd_op_desc {
+  int32_t dim;
+  int32_t levels[8];
+  int32_t p;                 /* number of subdomains                        */
+  int32_t q;                 /* coarse dofs per subdomain (0 = none)        */
+  int32_t variant;           /* SFCDD_VARIANT_*                             */
+  int32_t weighting;         /* SFCDD_WEIGHT_*                              */
+  int32_t device;            /* CUDA device ordinal                         */
+  const int64_t* ov_start;   /* host, p entries: overlapped cyclic ranges   */
+  const int64_t* ov_len;
+  const int64_t* dj_start;   /* host, p entries: disjoint ranges            */
+  const int64_t* dj_len;
+  const double* omega;       /* host, p entries (partition.py:151-157)      */
+  int32_t host_threads;      /* setup threads (0 = hardware concurrency)    */
+  int32_t reserved[7];
+} sfcdd_op_desc;
+
+typedef struct sfcdd_stats {
+  int64_t n;                 /* fine dofs                                   */
+  int64_t n0;                /* coarse dofs                                 */
+  int64_t factor_nnz;        /* sum_i stored entries of the local factors   */
+  int64_t factor_nnz_l;      /* sum_i nnz(L_i) (no amalgamation zeros)      */
+  int64_t coarse_nnz;        /* stored entries of the coarse operator       */
+  int64_t num_tasks;         /* DAG tasks per sweep                         */
+  int64_t num_supernodes;
+  double setup_seconds;      /* host+device setup wall time                 */
+  double order_seconds;
+  double factor_seconds;
+  int64_t apply_calls;
+  int64_t device_bytes;      /* device memory held by the handle            */
+  double last_solve_ms;      /* DAG local-solve kernel time of last apply   */
+  int64_t reserved[8];
+} sfcdd_stats;
+
+int sfcdd_op_create(const sfcdd_op_desc* desc, sfcdd_op** out);
+/* factorizes all A_i and A_0 (schwarz.py:58-61, coarse.py:59-60) */
+int sfcdd_op_setup(sfcdd_op* op, void* stream);
+/* h = C^{-1} g (schwarz.py:103-118); g_dev, h_dev length N               */
+int sfcdd_op_apply(sfcdd_op* op, const double* g_dev, double* h_dev, void* stream);
+/* y = Â x, matrix-free scaled 2d+1-point stencil (linalg.py:31-34)        */
+int sfcdd_op_matvec(sfcdd_op* op, const double* x_dev, double* y_dev, void* stream);
+/* PCG (krylov.py:257-291) with relative-residual stopping on Â, b̂.
+ * x_dev holds x0 on entry and the solution on exit; res_hist_host gets
+ * max_iters+1 entries (first *iters+1 valid).  Returns SFCDD_EBREAKDOWN on
+ * nonpositive curvature (krylov.py:278-279).                              */
+int sfcdd_op_pcg(sfcdd_op* op, const double* b_dev, double* x_dev, double tol,
+                 int32_t max_iters, double* res_hist_host, int32_t* iters,
+                 int32_t* converged, void* stream);
+/* Config-4 fault mode: in apply call number apply_index the
+ * local contributions of the listed subdomains are zeroed.  n = 0 clears. */
+int sfcdd_op_set_fault(sfcdd_op* op, int64_t apply_index, const int32_t* ids_host, int32_t n);
+int sfcdd_op_reset_calls(sfcdd_op* op);
+int sfcdd_op_stats(sfcdd_op* op, sfcdd_stats* out);
+/* diagnostics: Â's constants (diag, off per axis) and symmetric scaling t */
+int sfcdd_op_stencil(sfcdd_op* op, double* diag, double* off /*dim*/, double* t);
+/* diagnostics: coarse matrix A_0 as dense n0*n0 (host), n0 <= 8192         */
+int sfcdd_op_coarse_dense(sfcdd_op* op, double* a0_host);
+void sfcdd_op_destroy(sfcdd_op* op);
+
+/* ------------------------------------------------------- direct solver --
+ * Replaces linalg.Factorization (linalg.py:37-72) for a general SPD CSR
+ * matrix on the GPU: AMD ordering, supernodal Cholesky, block-inverse
+ * factor applied by the same DAG kernel as the local solves.              */
+typedef struct sfcdd_factor sfcdd_factor;
+int sfcdd_factor_create(int64_t n, const int64_t* indptr_host, const int32_t* indices_host,
+                        const double* data_host, int32_t device, sfcdd_factor** out);
+int sfcdd_factor_solve(sfcdd_factor* f, const double* b_dev, double* x_dev, void* stream);
+int sfcdd_factor_info(sfcdd_factor* f, int64_t* nnz_l, int64_t* stored, int64_t* nsuper);
+void sfcdd_factor_destroy(sfcdd_factor* f);
+
+/* --------------------------------------------------- host test hooks --
+ * CPU-only checks of the host setup logic (no device needed): AMD ordering
+ * and the block-inverse supernodal factor applied on the host.            */
+int sfcdd_host_amd(int64_t n, const int64_t* indptr, const int32_t* indices, int32_t* perm_out);
+int sfcdd_host_factor_solve(int64_t n, const int64_t* indptr, const int32_t* indices,
+                            const double* data, const double* b, double* x,
+                            int64_t* nnz_l, int64_t* stored);
+/* Factor the principal sub-blocks of a global SPD CSR matrix on p cyclic
+ * ranges (start, len), build the device execution plan and run it through
+ * the host interpreter of the device blob format.  xy receives the p local
+ * solutions A_i^{-1} rhs[range_i], concatenated in range order.  blob_max /
+ * scratch_max override the plan budgets (0 = default).                    */
+int sfcdd_host_plan_solve(int64_t n, const int64_t* indptr, const int32_t* indices,
+                          const double* data, int32_t p, const int64_t* start,
+                          const int64_t* len, const double* rhs, double* xy,
+                          int32_t blob_max, int32_t scratch_max, int64_t* nfrag);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SFCDD_B200_H */

@@ -1,0 +1,259 @@
+"""Generate golden fixtures by running the REFERENCE itself (build container only).
+
+    PYTHONPATH= python oracle/make_fixtures.py [--big]
+
+Imports the read-only reference package from /root/reference/pkg/src under
+the alias ``sfcdd_ref`` and writes small .npz/.json files
+under tests/golden/.  Nothing here runs on the GPU box; the fixtures travel
+with the repo.  ``--big`` adds the C2/C3 (and C4 perm hash) reference runs,
+which take a few minutes.
+
+Fixture contents (all produced by reference code paths, file:line relative
+to /root/reference/pkg/src/sfcdd/):
+  sfc_walks.npz      decode() of every key for small curves (sfc.py:139-147)
+  sfc_keys.json      encode() of sample coordinates incl. 66-bit keys (sfc.py:120)
+  perms.npz          sfc_permutation(levels) for small/anisotropic levels (grid.py:60)
+  perm_hashes.json   sha256 of sfc_permutation for config-size levels
+  partitions.json    disjoint/overlapped (start, length), omega, counts summary
+                     (partition.py:64-157) and aggregate boundaries (coarse.py:44-58)
+  coarse_c1.npz      A0 of config 1 (coarse.py:56-59)
+  solve_*.npz        PCG residual histories / solutions (krylov.py:257-291)
+  apply_c1.npz       SchwarzOperator.apply on seeded vectors (schwarz.py:103-118)
+"""
+
+from __future__ import annotations
+
+import argparse
+import hashlib
+import importlib.util
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+OUT = ROOT / "tests" / "golden"
+
+
+def load_reference():
+    spec = importlib.util.spec_from_file_location(
+        "sfcdd_ref", "/root/reference/pkg/src/sfcdd/__init__.py",
+        submodule_search_locations=["/root/reference/pkg/src/sfcdd"])
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules["sfcdd_ref"] = mod
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def perm_hash(perm: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(perm, dtype=np.int64).tobytes()).hexdigest()
+
+
+SMALL_LEVELS = [(1, 1), (2, 2), (2, 3), (3, 2), (3, 3), (4, 4), (5, 5), (7, 7),
+                (2, 2, 2), (2, 2, 3), (3, 3, 4), (4, 4, 4), (3, 2, 1, 2), (2, 2, 2, 2),
+                (6,), (1, 4), (4, 1, 3)]
+BIG_LEVELS = [(10, 10), (7, 7, 7)]
+HUGE_LEVELS = [(12, 12)]
+
+# (name, levels, P, gamma, q) -- SURVEY Appendix A mapping of BASELINE configs
+CONFIGS = [
+    ("c1_g025", (7, 7), 16, 0.25, 4),
+    ("c1_g05", (7, 7), 16, 0.5, 4),
+    ("c2", (10, 10), 64, 0.5, 16),
+    ("c3", (7, 7, 7), 512, 0.5, 8),
+    ("c4", (12, 12), 256, 0.5, 16),
+    ("c5_g1", (8, 8, 8), 512, 0.5, 64),
+    ("c5_g2", (8, 8, 9), 1024, 0.5, 64),
+    ("c5_g4", (8, 9, 9), 2048, 0.5, 64),
+    ("c5_g8", (9, 9, 9), 4096, 0.5, 64),
+    ("small_aniso", (3, 4), 6, 0.5, 2),
+    ("small_3d", (3, 3, 3), 8, 0.75, 3),
+    ("frac_g03", (5, 5), 7, 0.3, 5),
+    ("gamma_15", (4, 4), 8, 1.5, 2),
+]
+
+
+def make_sfc(ref):
+    sfc = ref.sfc
+    walks = {}
+    for d, n in [(2, 1), (2, 2), (2, 3), (3, 2), (4, 2), (5, 2), (3, 3)]:
+        cfg = sfc.CurveConfig(d, n)
+        walks[f"d{d}_n{n}"] = np.array([sfc.decode(k, cfg) for k in range(1 << cfg.key_bits)],
+                                       dtype=np.int64)
+    np.savez_compressed(OUT / "sfc_walks.npz", **walks)
+    rng = np.random.default_rng(11)
+    samples = []
+    for d, bits in [(2, 5), (3, 7), (4, 9), (6, 11), (2, 32), (3, 21), (5, 20), (8, 16), (2, 64)]:
+        cfg = sfc.CurveConfig(d, bits)
+        pts = [tuple([(1 << bits) - 1] * d), tuple([0] * d)]
+        for _ in range(6):
+            pts.append(tuple(int(v) for v in rng.integers(0, 1 << min(bits, 62), size=d)))
+        for c in pts:
+            samples.append({"dim": d, "bits": bits, "coords": list(c),
+                            "key": str(sfc.encode(c, cfg))})
+    grid_keys = []
+    for levels in [(2, 3), (3, 3), (3, 4, 2), (1, 5)]:
+        shape = [(1 << l) - 1 for l in levels]
+        for flat in range(0, int(np.prod(shape)), 3):
+            idx = np.unravel_index(flat, shape)
+            k = tuple(int(i) + 1 for i in idx)
+            grid_keys.append({"levels": list(levels), "index": list(k),
+                              "key": str(sfc.grid_point_key(k, levels))})
+    (OUT / "sfc_keys.json").write_text(json.dumps({"encode": samples, "grid_point_key": grid_keys}))
+
+
+def make_perms(ref, big):
+    perms = {}
+    for lv in SMALL_LEVELS:
+        perms["_".join(map(str, lv))] = ref.grid.sfc_permutation(lv)
+    np.savez_compressed(OUT / "perms.npz", **perms)
+    hashes = {}
+    path = OUT / "perm_hashes.json"
+    if path.exists():
+        hashes = json.loads(path.read_text())
+    for lv in SMALL_LEVELS:
+        hashes["_".join(map(str, lv))] = perm_hash(perms["_".join(map(str, lv))])
+    if big:
+        for lv in BIG_LEVELS + HUGE_LEVELS:
+            key = "_".join(map(str, lv))
+            if key in hashes:
+                continue
+            t0 = time.time()
+            p = ref.grid.sfc_permutation(lv)
+            hashes[key] = perm_hash(p)
+            print(f"perm {lv}: {time.time() - t0:.1f}s", flush=True)
+            ref.grid.sfc_permutation.cache_clear()
+    path.write_text(json.dumps(hashes, indent=1))
+
+
+def make_partitions(ref):
+    pt = ref.partition
+    out = {}
+    for name, levels, p, gamma, q in CONFIGS:
+        n = ref.grid.num_dofs(levels)
+        part = pt.build_partition(n, p, gamma)
+        entry = {
+            "levels": list(levels), "n": n, "p": p, "gamma": gamma, "q": q,
+            "disjoint": [[r.start, r.length] for r in part.disjoint],
+            "overlapped": [[r.start, r.length] for r in part.overlapped],
+        }
+        if n <= 3_000_000:
+            w = pt.compute_weights(part)
+            entry["omega"] = [float(v) for v in w.omega]
+            entry["counts_min"] = int(w.counts.min())
+            entry["counts_max"] = int(w.counts.max())
+            entry["counts_hash"] = hashlib.sha256(w.counts.astype(np.int64).tobytes()).hexdigest()
+            bounds = [0]
+            for r in part.disjoint:
+                for s in ref.coarse.aggregate_sizes(r.length, q):
+                    bounds.append(bounds[-1] + s)
+            entry["aggregate_bounds_hash"] = hashlib.sha256(
+                np.asarray(bounds, np.int64).tobytes()).hexdigest()
+        out[name] = entry
+    (OUT / "partitions.json").write_text(json.dumps(out))
+
+
+def reference_setup(ref, levels, p, gamma, q, seed=42):
+    """SURVEY §8(d) composition (mirrors combine.py:178-189 with a random RHS)."""
+    A = ref.grid.assemble_laplacian(levels)
+    n = A.shape[0]
+    b = np.random.default_rng(seed).uniform(-1.0, 1.0, size=n)
+    Ah, bh, t = ref.grid.symmetrize_diag(A, b)
+    part = ref.partition.build_partition(n, p, gamma)
+    cs = ref.coarse.build_coarse(part, Ah, q)
+    op = ref.schwarz.setup(Ah, part, cs, ref.schwarz.SchwarzConfig("balanced", "omega", gamma, q))
+    return Ah, bh, t, part, cs, op
+
+
+def install_fault(op, apply_index, dead):
+    """SURVEY §8(d) fault semantics by instance monkeypatching (no reference edits)."""
+    state = {"calls": 0}
+    orig_local = op._local_solve
+    orig_apply = op.apply
+    dead = set(int(i) for i in dead)
+
+    def local(i, g):
+        piece = orig_local(i, g)
+        if state["calls"] == apply_index and i in dead:
+            return np.zeros_like(piece)
+        return piece
+
+    def apply(g):
+        out = orig_apply(g)
+        state["calls"] += 1
+        return out
+
+    op._local_solve = local
+    op.apply = apply
+
+
+def make_solve(ref, name, levels, p, gamma, q, full_solution, fault_iter=None):
+    t0 = time.time()
+    Ah, bh, t, part, cs, op = reference_setup(ref, levels, p, gamma, q)
+    if fault_iter is not None:
+        dead = np.random.default_rng(42).choice(p, size=int(round(0.1 * p)), replace=False)
+        install_fault(op, fault_iter, dead)
+    cfg = ref.krylov.SolverConfig(method="pcg", tolerance=1e-8, tolerance_kind="relative_residual")
+    rep = ref.krylov.run(Ah, bh, op, cfg, np.zeros(Ah.shape[0]))
+    sol = rep.solution
+    data = {
+        "levels": np.asarray(levels), "p": p, "gamma": gamma, "q": q,
+        "iterations": rep.iterations, "converged": rep.converged,
+        "residual_history": np.asarray(rep.residual_history),
+        "solution_norm": np.linalg.norm(sol),
+        "solution_sample_idx": np.arange(0, sol.size, max(1, sol.size // 4096)),
+    }
+    data["solution_sample"] = sol[data["solution_sample_idx"]]
+    if full_solution:
+        data["solution"] = sol
+    if name.startswith("c1"):
+        data["coarse_matrix"] = cs.matrix.toarray()
+        rng = np.random.default_rng(5)
+        vs = rng.standard_normal((3, Ah.shape[0]))
+        data["apply_inputs"] = vs
+        data["apply_outputs"] = np.stack([op.apply(v) for v in vs])
+    np.savez_compressed(OUT / f"solve_{name}.npz", **data)
+    print(f"solve {name}: {rep.iterations} its, {time.time() - t0:.1f}s", flush=True)
+
+
+def make_dense_operator(ref):
+    """Small operator matrices via apply() (cf. test_schwarz.py:14-22)."""
+    out = {}
+    for levels, p, gamma, q in [((4, 4), 4, 0.5, 2), ((3, 3, 3), 8, 0.5, 2), ((4, 4), 5, 0.25, 3)]:
+        Ah, bh, t, part, cs, op = reference_setup(ref, levels, p, gamma, q)
+        n = Ah.shape[0]
+        M = np.empty((n, n))
+        e = np.zeros(n)
+        for j in range(n):
+            e[j] = 1.0
+            M[:, j] = op.apply(e)
+            e[j] = 0.0
+        out["_".join(map(str, levels)) + f"_p{p}_g{gamma}_q{q}"] = M
+    np.savez_compressed(OUT / "dense_operators.npz", **out)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--big", action="store_true")
+    args = ap.parse_args()
+    OUT.mkdir(parents=True, exist_ok=True)
+    ref = load_reference()
+    make_sfc(ref)
+    make_perms(ref, args.big)
+    make_partitions(ref)
+    make_dense_operator(ref)
+    make_solve(ref, "c1_g05", (7, 7), 16, 0.5, 4, True)
+    make_solve(ref, "c1_g025", (7, 7), 16, 0.25, 4, True)
+    make_solve(ref, "small_3d", (4, 4, 4), 8, 0.5, 4, True)
+    make_solve(ref, "aniso", (6, 7), 12, 0.5, 3, True)
+    make_solve(ref, "fault_88", (8, 8), 256, 0.5, 16, False, fault_iter=5)
+    make_solve(ref, "nofault_88", (8, 8), 256, 0.5, 16, False)
+    if args.big:
+        make_solve(ref, "c2", (10, 10), 64, 0.5, 16, False)
+        make_solve(ref, "c3", (7, 7, 7), 512, 0.5, 8, False)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,110 @@
+// C-ABI plumbing shared by all entry points, plus the host-only test hooks.
+#include <cstring>
+#include <string>
+
+#include "common.h"
+#include "host.h"
+#include "plan.h"
+
+namespace sfcdd {
+static thread_local std::string g_last_error;
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+}  // namespace sfcdd
+
+using namespace sfcdd;
+
+extern "C" const char* sfcdd_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" int sfcdd_version(void) { return 1; }
+
+static CsrMatrix csr_from(int64_t n, const int64_t* indptr, const int32_t* indices, const double* data) {
+  CsrMatrix A;
+  A.n = n;
+  A.indptr.assign(indptr, indptr + n + 1);
+  int64_t nnz = indptr[n];
+  A.indices.assign(indices, indices + nnz);
+  if (data)
+    A.data.assign(data, data + nnz);
+  else
+    A.data.assign(nnz, 1.0);
+  for (int64_t i = 0; i < nnz; ++i)
+    SFCDD_REQUIRE(A.indices[i] >= 0 && A.indices[i] < n, SFCDD_EVALUE, "column index out of range");
+  return A;
+}
+
+extern "C" int sfcdd_host_amd(int64_t n, const int64_t* indptr, const int32_t* indices, int32_t* perm_out) {
+  SFCDD_API_BEGIN
+  SFCDD_REQUIRE(n >= 0, SFCDD_EVALUE, "negative dimension");
+  CsrMatrix A = csr_from(n, indptr, indices, nullptr);
+  SymPattern P;
+  P.n = n;
+  P.indptr = A.indptr;
+  P.indices = A.indices;
+  std::vector<int32_t> o = amd_order(P);
+  std::memcpy(perm_out, o.data(), n * sizeof(int32_t));
+  SFCDD_API_END
+}
+
+extern "C" int sfcdd_host_factor_solve(int64_t n, const int64_t* indptr, const int32_t* indices,
+                                       const double* data, const double* b, double* x, int64_t* nnz_l,
+                                       int64_t* stored) {
+  SFCDD_API_BEGIN
+  SFCDD_REQUIRE(n >= 0, SFCDD_EVALUE, "negative dimension");
+  CsrMatrix A = csr_from(n, indptr, indices, data);
+  FactorOptions opt;
+  HostFactor F = factorize_host(A, opt);
+  host_block_solve(F, b, x);
+  if (nnz_l) *nnz_l = F.nnz_l;
+  if (stored) *stored = F.stored;
+  SFCDD_API_END
+}
+
+namespace sfcdd {
+void plan_exec_host(const DevicePlan& P, const double* rhs, double* xy);
+// principal sub-block of a global CSR matrix on a cyclic range
+CsrMatrix extract_block(const CsrMatrix& A, int64_t start, int64_t len) {
+  const int64_t n = A.n;
+  CsrMatrix B;
+  B.n = len;
+  B.indptr.assign(len + 1, 0);
+  for (int64_t r = 0; r < len; ++r) {
+    int64_t g = start + r;
+    if (g >= n) g -= n;
+    for (int64_t p = A.indptr[g]; p < A.indptr[g + 1]; ++p) {
+      int64_t c = A.indices[p] - start;
+      if (c < 0) c += n;
+      if (c < len) {
+        B.indices.push_back((int32_t)c);
+        B.data.push_back(A.data[p]);
+      }
+    }
+    B.indptr[r + 1] = B.indices.size();
+  }
+  return B;
+}
+}  // namespace sfcdd
+
+extern "C" int sfcdd_host_plan_solve(int64_t n, const int64_t* indptr, const int32_t* indices,
+                                     const double* data, int32_t p, const int64_t* start,
+                                     const int64_t* len, const double* rhs, double* xy,
+                                     int32_t blob_max, int32_t scratch_max, int64_t* nfrag) {
+  SFCDD_API_BEGIN
+  CsrMatrix A = csr_from(n, indptr, indices, data);
+  std::vector<HostFactor> fs(p);
+  FactorOptions fo;
+  for (int32_t i = 0; i < p; ++i) fs[i] = factorize_host(extract_block(A, start[i], len[i]), fo);
+  std::vector<const HostFactor*> ptrs;
+  std::vector<int64_t> gs, gm;
+  for (int32_t i = 0; i < p; ++i) {
+    ptrs.push_back(&fs[i]);
+    gs.push_back(start[i]);
+    gm.push_back(n);
+  }
+  PlanOptions po;
+  if (blob_max > 0) po.blob_max = blob_max;
+  if (scratch_max > 0) po.scratch_max = scratch_max;
+  DevicePlan plan = build_plan(ptrs, gs, gm, po);
+  plan_exec_host(plan, rhs, xy);
+  if (nfrag) *nfrag = plan.nfrag;
+  SFCDD_API_END
+}
