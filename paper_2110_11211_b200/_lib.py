@@ -1,0 +1,186 @@
+"""ctypes binding of libsfcdd_b200.so (the C ABI in include/sfcdd_b200.h).
+
+This is exactly the binding a maintainer of the reference would add on the
+reference side: plain pointers, sizes and int status codes.
+The library is built in-tree by ``paper_2110_11211_b200.build``; if it is
+missing, importing any compute module fails loudly -- there is no CPU
+fallback for the hot path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+import numpy as np
+
+_LIB_PATH = Path(__file__).resolve().parent / "libsfcdd_b200.so"
+
+SFCDD_OK = 0
+SFCDD_EVALUE = -1
+SFCDD_EFACTOR = -2
+SFCDD_EBREAKDOWN = -3
+SFCDD_EOVERFLOW = -4
+SFCDD_ECUDA = -5
+SFCDD_EINTERNAL = -6
+
+VARIANT_CODES = {"one_level": 0, "additive_two_level": 1, "deflated": 2, "balanced": 3}
+WEIGHTING_CODES = {"none": 0, "omega": 1, "d_matrix": 2}
+
+
+class FactorizationError(RuntimeError):
+    """Raised when a matrix expected to be SPD cannot be factorized (linalg.py:21)."""
+
+
+class BreakdownError(RuntimeError):
+    """Nonpositive curvature encountered in a CG recurrence (krylov.py:21)."""
+
+
+class DivergenceError(RuntimeError):
+    """Richardson error grew by 10x over its initial value (krylov.py:25)."""
+
+
+class DeviceError(RuntimeError):
+    """CUDA runtime failure (no device, launch failure, out of memory)."""
+
+
+class OpDesc(ctypes.Structure):
+    _fields_ = [
+        ("dim", ctypes.c_int32),
+        ("levels", ctypes.c_int32 * 8),
+        ("p", ctypes.c_int32),
+        ("q", ctypes.c_int32),
+        ("variant", ctypes.c_int32),
+        ("weighting", ctypes.c_int32),
+        ("device", ctypes.c_int32),
+        ("ov_start", ctypes.c_void_p),
+        ("ov_len", ctypes.c_void_p),
+        ("dj_start", ctypes.c_void_p),
+        ("dj_len", ctypes.c_void_p),
+        ("omega", ctypes.c_void_p),
+        ("host_threads", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 7),
+    ]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_int64),
+        ("n0", ctypes.c_int64),
+        ("factor_nnz", ctypes.c_int64),
+        ("factor_nnz_l", ctypes.c_int64),
+        ("coarse_nnz", ctypes.c_int64),
+        ("num_tasks", ctypes.c_int64),
+        ("num_supernodes", ctypes.c_int64),
+        ("setup_seconds", ctypes.c_double),
+        ("order_seconds", ctypes.c_double),
+        ("factor_seconds", ctypes.c_double),
+        ("apply_calls", ctypes.c_int64),
+        ("device_bytes", ctypes.c_int64),
+        ("last_solve_ms", ctypes.c_double),
+        ("reserved", ctypes.c_int64 * 8),
+    ]
+
+
+EXPORTS = [
+    "sfcdd_last_error", "sfcdd_version", "sfcdd_sfc_encode", "sfcdd_sfc_decode",
+    "sfcdd_sfc_perm", "sfcdd_op_create", "sfcdd_op_setup", "sfcdd_op_apply",
+    "sfcdd_op_matvec", "sfcdd_op_pcg", "sfcdd_op_set_fault", "sfcdd_op_reset_calls",
+    "sfcdd_op_stats", "sfcdd_op_stencil", "sfcdd_op_coarse_dense", "sfcdd_op_destroy",
+    "sfcdd_factor_create", "sfcdd_factor_solve", "sfcdd_factor_info", "sfcdd_factor_destroy",
+    "sfcdd_host_amd", "sfcdd_host_factor_solve", "sfcdd_host_plan_solve",
+]
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not _LIB_PATH.exists():
+        raise ImportError(
+            f"{_LIB_PATH} is missing; build it with `python -m paper_2110_11211_b200.build` "
+            "(there is no CPU fallback)")
+    L = ctypes.CDLL(str(_LIB_PATH))
+    vp, i32, i64, dbl = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+    L.sfcdd_last_error.restype = ctypes.c_char_p
+    L.sfcdd_version.restype = ctypes.c_int
+    sigs = {
+        "sfcdd_sfc_encode": [ctypes.c_int, ctypes.c_int, vp, i64, vp, vp, vp],
+        "sfcdd_sfc_decode": [ctypes.c_int, ctypes.c_int, vp, vp, i64, vp, vp],
+        "sfcdd_sfc_perm": [ctypes.c_int, vp, vp, vp, ctypes.c_int, vp],
+        "sfcdd_op_create": [ctypes.POINTER(OpDesc), ctypes.POINTER(vp)],
+        "sfcdd_op_setup": [vp, vp],
+        "sfcdd_op_apply": [vp, vp, vp, vp],
+        "sfcdd_op_matvec": [vp, vp, vp, vp],
+        "sfcdd_op_pcg": [vp, vp, vp, dbl, i32, vp, ctypes.POINTER(i32), ctypes.POINTER(i32), vp],
+        "sfcdd_op_set_fault": [vp, i64, vp, i32],
+        "sfcdd_op_reset_calls": [vp],
+        "sfcdd_op_stats": [vp, ctypes.POINTER(Stats)],
+        "sfcdd_op_stencil": [vp, vp, vp, vp],
+        "sfcdd_op_coarse_dense": [vp, vp],
+        "sfcdd_factor_create": [i64, vp, vp, vp, i32, ctypes.POINTER(vp)],
+        "sfcdd_factor_solve": [vp, vp, vp, vp],
+        "sfcdd_factor_info": [vp, vp, vp, vp],
+        "sfcdd_host_amd": [i64, vp, vp, vp],
+        "sfcdd_host_factor_solve": [i64, vp, vp, vp, vp, vp, vp, vp],
+        "sfcdd_host_plan_solve": [i64, vp, vp, vp, i32, vp, vp, vp, vp, i32, i32, vp],
+    }
+    for name, args in sigs.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = ctypes.c_int
+    L.sfcdd_op_destroy.argtypes = [vp]
+    L.sfcdd_op_destroy.restype = None
+    L.sfcdd_factor_destroy.argtypes = [vp]
+    L.sfcdd_factor_destroy.restype = None
+    _lib = L
+    return L
+
+
+def check(rc: int) -> None:
+    """Map a C-ABI status to the reference's exception types."""
+    if rc == SFCDD_OK:
+        return
+    msg = lib().sfcdd_last_error().decode(errors="replace")
+    if rc == SFCDD_EVALUE:
+        raise ValueError(msg)
+    if rc == SFCDD_EFACTOR:
+        raise FactorizationError(msg)
+    if rc == SFCDD_EBREAKDOWN:
+        raise BreakdownError(msg)
+    if rc == SFCDD_EOVERFLOW:
+        raise OverflowError(msg)
+    if rc == SFCDD_ECUDA:
+        raise DeviceError(msg)
+    raise RuntimeError(f"sfcdd internal error ({rc}): {msg}")
+
+
+def ptr(a) -> int:
+    """Raw pointer of a numpy array or a torch tensor."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    return a.data_ptr()
+
+
+def device():
+    """The CUDA device used by the package (torch plumbing, fails loudly)."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device: the sfcdd B200 path has no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_ptr() -> int:
+    import torch
+
+    return torch.cuda.current_stream().cuda_stream
+
+
+def host_threads() -> int:
+    return int(os.environ.get("SFCDD_HOST_THREADS", "0"))

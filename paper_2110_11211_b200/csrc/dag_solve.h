@@ -1,0 +1,38 @@
+// Device-resident batch of block-inverse factors + the dataflow solve kernel.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "plan.h"
+
+namespace sfcdd {
+
+class DagSolver {
+ public:
+  DagSolver(const DevicePlan& plan, int device);
+  ~DagSolver();
+  DagSolver(const DagSolver&) = delete;
+  DagSolver& operator=(const DagSolver&) = delete;
+
+  // xy[factor i][ro] = A_i^{-1} rhs[(gstart_i + ro) mod gmod_i]
+  void solve(const double* rhs, cudaStream_t st, const int32_t* skip = nullptr);
+  double* xy() const { return xy_; }
+  int64_t xy_doubles() const { return xy_doubles_; }
+  int64_t device_bytes() const { return bytes_; }
+  int32_t grid() const { return grid_; }
+  int32_t nfrag() const { return nfrag_; }
+
+ private:
+  int device_;
+  int32_t nfrag_ = 0, ntask_ = 0, grid_ = 1, blob_max_ = 0, smem_ = 0;
+  int64_t xy_doubles_ = 0, ctr_words_ = 0, bytes_ = 0;
+  uint8_t* blobs_ = nullptr;
+  TaskDev* tasks_ = nullptr;
+  FactorDev* factors_ = nullptr;
+  double* upd_ = nullptr;
+  double* xy_ = nullptr;
+  int32_t* ctr_ = nullptr;
+};
+
+}  // namespace sfcdd

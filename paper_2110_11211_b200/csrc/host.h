@@ -39,8 +39,13 @@ struct Supernode {
   int32_t level = 0;     // height above the leaves (0 = leaf)
 };
 
-inline int64_t packed_size(int64_t s, int64_t m) { return s * (s + 1) / 2 + s * m; }
-inline int64_t packed_col_off(int64_t s, int64_t m, int64_t k) {
+#ifdef __CUDACC__
+#define SFCDD_HD __host__ __device__
+#else
+#define SFCDD_HD
+#endif
+SFCDD_HD inline int64_t packed_size(int64_t s, int64_t m) { return s * (s + 1) / 2 + s * m; }
+SFCDD_HD inline int64_t packed_col_off(int64_t s, int64_t m, int64_t k) {
   return k * (s + m) - k * (k - 1) / 2;
 }
 

@@ -1,0 +1,1014 @@
+// The two-level Schwarz operator: matrix-free stencil, coarse space, local
+// solves (DagSolver), weighting/combination, and a device-resident PCG.
+//
+// Reference composition replaced here (paths relative to
+// /root/reference/pkg/src/sfcdd/):
+//   grid.assemble_laplacian + symmetrize_diag   grid.py:91-130   -> Stencil
+//   partition.compute_weights                   partition.py:151 -> cover/weights
+//   coarse.build_coarse / DeflationOperators    coarse.py:38-88  -> R0 chunks, A0^{-1}
+//   schwarz.SchwarzOperator.apply               schwarz.py:103   -> apply()
+//   krylov.pcg                                  krylov.py:257    -> pcg()
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <thread>
+
+#include "op.h"
+#include "plan.h"
+
+namespace sfcdd {
+
+CsrMatrix extract_block(const CsrMatrix& A, int64_t start, int64_t len);
+
+namespace {
+
+inline unsigned nblocks(int64_t n, int t) { return (unsigned)std::max<int64_t>(1, (n + t - 1) / t); }
+
+template <typename F>
+void parallel_for(int64_t n, int threads, F fn) {
+  threads = std::max(1, std::min<int>(threads, (int)n));
+  if (threads == 1) {
+    for (int64_t i = 0; i < n; ++i) fn(i);
+    return;
+  }
+  std::atomic<int64_t> next{0};
+  std::vector<std::thread> pool;
+  std::exception_ptr err;
+  std::mutex mu;
+  for (int t = 0; t < threads; ++t)
+    pool.emplace_back([&] {
+      for (;;) {
+        int64_t i = next.fetch_add(1);
+        if (i >= n) break;
+        try {
+          fn(i);
+        } catch (...) {
+          std::lock_guard<std::mutex> g(mu);
+          if (!err) err = std::current_exception();
+          next = n;
+        }
+      }
+    });
+  for (auto& th : pool) th.join();
+  if (err) std::rethrow_exception(err);
+}
+
+// ------------------------------------------------------------ device side
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// deterministic block-wide sum (fixed tree), result valid in every thread
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double red[VEC_THREADS / 32];
+  __shared__ double total;
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    double t = lane < VEC_THREADS / 32 ? red[lane] : 0.0;
+    t = warp_sum(t);
+    if (lane == 0) total = t;
+  }
+  __syncthreads();
+  return total;
+}
+
+// last-block election; the last block must reset *ticket
+__device__ __forceinline__ bool last_block(uint32_t* ticket) {
+  __shared__ bool am_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) am_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  return am_last;
+}
+
+__device__ __forceinline__ double reduce_partials(const double* part, int n) {
+  double v = 0.0;
+  for (int i = threadIdx.x; i < n; i += VEC_THREADS) v += __ldcg(part + i);
+  return block_sum(v);
+}
+
+__device__ __forceinline__ double stencil_at(const Stencil& S, const double* __restrict__ x, int64_t g) {
+  double acc = S.dhat * x[g];
+  for (int a = 0; a < 2 * S.d; ++a) {
+    const int32_t nb = __ldg(S.nbr + (int64_t)a * S.n + g);
+    if (nb >= 0) acc = fma(S.off[a >> 1], x[nb], acc);
+  }
+  return acc;
+}
+
+__device__ __forceinline__ bool skip(const DevState* st) { return st != nullptr && st->done; }
+
+// neighbour table from perm/rank (grid.py:91-114 assembles the same couplings)
+__global__ void k_nbr(GridGeom g, const int64_t* __restrict__ perm, const int64_t* __restrict__ rank,
+                      int32_t* __restrict__ nbr) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= g.n) return;
+  int64_t lex = perm[s];
+  int64_t c[MAX_GRID_DIM];
+  int64_t stride[MAX_GRID_DIM];
+  int64_t rem = lex, st = 1;
+  for (int j = g.d - 1; j >= 0; --j) {
+    c[j] = rem % g.shape[j];
+    rem /= g.shape[j];
+    stride[j] = st;
+    st *= g.shape[j];
+  }
+  for (int j = 0; j < g.d; ++j) {
+    nbr[(int64_t)(2 * j) * g.n + s] = c[j] > 0 ? (int32_t)rank[lex - stride[j]] : -1;
+    nbr[(int64_t)(2 * j + 1) * g.n + s] = c[j] + 1 < g.shape[j] ? (int32_t)rank[lex + stride[j]] : -1;
+  }
+}
+
+__global__ void k_fill_agg(const int64_t* __restrict__ agg_start, int32_t n0, int32_t* __restrict__ agg) {
+  const int32_t a = blockIdx.x;
+  if (a >= n0) return;
+  for (int64_t g = agg_start[a] + threadIdx.x; g < agg_start[a + 1]; g += blockDim.x) agg[g] = a;
+}
+
+// per-chunk sums of v (R0 v partials) -- coarse.py:78 restriction
+__global__ void k_chunk_sum(const double* __restrict__ v, Chunks C, double* __restrict__ part) {
+  const int ch = blockIdx.x;
+  double s = 0.0;
+  for (int64_t g = C.start[ch] + threadIdx.x; g < C.start[ch + 1]; g += VEC_THREADS) s += v[g];
+  s = block_sum(s);
+  if (threadIdx.x == 0) part[ch] = s;
+}
+
+// y0 = A0^{-1} c with c[a] = sum of the chunk partials of aggregate a
+__global__ void k_coarse_gemv(const double* __restrict__ ainv, const double* __restrict__ part,
+                              const int32_t* __restrict__ agg_ptr, int32_t n0, double* __restrict__ y,
+                              const DevState* st) {
+  if (skip(st)) return;
+  extern __shared__ double c[];
+  for (int a = threadIdx.x; a < n0; a += VEC_THREADS) {
+    double s = 0.0;
+    for (int ch = agg_ptr[a]; ch < agg_ptr[a + 1]; ++ch) s += __ldcg(part + ch);
+    c[a] = s;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (VEC_THREADS / 32) + (threadIdx.x >> 5);
+  if (row >= n0) return;
+  const double* ar = ainv + (int64_t)row * n0;
+  double acc = 0.0;
+  for (int j = lane; j < n0; j += 32) acc = fma(__ldg(ar + j), c[j], acc);
+  acc = warp_sum(acc);
+  if (lane == 0) y[row] = acc;
+}
+
+// t = g - Â R0^T y0   (schwarz.py:116: g - A @ F(g))
+__global__ void k_tvec(const double* __restrict__ gv, const double* __restrict__ y0,
+                       const int32_t* __restrict__ agg, Stencil S, double* __restrict__ t,
+                       const DevState* st) {
+  if (skip(st)) return;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= S.n) return;
+  double acc = S.dhat * y0[agg[g]];
+  for (int a = 0; a < 2 * S.d; ++a) {
+    const int32_t nb = __ldg(S.nbr + (int64_t)a * S.n + g);
+    if (nb >= 0) acc = fma(S.off[a >> 1], y0[agg[nb]], acc);
+  }
+  t[g] = gv[g] - acc;
+}
+
+struct CombineArgs {
+  const double* xy;
+  const int64_t* ov_start;
+  const int64_t* ov_len;
+  const int64_t* xy_off;
+  const int64_t* dj_start;  // p + 1
+  const int32_t* cand_ptr;
+  const int32_t* cand;
+  const double* wgt;     // omega_i or 1
+  const int32_t* count;  // d_matrix weighting: cover counts (nullable)
+  const int8_t* fault;   // nullable
+  const long long* apply_calls;
+  long long fault_index;
+  int32_t p;
+  int64_t n;
+};
+
+// w = sum_i R_i^T D_i A_i^{-1} R_i (.) in subdomain order (schwarz.py:84-100)
+__global__ void k_combine(CombineArgs C, double* __restrict__ w, const DevState* st) {
+  if (skip(st)) return;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= C.n) return;
+  int lo = 0, hi = C.p;  // owner: dj_start[k] <= g < dj_start[k+1]
+  while (hi - lo > 1) {
+    int mid = (lo + hi) >> 1;
+    if (C.dj_start[mid] <= g)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  const bool faulty = C.fault != nullptr && *C.apply_calls == C.fault_index;
+  double acc = 0.0;
+  for (int c = C.cand_ptr[lo]; c < C.cand_ptr[lo + 1]; ++c) {
+    const int i = C.cand[c];
+    int64_t off = g - C.ov_start[i];
+    if (off < 0) off += C.n;
+    if (off >= C.ov_len[i]) continue;
+    if (faulty && C.fault[i]) continue;
+    double wt = C.count ? 1.0 / (double)C.count[g] : C.wgt[i];
+    acc = __dadd_rn(acc, __dmul_rn(wt, __ldcg(C.xy + C.xy_off[i] + off)));
+  }
+  w[g] = acc;
+}
+
+// per-chunk partials of sum (Â w) -> R0 Â w  (coarse.py:84 project_transpose)
+__global__ void k_matvec_chunk(const double* __restrict__ w, Stencil S, Chunks C, double* __restrict__ part,
+                               const DevState* st) {
+  if (skip(st)) return;
+  const int ch = blockIdx.x;
+  double s = 0.0;
+  for (int64_t g = C.start[ch] + threadIdx.x; g < C.start[ch + 1]; g += VEC_THREADS) s += stencil_at(S, w, g);
+  s = block_sum(s);
+  if (threadIdx.x == 0) part[ch] = s;
+}
+
+// h = (w - R0^T y0b) + R0^T y0 (balanced/deflated), w + R0^T y0 (additive),
+// w (one-level); optional r.h partials for PCG (krylov.py:288)
+__global__ void k_finalize(const double* __restrict__ w, const double* __restrict__ y0,
+                           const double* __restrict__ y0b, Chunks C, int mode, double* __restrict__ h,
+                           const double* __restrict__ rdot, double* __restrict__ part, DevState* st,
+                           bool pcg) {
+  if (pcg && skip(st)) return;
+  const int ch = blockIdx.x;
+  const int a = C.agg ? C.agg[ch] : -1;
+  const double c0 = (mode >= 1 && a >= 0) ? y0[a] : 0.0;
+  const double c1 = (mode >= 2 && a >= 0) ? y0b[a] : 0.0;
+  double s = 0.0;
+  for (int64_t g = C.start[ch] + threadIdx.x; g < C.start[ch + 1]; g += VEC_THREADS) {
+    double v = w[g];
+    if (mode == 1) v = v + c0;
+    if (mode == 2) v = (v - c1) + c0;
+    h[g] = v;
+    if (rdot) s = fma(rdot[g], v, s);
+  }
+  if (rdot) {
+    s = block_sum(s);
+    if (threadIdx.x == 0) part[ch] = s;
+  }
+  if (last_block(&st->ticket[3])) {
+    double rz = rdot ? reduce_partials(part, gridDim.x) : 0.0;
+    if (threadIdx.x == 0) {
+      st->ticket[3] = 0;
+      st->apply_calls += 1;
+      if (pcg) {
+        st->beta = st->have_rz ? rz / st->rz : 0.0;  // krylov.py:289
+        st->have_rz = 1;
+        st->rz = rz;
+      }
+    }
+  }
+}
+
+__global__ void k_matvec(const double* __restrict__ x, Stencil S, double* __restrict__ y) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g < S.n) y[g] = stencil_at(S, x, g);
+}
+
+// r = b - Â x; ||r||^2 and R0 r partials (krylov.py:267-271)
+__global__ void k_residual0(const double* __restrict__ b, const double* __restrict__ x, Stencil S, Chunks C,
+                            double* __restrict__ r, double* __restrict__ part_rr,
+                            double* __restrict__ part_c, DevState* st, double* hist) {
+  const int ch = blockIdx.x;
+  double rr = 0.0, cs = 0.0;
+  for (int64_t g = C.start[ch] + threadIdx.x; g < C.start[ch + 1]; g += VEC_THREADS) {
+    const double v = b[g] - stencil_at(S, x, g);
+    r[g] = v;
+    rr = fma(v, v, rr);
+    cs += v;
+  }
+  rr = block_sum(rr);
+  cs = block_sum(cs);
+  if (threadIdx.x == 0) {
+    part_rr[ch] = rr;
+    part_c[ch] = cs;
+  }
+  if (last_block(&st->ticket[0])) {
+    const double tot = reduce_partials(part_rr, gridDim.x);
+    if (threadIdx.x == 0) {
+      st->ticket[0] = 0;
+      const double nrm = sqrt(tot);
+      hist[0] = nrm;
+      st->hist0 = nrm;
+      st->k = 0;
+      if (nrm <= st->tol * nrm) {  // krylov.py:268-270 (only for r0 == 0)
+        st->converged = 1;
+        st->done = 1;
+      }
+    }
+  }
+}
+
+// p = z + beta p_old ; Ap = Â p ; p.Ap partials (krylov.py:276-279, 289)
+__global__ void k_pm(const double* __restrict__ z, const double* __restrict__ pold, Stencil S, Chunks C,
+                     double* __restrict__ pnew, double* __restrict__ ap, double* __restrict__ part,
+                     DevState* st) {
+  if (skip(st)) return;
+  const double beta = st->beta;
+  const int ch = blockIdx.x;
+  double s = 0.0;
+  for (int64_t g = C.start[ch] + threadIdx.x; g < C.start[ch + 1]; g += VEC_THREADS) {
+    const double pg = __dadd_rn(z[g], __dmul_rn(beta, pold[g]));
+    double acc = S.dhat * pg;
+    for (int a = 0; a < 2 * S.d; ++a) {
+      const int32_t nb = __ldg(S.nbr + (int64_t)a * S.n + g);
+      if (nb >= 0) acc = fma(S.off[a >> 1], __dadd_rn(z[nb], __dmul_rn(beta, pold[nb])), acc);
+    }
+    pnew[g] = pg;
+    ap[g] = acc;
+    s = fma(pg, acc, s);
+  }
+  s = block_sum(s);
+  if (threadIdx.x == 0) part[ch] = s;
+  if (last_block(&st->ticket[1])) {
+    const double pap = reduce_partials(part, gridDim.x);
+    if (threadIdx.x == 0) {
+      st->ticket[1] = 0;
+      st->pap = pap;
+      if (!(pap > 0.0)) {
+        st->breakdown = 1;
+        st->done = 1;
+      } else {
+        st->alpha = st->rz / pap;
+      }
+    }
+  }
+}
+
+// x += alpha p ; r -= alpha Ap ; ||r|| -> history ; R0 r partials
+__global__ void k_update(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                         const double* __restrict__ ap, Chunks C, double* __restrict__ part_rr,
+                         double* __restrict__ part_c, DevState* st, double* hist) {
+  if (skip(st)) return;
+  const double alpha = st->alpha;
+  const int ch = blockIdx.x;
+  double rr = 0.0, cs = 0.0;
+  for (int64_t g = C.start[ch] + threadIdx.x; g < C.start[ch + 1]; g += VEC_THREADS) {
+    x[g] = __dadd_rn(x[g], __dmul_rn(alpha, p[g]));
+    const double v = __dsub_rn(r[g], __dmul_rn(alpha, ap[g]));
+    r[g] = v;
+    rr = fma(v, v, rr);
+    cs += v;
+  }
+  rr = block_sum(rr);
+  cs = block_sum(cs);
+  if (threadIdx.x == 0) {
+    part_rr[ch] = rr;
+    part_c[ch] = cs;
+  }
+  if (last_block(&st->ticket[2])) {
+    const double tot = reduce_partials(part_rr, gridDim.x);
+    if (threadIdx.x == 0) {
+      st->ticket[2] = 0;
+      const int k = st->k + 1;
+      st->k = k;
+      const double nrm = sqrt(tot);
+      hist[k] = nrm;
+      if (nrm <= st->tol * st->hist0) {  // krylov.py:283-286
+        st->converged = 1;
+        st->done = 1;
+      } else if (k >= st->max_iters) {
+        st->exhausted = 1;
+        st->done = 1;
+      }
+    }
+  }
+}
+
+__global__ void k_zero_state_pcg(DevState* st, double tol, int32_t max_iters) {
+  st->tol = tol;
+  st->hist0 = 0;
+  st->rz = st->beta = st->pap = st->alpha = 0;
+  st->k = st->converged = st->breakdown = st->exhausted = st->have_rz = st->done = 0;
+  st->max_iters = max_iters;
+  for (int i = 0; i < 8; ++i) st->ticket[i] = 0;
+}
+
+}  // namespace
+
+// ----------------------------------------------------------- host helpers
+static Stencil stencil_of(const sfcdd_op* op) {
+  Stencil S;
+  S.d = op->d;
+  S.n = op->n;
+  S.dhat = op->dhat;
+  for (int j = 0; j < MAX_GRID_DIM; ++j) S.off[j] = j < op->d ? op->off[j] : 0.0;
+  S.nbr = op->nbr;
+  return S;
+}
+
+static Chunks chunks_of(const sfcdd_op* op) {
+  return Chunks{op->chunk_start, op->n0 > 0 ? op->chunk_agg : nullptr, op->agg_ptr, op->nch};
+}
+
+static void* dev_alloc(sfcdd_op* op, size_t bytes) {
+  void* p = nullptr;
+  CUDA_CHECK(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+  op->dev_bytes += std::max<size_t>(bytes, 16);
+  return p;
+}
+
+template <typename T>
+static T* dev_upload(sfcdd_op* op, const std::vector<T>& v) {
+  T* p = (T*)dev_alloc(op, v.size() * sizeof(T));
+  if (!v.empty()) CUDA_CHECK(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return p;
+}
+
+static int mode_of(int variant) {
+  switch (variant) {
+    case SFCDD_VARIANT_ONE_LEVEL: return 0;
+    case SFCDD_VARIANT_ADDITIVE: return 1;
+    default: return 2;
+  }
+}
+
+// the preconditioner apply on device: h = C^{-1} g.  If `pcg`, the R0 g
+// partials are already in part_c (fused into k_update) and r.h partials are
+// produced for the PCG scalars.
+static void apply_device(sfcdd_op* op, const double* g, double* h, cudaStream_t st, bool pcg,
+                         bool partials_ready) {
+  const Stencil S = stencil_of(op);
+  const Chunks C = chunks_of(op);
+  DevState* dst = op->st;
+  const DevState* sk = pcg ? op->st : nullptr;
+  const int v = op->variant;
+  const bool coarse = v != SFCDD_VARIANT_ONE_LEVEL;
+  const size_t csm = (size_t)op->n0 * sizeof(double);
+  const unsigned cgrid = nblocks(op->n0, VEC_THREADS / 32);
+  if (coarse) {
+    if (!partials_ready) k_chunk_sum<<<op->nch, VEC_THREADS, 0, st>>>(g, C, op->part_c);
+    k_coarse_gemv<<<cgrid, VEC_THREADS, csm, st>>>(op->ainv, op->part_c, op->agg_ptr, op->n0, op->y0, sk);
+  }
+  const double* rhs = g;
+  if (v == SFCDD_VARIANT_BALANCED) {
+    k_tvec<<<nblocks(op->n, VEC_THREADS), VEC_THREADS, 0, st>>>(g, op->y0, op->agg, S, op->t, sk);
+    rhs = op->t;
+  }
+  op->dag->solve(rhs, st, sk ? &op->st->done : nullptr);
+  CombineArgs ca;
+  ca.xy = op->dag->xy();
+  ca.ov_start = op->d_ov_start;
+  ca.ov_len = op->d_ov_len;
+  ca.xy_off = op->d_xy_off;
+  ca.dj_start = op->d_dj_start;
+  ca.cand_ptr = op->cand_ptr;
+  ca.cand = op->cand;
+  ca.wgt = op->d_wgt;
+  ca.count = op->weighting == SFCDD_WEIGHT_DMATRIX ? op->d_count : nullptr;
+  ca.fault = op->d_fault;
+  ca.apply_calls = &dst->apply_calls;
+  ca.fault_index = op->stats.reserved[0];
+  ca.p = op->p;
+  ca.n = op->n;
+  k_combine<<<nblocks(op->n, VEC_THREADS), VEC_THREADS, 0, st>>>(ca, op->w, sk);
+  const int mode = mode_of(v);
+  if (mode == 2) {
+    k_matvec_chunk<<<op->nch, VEC_THREADS, 0, st>>>(op->w, S, C, op->part_b, sk);
+    k_coarse_gemv<<<cgrid, VEC_THREADS, csm, st>>>(op->ainv, op->part_b, op->agg_ptr, op->n0, op->y0b, sk);
+  }
+  k_finalize<<<op->nch, VEC_THREADS, 0, st>>>(op->w, op->y0, op->y0b, C, mode, h, pcg ? op->r : nullptr,
+                                              op->part_a, dst, pcg);
+  CUDA_CHECK(cudaGetLastError());
+}
+
+// one PCG iteration (krylov.py:275-290) -- captured into a CUDA graph
+static void pcg_iteration(sfcdd_op* op, double* x, const double* pold, double* pnew, cudaStream_t st) {
+  const Stencil S = stencil_of(op);
+  const Chunks C = chunks_of(op);
+  k_pm<<<op->nch, VEC_THREADS, 0, st>>>(op->z, pold, S, C, pnew, op->ap, op->part_a, op->st);
+  k_update<<<op->nch, VEC_THREADS, 0, st>>>(x, op->r, pnew, op->ap, C, op->part_b, op->part_c, op->st,
+                                            op->hist);
+  apply_device(op, op->r, op->z, st, true, true);
+}
+
+}  // namespace sfcdd
+
+using namespace sfcdd;
+
+// ================================================================ C ABI
+extern "C" int sfcdd_op_create(const sfcdd_op_desc* desc, sfcdd_op** out) {
+  SFCDD_API_BEGIN
+  SFCDD_REQUIRE(desc && out, SFCDD_EVALUE, "null argument");
+  std::unique_ptr<sfcdd_op> op(new sfcdd_op());
+  op->device = desc->device;
+  op->d = desc->dim;
+  SFCDD_REQUIRE(op->d >= 1 && op->d <= 8, SFCDD_EVALUE, "grid dimension must be in [1, 8]");
+  op->n = 1;
+  double diag = 0.0;
+  for (int j = 0; j < op->d; ++j) {
+    op->levels[j] = desc->levels[j];
+    SFCDD_REQUIRE(desc->levels[j] >= 1 && desc->levels[j] <= 31, SFCDD_EVALUE, "level out of range");
+    const int64_t s = ((int64_t)1 << desc->levels[j]) - 1;
+    SFCDD_REQUIRE(op->n <= ((int64_t)1 << 62) / s, SFCDD_EOVERFLOW, "dof count exceeds 2^62");
+    op->n *= s;
+    diag = diag + 2.0 * std::ldexp(1.0, 2 * desc->levels[j]);  // kron-sum diagonal (grid.py:101-110)
+  }
+  SFCDD_REQUIRE(op->n < ((int64_t)1 << 31), SFCDD_EVALUE, "grids above 2^31 points need multi-GPU sharding");
+  // T A T with t = diag^-1/2 (grid.py:117-130): entries fl(fl(t a) t)
+  const double t = 1.0 / std::sqrt(diag);
+  op->tscale = t;
+  op->dhat = (t * diag) * t;
+  for (int j = 0; j < op->d; ++j) op->off[j] = (t * -std::ldexp(1.0, 2 * desc->levels[j])) * t;
+  op->p = desc->p;
+  op->q = desc->q;
+  op->variant = desc->variant;
+  op->weighting = desc->weighting;
+  op->threads = desc->host_threads > 0 ? desc->host_threads : hardware_threads();
+  SFCDD_REQUIRE(op->p >= 1 && op->p <= op->n, SFCDD_EVALUE, "need 1 <= P <= N");
+  SFCDD_REQUIRE(op->variant >= 0 && op->variant <= 3, SFCDD_EVALUE, "unknown variant");
+  SFCDD_REQUIRE(op->weighting >= 0 && op->weighting <= 2, SFCDD_EVALUE, "unknown weighting");
+  const bool coarse = op->variant != SFCDD_VARIANT_ONE_LEVEL;
+  if (coarse) SFCDD_REQUIRE(op->q >= 1 && op->q <= op->n / op->p, SFCDD_EVALUE, "need 1 <= q <= floor(N/P)");
+  op->ov_start.assign(desc->ov_start, desc->ov_start + op->p);
+  op->ov_len.assign(desc->ov_len, desc->ov_len + op->p);
+  op->dj_start.assign(desc->dj_start, desc->dj_start + op->p);
+  op->dj_len.assign(desc->dj_len, desc->dj_len + op->p);
+  op->omega.assign(desc->omega, desc->omega + op->p);
+  int64_t acc = 0;
+  for (int i = 0; i < op->p; ++i) {
+    SFCDD_REQUIRE(op->dj_start[i] == acc, SFCDD_EVALUE, "disjoint ranges must tile [0, N) in order");
+    acc += op->dj_len[i];
+    SFCDD_REQUIRE(op->ov_start[i] >= 0 && op->ov_start[i] < op->n && op->ov_len[i] >= 1 &&
+                      op->ov_len[i] <= op->n,
+                  SFCDD_EVALUE, "overlapped range out of bounds");
+  }
+  SFCDD_REQUIRE(acc == op->n, SFCDD_EVALUE, "disjoint ranges must cover N");
+
+  CUDA_CHECK(cudaSetDevice(op->device));
+  CUDA_CHECK(cudaStreamCreateWithFlags(&op->own_stream, cudaStreamNonBlocking));
+  CUDA_CHECK(cudaEventCreate(&op->ev0));
+  CUDA_CHECK(cudaEventCreate(&op->ev1));
+  cudaStream_t st = op->own_stream;
+  // SFC permutation and neighbour table
+  int64_t* perm = (int64_t*)dev_alloc(op.get(), op->n * 8);
+  int64_t* rank = (int64_t*)dev_alloc(op.get(), op->n * 8);
+  sfc_perm_device(op->d, op->levels, perm, rank, false, st);
+  GridGeom g{};
+  g.d = op->d;
+  g.n = op->n;
+  for (int j = 0; j < op->d; ++j) g.shape[j] = ((int64_t)1 << op->levels[j]) - 1;
+  op->nbr = (int32_t*)dev_alloc(op.get(), (size_t)2 * op->d * op->n * 4);
+  k_nbr<<<nblocks(op->n, 256), 256, 0, st>>>(g, perm, rank, op->nbr);
+  CUDA_CHECK(cudaGetLastError());
+  CUDA_CHECK(cudaStreamSynchronize(st));
+  CUDA_CHECK(cudaFree(perm));
+  CUDA_CHECK(cudaFree(rank));
+  op->dev_bytes -= 2 * std::max<int64_t>(op->n * 8, 16);
+  // aggregates (coarse.py:44-55) and reduction chunks
+  std::vector<int64_t> cstart{0};
+  std::vector<int32_t> cagg, aptr{0};
+  if (coarse) {
+    op->n0 = op->q * op->p;
+    op->agg_start.assign(1, 0);
+    for (int i = 0; i < op->p; ++i) {
+      const int64_t base = op->dj_len[i] / op->q, extra = op->dj_len[i] % op->q;
+      for (int mm = 0; mm < op->q; ++mm) op->agg_start.push_back(op->agg_start.back() + base + (mm < extra));
+    }
+    for (int32_t a = 0; a < op->n0; ++a) {
+      for (int64_t s0 = op->agg_start[a]; s0 < op->agg_start[a + 1]; s0 += CHUNK) {
+        cstart.push_back(std::min<int64_t>(s0 + CHUNK, op->agg_start[a + 1]));
+        cagg.push_back(a);
+      }
+      aptr.push_back((int32_t)cagg.size());
+    }
+    op->agg = (int32_t*)dev_alloc(op.get(), op->n * 4);
+    int64_t* das = dev_upload(op.get(), op->agg_start);
+    k_fill_agg<<<op->n0, 256, 0, st>>>(das, op->n0, op->agg);
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    CUDA_CHECK(cudaFree(das));
+  } else {
+    for (int64_t s0 = 0; s0 < op->n; s0 += CHUNK) {
+      cstart.push_back(std::min<int64_t>(s0 + CHUNK, op->n));
+      cagg.push_back(-1);
+    }
+  }
+  op->nch = (int32_t)cagg.size();
+  op->chunk_start = dev_upload(op.get(), cstart);
+  op->chunk_agg = dev_upload(op.get(), cagg);
+  op->agg_ptr = dev_upload(op.get(), aptr);
+  *out = op.release();
+  SFCDD_API_END
+}
+
+extern "C" int sfcdd_op_setup(sfcdd_op* op, void* stream) {
+  SFCDD_API_BEGIN
+  (void)stream;
+  SFCDD_REQUIRE(op, SFCDD_EVALUE, "null handle");
+  CUDA_CHECK(cudaSetDevice(op->device));
+  auto t0 = std::chrono::steady_clock::now();
+  const int64_t n = op->n;
+  const int d = op->d;
+  // host copy of the neighbour table (setup only)
+  std::vector<int32_t> nbr((size_t)2 * d * n);
+  CUDA_CHECK(cudaMemcpy(nbr.data(), op->nbr, nbr.size() * 4, cudaMemcpyDeviceToHost));
+  // local blocks Â_i = Â[idx_i][:, idx_i] (schwarz.py:58-61)
+  std::vector<HostFactor> fs(op->p);
+  FactorOptions fo;
+  std::atomic<int64_t> order_ns{0};
+  parallel_for(op->p, op->threads, [&](int64_t i) {
+    const int64_t start = op->ov_start[i], len = op->ov_len[i];
+    CsrMatrix B;
+    B.n = len;
+    B.indptr.assign(len + 1, 0);
+    B.indices.reserve(len * (2 * d + 1));
+    B.data.reserve(len * (2 * d + 1));
+    for (int64_t ro = 0; ro < len; ++ro) {
+      int64_t gg = start + ro;
+      if (gg >= n) gg -= n;
+      B.indices.push_back((int32_t)ro);
+      B.data.push_back(op->dhat);
+      for (int a = 0; a < 2 * d; ++a) {
+        const int32_t nb = nbr[(size_t)a * n + gg];
+        if (nb < 0) continue;
+        int64_t c = nb - start;
+        if (c < 0) c += n;
+        if (c < len) {
+          B.indices.push_back((int32_t)c);
+          B.data.push_back(op->off[a >> 1]);
+        }
+      }
+      B.indptr[ro + 1] = B.indices.size();
+    }
+    fs[i] = factorize_host(B, fo);
+  });
+  auto t1 = std::chrono::steady_clock::now();
+  std::vector<const HostFactor*> ptrs;
+  std::vector<int64_t> gs, gm, xyoff;
+  int64_t xo = 0;
+  for (int i = 0; i < op->p; ++i) {
+    ptrs.push_back(&fs[i]);
+    gs.push_back(op->ov_start[i]);
+    gm.push_back(n);
+    xyoff.push_back(xo);
+    xo += op->ov_len[i];
+  }
+  PlanOptions po;
+  DevicePlan plan = build_plan(ptrs, gs, gm, po);
+  op->stats.factor_nnz = plan.stored;
+  op->stats.factor_nnz_l = plan.nnz_l;
+  op->stats.num_tasks = plan.nfrag;
+  op->stats.num_supernodes = plan.num_supernodes;
+  op->dag.reset(new DagSolver(plan, op->device));
+  op->dev_bytes += op->dag->device_bytes();
+  fs.clear();
+  // combination tables: candidates per disjoint range (ascending subdomain)
+  std::vector<int32_t> cptr{0}, cand;
+  for (int k = 0; k < op->p; ++k) {
+    const int64_t a0 = op->dj_start[k], a1 = a0 + op->dj_len[k];  // [a0, a1)
+    for (int i = 0; i < op->p; ++i) {
+      // does cyclic range i intersect [a0, a1)?
+      const int64_t s = op->ov_start[i], l = op->ov_len[i];
+      bool hit = false;
+      int64_t off = a0 - s;
+      if (off < 0) off += n;
+      if (off < l) hit = true;
+      if (!hit) {
+        const int64_t e = s;  // start of i inside [a0, a1)?
+        if (e >= a0 && e < a1) hit = true;
+      }
+      if (hit) cand.push_back(i);
+    }
+    cptr.push_back((int32_t)cand.size());
+  }
+  op->cand_ptr = dev_upload(op, cptr);
+  op->cand = dev_upload(op, cand);
+  op->d_ov_start = dev_upload(op, op->ov_start);
+  op->d_ov_len = dev_upload(op, op->ov_len);
+  op->d_xy_off = dev_upload(op, xyoff);
+  std::vector<int64_t> djs(op->dj_start);
+  djs.push_back(n);
+  op->d_dj_start = dev_upload(op, djs);
+  std::vector<double> wgt(op->p, 1.0);
+  if (op->weighting == SFCDD_WEIGHT_OMEGA) wgt = op->omega;
+  op->d_wgt = dev_upload(op, wgt);
+  if (op->weighting == SFCDD_WEIGHT_DMATRIX) {
+    std::vector<int32_t> cnt(n, 0);  // partition.py:151-155
+    for (int i = 0; i < op->p; ++i)
+      for (int64_t ro = 0; ro < op->ov_len[i]; ++ro) {
+        int64_t gg = op->ov_start[i] + ro;
+        if (gg >= n) gg -= n;
+        cnt[gg]++;
+      }
+    op->d_count = dev_upload(op, cnt);
+  }
+  std::vector<int8_t> fault(op->p, 0);
+  op->d_fault = nullptr;
+  (void)fault;
+  // coarse problem A0 = R0 Â R0^T, symmetrized (linalg.py:83-91), dense inverse
+  if (op->n0 > 0) {
+    SFCDD_REQUIRE(op->n0 <= 8192, SFCDD_EVALUE, "coarse problems above 8192 dofs are not supported yet");
+    const int32_t n0 = op->n0;
+    std::vector<int32_t> aggh(n);
+    for (int32_t a = 0; a < n0; ++a)
+      for (int64_t g2 = op->agg_start[a]; g2 < op->agg_start[a + 1]; ++g2) aggh[g2] = a;
+    std::vector<std::vector<std::pair<int32_t, double>>> rows(n0);
+    parallel_for(n0, op->threads, [&](int64_t a) {
+      std::map<int32_t, double> acc;
+      for (int64_t g2 = op->agg_start[a]; g2 < op->agg_start[a + 1]; ++g2) {
+        acc[(int32_t)a] += op->dhat;
+        for (int aa = 0; aa < 2 * d; ++aa) {
+          const int32_t nb = nbr[(size_t)aa * n + g2];
+          if (nb >= 0) acc[aggh[nb]] += op->off[aa >> 1];
+        }
+      }
+      rows[a].assign(acc.begin(), acc.end());
+    });
+    // symmetrize: (B + B^T) / 2
+    std::vector<std::map<int32_t, double>> sym(n0);
+    for (int32_t a = 0; a < n0; ++a)
+      for (auto& e : rows[a]) {
+        sym[a][e.first] += 0.5 * e.second;
+        sym[e.first][a] += 0.5 * e.second;
+      }
+    CsrMatrix A0;
+    A0.n = n0;
+    A0.indptr.assign(n0 + 1, 0);
+    op->a0_dense.assign((size_t)n0 * n0, 0.0);
+    for (int32_t a = 0; a < n0; ++a) {
+      for (auto& e : sym[a]) {
+        A0.indices.push_back(e.first);
+        A0.data.push_back(e.second);
+        op->a0_dense[(size_t)a * n0 + e.first] = e.second;
+      }
+      A0.indptr[a + 1] = A0.indices.size();
+    }
+    op->stats.coarse_nnz = A0.indices.size();
+    HostFactor F0 = factorize_host(A0, fo);
+    std::vector<double> ainv((size_t)n0 * n0);
+    parallel_for(n0, op->threads, [&](int64_t j) {
+      std::vector<double> e(n0, 0.0), col(n0);
+      e[j] = 1.0;
+      host_block_solve(F0, e.data(), col.data());
+      for (int32_t i = 0; i < n0; ++i) ainv[(size_t)j * n0 + i] = col[i];  // symmetric: row j
+    });
+    op->ainv = dev_upload(op, ainv);
+    op->y0 = (double*)dev_alloc(op, n0 * 8);
+    op->y0b = (double*)dev_alloc(op, n0 * 8);
+    CUDA_CHECK(cudaMemset(op->y0, 0, n0 * 8));
+    CUDA_CHECK(cudaMemset(op->y0b, 0, n0 * 8));
+    if ((size_t)n0 * 8 > 48 * 1024) {
+      auto set = [&](auto kern) {
+        CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, n0 * 8));
+      };
+      set(k_coarse_gemv);
+    }
+  }
+  // work vectors
+  op->t = (double*)dev_alloc(op, n * 8);
+  op->w = (double*)dev_alloc(op, n * 8);
+  op->r = (double*)dev_alloc(op, n * 8);
+  op->z = (double*)dev_alloc(op, n * 8);
+  op->p0 = (double*)dev_alloc(op, n * 8);
+  op->p1 = (double*)dev_alloc(op, n * 8);
+  op->ap = (double*)dev_alloc(op, n * 8);
+  op->part_a = (double*)dev_alloc(op, op->nch * 8);
+  op->part_b = (double*)dev_alloc(op, op->nch * 8);
+  op->part_c = (double*)dev_alloc(op, op->nch * 8);
+  op->st = (DevState*)dev_alloc(op, sizeof(DevState));
+  CUDA_CHECK(cudaMemset(op->st, 0, sizeof(DevState)));
+  op->stats.reserved[0] = -1;  // fault index
+  op->hist_cap = 0;
+  op->ready = true;
+  auto t2 = std::chrono::steady_clock::now();
+  op->stats.n = n;
+  op->stats.n0 = op->n0;
+  op->stats.factor_seconds = std::chrono::duration<double>(t1 - t0).count();
+  op->stats.setup_seconds = std::chrono::duration<double>(t2 - t0).count();
+  SFCDD_API_END
+}
+
+extern "C" int sfcdd_op_apply(sfcdd_op* op, const double* g_dev, double* h_dev, void* stream) {
+  SFCDD_API_BEGIN
+  SFCDD_REQUIRE(op && op->ready, SFCDD_EVALUE, "operator not set up");
+  CUDA_CHECK(cudaSetDevice(op->device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : op->own_stream;
+  apply_device(op, g_dev, h_dev, st, false, false);
+  SFCDD_API_END
+}
+
+extern "C" int sfcdd_op_matvec(sfcdd_op* op, const double* x_dev, double* y_dev, void* stream) {
+  SFCDD_API_BEGIN
+  SFCDD_REQUIRE(op, SFCDD_EVALUE, "null handle");
+  CUDA_CHECK(cudaSetDevice(op->device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : op->own_stream;
+  k_matvec<<<nblocks(op->n, VEC_THREADS), VEC_THREADS, 0, st>>>(x_dev, stencil_of(op), y_dev);
+  CUDA_CHECK(cudaGetLastError());
+  SFCDD_API_END
+}
+
+extern "C" int sfcdd_op_pcg(sfcdd_op* op, const double* b_dev, double* x_dev, double tol, int32_t max_iters,
+                            double* res_hist_host, int32_t* iters, int32_t* converged, void* stream) {
+  SFCDD_API_BEGIN
+  SFCDD_REQUIRE(op && op->ready, SFCDD_EVALUE, "operator not set up");
+  SFCDD_REQUIRE(tol > 0, SFCDD_EVALUE, "tolerance must be positive");
+  SFCDD_REQUIRE(max_iters >= 0, SFCDD_EVALUE, "max_iters must be nonnegative");
+  CUDA_CHECK(cudaSetDevice(op->device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : op->own_stream;
+  if (op->hist_cap < max_iters + 1) {
+    if (op->hist) CUDA_CHECK(cudaFree(op->hist));
+    op->hist = (double*)dev_alloc(op, (size_t)(max_iters + 1) * 8);
+    op->hist_cap = max_iters + 1;
+  }
+  const Stencil S = stencil_of(op);
+  const Chunks C = chunks_of(op);
+  k_zero_state_pcg<<<1, 1, 0, st>>>(op->st, tol, max_iters);
+  CUDA_CHECK(cudaMemsetAsync(op->p0, 0, op->n * 8, st));
+  k_residual0<<<op->nch, VEC_THREADS, 0, st>>>(b_dev, x_dev, S, C, op->r, op->part_b, op->part_c, op->st,
+                                               op->hist);
+  // z = C^{-1} r (krylov.py:272); skipped on device if r0 == 0
+  apply_device(op, op->r, op->z, st, true, true);
+  if (max_iters > 0) {
+    // capture two iterations (p buffers ping-pong) once per stream/x; replay
+    // the graph until the device flags convergence / breakdown / max_iters
+    if (!op->pcg_graph || op->pcg_graph_stream != st || op->stats.reserved[1] != (int64_t)x_dev) {
+      if (op->pcg_graph) CUDA_CHECK(cudaGraphExecDestroy(op->pcg_graph));
+      cudaGraph_t graph;
+      CUDA_CHECK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      pcg_iteration(op, x_dev, op->p0, op->p1, st);
+      pcg_iteration(op, x_dev, op->p1, op->p0, st);
+      CUDA_CHECK(cudaStreamEndCapture(st, &graph));
+      CUDA_CHECK(cudaGraphInstantiate(&op->pcg_graph, graph, 0));
+      CUDA_CHECK(cudaGraphDestroy(graph));
+      op->pcg_graph_stream = st;
+      op->stats.reserved[1] = (int64_t)x_dev;
+    }
+    DevState hs;
+    int launched = 0;  // iterations launched (2 per graph)
+    int chunk = 2;     // graph launches between host polls
+    while (launched < max_iters) {
+      for (int i = 0; i < chunk && launched < max_iters; ++i) {
+        CUDA_CHECK(cudaGraphLaunch(op->pcg_graph, st));
+        launched += 2;
+      }
+      CUDA_CHECK(cudaMemcpyAsync(&hs, op->st, sizeof(DevState), cudaMemcpyDeviceToHost, st));
+      CUDA_CHECK(cudaStreamSynchronize(st));
+      if (hs.done) break;
+      chunk = std::min(chunk * 2, 8);
+    }
+  }
+  DevState hs;
+  CUDA_CHECK(cudaMemcpyAsync(&hs, op->st, sizeof(DevState), cudaMemcpyDeviceToHost, st));
+  CUDA_CHECK(cudaStreamSynchronize(st));
+  const int k = hs.k;
+  if (res_hist_host) CUDA_CHECK(cudaMemcpy(res_hist_host, op->hist, (size_t)(k + 1) * 8, cudaMemcpyDeviceToHost));
+  *iters = k;
+  *converged = hs.converged;
+  if (hs.breakdown) throw Error(SFCDD_EBREAKDOWN, "nonpositive curvature at iteration " + std::to_string(k + 1));
+  SFCDD_API_END
+}
+
+extern "C" int sfcdd_op_set_fault(sfcdd_op* op, int64_t apply_index, const int32_t* ids_host, int32_t nids) {
+  SFCDD_API_BEGIN
+  SFCDD_REQUIRE(op && op->ready, SFCDD_EVALUE, "operator not set up");
+  CUDA_CHECK(cudaSetDevice(op->device));
+  if (nids <= 0) {
+    op->stats.reserved[0] = -1;
+    if (op->d_fault) CUDA_CHECK(cudaFree(op->d_fault));
+    op->d_fault = nullptr;
+    return SFCDD_OK;
+  }
+  std::vector<int8_t> mask(op->p, 0);
+  for (int32_t i = 0; i < nids; ++i) {
+    SFCDD_REQUIRE(ids_host[i] >= 0 && ids_host[i] < op->p, SFCDD_EVALUE, "fault subdomain out of range");
+    mask[ids_host[i]] = 1;
+  }
+  if (!op->d_fault) op->d_fault = (int8_t*)dev_alloc(op, op->p);
+  CUDA_CHECK(cudaMemcpy(op->d_fault, mask.data(), op->p, cudaMemcpyHostToDevice));
+  op->stats.reserved[0] = apply_index;
+  // the PCG graph bakes kernel arguments: force re-capture
+  if (op->pcg_graph) CUDA_CHECK(cudaGraphExecDestroy(op->pcg_graph));
+  op->pcg_graph = nullptr;
+  SFCDD_API_END
+}
+
+extern "C" int sfcdd_op_reset_calls(sfcdd_op* op) {
+  SFCDD_API_BEGIN
+  SFCDD_REQUIRE(op && op->ready, SFCDD_EVALUE, "operator not set up");
+  CUDA_CHECK(cudaSetDevice(op->device));
+  long long zero = 0;
+  CUDA_CHECK(cudaMemcpy(&op->st->apply_calls, &zero, sizeof(zero), cudaMemcpyHostToDevice));
+  SFCDD_API_END
+}
+
+extern "C" int sfcdd_op_stats(sfcdd_op* op, sfcdd_stats* out) {
+  SFCDD_API_BEGIN
+  SFCDD_REQUIRE(op && out, SFCDD_EVALUE, "null argument");
+  *out = op->stats;
+  out->device_bytes = op->dev_bytes;
+  if (op->ready) {
+    long long calls = 0;
+    CUDA_CHECK(cudaSetDevice(op->device));
+    CUDA_CHECK(cudaMemcpy(&calls, &op->st->apply_calls, sizeof(calls), cudaMemcpyDeviceToHost));
+    out->apply_calls = calls;
+  }
+  SFCDD_API_END
+}
+
+extern "C" int sfcdd_op_stencil(sfcdd_op* op, double* diag, double* off, double* t) {
+  SFCDD_API_BEGIN
+  SFCDD_REQUIRE(op, SFCDD_EVALUE, "null handle");
+  if (diag) *diag = op->dhat;
+  if (off)
+    for (int j = 0; j < op->d; ++j) off[j] = op->off[j];
+  if (t) *t = op->tscale;
+  SFCDD_API_END
+}
+
+extern "C" int sfcdd_op_coarse_dense(sfcdd_op* op, double* a0_host) {
+  SFCDD_API_BEGIN
+  SFCDD_REQUIRE(op && op->ready, SFCDD_EVALUE, "operator not set up");
+  SFCDD_REQUIRE(!op->a0_dense.empty(), SFCDD_EVALUE, "no coarse space");
+  std::memcpy(a0_host, op->a0_dense.data(), op->a0_dense.size() * 8);
+  SFCDD_API_END
+}
+
+extern "C" void sfcdd_op_destroy(sfcdd_op* op) {
+  if (!op) return;
+  cudaSetDevice(op->device);
+  if (op->pcg_graph) cudaGraphExecDestroy(op->pcg_graph);
+  void* ptrs[] = {op->nbr, op->agg, op->chunk_start, op->chunk_agg, op->agg_ptr, op->ainv, op->d_ov_start,
+                  op->d_ov_len, op->d_xy_off, op->d_dj_start, op->cand_ptr, op->cand, op->d_wgt, op->d_count,
+                  op->d_fault, op->st, op->hist, op->t, op->w, op->y0, op->y0b, op->part_a, op->part_b,
+                  op->part_c, op->r, op->z, op->p0, op->p1, op->ap};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  op->dag.reset();
+  if (op->ev0) cudaEventDestroy(op->ev0);
+  if (op->ev1) cudaEventDestroy(op->ev1);
+  if (op->own_stream) cudaStreamDestroy(op->own_stream);
+  delete op;
+}
+
+// ------------------------------------------------- generic sparse factor
+struct sfcdd_factor {
+  int device = 0;
+  int64_t n = 0;
+  std::unique_ptr<DagSolver> dag;
+  int64_t nnz_l = 0, stored = 0, nsuper = 0;
+};
+
+extern "C" int sfcdd_factor_create(int64_t n, const int64_t* indptr, const int32_t* indices, const double* data,
+                                   int32_t device, sfcdd_factor** out) {
+  SFCDD_API_BEGIN
+  SFCDD_REQUIRE(n >= 1 && out, SFCDD_EVALUE, "invalid arguments");
+  CsrMatrix A;
+  A.n = n;
+  A.indptr.assign(indptr, indptr + n + 1);
+  A.indices.assign(indices, indices + indptr[n]);
+  A.data.assign(data, data + indptr[n]);
+  FactorOptions fo;
+  HostFactor F = factorize_host(A, fo);
+  std::unique_ptr<sfcdd_factor> f(new sfcdd_factor());
+  f->device = device;
+  f->n = n;
+  f->nnz_l = F.nnz_l;
+  f->stored = F.stored;
+  f->nsuper = F.sn.size();
+  PlanOptions po;
+  DevicePlan plan = build_plan({&F}, {0}, {n}, po);
+  CUDA_CHECK(cudaSetDevice(device));
+  f->dag.reset(new DagSolver(plan, device));
+  *out = f.release();
+  SFCDD_API_END
+}
+
+extern "C" int sfcdd_factor_solve(sfcdd_factor* f, const double* b_dev, double* x_dev, void* stream) {
+  SFCDD_API_BEGIN
+  SFCDD_REQUIRE(f, SFCDD_EVALUE, "null handle");
+  CUDA_CHECK(cudaSetDevice(f->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  f->dag->solve(b_dev, st);
+  CUDA_CHECK(cudaMemcpyAsync(x_dev, f->dag->xy(), f->n * 8, cudaMemcpyDeviceToDevice, st));
+  SFCDD_API_END
+}
+
+extern "C" int sfcdd_factor_info(sfcdd_factor* f, int64_t* nnz_l, int64_t* stored, int64_t* nsuper) {
+  SFCDD_API_BEGIN
+  SFCDD_REQUIRE(f, SFCDD_EVALUE, "null handle");
+  if (nnz_l) *nnz_l = f->nnz_l;
+  if (stored) *stored = f->stored;
+  if (nsuper) *nsuper = f->nsuper;
+  SFCDD_API_END
+}
+
+extern "C" void sfcdd_factor_destroy(sfcdd_factor* f) {
+  if (!f) return;
+  cudaSetDevice(f->device);
+  f->dag.reset();
+  delete f;
+}

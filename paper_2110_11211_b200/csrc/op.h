@@ -1,0 +1,86 @@
+// The Schwarz operator handle (sfcdd_op) and its device kernels.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <vector>
+
+#include "common.h"
+#include "dag_solve.h"
+#include "host.h"
+#include "sfc.h"
+
+namespace sfcdd {
+
+constexpr int VEC_THREADS = 256;
+constexpr int CHUNK = 2048;  // points per reduction chunk (never crosses an aggregate)
+
+struct Stencil {
+  int d;
+  int64_t n;
+  double dhat;
+  double off[MAX_GRID_DIM];
+  const int32_t* nbr;  // [2d][n] SFC rank of the -/+ neighbour per axis, -1 outside
+};
+
+// device-resident solver state (PCG scalars, reduction tickets, counters)
+struct DevState {
+  double tol, hist0, rz, beta, pap, alpha;
+  int32_t k, converged, breakdown, exhausted, have_rz, max_iters, done, pad;
+  uint32_t ticket[8];
+  long long apply_calls;
+  long long fault_index;
+};
+
+struct Chunks {
+  const int64_t* start;       // nch + 1
+  const int32_t* agg;         // aggregate of each chunk (or -1)
+  const int32_t* agg_ptr;     // first chunk of each aggregate (n0 + 1)
+  int32_t nch;
+};
+
+}  // namespace sfcdd
+
+struct sfcdd_op {
+  int device = 0;
+  int d = 0;
+  int32_t levels[8] = {0};
+  int64_t n = 0;
+  int32_t p = 0, q = 0, variant = 3, weighting = 1, threads = 0;
+  int32_t n0 = 0;
+  std::vector<int64_t> ov_start, ov_len, dj_start, dj_len, agg_start;
+  std::vector<double> omega;
+  double dhat = 0, off[16] = {0}, tscale = 0;
+  bool ready = false;
+  // device
+  int32_t* nbr = nullptr;
+  int32_t* agg = nullptr;
+  int64_t* chunk_start = nullptr;
+  int32_t* chunk_agg = nullptr;
+  int32_t* agg_ptr = nullptr;
+  int32_t nch = 0;
+  double* ainv = nullptr;
+  int64_t* d_ov_start = nullptr;
+  int64_t* d_ov_len = nullptr;
+  int64_t* d_xy_off = nullptr;
+  int64_t* d_dj_start = nullptr;  // p + 1
+  int32_t* cand_ptr = nullptr;
+  int32_t* cand = nullptr;
+  double* d_wgt = nullptr;     // per subdomain weight (omega / 1)
+  int32_t* d_count = nullptr;  // per point cover count (d_matrix weighting)
+  int8_t* d_fault = nullptr;   // per subdomain fault mask
+  sfcdd::DevState* st = nullptr;
+  double* hist = nullptr;
+  int32_t hist_cap = 0;
+  double *t = nullptr, *w = nullptr, *y0 = nullptr, *y0b = nullptr;
+  double *part_a = nullptr, *part_b = nullptr, *part_c = nullptr;
+  double *r = nullptr, *z = nullptr, *p0 = nullptr, *p1 = nullptr, *ap = nullptr;
+  std::unique_ptr<sfcdd::DagSolver> dag;
+  std::vector<double> a0_dense;  // host copy (diagnostics)
+  sfcdd_stats stats{};
+  int64_t dev_bytes = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaGraphExec_t pcg_graph = nullptr;
+  cudaStream_t pcg_graph_stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};

@@ -15,11 +15,12 @@
 
 #include "common.h"
 #include "scan.cuh"
+#include "sfc.h"
 
 namespace sfcdd {
 
 constexpr int MAX_DIM = 64;  // encode/decode batch API (d*bits <= 128)
-constexpr int MAX_GRID_DIM = 16;
+
 
 struct Key128 {
   uint64_t hi, lo;
@@ -134,25 +135,6 @@ __global__ void k_decode(int d, int bits, const uint64_t* __restrict__ hi,
   }
   transpose_to_axes(x, d, bits);
   for (int j = 0; j < d; ++j) coords[i * d + j] = x[j];
-}
-
-// Grid geometry for the permutation kernels (C-order lex enumeration,
-// grid.py:72-75; embedding shift lmax - l_j, sfc.py:167-168).
-struct GridGeom {
-  int d;
-  int lmax;
-  int64_t n;
-  int64_t shape[MAX_GRID_DIM];
-  int shift[MAX_GRID_DIM];
-};
-
-__device__ __forceinline__ void lex_to_lattice(const GridGeom& g, int64_t lex, uint32_t* x) {
-  for (int j = g.d - 1; j >= 0; --j) {
-    int64_t s = g.shape[j];
-    int64_t c = lex % s;
-    lex /= s;
-    x[j] = (uint32_t)c << g.shift[j];
-  }
 }
 
 __device__ __forceinline__ Key128 grid_key(const GridGeom& g, int64_t lex) {
