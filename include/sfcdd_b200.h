@@ -126,6 +126,14 @@ int sfcdd_op_pcg(sfcdd_op* op, const double* b_dev, double* x_dev, double tol,
  * local contributions of the listed subdomains are zeroed.  n = 0 clears. */
 int sfcdd_op_set_fault(sfcdd_op* op, int64_t apply_index, const int32_t* ids_host, int32_t n);
 int sfcdd_op_reset_calls(sfcdd_op* op);
+/* Measurement hook for bench.py: average device time (CUDA events on the
+ * launching stream) over `reps` launches of
+ *   ms[0] the local-solve DAG kernel alone (input g_dev),
+ *   ms[1] one full preconditioner apply,
+ *   ms[2] one stencil matvec.
+ * launches[0..2] = kernels launched per measured unit.                    */
+int sfcdd_op_profile(sfcdd_op* op, const double* g_dev, double* scratch_dev, int32_t reps,
+                     double* ms, int32_t* launches, void* stream);
 int sfcdd_op_stats(sfcdd_op* op, sfcdd_stats* out);
 /* diagnostics: Â's constants (diag, off per axis) and symmetric scaling t */
 int sfcdd_op_stencil(sfcdd_op* op, double* diag, double* off /*dim*/, double* t);

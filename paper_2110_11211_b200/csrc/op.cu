@@ -796,7 +796,7 @@ extern "C" int sfcdd_op_apply(sfcdd_op* op, const double* g_dev, double* h_dev, 
   SFCDD_API_BEGIN
   SFCDD_REQUIRE(op && op->ready, SFCDD_EVALUE, "operator not set up");
   CUDA_CHECK(cudaSetDevice(op->device));
-  cudaStream_t st = stream ? (cudaStream_t)stream : op->own_stream;
+  cudaStream_t st = (cudaStream_t)stream;  // NULL = legacy default stream
   apply_device(op, g_dev, h_dev, st, false, false);
   SFCDD_API_END
 }
@@ -805,7 +805,7 @@ extern "C" int sfcdd_op_matvec(sfcdd_op* op, const double* x_dev, double* y_dev,
   SFCDD_API_BEGIN
   SFCDD_REQUIRE(op, SFCDD_EVALUE, "null handle");
   CUDA_CHECK(cudaSetDevice(op->device));
-  cudaStream_t st = stream ? (cudaStream_t)stream : op->own_stream;
+  cudaStream_t st = (cudaStream_t)stream;  // NULL = legacy default stream
   k_matvec<<<nblocks(op->n, VEC_THREADS), VEC_THREADS, 0, st>>>(x_dev, stencil_of(op), y_dev);
   CUDA_CHECK(cudaGetLastError());
   SFCDD_API_END
@@ -818,7 +818,7 @@ extern "C" int sfcdd_op_pcg(sfcdd_op* op, const double* b_dev, double* x_dev, do
   SFCDD_REQUIRE(tol > 0, SFCDD_EVALUE, "tolerance must be positive");
   SFCDD_REQUIRE(max_iters >= 0, SFCDD_EVALUE, "max_iters must be nonnegative");
   CUDA_CHECK(cudaSetDevice(op->device));
-  cudaStream_t st = stream ? (cudaStream_t)stream : op->own_stream;
+  cudaStream_t st = (cudaStream_t)stream;  // NULL = legacy default stream
   if (op->hist_cap < max_iters + 1) {
     if (op->hist) CUDA_CHECK(cudaFree(op->hist));
     op->hist = (double*)dev_alloc(op, (size_t)(max_iters + 1) * 8);
@@ -835,16 +835,18 @@ extern "C" int sfcdd_op_pcg(sfcdd_op* op, const double* b_dev, double* x_dev, do
   if (max_iters > 0) {
     // capture two iterations (p buffers ping-pong) once per stream/x; replay
     // the graph until the device flags convergence / breakdown / max_iters
-    if (!op->pcg_graph || op->pcg_graph_stream != st || op->stats.reserved[1] != (int64_t)x_dev) {
+    // (captured on the handle's private stream: the legacy default stream
+    // cannot be captured; the graph is then launched on the caller's stream)
+    if (!op->pcg_graph || op->stats.reserved[1] != (int64_t)x_dev) {
       if (op->pcg_graph) CUDA_CHECK(cudaGraphExecDestroy(op->pcg_graph));
       cudaGraph_t graph;
-      CUDA_CHECK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-      pcg_iteration(op, x_dev, op->p0, op->p1, st);
-      pcg_iteration(op, x_dev, op->p1, op->p0, st);
-      CUDA_CHECK(cudaStreamEndCapture(st, &graph));
+      cudaStream_t cs = op->own_stream;
+      CUDA_CHECK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+      pcg_iteration(op, x_dev, op->p0, op->p1, cs);
+      pcg_iteration(op, x_dev, op->p1, op->p0, cs);
+      CUDA_CHECK(cudaStreamEndCapture(cs, &graph));
       CUDA_CHECK(cudaGraphInstantiate(&op->pcg_graph, graph, 0));
       CUDA_CHECK(cudaGraphDestroy(graph));
-      op->pcg_graph_stream = st;
       op->stats.reserved[1] = (int64_t)x_dev;
     }
     DevState hs;
@@ -860,10 +862,20 @@ extern "C" int sfcdd_op_pcg(sfcdd_op* op, const double* b_dev, double* x_dev, do
       if (hs.done) break;
       chunk = std::min(chunk * 2, 8);
     }
+    op->stats.reserved[3] = launched;
+  } else {
+    op->stats.reserved[3] = 0;
   }
   DevState hs;
   CUDA_CHECK(cudaMemcpyAsync(&hs, op->st, sizeof(DevState), cudaMemcpyDeviceToHost, st));
   CUDA_CHECK(cudaStreamSynchronize(st));
+  {
+    // kernel launches of this call: init (zero, residual, apply) + 2 iterations per graph
+    const int v = op->variant;
+    const int64_t per_apply = 1 + 1 + (v != SFCDD_VARIANT_ONE_LEVEL ? 1 : 0) + (v == SFCDD_VARIANT_BALANCED) +
+                              (mode_of(v) == 2 ? 2 : 0) + 1;
+    op->stats.reserved[2] = 2 + per_apply + op->stats.reserved[3] * (2 + per_apply);
+  }
   const int k = hs.k;
   if (res_hist_host) CUDA_CHECK(cudaMemcpy(res_hist_host, op->hist, (size_t)(k + 1) * 8, cudaMemcpyDeviceToHost));
   *iters = k;
@@ -893,6 +905,48 @@ extern "C" int sfcdd_op_set_fault(sfcdd_op* op, int64_t apply_index, const int32
   // the PCG graph bakes kernel arguments: force re-capture
   if (op->pcg_graph) CUDA_CHECK(cudaGraphExecDestroy(op->pcg_graph));
   op->pcg_graph = nullptr;
+  SFCDD_API_END
+}
+
+extern "C" int sfcdd_op_profile(sfcdd_op* op, const double* g_dev, double* scratch_dev, int32_t reps,
+                                double* ms, int32_t* launches, void* stream) {
+  SFCDD_API_BEGIN
+  SFCDD_REQUIRE(op && op->ready && reps >= 1, SFCDD_EVALUE, "operator not set up");
+  CUDA_CHECK(cudaSetDevice(op->device));
+  cudaStream_t st = (cudaStream_t)stream;  // NULL = legacy default stream
+  float t = 0.f;
+  // local solves alone
+  op->dag->solve(g_dev, st);
+  CUDA_CHECK(cudaEventRecord(op->ev0, st));
+  for (int i = 0; i < reps; ++i) op->dag->solve(g_dev, st);
+  CUDA_CHECK(cudaEventRecord(op->ev1, st));
+  CUDA_CHECK(cudaEventSynchronize(op->ev1));
+  CUDA_CHECK(cudaEventElapsedTime(&t, op->ev0, op->ev1));
+  ms[0] = t / reps;
+  // full apply
+  CUDA_CHECK(cudaEventRecord(op->ev0, st));
+  for (int i = 0; i < reps; ++i) apply_device(op, g_dev, scratch_dev, st, false, false);
+  CUDA_CHECK(cudaEventRecord(op->ev1, st));
+  CUDA_CHECK(cudaEventSynchronize(op->ev1));
+  CUDA_CHECK(cudaEventElapsedTime(&t, op->ev0, op->ev1));
+  ms[1] = t / reps;
+  // matvec
+  CUDA_CHECK(cudaEventRecord(op->ev0, st));
+  for (int i = 0; i < reps; ++i)
+    k_matvec<<<nblocks(op->n, VEC_THREADS), VEC_THREADS, 0, st>>>(g_dev, stencil_of(op), scratch_dev);
+  CUDA_CHECK(cudaEventRecord(op->ev1, st));
+  CUDA_CHECK(cudaEventSynchronize(op->ev1));
+  CUDA_CHECK(cudaEventElapsedTime(&t, op->ev0, op->ev1));
+  ms[2] = t / reps;
+  long long zero = 0;
+  CUDA_CHECK(cudaMemcpy(&op->st->apply_calls, &zero, sizeof(zero), cudaMemcpyHostToDevice));
+  if (launches) {
+    const int v = op->variant;
+    launches[0] = 1;
+    launches[1] = 1 + 1 + (v != SFCDD_VARIANT_ONE_LEVEL ? 2 : 0) + (v == SFCDD_VARIANT_BALANCED) +
+                  (mode_of(v) == 2 ? 2 : 0) + 1;
+    launches[2] = 1;
+  }
   SFCDD_API_END
 }
 
