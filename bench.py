@@ -205,6 +205,7 @@ def run_gpu(args, cfg):
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t0
     stats = op.stats()
+    log(f"setup {setup_s:.2f}s stats={stats}")
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
     b_dev = torch.from_numpy(bh).to(dev)
@@ -223,7 +224,7 @@ def run_gpu(args, cfg):
         return its.value
 
     for _ in range(max(args.warmup, 3)):
-        solve()
+        log(f"warm-up solve: {solve()} iterations")
     iters = []
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if dist:
@@ -247,6 +248,7 @@ def run_gpu(args, cfg):
         dist.barrier()
     total_its = sum(iters)
     value = world * n * total_its / (ms / 1e3)
+    log(f"timed: {ms:.2f} ms for {args.steps} solves, {total_its} iterations")
 
     # e2e through the public API with host buffers (H2D b, x0; D2H x, history)
     cfgs = sf.SolverConfig(method="pcg", tolerance=1e-8, tolerance_kind="relative_residual")
@@ -276,6 +278,7 @@ def run_gpu(args, cfg):
     _lib.check(_lib.lib().sfcdd_op_profile(op.handle, g_dev.data_ptr(), scratch.data_ptr(), 10,
                                            prof.ctypes.data, nl, stream.cuda_stream))
     dag_ms, apply_ms, mv_ms = prof
+    log(f"e2e {e_ms:.2f} ms; profile dag={dag_ms:.4f} apply={apply_ms:.4f} matvec={mv_ms:.4f} ms")
     if rank != 0:
         if dist:
             dist.destroy_process_group()
@@ -328,7 +331,14 @@ def run_gpu(args, cfg):
         dist.destroy_process_group()
 
 
+def log(msg):
+    print(f"[bench] {msg}", file=sys.stderr, flush=True)
+
+
 def main():
+    import faulthandler
+
+    faulthandler.enable()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
