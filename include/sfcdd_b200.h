@@ -134,6 +134,11 @@ int sfcdd_op_reset_calls(sfcdd_op* op);
  * launches[0..2] = kernels launched per measured unit.                    */
 int sfcdd_op_profile(sfcdd_op* op, const double* g_dev, double* scratch_dev, int32_t reps,
                      double* ms, int32_t* launches, void* stream);
+/* Diagnostics: one traced local-solve DAG launch.  out_host receives 24
+ * uint64 per task {sm, t_top, t_deps_ok, t_data_ok, t_end (globaltimer ns),
+ * flags, copy_bytes, fragment, 16 clock64 phase stamps of small forward
+ * tasks}; *ntask gets the task count (call with out_host = NULL first).   */
+int sfcdd_op_trace(sfcdd_op* op, const double* g_dev, uint64_t* out_host, int64_t* ntask);
 int sfcdd_op_stats(sfcdd_op* op, sfcdd_stats* out);
 /* diagnostics: Â's constants (diag, off per axis) and symmetric scaling t */
 int sfcdd_op_stencil(sfcdd_op* op, double* diag, double* off /*dim*/, double* t);

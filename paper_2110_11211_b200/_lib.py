@@ -88,7 +88,7 @@ EXPORTS = [
     "sfcdd_sfc_perm", "sfcdd_op_create", "sfcdd_op_setup", "sfcdd_op_apply",
     "sfcdd_op_matvec", "sfcdd_op_pcg", "sfcdd_op_set_fault", "sfcdd_op_reset_calls",
     "sfcdd_op_stats", "sfcdd_op_stencil", "sfcdd_op_coarse_dense", "sfcdd_op_destroy",
-    "sfcdd_op_profile",
+    "sfcdd_op_profile", "sfcdd_op_trace",
     "sfcdd_factor_create", "sfcdd_factor_solve", "sfcdd_factor_info", "sfcdd_factor_destroy",
     "sfcdd_host_amd", "sfcdd_host_factor_solve", "sfcdd_host_plan_solve",
 ]
@@ -123,6 +123,7 @@ def lib() -> ctypes.CDLL:
         "sfcdd_op_stencil": [vp, vp, vp, vp],
         "sfcdd_op_coarse_dense": [vp, vp],
         "sfcdd_op_profile": [vp, vp, vp, i32, vp, vp, vp],
+        "sfcdd_op_trace": [vp, vp, vp, ctypes.POINTER(i64)],
         "sfcdd_factor_create": [i64, vp, vp, vp, i32, ctypes.POINTER(vp)],
         "sfcdd_factor_solve": [vp, vp, vp, vp],
         "sfcdd_factor_info": [vp, vp, vp, vp],

@@ -10,6 +10,8 @@
 // sweeps become dependency-free GEMVs per supernode.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -18,6 +20,12 @@
 #include "host.h"
 
 namespace sfcdd {
+
+FactorOptions::FactorOptions() {
+  if (const char* v = std::getenv("SFCDD_RELAX_SMALL")) relax_small = std::atoi(v);
+  if (const char* v = std::getenv("SFCDD_RELAX_SMALL_FRAC")) relax_small_frac = std::atof(v);
+  if (const char* v = std::getenv("SFCDD_RELAX_FRAC")) relax_frac = std::atof(v);
+}
 
 int hardware_threads() {
   unsigned h = std::thread::hardware_concurrency();
@@ -309,6 +317,25 @@ HostFactor analyze_host(const CsrMatrix& A, const FactorOptions& opt) {
     }
     for (int32_t t = 0; t < P.s; ++t) pos[P.col0 + t] = -1;
     for (int32_t a = 0; a < P.m; ++a) pos[F.rows[P.rows_off + a]] = -1;
+  }
+  if (std::getenv("SFCDD_FACTOR_DEBUG")) {
+    // critical path of the supernodal tree (supernodes and stored entries)
+    std::vector<int64_t> cp_n(ns, 0), cp_b(ns, 0);
+    int64_t hmax = 0, bmax = 0;
+    for (int64_t k = 0; k < ns; ++k) {
+      cp_n[k] += 1;
+      cp_b[k] += packed_size(F.sn[k].s, F.sn[k].m);
+      hmax = std::max(hmax, cp_n[k]);
+      bmax = std::max(bmax, cp_b[k]);
+      const int32_t p = F.sn[k].parent;
+      if (p >= 0) {
+        cp_n[p] = std::max(cp_n[p], cp_n[k]);
+        cp_b[p] = std::max(cp_b[p], cp_b[k]);
+      }
+    }
+    std::fprintf(stderr, "[factor] n=%lld supernodes=%lld nnzL=%lld stored=%lld (%.3f) height=%lld critpath=%.1f%%\n",
+                 (long long)n, (long long)ns, (long long)F.nnz_l, (long long)F.stored,
+                 (double)F.stored / F.nnz_l, (long long)hmax, 100.0 * bmax / F.stored);
   }
   return F;
 }

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 #include "plan.h"
 
@@ -22,10 +23,17 @@ class DagSolver {
   int64_t device_bytes() const { return bytes_; }
   int32_t grid() const { return grid_; }
   int32_t nfrag() const { return nfrag_; }
+  // largest front (s+m) of a big supernode the chunk ring can stream
+  static int big_front_max(int blob_max);
+  // diagnostics: per-task timestamps {sm, top, deps ok, data ok, end} (5 x u64
+  // per task), followed by 16 clock64 phase stamps per task (21 x ntask words)
+  void set_trace(unsigned long long* dev_buf);
+  int32_t ntask() const { return ntask_; }
+  int32_t grid_size() const { return grid_; }
 
  private:
   int device_;
-  int32_t nfrag_ = 0, ntask_ = 0, grid_ = 1, blob_max_ = 0, smem_ = 0;
+  int32_t nfrag_ = 0, ntask_ = 0, grid_ = 1, blob_max_ = 0, smem_ = 0, chunk_bytes_ = 0;
   int64_t xy_doubles_ = 0, ctr_words_ = 0, bytes_ = 0;
   uint8_t* blobs_ = nullptr;
   TaskDev* tasks_ = nullptr;
@@ -33,6 +41,10 @@ class DagSolver {
   double* upd_ = nullptr;
   double* xy_ = nullptr;
   int32_t* ctr_ = nullptr;
+  unsigned long long* trace_ = nullptr;
+
+ public:
+  std::vector<TaskDev> host_tasks;
 };
 
 }  // namespace sfcdd

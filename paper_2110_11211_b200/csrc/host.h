@@ -65,10 +65,12 @@ struct HostFactor {
 struct FactorOptions {
   // relaxed amalgamation: merge child into parent when the merged block has
   // at most `relax_small` columns and zero fraction <= relax_small_frac, or
-  // zero fraction <= relax_frac.
+  // zero fraction <= relax_frac.  Environment overrides (tuning):
+  // SFCDD_RELAX_SMALL, SFCDD_RELAX_SMALL_FRAC, SFCDD_RELAX_FRAC.
   int32_t relax_small = 16;
   double relax_small_frac = 0.30;
   double relax_frac = 0.02;
+  FactorOptions();
 };
 
 // order + symbolic + numeric; throws Error(SFCDD_EFACTOR) if not SPD

@@ -658,6 +658,7 @@ extern "C" int sfcdd_op_setup(sfcdd_op* op, void* stream) {
     xo += op->ov_len[i];
   }
   PlanOptions po;
+  po.big_front_max = DagSolver::big_front_max(po.blob_max);
   DevicePlan plan = build_plan(ptrs, gs, gm, po);
   op->stats.factor_nnz = plan.stored;
   op->stats.factor_nnz_l = plan.nnz_l;
@@ -950,6 +951,34 @@ extern "C" int sfcdd_op_profile(sfcdd_op* op, const double* g_dev, double* scrat
   SFCDD_API_END
 }
 
+extern "C" int sfcdd_op_trace(sfcdd_op* op, const double* g_dev, uint64_t* out_host, int64_t* ntask) {
+  SFCDD_API_BEGIN
+  SFCDD_REQUIRE(op && op->ready, SFCDD_EVALUE, "operator not set up");
+  const int64_t nt = op->dag->ntask();
+  *ntask = nt;
+  if (!out_host) return SFCDD_OK;
+  CUDA_CHECK(cudaSetDevice(op->device));
+  unsigned long long* buf = nullptr;
+  CUDA_CHECK(cudaMalloc(&buf, nt * 21 * 8));
+  CUDA_CHECK(cudaMemset(buf, 0, nt * 21 * 8));
+  op->dag->solve(g_dev, nullptr);  // warm
+  op->dag->set_trace(buf);
+  op->dag->solve(g_dev, nullptr);
+  op->dag->set_trace(nullptr);
+  CUDA_CHECK(cudaDeviceSynchronize());
+  std::vector<unsigned long long> h(nt * 21);
+  CUDA_CHECK(cudaMemcpy(h.data(), buf, nt * 21 * 8, cudaMemcpyDeviceToHost));
+  CUDA_CHECK(cudaFree(buf));
+  for (int64_t t = 0; t < nt; ++t) {
+    for (int j = 0; j < 5; ++j) out_host[24 * t + j] = h[5 * t + j];
+    out_host[24 * t + 5] = op->dag->host_tasks[t].flags;
+    out_host[24 * t + 6] = op->dag->host_tasks[t].copy_bytes;
+    out_host[24 * t + 7] = op->dag->host_tasks[t].frag;
+    for (int j = 0; j < 16; ++j) out_host[24 * t + 8 + j] = h[5 * nt + 16 * t + j];
+  }
+  SFCDD_API_END
+}
+
 extern "C" int sfcdd_op_reset_calls(sfcdd_op* op) {
   SFCDD_API_BEGIN
   SFCDD_REQUIRE(op && op->ready, SFCDD_EVALUE, "operator not set up");
@@ -1034,6 +1063,7 @@ extern "C" int sfcdd_factor_create(int64_t n, const int64_t* indptr, const int32
   f->stored = F.stored;
   f->nsuper = F.sn.size();
   PlanOptions po;
+  po.big_front_max = DagSolver::big_front_max(po.blob_max);
   DevicePlan plan = build_plan({&F}, {0}, {n}, po);
   CUDA_CHECK(cudaSetDevice(device));
   f->dag.reset(new DagSolver(plan, device));

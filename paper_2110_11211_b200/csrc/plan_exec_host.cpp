@@ -1,8 +1,8 @@
 // Host interpreter of a DevicePlan: executes the forward/backward tasks in
 // queue order with exactly the blob semantics of the device kernel
-// (dag_solve.cu).  Test hook only -- lets the CPU test suite check the plan
-// layout (fragments, child records, relative maps, update slots) without a
-// GPU.  Not used by the product path.
+// (dag_solve.cu): the same level tables, gather runs, row pairs and warp
+// items.  Test hook only -- lets the CPU test suite check the plan layout
+// without a GPU.  Not used by the product path.
 #include <cstring>
 #include <vector>
 
@@ -11,83 +11,152 @@
 
 namespace sfcdd {
 
+namespace {
+inline int32_t lo16(int32_t v) { return (int32_t)((uint32_t)v & 0xffffu); }
+inline int32_t hi16(int32_t v) { return (int32_t)((uint32_t)v >> 16); }
+}  // namespace
+
 void plan_exec_host(const DevicePlan& P, const double* rhs, double* xy) {
   std::vector<double> upd(P.upd_doubles, 0.0);
   std::vector<double> scratch;
   const int32_t nf = P.nfrag;
   for (int32_t t = 0; t < 2 * nf; ++t) {
     const TaskDev& T = P.tasks[t];
-    const bool fwd = t < nf;
+    const bool fwd = !(T.flags & TASK_BWD);
     const uint8_t* blob = P.blobs.data() + T.blob_off;
     const int32_t* h = reinterpret_cast<const int32_t*>(blob);
     const double* vals = reinterpret_cast<const double*>(blob + h[H_VAL_OFF]);
     const FactorDev& Fd = P.factors[T.factor];
-    const int32_t nlev = h[H_NLEV];
-    const int32_t* lev_ptr = h + h[H_LEV_PTR];
-    const int32_t* lev_list = h + h[H_LEV_LIST];
     const int32_t* recs = h + h[H_REC];
-    scratch.assign(h[H_SCRATCH], 0.0);
+    const int32_t* cols = h + h[H_COLS];
     auto gidx = [&](int32_t ro) {
       int64_t g = Fd.gstart + ro;
       if (g >= Fd.gmod) g -= Fd.gmod;
       return g;
     };
+    double* x = xy + Fd.xy_off;
+    if (h[H_BIG]) {
+      const int32_t* R = recs;
+      const int32_t s = R[R_S], m = R[R_M];
+      const int32_t* rows = h + R[R_ROWS];
+      const double* M = vals + R[R_VAL];
+      scratch.assign(s + m, 0.0);
+      double* f = scratch.data();
+      if (fwd) {
+        for (int32_t c = 0; c < s; ++c) f[c] = rhs[gidx(cols[c])];
+        for (int32_t q = 0; q < R[R_NCH]; ++q) {
+          const int32_t* cr = h + R[R_CH] + CH_WORDS * q;
+          const int32_t* rel = h + cr[2];
+          for (int32_t a = 0; a < cr[1]; ++a) f[rel[a]] += upd[cr[0] + a];
+        }
+        for (int32_t i = 0; i < s + m; ++i) {
+          double acc = 0.0;
+          const int32_t kmax = i < s ? i : s - 1;
+          for (int32_t k = 0; k <= kmax; ++k) acc += M[packed_col_off(s, m, k) + (i - k)] * f[k];
+          if (i < s)
+            x[cols[i]] = acc;
+          else if (h[H_TOP_UPD] >= 0)
+            upd[h[H_TOP_UPD] + i - s] = f[i] - acc;
+        }
+      } else {
+        for (int32_t c = 0; c < s; ++c) f[c] = x[cols[c]];
+        for (int32_t a = 0; a < m; ++a) f[s + a] = -x[rows[a]];
+        for (int32_t k = 0; k < s; ++k) {
+          double acc = 0.0;
+          const double* col = M + packed_col_off(s, m, k);
+          for (int32_t i = k; i < s + m; ++i) acc += col[i - k] * f[i];
+          x[cols[k]] = acc;
+        }
+      }
+      continue;
+    }
+    scratch.assign(h[H_SCRATCH], 0.0);
+    double* S = scratch.data();
+    const int32_t ncol = h[H_NCOL];
+    const int32_t* colpos = h + h[H_COLPOS];
+    const int32_t nlev = h[H_NLEV];
+    const int32_t* levtab = h + h[H_LEVELS];
+    const int32_t* runs = h + h[H_RUNS];
+    const int32_t* gp = h + h[H_GPAIRS];
+    const int32_t* bp = h + h[H_BPAIRS];
+    const int32_t* items = h + h[H_ITEMS];
+    // rows handled by a warp item, in lane order (for the checks below)
+    auto item_rows = [&](int32_t x0, int32_t y, bool forward, auto&& fn) {
+      const int32_t cnt = x0 >> 16;
+      if (cnt > 0) {
+        x0 &= 0xffff;
+        uint32_t mask = 0;
+        int32_t rows = 0;
+        for (int32_t j = x0; j < x0 + cnt; ++j) {
+          mask |= 1u << rows;
+          rows += recs[R_WORDS * j + R_S] + recs[R_WORDS * j + R_M];
+        }
+        if (rows < 32) mask |= 1u << rows;
+        SFCDD_REQUIRE(rows <= 32 && mask == (uint32_t)y, SFCDD_EINTERNAL, "packed item lane mask mismatch");
+        for (int32_t j = x0; j < x0 + cnt; ++j) {
+          const int32_t* R = recs + R_WORDS * j;
+          if (forward)
+            for (int32_t i = 0; i < R[R_S] + R[R_M]; ++i) fn(R, i);
+          else
+            for (int32_t k = 0; k < R[R_S]; ++k) fn(R, k);
+        }
+      } else {
+        const int32_t* R = recs + R_WORDS * x0;
+        if (forward)
+          for (int32_t i = 32 * y; i < std::min(32 * y + 32, R[R_S] + R[R_M]); ++i) fn(R, i);
+        else
+          fn(R, y);
+      }
+    };
     if (fwd) {
-      for (int32_t lv = 0; lv < nlev; ++lv) {
-        for (int32_t j = lev_ptr[lv]; j < lev_ptr[lv + 1]; ++j) {
-          const int32_t l = lev_list[j];
-          const int32_t* R = recs + R_WORDS * l;
-          const int32_t s = R[R_S], m = R[R_M];
-          double* f = scratch.data() + R[R_SCR];
-          const int32_t* ro = h + R[R_IDX];
-          for (int32_t i = 0; i < s; ++i) f[i] = rhs[gidx(ro[i])];
-          for (int32_t i = s; i < s + m; ++i) f[i] = 0.0;
-          for (int32_t q = 0; q < R[R_NCH]; ++q) {
-            const int32_t* cr = h + R[R_CH] + CH_WORDS * q;
-            const double* src;
-            if (cr[0] >= 0) {
-              const int32_t* RC = recs + R_WORDS * cr[0];
-              src = scratch.data() + RC[R_SCR] + RC[R_S];
-            } else {
-              src = upd.data() + cr[3];
-            }
-            const int32_t* rel = h + cr[2];
-            for (int32_t a = 0; a < cr[1]; ++a) f[rel[a]] += src[a];
-          }
-          const double* M = vals + R[R_VAL];
-          for (int32_t i = 0; i < s + m; ++i) {
+      for (int32_t c = 0; c < ncol; ++c) S[lo16(colpos[c])] = rhs[gidx(cols[c])];
+      const int32_t* eu = h + h[H_EXTU];
+      for (int32_t e = 0; e < h[H_NEXTU]; ++e) S[h[H_EXTU_BASE] + e] = upd[eu[e]];
+      for (int32_t l = 0; l < nlev; ++l) {
+        const int32_t* L = levtab + L_WORDS * l;
+        for (int32_t r = L[L_RUN0]; r < L[L_RUN1]; ++r) {
+          const int32_t dst = lo16(gp[runs[r]]);
+          double acc = S[dst];
+          for (int32_t p = runs[r]; p < runs[r + 1]; ++p) acc += S[hi16(gp[p])];
+          S[dst] = acc;
+        }
+        for (int32_t it = L[L_FW]; it < L[L_FW + NWARP_PLAN]; ++it)
+          item_rows(items[2 * it], items[2 * it + 1], true, [&](const int32_t* R, int32_t i) {
+            const int32_t s = R[R_S], m = R[R_M];
+            const double* M = vals + R[R_VAL];
+            double* f = S + R[R_SCR];
             double acc = 0.0;
             const int32_t kmax = i < s ? i : s - 1;
             for (int32_t k = 0; k <= kmax; ++k) acc += M[packed_col_off(s, m, k) + (i - k)] * f[k];
             if (i < s)
-              xy[Fd.xy_off + ro[i]] = acc;
+              S[R[R_CPOS] + i] = acc;
             else
               f[i] -= acc;
-          }
-          if (R[R_PARENT] < 0 && h[H_TOP_UPD] >= 0)
-            for (int32_t a = 0; a < m; ++a) upd[h[H_TOP_UPD] + a] = f[s + a];
-        }
+          });
+      }
+      for (int32_t c = 0; c < ncol; ++c) x[cols[c]] = S[hi16(colpos[c])];
+      if (h[H_TOP_UPD] >= 0) {
+        const int32_t* R = recs + R_WORDS * h[H_TOP];
+        for (int32_t a = 0; a < R[R_M]; ++a) upd[h[H_TOP_UPD] + a] = S[R[R_SCR] + R[R_S] + a];
       }
     } else {
-      std::vector<double> v;
-      for (int32_t lv = nlev - 1; lv >= 0; --lv) {
-        for (int32_t j = lev_ptr[lv]; j < lev_ptr[lv + 1]; ++j) {
-          const int32_t l = lev_list[j];
-          const int32_t* R = recs + R_WORDS * l;
-          const int32_t s = R[R_S], m = R[R_M];
-          const int32_t* ro = h + R[R_IDX];
-          v.resize(s + m);
-          for (int32_t i = 0; i < s; ++i) v[i] = xy[Fd.xy_off + ro[i]];
-          for (int32_t a = 0; a < m; ++a) v[s + a] = -xy[Fd.xy_off + ro[s + a]];
-          const double* M = vals + R[R_VAL];
-          for (int32_t k = 0; k < s; ++k) {
+      for (int32_t c = 0; c < ncol; ++c) S[lo16(colpos[c])] = x[cols[c]];
+      const int32_t* ex = h + h[H_EXTX];
+      for (int32_t e = 0; e < h[H_NEXTX]; ++e) S[h[H_EXTX_BASE] + e] = x[ex[e]];
+      for (int32_t l = nlev - 1; l >= 0; --l) {
+        const int32_t* L = levtab + L_WORDS * l;
+        for (int32_t p = L[L_BP0]; p < L[L_BP1]; ++p) S[lo16(bp[p])] = -S[hi16(bp[p])];
+        for (int32_t it = L[L_BW]; it < L[L_BW + NWARP_PLAN]; ++it)
+          item_rows(items[2 * it], items[2 * it + 1], false, [&](const int32_t* R, int32_t k) {
+            const int32_t s = R[R_S], m = R[R_M];
+            const double* col = vals + R[R_VAL] + packed_col_off(s, m, k);
+            const double* v = S + R[R_SCR];
             double acc = 0.0;
-            const double* col = M + packed_col_off(s, m, k);
             for (int32_t i = k; i < s + m; ++i) acc += col[i - k] * v[i];
-            xy[Fd.xy_off + ro[k]] = acc;
-          }
-        }
+            S[R[R_CPOS] + k] = acc;
+          });
       }
+      for (int32_t c = 0; c < ncol; ++c) x[cols[c]] = S[hi16(colpos[c])];
     }
   }
 }
