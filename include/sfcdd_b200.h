@@ -88,7 +88,9 @@ typedef struct sfcdd_op_desc {
   const int64_t* dj_len;
   const double* omega;       /* host, p entries (partition.py:151-157)      */
   int32_t host_threads;      /* setup threads (0 = hardware concurrency)    */
-  int32_t reserved[7];
+  int32_t shard_first;       /* shard mode: first owned subdomain           */
+  int32_t shard_count;       /* shard mode: owned subdomains (0 = all)      */
+  int32_t reserved[5];
 } sfcdd_op_desc;
 
 typedef struct sfcdd_stats {
@@ -145,6 +147,38 @@ int sfcdd_op_stencil(sfcdd_op* op, double* diag, double* off /*dim*/, double* t)
 /* diagnostics: coarse matrix A_0 as dense n0*n0 (host), n0 <= 8192         */
 int sfcdd_op_coarse_dense(sfcdd_op* op, double* a0_host);
 void sfcdd_op_destroy(sfcdd_op* op);
+
+/* ---------------------------------------------------------- shard mode --
+ * Multi-GPU: one handle per rank, created with
+ * desc.shard_first/shard_count = the rank's contiguous block of subdomains
+ * (an SFC segment).  Only those subdomains are factorized.  Vectors stay full
+ * length N; every step below computes the owned segment / owned aggregates
+ * only.  Partial scalars are written to device doubles for the caller's
+ * allreduce; coarse restrictions are per owned aggregate for the caller's
+ * allgather (Bank-Holst: every rank then solves the full coarse problem).
+ * info = {g0, g1 (owned points), ch0, ch1 (owned chunks), a0, a1 (owned
+ * aggregates), xy doubles, n0}; xy_off_host[P] = slot of every subdomain's
+ * local solution in the xy buffer (-1: not needed on this rank).          */
+int sfcdd_shard_info(sfcdd_op* op, int64_t* info, int64_t* xy_off_host);
+/* host copy of the stencil neighbour table int32[2d][N] (-1 = boundary)  */
+int sfcdd_op_neighbors(sfcdd_op* op, int32_t* nbr_host);
+int sfcdd_shard_xy(sfcdd_op* op, double** xy_dev);
+int sfcdd_shard_residual(sfcdd_op* op, const double* b, const double* x, double* r, double* rr_out,
+                         double* cagg_out, void* stream);
+int sfcdd_shard_pm(sfcdd_op* op, const double* z, const double* pold, double beta, double* pnew,
+                   double* ap, double* pap_out, void* stream);
+int sfcdd_shard_update(sfcdd_op* op, double* x, double* r, const double* p, const double* ap,
+                       double alpha, double* rr_out, double* cagg_out, void* stream);
+int sfcdd_shard_coarse(sfcdd_op* op, const double* c, double* y, void* stream);
+int sfcdd_shard_tvec(sfcdd_op* op, const double* g, const double* y0, double* t, void* stream);
+int sfcdd_shard_local_solve(sfcdd_op* op, const double* t, void* stream);
+int sfcdd_shard_combine(sfcdd_op* op, double* w, void* stream);
+int sfcdd_shard_stencil_restrict(sfcdd_op* op, const double* w, double* cagg_out, void* stream);
+int sfcdd_shard_finalize(sfcdd_op* op, const double* w, const double* y0, const double* y0b, double* z,
+                         const double* r, double* rz_out, void* stream);
+/* exchange packing: dst[i] = src[idx[i]] / dst[idx[i]] = src[i]           */
+int sfcdd_pack(const double* src, const int64_t* idx, int64_t n, double* dst, void* stream);
+int sfcdd_unpack(const double* src, const int64_t* idx, int64_t n, double* dst, void* stream);
 
 /* ------------------------------------------------------- direct solver --
  * Replaces linalg.Factorization (linalg.py:37-72) for a general SPD CSR

@@ -60,7 +60,9 @@ class OpDesc(ctypes.Structure):
         ("dj_len", ctypes.c_void_p),
         ("omega", ctypes.c_void_p),
         ("host_threads", ctypes.c_int32),
-        ("reserved", ctypes.c_int32 * 7),
+        ("shard_first", ctypes.c_int32),
+        ("shard_count", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 5),
     ]
 
 
@@ -89,6 +91,9 @@ EXPORTS = [
     "sfcdd_op_matvec", "sfcdd_op_pcg", "sfcdd_op_set_fault", "sfcdd_op_reset_calls",
     "sfcdd_op_stats", "sfcdd_op_stencil", "sfcdd_op_coarse_dense", "sfcdd_op_destroy",
     "sfcdd_op_profile", "sfcdd_op_trace",
+    "sfcdd_shard_info", "sfcdd_op_neighbors", "sfcdd_shard_xy", "sfcdd_shard_residual", "sfcdd_shard_pm", "sfcdd_shard_update",
+    "sfcdd_shard_coarse", "sfcdd_shard_tvec", "sfcdd_shard_local_solve", "sfcdd_shard_combine",
+    "sfcdd_shard_stencil_restrict", "sfcdd_shard_finalize", "sfcdd_pack", "sfcdd_unpack",
     "sfcdd_factor_create", "sfcdd_factor_solve", "sfcdd_factor_info", "sfcdd_factor_destroy",
     "sfcdd_host_amd", "sfcdd_host_factor_solve", "sfcdd_host_plan_solve",
 ]
@@ -124,6 +129,20 @@ def lib() -> ctypes.CDLL:
         "sfcdd_op_coarse_dense": [vp, vp],
         "sfcdd_op_profile": [vp, vp, vp, i32, vp, vp, vp],
         "sfcdd_op_trace": [vp, vp, vp, ctypes.POINTER(i64)],
+        "sfcdd_shard_info": [vp, vp, vp],
+        "sfcdd_op_neighbors": [vp, vp],
+        "sfcdd_shard_xy": [vp, ctypes.POINTER(vp)],
+        "sfcdd_shard_residual": [vp, vp, vp, vp, vp, vp, vp],
+        "sfcdd_shard_pm": [vp, vp, vp, dbl, vp, vp, vp, vp],
+        "sfcdd_shard_update": [vp, vp, vp, vp, vp, dbl, vp, vp, vp],
+        "sfcdd_shard_coarse": [vp, vp, vp, vp],
+        "sfcdd_shard_tvec": [vp, vp, vp, vp, vp],
+        "sfcdd_shard_local_solve": [vp, vp, vp],
+        "sfcdd_shard_combine": [vp, vp, vp],
+        "sfcdd_shard_stencil_restrict": [vp, vp, vp, vp],
+        "sfcdd_shard_finalize": [vp, vp, vp, vp, vp, vp, vp, vp],
+        "sfcdd_pack": [vp, vp, i64, vp, vp],
+        "sfcdd_unpack": [vp, vp, i64, vp, vp],
         "sfcdd_factor_create": [i64, vp, vp, vp, i32, ctypes.POINTER(vp)],
         "sfcdd_factor_solve": [vp, vp, vp, vp],
         "sfcdd_factor_info": [vp, vp, vp, vp],

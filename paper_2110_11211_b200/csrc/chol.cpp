@@ -336,6 +336,17 @@ HostFactor analyze_host(const CsrMatrix& A, const FactorOptions& opt) {
     std::fprintf(stderr, "[factor] n=%lld supernodes=%lld nnzL=%lld stored=%lld (%.3f) height=%lld critpath=%.1f%%\n",
                  (long long)n, (long long)ns, (long long)F.nnz_l, (long long)F.stored,
                  (double)F.stored / F.nnz_l, (long long)hmax, 100.0 * bmax / F.stored);
+    const int edges[] = {1, 2, 4, 8, 16, 32, 64, 128, 1 << 30};
+    int64_t cnt[9] = {0}, byt[9] = {0};
+    for (int64_t k = 0; k < ns; ++k) {
+      int b = 0;
+      while (F.sn[k].s > edges[b]) ++b;
+      cnt[b]++;
+      byt[b] += packed_size(F.sn[k].s, F.sn[k].m);
+    }
+    for (int b = 0; b < 9; ++b)
+      std::fprintf(stderr, "  s<=%d: %lld supernodes, %.1f%% of stored\n", edges[b], (long long)cnt[b],
+                   100.0 * byt[b] / F.stored);
   }
   return F;
 }

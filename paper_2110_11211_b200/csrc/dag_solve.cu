@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
 
 #include "common.h"
 #include "dag_solve.h"
@@ -260,7 +261,7 @@ __device__ __forceinline__ void bwd_packed(const int32_t* recs, const double* va
   }
 }
 
-__device__ void run_small(const int32_t* h, bool fwd, double* S, const DagArgs& A, const FactorDev& F,
+__device__ __forceinline__ void run_small(const int32_t* h, bool fwd, double* S, const DagArgs& A, const FactorDev& F,
                           int lane, int warp, unsigned long long* pt) {
   const double* vals = reinterpret_cast<const double*>(reinterpret_cast<const uint8_t*>(h) + h[H_VAL_OFF]);
   const int nlev = h[H_NLEV];
@@ -368,7 +369,7 @@ __device__ __forceinline__ void issue_chunk(uint8_t* stage, uint64_t* bar, const
   bulk_g2s(stage, vbase + e0, bytes, bar);
 }
 
-__device__ void run_big(const uint8_t* gblob, bool fwd, uint8_t* ring, uint64_t* cbar, uint32_t& cphase,
+__device__ __forceinline__ void run_big(const uint8_t* gblob, bool fwd, uint8_t* ring, uint64_t* cbar, uint32_t& cphase,
                         double* S, const DagArgs& A, const FactorDev& F, int lane, int warp) {
   const int32_t* hg = reinterpret_cast<const int32_t*>(gblob);
   const int32_t* R = hg + __ldg(hg + H_REC);
@@ -633,7 +634,9 @@ __global__ void __launch_bounds__(DAG_THREADS + 32, 2) k_dag(DagArgs A) {
     if (big)
       run_big(A.blobs + T.blob_off, fwd, smem, cbar, cphase, S, A, F, lane, warp);
     else
-      run_small(reinterpret_cast<const int32_t*>(buf[slot]), fwd, S, A, F, lane, warp,
+      // address computed from the shared base (not via buf[]) so the compiler
+      // keeps the shared state space and emits LDS for all blob reads
+      run_small(reinterpret_cast<const int32_t*>(smem + (size_t)slot * A.blob_max), fwd, S, A, F, lane, warp,
                 A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr);
     bar_sync(1, DAG_THREADS);
     if (tid == 0) {
@@ -652,7 +655,7 @@ __global__ void __launch_bounds__(DAG_THREADS + 32, 2) k_dag(DagArgs A) {
 
 }  // namespace
 
-DagSolver::DagSolver(const DevicePlan& plan, int device) : device_(device) {
+DagSolver::DagSolver(const DevicePlan& plan, int device, int64_t extra_xy) : device_(device) {
   CUDA_CHECK(cudaSetDevice(device));
   nfrag_ = plan.nfrag;
   ntask_ = (int32_t)plan.tasks.size();
@@ -671,11 +674,22 @@ DagSolver::DagSolver(const DevicePlan& plan, int device) : device_(device) {
   up((void**)&tasks_, plan.tasks.data(), plan.tasks.size() * sizeof(TaskDev));
   up((void**)&factors_, plan.factors.data(), plan.factors.size() * sizeof(FactorDev));
   CUDA_CHECK(cudaMalloc(&upd_, std::max<int64_t>(plan.upd_doubles, 2) * 8));
-  CUDA_CHECK(cudaMalloc(&xy_, std::max<int64_t>(plan.xy_doubles, 2) * 8));
+  CUDA_CHECK(cudaMalloc(&xy_, std::max<int64_t>(plan.xy_doubles + extra_xy, 2) * 8));
+  xy_doubles_ = plan.xy_doubles + extra_xy;
   ctr_words_ = 1 + 3 * nfrag_;
   CUDA_CHECK(cudaMalloc(&ctr_, ctr_words_ * 4));
   bytes_ += std::max<int64_t>(plan.upd_doubles, 2) * 8 + std::max<int64_t>(plan.xy_doubles, 2) * 8 + ctr_words_ * 4;
-  CUDA_CHECK(cudaFuncSetAttribute(k_dag, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
+  {
+    // the attribute is per function: only ever raise it, so every live
+    // solver (several handles per process in shard emulation) can launch
+    static std::mutex mu;
+    static int max_smem = 0;
+    std::lock_guard<std::mutex> g(mu);
+    if (smem_ > max_smem) {
+      CUDA_CHECK(cudaFuncSetAttribute(k_dag, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
+      max_smem = smem_;
+    }
+  }
   int per_sm = 0, sms = 0;
   CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dag, DAG_THREADS + 32, smem_));
   CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));

@@ -11,7 +11,9 @@ namespace sfcdd {
 
 class DagSolver {
  public:
-  DagSolver(const DevicePlan& plan, int device);
+  // extra_xy: doubles appended to the xy work buffer (shard mode: slots for
+  // foreign subdomains' solutions received from other ranks)
+  DagSolver(const DevicePlan& plan, int device, int64_t extra_xy = 0);
   ~DagSolver();
   DagSolver(const DagSolver&) = delete;
   DagSolver& operator=(const DagSolver&) = delete;

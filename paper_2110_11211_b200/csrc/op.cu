@@ -529,6 +529,11 @@ extern "C" int sfcdd_op_create(const sfcdd_op_desc* desc, sfcdd_op** out) {
   op->variant = desc->variant;
   op->weighting = desc->weighting;
   op->threads = desc->host_threads > 0 ? desc->host_threads : hardware_threads();
+  op->shard_first = desc->shard_first;
+  op->shard_count = desc->shard_count;
+  if (op->shard_count > 0)
+    SFCDD_REQUIRE(desc->shard_first >= 0 && desc->shard_first + desc->shard_count <= desc->p && desc->q >= 1,
+                  SFCDD_EVALUE, "invalid shard (needs a coarse space and owned subdomains within [0, P))");
   SFCDD_REQUIRE(op->p >= 1 && op->p <= op->n, SFCDD_EVALUE, "need 1 <= P <= N");
   SFCDD_REQUIRE(op->variant >= 0 && op->variant <= 3, SFCDD_EVALUE, "unknown variant");
   SFCDD_REQUIRE(op->weighting >= 0 && op->weighting <= 2, SFCDD_EVALUE, "unknown weighting");
@@ -617,10 +622,13 @@ extern "C" int sfcdd_op_setup(sfcdd_op* op, void* stream) {
   std::vector<int32_t> nbr((size_t)2 * d * n);
   CUDA_CHECK(cudaMemcpy(nbr.data(), op->nbr, nbr.size() * 4, cudaMemcpyDeviceToHost));
   // local blocks Â_i = Â[idx_i][:, idx_i] (schwarz.py:58-61)
-  std::vector<HostFactor> fs(op->p);
+  // shard mode: only the owned subdomains [sf, sf + sc) are factorized
+  const int32_t sf = op->shard_count > 0 ? op->shard_first : 0;
+  const int32_t sc = op->shard_count > 0 ? op->shard_count : op->p;
+  std::vector<HostFactor> fs(sc);
   FactorOptions fo;
-  std::atomic<int64_t> order_ns{0};
-  parallel_for(op->p, op->threads, [&](int64_t i) {
+  parallel_for(sc, op->threads, [&](int64_t li) {
+    const int64_t i = sf + li;
     const int64_t start = op->ov_start[i], len = op->ov_len[i];
     CsrMatrix B;
     B.n = len;
@@ -644,19 +652,35 @@ extern "C" int sfcdd_op_setup(sfcdd_op* op, void* stream) {
       }
       B.indptr[ro + 1] = B.indices.size();
     }
-    fs[i] = factorize_host(B, fo);
+    fs[li] = factorize_host(B, fo);
   });
   auto t1 = std::chrono::steady_clock::now();
   std::vector<const HostFactor*> ptrs;
-  std::vector<int64_t> gs, gm, xyoff;
+  std::vector<int64_t> gs, gm, xyoff(op->p, -1);
   int64_t xo = 0;
-  for (int i = 0; i < op->p; ++i) {
-    ptrs.push_back(&fs[i]);
-    gs.push_back(op->ov_start[i]);
+  for (int li = 0; li < sc; ++li) {
+    ptrs.push_back(&fs[li]);
+    gs.push_back(op->ov_start[sf + li]);
     gm.push_back(n);
-    xyoff.push_back(xo);
-    xo += op->ov_len[i];
+    xyoff[sf + li] = xo;
+    xo += op->ov_len[sf + li];
   }
+  // shard mode: slots for the foreign subdomains covering owned points, filled
+  // by the orchestrator's exchange before the combination
+  op->own_g0 = op->dj_start[sf];
+  op->own_g1 = op->dj_start[sf + sc - 1] + op->dj_len[sf + sc - 1];
+  int64_t extra = 0;
+  for (int j = 0; j < op->p; ++j) {
+    if (j >= sf && j < sf + sc) continue;
+    int64_t off = op->own_g0 - op->ov_start[j];
+    if (off < 0) off += n;
+    const bool hit = off < op->ov_len[j] || (op->ov_start[j] >= op->own_g0 && op->ov_start[j] < op->own_g1);
+    if (op->shard_count > 0 && hit) {
+      xyoff[j] = xo + extra;
+      extra += op->ov_len[j];
+    }
+  }
+  op->xy_off_host = xyoff;
   PlanOptions po;
   po.big_front_max = DagSolver::big_front_max(po.blob_max);
   DevicePlan plan = build_plan(ptrs, gs, gm, po);
@@ -664,7 +688,7 @@ extern "C" int sfcdd_op_setup(sfcdd_op* op, void* stream) {
   op->stats.factor_nnz_l = plan.nnz_l;
   op->stats.num_tasks = plan.nfrag;
   op->stats.num_supernodes = plan.num_supernodes;
-  op->dag.reset(new DagSolver(plan, op->device));
+  op->dag.reset(new DagSolver(plan, op->device, extra));
   op->dev_bytes += op->dag->device_bytes();
   fs.clear();
   // combination tables: candidates per disjoint range (ascending subdomain)
@@ -762,12 +786,8 @@ extern "C" int sfcdd_op_setup(sfcdd_op* op, void* stream) {
     op->y0b = (double*)dev_alloc(op, n0 * 8);
     CUDA_CHECK(cudaMemset(op->y0, 0, n0 * 8));
     CUDA_CHECK(cudaMemset(op->y0b, 0, n0 * 8));
-    if ((size_t)n0 * 8 > 48 * 1024) {
-      auto set = [&](auto kern) {
-        CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, n0 * 8));
-      };
-      set(k_coarse_gemv);
-    }
+    if ((size_t)n0 * 8 > 48 * 1024)  // per-function attribute: always the maximum (n0 <= 8192)
+      CUDA_CHECK(cudaFuncSetAttribute(k_coarse_gemv, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8));
   }
   // work vectors
   op->t = (double*)dev_alloc(op, n * 8);
@@ -1035,6 +1055,370 @@ extern "C" void sfcdd_op_destroy(sfcdd_op* op) {
   if (op->ev1) cudaEventDestroy(op->ev1);
   if (op->own_stream) cudaStreamDestroy(op->own_stream);
   delete op;
+}
+
+// ========================================================= shard mode
+// One handle per rank (multi-GPU).  Vectors stay full length N
+// on every rank but each step only computes the owned SFC segment / owned
+// chunks; the Python orchestrator (paper_2110_11211_b200/distributed.py)
+// moves halo / overlap / foreign-solution values with NCCL between steps and
+// reduces the partial scalars.
+namespace sfcdd {
+namespace {
+
+__global__ void k_sh_residual(const double* __restrict__ b, const double* __restrict__ x, Stencil S, Chunks C,
+                              int ch0, double* __restrict__ r, double* __restrict__ prr, double* __restrict__ pc) {
+  const int ch = ch0 + blockIdx.x;
+  double rr = 0.0, cs = 0.0;
+  for (int64_t g = C.start[ch] + threadIdx.x; g < C.start[ch + 1]; g += VEC_THREADS) {
+    const double v = b[g] - stencil_at(S, x, g);
+    r[g] = v;
+    rr = fma(v, v, rr);
+    cs += v;
+  }
+  rr = block_sum(rr);
+  cs = block_sum(cs);
+  if (threadIdx.x == 0) {
+    prr[ch] = rr;
+    pc[ch] = cs;
+  }
+}
+
+__global__ void k_sh_pm(const double* __restrict__ z, const double* __restrict__ pold, double beta, Stencil S,
+                        Chunks C, int ch0, double* __restrict__ pnew, double* __restrict__ ap,
+                        double* __restrict__ part) {
+  const int ch = ch0 + blockIdx.x;
+  double s = 0.0;
+  for (int64_t g = C.start[ch] + threadIdx.x; g < C.start[ch + 1]; g += VEC_THREADS) {
+    const double pg = __dadd_rn(z[g], __dmul_rn(beta, pold[g]));
+    double acc = S.dhat * pg;
+    for (int a = 0; a < 2 * S.d; ++a) {
+      const int32_t nb = __ldg(S.nbr + (int64_t)a * S.n + g);
+      if (nb >= 0) acc = fma(S.off[a >> 1], __dadd_rn(z[nb], __dmul_rn(beta, pold[nb])), acc);
+    }
+    pnew[g] = pg;
+    ap[g] = acc;
+    s = fma(pg, acc, s);
+  }
+  s = block_sum(s);
+  if (threadIdx.x == 0) part[ch] = s;
+}
+
+__global__ void k_sh_update(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                            const double* __restrict__ ap, double alpha, Chunks C, int ch0,
+                            double* __restrict__ prr, double* __restrict__ pc) {
+  const int ch = ch0 + blockIdx.x;
+  double rr = 0.0, cs = 0.0;
+  for (int64_t g = C.start[ch] + threadIdx.x; g < C.start[ch + 1]; g += VEC_THREADS) {
+    x[g] = __dadd_rn(x[g], __dmul_rn(alpha, p[g]));
+    const double v = __dsub_rn(r[g], __dmul_rn(alpha, ap[g]));
+    r[g] = v;
+    rr = fma(v, v, rr);
+    cs += v;
+  }
+  rr = block_sum(rr);
+  cs = block_sum(cs);
+  if (threadIdx.x == 0) {
+    prr[ch] = rr;
+    pc[ch] = cs;
+  }
+}
+
+__global__ void k_sh_stencil_chunks(const double* __restrict__ w, Stencil S, Chunks C, int ch0,
+                                    double* __restrict__ part) {
+  const int ch = ch0 + blockIdx.x;
+  double s = 0.0;
+  for (int64_t g = C.start[ch] + threadIdx.x; g < C.start[ch + 1]; g += VEC_THREADS) s += stencil_at(S, w, g);
+  s = block_sum(s);
+  if (threadIdx.x == 0) part[ch] = s;
+}
+
+__global__ void k_sh_finalize(const double* __restrict__ w, const double* __restrict__ y0,
+                              const double* __restrict__ y0b, Chunks C, int ch0, int mode, double* __restrict__ h,
+                              const double* __restrict__ rdot, double* __restrict__ part) {
+  const int ch = ch0 + blockIdx.x;
+  const int a = C.agg[ch];
+  const double c0 = mode >= 1 ? y0[a] : 0.0;
+  const double c1 = mode >= 2 ? y0b[a] : 0.0;
+  double s = 0.0;
+  for (int64_t g = C.start[ch] + threadIdx.x; g < C.start[ch + 1]; g += VEC_THREADS) {
+    double v = w[g];
+    if (mode == 1) v = v + c0;
+    if (mode == 2) v = (v - c1) + c0;
+    h[g] = v;
+    if (rdot) s = fma(rdot[g], v, s);
+  }
+  if (rdot) {
+    s = block_sum(s);
+    if (threadIdx.x == 0) part[ch] = s;
+  }
+}
+
+// fixed-order sum of part[ch0, ch1) into *out (one block)
+__global__ void k_sum_range(const double* __restrict__ part, int ch0, int ch1, double* __restrict__ out) {
+  double v = 0.0;
+  for (int i = ch0 + threadIdx.x; i < ch1; i += VEC_THREADS) v += part[i];
+  v = block_sum(v);
+  if (threadIdx.x == 0) *out = v;
+}
+
+// per-aggregate sums of the chunk partials for aggregates [a0, a1)
+__global__ void k_agg_sums(const double* __restrict__ part, const int32_t* __restrict__ agg_ptr, int a0, int a1,
+                           double* __restrict__ out) {
+  const int a = a0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= a1) return;
+  double s = 0.0;
+  for (int ch = agg_ptr[a]; ch < agg_ptr[a + 1]; ++ch) s += part[ch];
+  out[a - a0] = s;
+}
+
+__global__ void k_gemv_c(const double* __restrict__ ainv, const double* __restrict__ cin, int32_t n0,
+                         double* __restrict__ y) {
+  extern __shared__ double c[];
+  for (int a = threadIdx.x; a < n0; a += VEC_THREADS) c[a] = cin[a];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (VEC_THREADS / 32) + (threadIdx.x >> 5);
+  if (row >= n0) return;
+  const double* ar = ainv + (int64_t)row * n0;
+  double acc = 0.0;
+  for (int j = lane; j < n0; j += 32) acc = fma(__ldg(ar + j), c[j], acc);
+  acc = warp_sum(acc);
+  if (lane == 0) y[row] = acc;
+}
+
+__global__ void k_sh_tvec(const double* __restrict__ gv, const double* __restrict__ y0,
+                          const int32_t* __restrict__ agg, Stencil S, int64_t g0, int64_t g1,
+                          double* __restrict__ t) {
+  const int64_t g = g0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= g1) return;
+  double acc = S.dhat * y0[agg[g]];
+  for (int a = 0; a < 2 * S.d; ++a) {
+    const int32_t nb = __ldg(S.nbr + (int64_t)a * S.n + g);
+    if (nb >= 0) acc = fma(S.off[a >> 1], y0[agg[nb]], acc);
+  }
+  t[g] = gv[g] - acc;
+}
+
+__global__ void k_sh_combine(CombineArgs C, int64_t g0, int64_t g1, double* __restrict__ w) {
+  const int64_t g = g0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= g1) return;
+  int lo = 0, hi = C.p;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (C.dj_start[mid] <= g)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  double acc = 0.0;
+  for (int c = C.cand_ptr[lo]; c < C.cand_ptr[lo + 1]; ++c) {
+    const int i = C.cand[c];
+    int64_t off = g - C.ov_start[i];
+    if (off < 0) off += C.n;
+    if (off >= C.ov_len[i]) continue;
+    const double wt = C.count ? 1.0 / (double)C.count[g] : C.wgt[i];
+    acc = __dadd_rn(acc, __dmul_rn(wt, __ldcg(C.xy + C.xy_off[i] + off)));
+  }
+  w[g] = acc;
+}
+
+__global__ void k_pack(const double* __restrict__ src, const int64_t* __restrict__ idx, int64_t n,
+                       double* __restrict__ dst) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[idx[i]];
+}
+
+__global__ void k_unpack(const double* __restrict__ src, const int64_t* __restrict__ idx, int64_t n,
+                         double* __restrict__ dst) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[idx[i]] = src[i];
+}
+
+}  // namespace
+
+struct ShardRange {
+  int ch0, ch1, a0, a1;
+  int64_t g0, g1;
+};
+
+static ShardRange shard_range(const sfcdd_op* op) {
+  const int32_t sf = op->shard_count > 0 ? op->shard_first : 0;
+  const int32_t sc = op->shard_count > 0 ? op->shard_count : op->p;
+  ShardRange r;
+  r.a0 = sf * op->q;
+  r.a1 = (sf + sc) * op->q;
+  std::vector<int32_t> aptr(op->n0 + 1);
+  // agg_ptr lives on device; the host copy is rebuilt from agg_start sizes
+  int32_t c = 0;
+  aptr[0] = 0;
+  for (int32_t a = 0; a < op->n0; ++a) {
+    const int64_t len = op->agg_start[a + 1] - op->agg_start[a];
+    c += (int32_t)((len + CHUNK - 1) / CHUNK);
+    aptr[a + 1] = c;
+  }
+  r.ch0 = aptr[r.a0];
+  r.ch1 = aptr[r.a1];
+  r.g0 = op->agg_start[r.a0];
+  r.g1 = op->agg_start[r.a1];
+  return r;
+}
+
+}  // namespace sfcdd
+
+extern "C" int sfcdd_shard_info(sfcdd_op* op, int64_t* info, int64_t* xy_off_host) {
+  SFCDD_API_BEGIN
+  SFCDD_REQUIRE(op && op->ready && op->n0 > 0, SFCDD_EVALUE, "shard mode needs a set-up operator with a coarse space");
+  const ShardRange r = shard_range(op);
+  info[0] = r.g0;
+  info[1] = r.g1;
+  info[2] = r.ch0;
+  info[3] = r.ch1;
+  info[4] = r.a0;
+  info[5] = r.a1;
+  info[6] = op->dag->xy_doubles();
+  info[7] = op->n0;
+  if (xy_off_host)
+    for (int i = 0; i < op->p; ++i) xy_off_host[i] = op->xy_off_host[i];
+  SFCDD_API_END
+}
+
+extern "C" int sfcdd_op_neighbors(sfcdd_op* op, int32_t* nbr_host) {
+  SFCDD_API_BEGIN
+  SFCDD_REQUIRE(op && nbr_host, SFCDD_EVALUE, "null argument");
+  CUDA_CHECK(cudaSetDevice(op->device));
+  CUDA_CHECK(cudaMemcpy(nbr_host, op->nbr, (size_t)2 * op->d * op->n * 4, cudaMemcpyDeviceToHost));
+  SFCDD_API_END
+}
+
+extern "C" int sfcdd_shard_xy(sfcdd_op* op, double** xy) {
+  SFCDD_API_BEGIN
+  SFCDD_REQUIRE(op && op->ready, SFCDD_EVALUE, "operator not set up");
+  *xy = op->dag->xy();
+  SFCDD_API_END
+}
+
+extern "C" int sfcdd_shard_residual(sfcdd_op* op, const double* b, const double* x, double* r, double* rr_out,
+                                    double* cagg_out, void* stream) {
+  SFCDD_API_BEGIN
+  const ShardRange R = shard_range(op);
+  cudaStream_t st = (cudaStream_t)stream;
+  k_sh_residual<<<R.ch1 - R.ch0, VEC_THREADS, 0, st>>>(b, x, stencil_of(op), chunks_of(op), R.ch0, r, op->part_b,
+                                                       op->part_c);
+  k_sum_range<<<1, VEC_THREADS, 0, st>>>(op->part_b, R.ch0, R.ch1, rr_out);
+  k_agg_sums<<<nblocks(R.a1 - R.a0, 128), 128, 0, st>>>(op->part_c, op->agg_ptr, R.a0, R.a1, cagg_out);
+  CUDA_CHECK(cudaGetLastError());
+  SFCDD_API_END
+}
+
+extern "C" int sfcdd_shard_pm(sfcdd_op* op, const double* z, const double* pold, double beta, double* pnew,
+                              double* ap, double* pap_out, void* stream) {
+  SFCDD_API_BEGIN
+  const ShardRange R = shard_range(op);
+  cudaStream_t st = (cudaStream_t)stream;
+  k_sh_pm<<<R.ch1 - R.ch0, VEC_THREADS, 0, st>>>(z, pold, beta, stencil_of(op), chunks_of(op), R.ch0, pnew, ap,
+                                                 op->part_a);
+  k_sum_range<<<1, VEC_THREADS, 0, st>>>(op->part_a, R.ch0, R.ch1, pap_out);
+  CUDA_CHECK(cudaGetLastError());
+  SFCDD_API_END
+}
+
+extern "C" int sfcdd_shard_update(sfcdd_op* op, double* x, double* r, const double* p, const double* ap, double alpha,
+                                  double* rr_out, double* cagg_out, void* stream) {
+  SFCDD_API_BEGIN
+  const ShardRange R = shard_range(op);
+  cudaStream_t st = (cudaStream_t)stream;
+  k_sh_update<<<R.ch1 - R.ch0, VEC_THREADS, 0, st>>>(x, r, p, ap, alpha, chunks_of(op), R.ch0, op->part_b,
+                                                     op->part_c);
+  k_sum_range<<<1, VEC_THREADS, 0, st>>>(op->part_b, R.ch0, R.ch1, rr_out);
+  k_agg_sums<<<nblocks(R.a1 - R.a0, 128), 128, 0, st>>>(op->part_c, op->agg_ptr, R.a0, R.a1, cagg_out);
+  CUDA_CHECK(cudaGetLastError());
+  SFCDD_API_END
+}
+
+extern "C" int sfcdd_shard_coarse(sfcdd_op* op, const double* c, double* y, void* stream) {
+  SFCDD_API_BEGIN
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t smem = (size_t)op->n0 * 8;
+  if (smem > 48 * 1024)
+    CUDA_CHECK(cudaFuncSetAttribute(k_gemv_c, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8));
+  k_gemv_c<<<nblocks(op->n0, VEC_THREADS / 32), VEC_THREADS, smem, st>>>(op->ainv, c, op->n0, y);
+  CUDA_CHECK(cudaGetLastError());
+  SFCDD_API_END
+}
+
+extern "C" int sfcdd_shard_tvec(sfcdd_op* op, const double* g, const double* y0, double* t, void* stream) {
+  SFCDD_API_BEGIN
+  const ShardRange R = shard_range(op);
+  k_sh_tvec<<<nblocks(R.g1 - R.g0, VEC_THREADS), VEC_THREADS, 0, (cudaStream_t)stream>>>(g, y0, op->agg,
+                                                                                       stencil_of(op), R.g0, R.g1, t);
+  CUDA_CHECK(cudaGetLastError());
+  SFCDD_API_END
+}
+
+extern "C" int sfcdd_shard_local_solve(sfcdd_op* op, const double* t, void* stream) {
+  SFCDD_API_BEGIN
+  op->dag->solve(t, (cudaStream_t)stream);
+  SFCDD_API_END
+}
+
+extern "C" int sfcdd_shard_combine(sfcdd_op* op, double* w, void* stream) {
+  SFCDD_API_BEGIN
+  const ShardRange R = shard_range(op);
+  CombineArgs ca;
+  ca.xy = op->dag->xy();
+  ca.ov_start = op->d_ov_start;
+  ca.ov_len = op->d_ov_len;
+  ca.xy_off = op->d_xy_off;
+  ca.dj_start = op->d_dj_start;
+  ca.cand_ptr = op->cand_ptr;
+  ca.cand = op->cand;
+  ca.wgt = op->d_wgt;
+  ca.count = op->weighting == SFCDD_WEIGHT_DMATRIX ? op->d_count : nullptr;
+  ca.fault = nullptr;
+  ca.apply_calls = nullptr;
+  ca.fault_index = -1;
+  ca.p = op->p;
+  ca.n = op->n;
+  k_sh_combine<<<nblocks(R.g1 - R.g0, VEC_THREADS), VEC_THREADS, 0, (cudaStream_t)stream>>>(ca, R.g0, R.g1, w);
+  CUDA_CHECK(cudaGetLastError());
+  SFCDD_API_END
+}
+
+extern "C" int sfcdd_shard_stencil_restrict(sfcdd_op* op, const double* w, double* cagg_out, void* stream) {
+  SFCDD_API_BEGIN
+  const ShardRange R = shard_range(op);
+  cudaStream_t st = (cudaStream_t)stream;
+  k_sh_stencil_chunks<<<R.ch1 - R.ch0, VEC_THREADS, 0, st>>>(w, stencil_of(op), chunks_of(op), R.ch0, op->part_b);
+  k_agg_sums<<<nblocks(R.a1 - R.a0, 128), 128, 0, st>>>(op->part_b, op->agg_ptr, R.a0, R.a1, cagg_out);
+  CUDA_CHECK(cudaGetLastError());
+  SFCDD_API_END
+}
+
+extern "C" int sfcdd_shard_finalize(sfcdd_op* op, const double* w, const double* y0, const double* y0b, double* z,
+                                    const double* r, double* rz_out, void* stream) {
+  SFCDD_API_BEGIN
+  const ShardRange R = shard_range(op);
+  cudaStream_t st = (cudaStream_t)stream;
+  k_sh_finalize<<<R.ch1 - R.ch0, VEC_THREADS, 0, st>>>(w, y0, y0b, chunks_of(op), R.ch0, mode_of(op->variant), z, r,
+                                                       op->part_a);
+  if (r) k_sum_range<<<1, VEC_THREADS, 0, st>>>(op->part_a, R.ch0, R.ch1, rz_out);
+  CUDA_CHECK(cudaGetLastError());
+  SFCDD_API_END
+}
+
+extern "C" int sfcdd_pack(const double* src, const int64_t* idx, int64_t n, double* dst, void* stream) {
+  SFCDD_API_BEGIN
+  if (n > 0) k_pack<<<nblocks(n, 256), 256, 0, (cudaStream_t)stream>>>(src, idx, n, dst);
+  CUDA_CHECK(cudaGetLastError());
+  SFCDD_API_END
+}
+
+extern "C" int sfcdd_unpack(const double* src, const int64_t* idx, int64_t n, double* dst, void* stream) {
+  SFCDD_API_BEGIN
+  if (n > 0) k_unpack<<<nblocks(n, 256), 256, 0, (cudaStream_t)stream>>>(src, idx, n, dst);
+  CUDA_CHECK(cudaGetLastError());
+  SFCDD_API_END
 }
 
 // ------------------------------------------------- generic sparse factor
