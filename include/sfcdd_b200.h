@@ -138,8 +138,9 @@ int sfcdd_op_profile(sfcdd_op* op, const double* g_dev, double* scratch_dev, int
                      double* ms, int32_t* launches, void* stream);
 /* Diagnostics: one traced local-solve DAG launch.  out_host receives 24
  * uint64 per task {sm, t_top, t_deps_ok, t_data_ok, t_end (globaltimer ns),
- * flags, copy_bytes, fragment, 16 clock64 phase stamps of small forward
- * tasks}; *ntask gets the task count (call with out_host = NULL first).   */
+ * kind, copy_bytes, group, values, wait_idx, wait_target, signal_idx,
+ * 12 reserved zeros}; *ntask gets the task count (call with out_host =
+ * NULL first).                                                            */
 int sfcdd_op_trace(sfcdd_op* op, const double* g_dev, uint64_t* out_host, int64_t* ntask);
 int sfcdd_op_stats(sfcdd_op* op, sfcdd_stats* out);
 /* diagnostics: Â's constants (diag, off per axis) and symmetric scaling t */

@@ -60,7 +60,6 @@ extern "C" int sfcdd_host_factor_solve(int64_t n, const int64_t* indptr, const i
 }
 
 namespace sfcdd {
-void plan_exec_host(const DevicePlan& P, const double* rhs, double* xy);
 // principal sub-block of a global CSR matrix on a cyclic range
 CsrMatrix extract_block(const CsrMatrix& A, int64_t start, int64_t len) {
   const int64_t n = A.n;
@@ -105,6 +104,6 @@ extern "C" int sfcdd_host_plan_solve(int64_t n, const int64_t* indptr, const int
   if (scratch_max > 0) po.scratch_max = scratch_max;
   DevicePlan plan = build_plan(ptrs, gs, gm, po);
   plan_exec_host(plan, rhs, xy);
-  if (nfrag) *nfrag = plan.nfrag;
+  if (nfrag) *nfrag = plan.ngroups;
   SFCDD_API_END
 }

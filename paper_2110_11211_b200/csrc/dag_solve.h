@@ -24,18 +24,14 @@ class DagSolver {
   int64_t xy_doubles() const { return xy_doubles_; }
   int64_t device_bytes() const { return bytes_; }
   int32_t grid() const { return grid_; }
-  int32_t nfrag() const { return nfrag_; }
-  // largest front (s+m) of a big supernode the chunk ring can stream
-  static int big_front_max(int blob_max);
-  // diagnostics: per-task timestamps {sm, top, deps ok, data ok, end} (5 x u64
-  // per task), followed by 16 clock64 phase stamps per task (21 x ntask words)
+  int32_t ngroups() const { return ngroups_; }
+  // diagnostics: per-task timestamps {sm, top, deps ok, data ok, end} (5 x u64 per task)
   void set_trace(unsigned long long* dev_buf);
   int32_t ntask() const { return ntask_; }
-  int32_t grid_size() const { return grid_; }
 
  private:
   int device_;
-  int32_t nfrag_ = 0, ntask_ = 0, grid_ = 1, blob_max_ = 0, smem_ = 0, chunk_bytes_ = 0;
+  int32_t ngroups_ = 0, ntask_ = 0, grid_ = 1, blob_max_ = 0, slot_bytes_ = 0, smem_ = 0;
   int64_t xy_doubles_ = 0, ctr_words_ = 0, bytes_ = 0;
   uint8_t* blobs_ = nullptr;
   TaskDev* tasks_ = nullptr;

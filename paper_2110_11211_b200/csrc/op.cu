@@ -682,11 +682,10 @@ extern "C" int sfcdd_op_setup(sfcdd_op* op, void* stream) {
   }
   op->xy_off_host = xyoff;
   PlanOptions po;
-  po.big_front_max = DagSolver::big_front_max(po.blob_max);
   DevicePlan plan = build_plan(ptrs, gs, gm, po);
   op->stats.factor_nnz = plan.stored;
   op->stats.factor_nnz_l = plan.nnz_l;
-  op->stats.num_tasks = plan.nfrag;
+  op->stats.num_tasks = (int64_t)plan.tasks.size();
   op->stats.num_supernodes = plan.num_supernodes;
   op->dag.reset(new DagSolver(plan, op->device, extra));
   op->dev_bytes += op->dag->device_bytes();
@@ -979,22 +978,27 @@ extern "C" int sfcdd_op_trace(sfcdd_op* op, const double* g_dev, uint64_t* out_h
   if (!out_host) return SFCDD_OK;
   CUDA_CHECK(cudaSetDevice(op->device));
   unsigned long long* buf = nullptr;
-  CUDA_CHECK(cudaMalloc(&buf, nt * 21 * 8));
-  CUDA_CHECK(cudaMemset(buf, 0, nt * 21 * 8));
+  CUDA_CHECK(cudaMalloc(&buf, nt * 5 * 8));
+  CUDA_CHECK(cudaMemset(buf, 0, nt * 5 * 8));
   op->dag->solve(g_dev, nullptr);  // warm
   op->dag->set_trace(buf);
   op->dag->solve(g_dev, nullptr);
   op->dag->set_trace(nullptr);
   CUDA_CHECK(cudaDeviceSynchronize());
-  std::vector<unsigned long long> h(nt * 21);
-  CUDA_CHECK(cudaMemcpy(h.data(), buf, nt * 21 * 8, cudaMemcpyDeviceToHost));
+  std::vector<unsigned long long> h(nt * 5);
+  CUDA_CHECK(cudaMemcpy(h.data(), buf, nt * 5 * 8, cudaMemcpyDeviceToHost));
   CUDA_CHECK(cudaFree(buf));
   for (int64_t t = 0; t < nt; ++t) {
+    const TaskDev& T = op->dag->host_tasks[t];
     for (int j = 0; j < 5; ++j) out_host[24 * t + j] = h[5 * t + j];
-    out_host[24 * t + 5] = op->dag->host_tasks[t].flags;
-    out_host[24 * t + 6] = op->dag->host_tasks[t].copy_bytes;
-    out_host[24 * t + 7] = op->dag->host_tasks[t].frag;
-    for (int j = 0; j < 16; ++j) out_host[24 * t + 8 + j] = h[5 * nt + 16 * t + j];
+    out_host[24 * t + 5] = (uint64_t)T.kind;
+    out_host[24 * t + 6] = (uint64_t)T.copy_bytes;
+    out_host[24 * t + 7] = (uint64_t)T.group;
+    out_host[24 * t + 8] = (uint64_t)T.values;
+    out_host[24 * t + 9] = (uint64_t)(int64_t)T.wait_idx;
+    out_host[24 * t + 10] = (uint64_t)T.wait_target;
+    out_host[24 * t + 11] = (uint64_t)T.signal_idx;
+    for (int j = 12; j < 24; ++j) out_host[24 * t + j] = 0;
   }
   SFCDD_API_END
 }
@@ -1447,7 +1451,6 @@ extern "C" int sfcdd_factor_create(int64_t n, const int64_t* indptr, const int32
   f->stored = F.stored;
   f->nsuper = F.sn.size();
   PlanOptions po;
-  po.big_front_max = DagSolver::big_front_max(po.blob_max);
   DevicePlan plan = build_plan({&F}, {0}, {n}, po);
   CUDA_CHECK(cudaSetDevice(device));
   f->dag.reset(new DagSolver(plan, device));

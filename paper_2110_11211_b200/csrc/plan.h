@@ -1,8 +1,17 @@
-// Device execution plan for a batch of block-inverse factors: the factor
-// trees are cut into fragments (connected subtrees whose factor bytes and
-// metadata fit one shared-memory blob, or a single big supernode streamed
-// from HBM in chunks), and each fragment becomes one forward and one
-// backward task of the dataflow kernel in dag_solve.cu.
+// Device execution plan for a batch of block-inverse factors (v4, warp
+// tasks).  Every task is executed by ONE warp out of a per-warp shared-memory
+// slot (blob area + scratch area); a task's blob (int32 metadata + fp64 factor
+// values) is moved HBM -> slot by one cp.async.bulk.
+//
+// Work units ("groups"):
+//  * FRAG: a connected subtree of small supernodes.  One forward task and one
+//    backward task share the blob; the warp runs the subtree level by level
+//    entirely in its slot.
+//  * BIG: one supernode J too large for a slot.  Forward = ROW tasks (blocks
+//    of rows of M = [L_JJ^-1 ; L_BJ L_JJ^-1], each re-assembling f_J from the
+//    children's update vectors), backward = COL tasks (blocks of columns of M).
+//    y_J travels from the ROW to the COL tasks through a global y slot.
+// Dependencies are per-group counters (see TaskDev).
 #pragma once
 #include <cstdint>
 #include <vector>
@@ -19,31 +28,33 @@ struct FactorDev {
   int64_t n;
 };
 
-// One DAG task (forward or backward sweep of one fragment).  The queue holds
-// the 2 nfrag tasks in decreasing critical-path rank (longest weighted path
-// to the end of the solve), which is a topological order: every task waits
-// only on tasks earlier in the queue.
-struct TaskDev {
-  int64_t blob_off;    // byte offset of the fragment blob
-  int32_t copy_bytes;  // bytes bulk-copied into shared memory (0 for big)
-  int32_t frag;        // fragment id
-  int32_t factor;      // factor id
-  int32_t wait_on;     // forward: #child fragments; backward: fragment to wait on (-1 = own fwd)
-  int32_t signal;      // forward: parent fragment (-1 none)
-  int32_t flags;       // TASK_BIG | TASK_BWD
-};
-constexpr int32_t TASK_BIG = 1;  // single supernode, values streamed from HBM in chunks
-constexpr int32_t TASK_BWD = 2;  // backward sweep
+enum TaskKind : int32_t { TK_FRAG_FWD = 0, TK_FRAG_BWD = 1, TK_ROW_FWD = 2, TK_COL_BWD = 3 };
 
-// Blob = [int32 meta | pad16 | fp64 packed M blocks].
-//
-// SMALL fragment (whole blob copied to shared memory).  Supernodes are
+// One warp task.  The queue holds all tasks in decreasing critical-path rank
+// (HLFET), a topological order: a task only waits on tasks earlier in the
+// queue.  Counters (int32, zeroed per solve): ctr[0] = queue head; per group
+// g of G: fin = 1+g (forward arrivals of g's children), bdone = 1+G+g
+// (g's backward tasks done), rdone = 1+2G+g (a root group's forward done).
+struct TaskDev {
+  int64_t blob_off;     // byte offset of the task blob (16-byte aligned)
+  int32_t copy_bytes;   // bytes bulk-copied into the slot (multiple of 16)
+  int32_t kind;         // TaskKind
+  int32_t factor;       // factor id
+  int32_t group;        // group id (diagnostics)
+  int32_t wait_idx;     // counter to wait on (-1: none)
+  int32_t wait_target;  // wait until ctr[wait_idx] >= wait_target
+  int32_t signal_idx;   // counter incremented on completion
+  int32_t values;       // factor values touched (diagnostics)
+};
+
+// ---------------------------------------------------------------- FRAG blob
+// Blob = [int32 meta | pad16 | fp64 packed M blocks].  Supernodes are
 // numbered in level order (level 0 = fragment leaves).  Shared scratch
-// (doubles):  [frontal slots (s+m each)] [column values (sum s)]
-//             [ext_x staging] [ext_u staging]
+// (doubles): [frontal slots (s+m each)] [column values (sum s)]
+//            [ext_x staging] [ext_u staging]
 // Frontal slot of J: f = [b_J + child updates ; f_B] (forward) or
-// v = [y_J ; -x_B] (backward).  Column values receive y_J (forward) or
-// x_J (backward).  Per level l the meta holds
+// v = [y_J ; -x_B] (backward).  Column values receive y_J (forward) or x_J
+// (backward).  Per level l the meta holds
 //   * gather runs (forward assembly, gather form, fixed child order):
 //     pairs (dst | src << 16) sorted by dst; run r = pairs [run[r], run[r+1])
 //     all with the same dst: S[dst] += sum S[src];
@@ -52,71 +63,105 @@ constexpr int32_t TASK_BWD = 2;  // backward sweep
 //     x < 65536: row block y (forward) / column y (backward) of supernode x;
 //     x = j | cnt << 16: cnt consecutive small supernodes j.. packed into the
 //     32 lanes, y = bit mask of the lanes where each one starts (+ end lane).
-//
-// BIG fragment (one supernode): meta read from global, values streamed in
-// column chunks; rows hold range offsets (ro) and child records reference
-// global update slots.
-enum BlobHdr {
+enum FragHdr {
   H_NSN = 0,
   H_NLEV,
-  H_SCRATCH,   // doubles of scratch used
-  H_VAL_OFF,   // byte offset of the value area within the blob
-  H_TOP,       // local id of the fragment's top supernode
-  H_TOP_UPD,   // global update slot of the top supernode (-1 none)
-  H_NCOL,      // number of fragment columns
-  H_COLS,      // int offset: ro[ncol]
-  H_COLPOS,    // int offset: (fpos | cpos << 16)[ncol]
-  H_NEXTX,     // number of external rows (staged contiguously from H_EXTX_BASE)
-  H_EXTX,      // int offset of their ro[nextx]
-  H_NEXTU,     // number of staged external update doubles (contiguous from H_EXTU_BASE)
-  H_EXTU,      // int offset of their global update indices [nextu]
-  H_BIG,       // 1 = big fragment
-  H_REC,       // int offset of SnRec[nsn] (level order)
-  H_LEVELS,    // int offset of the per-level table (L_WORDS per level)
-  H_RUNS,      // int offset of gather run starts (int32, absolute pair index)
-  H_GPAIRS,    // int offset of forward gather pairs (uint32)
-  H_BPAIRS,    // int offset of backward row pairs (uint32)
-  H_ITEMS,     // int offset of items (int2)
-  H_EXTX_BASE, // scratch position of the first ext_x slot
-  H_EXTU_BASE, // scratch position of the first ext_u slot
-  H_WORDS = 22
+  H_SCRATCH,    // doubles of scratch used
+  H_VAL_OFF,    // byte offset of the value area within the blob
+  H_TOP,        // local id of the fragment's top supernode
+  H_TOP_UPD,    // global update slot of the top supernode (-1 none)
+  H_NCOL,       // number of fragment columns
+  H_COLS,       // int offset: ro[ncol]
+  H_COLPOS,     // int offset: (fpos | cpos << 16)[ncol]
+  H_NEXTX,      // number of external rows (staged contiguously from H_EXTX_BASE)
+  H_EXTX,       // int offset of their ro[nextx]
+  H_NEXTU,      // number of staged external update doubles (contiguous from H_EXTU_BASE)
+  H_EXTU,       // int offset of their global update indices [nextu]
+  H_REC,        // int offset of SnRec[nsn] (level order)
+  H_LEVELS,     // int offset of the per-level table (L_WORDS per level)
+  H_RUNS,       // int offset of gather run starts (int32, absolute pair index)
+  H_GPAIRS,     // int offset of forward gather pairs (uint32)
+  H_BPAIRS,     // int offset of backward row pairs (uint32)
+  H_ITEMS,      // int offset of items (int2)
+  H_EXTX_BASE,  // scratch position of the first ext_x slot
+  H_EXTU_BASE,  // scratch position of the first ext_u slot
+  H_WORDS
 };
-// per-level table: [rec0, rec1, run0, run1, bpair0, bpair1,
-//   fwarp[NWARP_PLAN+1], bwarp[NWARP_PLAN+1]]  -- the level's forward /
-// backward items are pre-assigned to the compute warps (longest-processing-
-// time first by an item cost model): warp w runs items [fwarp[w], fwarp[w+1]).
-constexpr int NWARP_PLAN = 8;
-enum LevField { L_REC0 = 0, L_REC1, L_RUN0, L_RUN1, L_BP0, L_BP1, L_FW, L_BW = L_FW + NWARP_PLAN + 1,
-                L_WORDS = L_BW + NWARP_PLAN + 1 };
-// per-supernode record (int32 words).  Small: S, M, VAL, SCR, CPOS used.
-// Big: S, M, VAL, ROWS (ro of the m rows), NCH, CH (child records).
-enum SnRecField { R_S = 0, R_M, R_VAL, R_SCR, R_ROWS, R_NCH, R_CH, R_CPOS, R_WORDS };
-// big-fragment child record: {global update slot, m, rel int offset}
-constexpr int CH_WORDS = 3;
-constexpr int SMALL_MAX_S = 128;  // supernodes wider than this are "big"
+// per-level table: record range, forward gather runs, backward row pairs,
+// forward items, backward items
+enum LevField { L_REC0 = 0, L_REC1, L_RUN0, L_RUN1, L_BP0, L_BP1, L_FI0, L_FI1, L_BI0, L_BI1, L_WORDS };
+// per-supernode record (int32 words)
+enum SnRecField { R_S = 0, R_M, R_VAL, R_SCR, R_CPOS, R_WORDS };
+
+// ------------------------------------------------------ BIG supernode meta
+// Per big supernode J one read-only ASSEMBLY record lives in the blob buffer
+// (16-aligned, read through the cache by all of J's tasks, never staged):
+//   [ro of the s columns] [ro of the m below rows] [ptr (s+m+1)] [src (nnz)]
+// -- a CSR over J's front positions listing, in fixed order (children, then
+// rows), the global update indices summed into that position.
+//
+// ROW blob: forward rows [r0, r0+R) of J (either all < s: y rows, or all
+// >= s: update rows).  Values: R x C dense column-major (leading dim R),
+// entry (i, k) = M[r0+i, k] (zero where k > r0+i), C = min(r0+R, s).
+// Scratch: [f_J (C)] [f_B of the block rows (NB)].
+enum RowHdr {
+  RW_S = 0,
+  RW_M,
+  RW_R,        // rows in the block
+  RW_C,        // columns
+  RW_R0,       // first front row
+  RW_NB,       // block rows >= s (0 or R)
+  RW_YOFF,     // global y slot of J (upd buffer)
+  RW_UOFF,     // global update slot of J (-1: root)
+  RW_ASM16,    // byte offset / 16 of J's assembly record in the blob buffer
+  RW_VAL_OFF,  // byte offset of the values
+  RW_SCRATCH,  // doubles of scratch used
+  RW_WORDS
+};
+
+// COL blob: backward columns [k0, k1) of J.  Values: packed columns k0..k1-1
+// of M (column k holds rows k..s+m-1).  Scratch: v = [y_J[k0:s) ; -x_B].
+enum ColHdr {
+  CL_S = 0,
+  CL_M,
+  CL_K0,
+  CL_K1,
+  CL_YOFF,     // global y slot of J
+  CL_ASM16,    // byte offset / 16 of J's assembly record
+  CL_VAL_OFF,  // byte offset of the values
+  CL_SCRATCH,
+  CL_WORDS
+};
+
+constexpr int SMALL_MAX_S = 64;  // wider supernodes are always BIG
 
 struct PlanOptions {
-  int32_t blob_max = 46 * 1024;     // bytes per small fragment (meta + values)
-  int32_t scratch_max = 2048;       // doubles of shared scratch per fragment (< 65536)
-  int32_t big_front_max = 1950;     // s+m limit of a streamed big supernode (DagSolver::big_front_max)
+  int32_t blob_max = 12 * 1024;  // bytes of a task blob (slot blob area)
+  int32_t scratch_max = 768;     // doubles of FRAG scratch (< 65536)
+  int32_t big_scratch_max = 8192;  // doubles of scratch a BIG task may use
+  PlanOptions();                 // environment overrides SFCDD_BLOB_MAX, SFCDD_SCRATCH_MAX
 };
 
 struct DevicePlan {
   std::vector<uint8_t> blobs;
-  std::vector<TaskDev> tasks;  // 2 * nfrag
+  std::vector<TaskDev> tasks;
   std::vector<FactorDev> factors;
-  int32_t nfrag = 0;
-  int32_t nbig = 0;
+  int32_t ngroups = 0;
+  int32_t nfrag = 0;      // FRAG groups
+  int32_t nbig = 0;       // BIG groups
   int64_t upd_doubles = 0;
   int64_t xy_doubles = 0;
   int64_t num_supernodes = 0;
   int64_t stored = 0, nnz_l = 0;
-  int32_t max_scratch = 0;  // doubles
+  int32_t max_scratch = 0;  // doubles, over all tasks
   int32_t max_copy = 0;     // bytes
   int32_t blob_max = 0;
 };
 
 DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::vector<int64_t>& gstart,
                       const std::vector<int64_t>& gmod, const PlanOptions& opt);
+
+// host interpreter of the plan (test hook): same blob semantics as the kernel
+void plan_exec_host(const DevicePlan& P, const double* rhs, double* xy);
 
 }  // namespace sfcdd

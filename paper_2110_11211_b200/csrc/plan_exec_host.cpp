@@ -1,8 +1,10 @@
-// Host interpreter of a DevicePlan: executes the forward/backward tasks in
-// queue order with exactly the blob semantics of the device kernel
-// (dag_solve.cu): the same level tables, gather runs, row pairs and warp
-// items.  Test hook only -- lets the CPU test suite check the plan layout
-// without a GPU.  Not used by the product path.
+// Host interpreter of a DevicePlan: executes the warp tasks in queue order
+// with exactly the blob semantics of the device kernel (dag_solve.cu) --
+// FRAG level tables, gather runs, row pairs and warp items; ROW blocks with
+// their gather runs; COL blocks -- and checks every task's dependency counter
+// is satisfied when the queue reaches it.  Test hook only (lets the CPU test
+// suite validate plan layouts without a GPU); not on the product path.
+#include <algorithm>
 #include <cstring>
 #include <vector>
 
@@ -19,145 +21,159 @@ inline int32_t hi16(int32_t v) { return (int32_t)((uint32_t)v >> 16); }
 void plan_exec_host(const DevicePlan& P, const double* rhs, double* xy) {
   std::vector<double> upd(P.upd_doubles, 0.0);
   std::vector<double> scratch;
-  const int32_t nf = P.nfrag;
-  for (int32_t t = 0; t < 2 * nf; ++t) {
+  std::vector<int64_t> ctr(1 + 3 * (size_t)P.ngroups, 0);
+  for (size_t t = 0; t < P.tasks.size(); ++t) {
     const TaskDev& T = P.tasks[t];
-    const bool fwd = !(T.flags & TASK_BWD);
+    SFCDD_REQUIRE(T.wait_idx < 0 || ctr[T.wait_idx] >= T.wait_target, SFCDD_EINTERNAL,
+                  "task queue is not a topological order");
     const uint8_t* blob = P.blobs.data() + T.blob_off;
     const int32_t* h = reinterpret_cast<const int32_t*>(blob);
-    const double* vals = reinterpret_cast<const double*>(blob + h[H_VAL_OFF]);
     const FactorDev& Fd = P.factors[T.factor];
-    const int32_t* recs = h + h[H_REC];
-    const int32_t* cols = h + h[H_COLS];
     auto gidx = [&](int32_t ro) {
       int64_t g = Fd.gstart + ro;
       if (g >= Fd.gmod) g -= Fd.gmod;
       return g;
     };
     double* x = xy + Fd.xy_off;
-    if (h[H_BIG]) {
-      const int32_t* R = recs;
-      const int32_t s = R[R_S], m = R[R_M];
-      const int32_t* rows = h + R[R_ROWS];
-      const double* M = vals + R[R_VAL];
-      scratch.assign(s + m, 0.0);
-      double* f = scratch.data();
-      if (fwd) {
-        for (int32_t c = 0; c < s; ++c) f[c] = rhs[gidx(cols[c])];
-        for (int32_t q = 0; q < R[R_NCH]; ++q) {
-          const int32_t* cr = h + R[R_CH] + CH_WORDS * q;
-          const int32_t* rel = h + cr[2];
-          for (int32_t a = 0; a < cr[1]; ++a) f[rel[a]] += upd[cr[0] + a];
+    if (T.kind == TK_ROW_FWD || T.kind == TK_COL_BWD) {
+      const bool row = T.kind == TK_ROW_FWD;
+      const int32_t s = h[row ? RW_S : CL_S], m = h[row ? RW_M : CL_M];
+      const int32_t* am = reinterpret_cast<const int32_t*>(P.blobs.data() + 16 * (int64_t)h[row ? RW_ASM16 : CL_ASM16]);
+      const int32_t* cols = am;
+      const int32_t* rows = am + s;
+      const int32_t* ptr = rows + m;
+      const int32_t* src = ptr + s + m + 1;
+      if (row) {
+        const double* V = reinterpret_cast<const double*>(blob + h[RW_VAL_OFF]);
+        const int32_t R = h[RW_R], C = h[RW_C], r0 = h[RW_R0], NB = h[RW_NB];
+        scratch.assign(C + NB, 0.0);
+        double* S = scratch.data();
+        for (int32_t q = 0; q < C + NB; ++q) {
+          const int32_t p = q < C ? q : r0 + (q - C);
+          double acc = q < C ? rhs[gidx(cols[q])] : 0.0;
+          for (int32_t e = ptr[p]; e < ptr[p + 1]; ++e) acc += upd[src[e]];
+          S[q] = acc;
         }
-        for (int32_t i = 0; i < s + m; ++i) {
+        for (int32_t i = 0; i < R; ++i) {
           double acc = 0.0;
-          const int32_t kmax = i < s ? i : s - 1;
-          for (int32_t k = 0; k <= kmax; ++k) acc += M[packed_col_off(s, m, k) + (i - k)] * f[k];
-          if (i < s)
-            x[cols[i]] = acc;
-          else if (h[H_TOP_UPD] >= 0)
-            upd[h[H_TOP_UPD] + i - s] = f[i] - acc;
-        }
-      } else {
-        for (int32_t c = 0; c < s; ++c) f[c] = x[cols[c]];
-        for (int32_t a = 0; a < m; ++a) f[s + a] = -x[rows[a]];
-        for (int32_t k = 0; k < s; ++k) {
-          double acc = 0.0;
-          const double* col = M + packed_col_off(s, m, k);
-          for (int32_t i = k; i < s + m; ++i) acc += col[i - k] * f[i];
-          x[cols[k]] = acc;
-        }
-      }
-      continue;
-    }
-    scratch.assign(h[H_SCRATCH], 0.0);
-    double* S = scratch.data();
-    const int32_t ncol = h[H_NCOL];
-    const int32_t* colpos = h + h[H_COLPOS];
-    const int32_t nlev = h[H_NLEV];
-    const int32_t* levtab = h + h[H_LEVELS];
-    const int32_t* runs = h + h[H_RUNS];
-    const int32_t* gp = h + h[H_GPAIRS];
-    const int32_t* bp = h + h[H_BPAIRS];
-    const int32_t* items = h + h[H_ITEMS];
-    // rows handled by a warp item, in lane order (for the checks below)
-    auto item_rows = [&](int32_t x0, int32_t y, bool forward, auto&& fn) {
-      const int32_t cnt = x0 >> 16;
-      if (cnt > 0) {
-        x0 &= 0xffff;
-        uint32_t mask = 0;
-        int32_t rows = 0;
-        for (int32_t j = x0; j < x0 + cnt; ++j) {
-          mask |= 1u << rows;
-          rows += recs[R_WORDS * j + R_S] + recs[R_WORDS * j + R_M];
-        }
-        if (rows < 32) mask |= 1u << rows;
-        SFCDD_REQUIRE(rows <= 32 && mask == (uint32_t)y, SFCDD_EINTERNAL, "packed item lane mask mismatch");
-        for (int32_t j = x0; j < x0 + cnt; ++j) {
-          const int32_t* R = recs + R_WORDS * j;
-          if (forward)
-            for (int32_t i = 0; i < R[R_S] + R[R_M]; ++i) fn(R, i);
+          for (int32_t k = 0; k < C; ++k) acc += V[(size_t)k * R + i] * S[k];
+          const int32_t rw = r0 + i;
+          if (rw < s)
+            upd[h[RW_YOFF] + rw] = acc;
           else
-            for (int32_t k = 0; k < R[R_S]; ++k) fn(R, k);
+            upd[h[RW_UOFF] + rw - s] = S[C + i] - acc;
         }
       } else {
-        const int32_t* R = recs + R_WORDS * x0;
-        if (forward)
-          for (int32_t i = 32 * y; i < std::min(32 * y + 32, R[R_S] + R[R_M]); ++i) fn(R, i);
-        else
-          fn(R, y);
-      }
-    };
-    if (fwd) {
-      for (int32_t c = 0; c < ncol; ++c) S[lo16(colpos[c])] = rhs[gidx(cols[c])];
-      const int32_t* eu = h + h[H_EXTU];
-      for (int32_t e = 0; e < h[H_NEXTU]; ++e) S[h[H_EXTU_BASE] + e] = upd[eu[e]];
-      for (int32_t l = 0; l < nlev; ++l) {
-        const int32_t* L = levtab + L_WORDS * l;
-        for (int32_t r = L[L_RUN0]; r < L[L_RUN1]; ++r) {
-          const int32_t dst = lo16(gp[runs[r]]);
-          double acc = S[dst];
-          for (int32_t p = runs[r]; p < runs[r + 1]; ++p) acc += S[hi16(gp[p])];
-          S[dst] = acc;
+        const double* V = reinterpret_cast<const double*>(blob + h[CL_VAL_OFF]);
+        const int32_t k0 = h[CL_K0], k1 = h[CL_K1];
+        scratch.assign(s - k0 + m, 0.0);
+        double* v = scratch.data();
+        for (int32_t i = k0; i < s; ++i) v[i - k0] = upd[h[CL_YOFF] + i];
+        for (int32_t a = 0; a < m; ++a) v[s - k0 + a] = -x[rows[a]];
+        int64_t off = 0;
+        for (int32_t k = k0; k < k1; ++k) {
+          const int32_t len = s + m - k;
+          double acc = 0.0;
+          for (int32_t q = 0; q < len; ++q) acc += V[off + q] * v[k - k0 + q];
+          x[cols[k]] = acc;
+          off += len;
         }
-        for (int32_t it = L[L_FW]; it < L[L_FW + NWARP_PLAN]; ++it)
-          item_rows(items[2 * it], items[2 * it + 1], true, [&](const int32_t* R, int32_t i) {
-            const int32_t s = R[R_S], m = R[R_M];
-            const double* M = vals + R[R_VAL];
-            double* f = S + R[R_SCR];
-            double acc = 0.0;
-            const int32_t kmax = i < s ? i : s - 1;
-            for (int32_t k = 0; k <= kmax; ++k) acc += M[packed_col_off(s, m, k) + (i - k)] * f[k];
-            if (i < s)
-              S[R[R_CPOS] + i] = acc;
-            else
-              f[i] -= acc;
-          });
-      }
-      for (int32_t c = 0; c < ncol; ++c) x[cols[c]] = S[hi16(colpos[c])];
-      if (h[H_TOP_UPD] >= 0) {
-        const int32_t* R = recs + R_WORDS * h[H_TOP];
-        for (int32_t a = 0; a < R[R_M]; ++a) upd[h[H_TOP_UPD] + a] = S[R[R_SCR] + R[R_S] + a];
       }
     } else {
-      for (int32_t c = 0; c < ncol; ++c) S[lo16(colpos[c])] = x[cols[c]];
-      const int32_t* ex = h + h[H_EXTX];
-      for (int32_t e = 0; e < h[H_NEXTX]; ++e) S[h[H_EXTX_BASE] + e] = x[ex[e]];
-      for (int32_t l = nlev - 1; l >= 0; --l) {
-        const int32_t* L = levtab + L_WORDS * l;
-        for (int32_t p = L[L_BP0]; p < L[L_BP1]; ++p) S[lo16(bp[p])] = -S[hi16(bp[p])];
-        for (int32_t it = L[L_BW]; it < L[L_BW + NWARP_PLAN]; ++it)
-          item_rows(items[2 * it], items[2 * it + 1], false, [&](const int32_t* R, int32_t k) {
-            const int32_t s = R[R_S], m = R[R_M];
-            const double* col = vals + R[R_VAL] + packed_col_off(s, m, k);
-            const double* v = S + R[R_SCR];
-            double acc = 0.0;
-            for (int32_t i = k; i < s + m; ++i) acc += col[i - k] * v[i];
-            S[R[R_CPOS] + k] = acc;
-          });
+      const bool fwd = T.kind == TK_FRAG_FWD;
+      const double* vals = reinterpret_cast<const double*>(blob + h[H_VAL_OFF]);
+      const int32_t* recs = h + h[H_REC];
+      const int32_t* cols = h + h[H_COLS];
+      scratch.assign(h[H_SCRATCH], 0.0);
+      double* S = scratch.data();
+      const int32_t ncol = h[H_NCOL];
+      const int32_t* colpos = h + h[H_COLPOS];
+      const int32_t nlev = h[H_NLEV];
+      const int32_t* levtab = h + h[H_LEVELS];
+      const int32_t* runs = h + h[H_RUNS];
+      const int32_t* gp = h + h[H_GPAIRS];
+      const int32_t* bp = h + h[H_BPAIRS];
+      const int32_t* items = h + h[H_ITEMS];
+      // rows handled by a warp item, in lane order (also checks the lane masks)
+      auto item_rows = [&](int32_t x0, int32_t y, bool forward, auto&& fn) {
+        const int32_t cnt = x0 >> 16;
+        if (cnt > 0) {
+          x0 &= 0xffff;
+          uint32_t mask = 0;
+          int32_t rows = 0;
+          for (int32_t j = x0; j < x0 + cnt; ++j) {
+            mask |= 1u << rows;
+            rows += recs[R_WORDS * j + R_S] + recs[R_WORDS * j + R_M];
+          }
+          if (rows < 32) mask |= 1u << rows;
+          SFCDD_REQUIRE(rows <= 32 && mask == (uint32_t)y, SFCDD_EINTERNAL, "packed item lane mask mismatch");
+          for (int32_t j = x0; j < x0 + cnt; ++j) {
+            const int32_t* R = recs + R_WORDS * j;
+            if (forward)
+              for (int32_t i = 0; i < R[R_S] + R[R_M]; ++i) fn(R, i);
+            else
+              for (int32_t k = 0; k < R[R_S]; ++k) fn(R, k);
+          }
+        } else {
+          const int32_t* R = recs + R_WORDS * x0;
+          if (forward)
+            for (int32_t i = 32 * y; i < std::min(32 * y + 32, R[R_S] + R[R_M]); ++i) fn(R, i);
+          else
+            fn(R, y);
+        }
+      };
+      if (fwd) {
+        for (int32_t c = 0; c < ncol; ++c) S[lo16(colpos[c])] = rhs[gidx(cols[c])];
+        const int32_t* eu = h + h[H_EXTU];
+        for (int32_t e = 0; e < h[H_NEXTU]; ++e) S[h[H_EXTU_BASE] + e] = upd[eu[e]];
+        for (int32_t l = 0; l < nlev; ++l) {
+          const int32_t* L = levtab + L_WORDS * l;
+          for (int32_t r = L[L_RUN0]; r < L[L_RUN1]; ++r) {
+            const int32_t dst = lo16(gp[runs[r]]);
+            double acc = S[dst];
+            for (int32_t p = runs[r]; p < runs[r + 1]; ++p) acc += S[hi16(gp[p])];
+            S[dst] = acc;
+          }
+          for (int32_t it = L[L_FI0]; it < L[L_FI1]; ++it)
+            item_rows(items[2 * it], items[2 * it + 1], true, [&](const int32_t* R, int32_t i) {
+              const int32_t s = R[R_S], m = R[R_M];
+              const double* M = vals + R[R_VAL];
+              double* f = S + R[R_SCR];
+              double acc = 0.0;
+              const int32_t kmax = i < s ? i : s - 1;
+              for (int32_t k = 0; k <= kmax; ++k) acc += M[packed_col_off(s, m, k) + (i - k)] * f[k];
+              if (i < s)
+                S[R[R_CPOS] + i] = acc;
+              else
+                f[i] -= acc;
+            });
+        }
+        for (int32_t c = 0; c < ncol; ++c) x[cols[c]] = S[hi16(colpos[c])];
+        if (h[H_TOP_UPD] >= 0) {
+          const int32_t* R = recs + R_WORDS * h[H_TOP];
+          for (int32_t a = 0; a < R[R_M]; ++a) upd[h[H_TOP_UPD] + a] = S[R[R_SCR] + R[R_S] + a];
+        }
+      } else {
+        for (int32_t c = 0; c < ncol; ++c) S[lo16(colpos[c])] = x[cols[c]];
+        const int32_t* ex = h + h[H_EXTX];
+        for (int32_t e = 0; e < h[H_NEXTX]; ++e) S[h[H_EXTX_BASE] + e] = x[ex[e]];
+        for (int32_t l = nlev - 1; l >= 0; --l) {
+          const int32_t* L = levtab + L_WORDS * l;
+          for (int32_t p = L[L_BP0]; p < L[L_BP1]; ++p) S[lo16(bp[p])] = -S[hi16(bp[p])];
+          for (int32_t it = L[L_BI0]; it < L[L_BI1]; ++it)
+            item_rows(items[2 * it], items[2 * it + 1], false, [&](const int32_t* R, int32_t k) {
+              const int32_t s = R[R_S], m = R[R_M];
+              const double* col = vals + R[R_VAL] + packed_col_off(s, m, k);
+              const double* v = S + R[R_SCR];
+              double acc = 0.0;
+              for (int32_t i = k; i < s + m; ++i) acc += col[i - k] * v[i];
+              S[R[R_CPOS] + k] = acc;
+            });
+        }
+        for (int32_t c = 0; c < ncol; ++c) x[cols[c]] = S[hi16(colpos[c])];
       }
-      for (int32_t c = 0; c < ncol; ++c) x[cols[c]] = S[hi16(colpos[c])];
     }
+    ctr[T.signal_idx] += 1;
   }
 }
 
