@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.h"
@@ -31,7 +32,6 @@ namespace sfcdd {
 
 namespace {
 
-constexpr int WPB = 4;  // worker warps per CTA (independent; share nothing but the SM)
 constexpr unsigned FULL = 0xffffffffu;
 
 struct DagArgs {
@@ -47,6 +47,8 @@ struct DagArgs {
   int32_t* ctr;  // [0] queue head | per group: fin, bdone, rdone (plan.h)
   const int32_t* skip;  // optional: nonzero -> whole solve skipped (PCG done)
   unsigned long long* trace;  // optional: per task {sm, t_top, t_deps, t_data, t_end} (ns)
+  unsigned long long* ptrace;  // optional: per task 16 clock64 stamps (FRAG phases)
+  int32_t mode;  // tuning switches (SFCDD_DAG_MODE): 1 = acquire polling, 2 = fence before signal
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -102,6 +104,12 @@ __device__ __forceinline__ void fence_proxy_async() {
 __device__ __forceinline__ int32_t ld_acquire(const int32_t* p) {
   int32_t v;
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ int32_t ld_relaxed(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 
@@ -232,7 +240,10 @@ __device__ __forceinline__ void bwd_packed(const int32_t* recs, const double* va
 }
 
 __device__ __forceinline__ void run_frag(const int32_t* h, bool fwd, double* S, const DagArgs& A, const FactorDev& F,
-                                         int lane) {
+                                         int lane, unsigned long long* pt) {
+  auto stamp = [&](int i) {
+    if (pt && lane == 0 && i < 15) pt[i] = clock64();
+  };
   const double* vals = reinterpret_cast<const double*>(reinterpret_cast<const uint8_t*>(h) + h[H_VAL_OFF]);
   const int nlev = h[H_NLEV];
   const int32_t* levtab = h + h[H_LEVELS];
@@ -246,6 +257,7 @@ __device__ __forceinline__ void run_frag(const int32_t* h, bool fwd, double* S, 
   const int ncol = h[H_NCOL];
   double* xy = A.xy + F.xy_off;
   if (fwd) {
+    stamp(0);
     const int nscr = h[H_SCRATCH];
     for (int i = lane; i < nscr; i += 32) S[i] = 0.0;
     __syncwarp();
@@ -258,12 +270,14 @@ __device__ __forceinline__ void run_frag(const int32_t* h, bool fwd, double* S, 
           [&](int c, double v) { S[c < ncol ? lo16(colpos[c]) : ub + (c - ncol)] = v; });
     }
     __syncwarp();
+    stamp(1);
     for (int lv = 0; lv < nlev; ++lv) {
       const int32_t* L = levtab + L_WORDS * lv;
       if (L[L_RUN1] > L[L_RUN0]) {  // multifrontal assembly, gather form
         gather_runs(runs, gp, L[L_RUN0], L[L_RUN1], S, lane);
         __syncwarp();
       }
+      if (lv < 6) stamp(2 + 2 * lv);
       for (int it = L[L_FI0]; it < L[L_FI1]; ++it) {  // rows of the level's supernodes
         const int2 item = items[it];
         const int cnt = item.x >> 16;
@@ -276,6 +290,7 @@ __device__ __forceinline__ void run_frag(const int32_t* h, bool fwd, double* S, 
         }
       }
       __syncwarp();
+      if (lv < 6) stamp(3 + 2 * lv);
     }
     for (int c = lane; c < ncol; c += 32) __stcg(xy + cols[c], S[hi16(colpos[c])]);
     if (h[H_TOP_UPD] >= 0) {
@@ -283,6 +298,8 @@ __device__ __forceinline__ void run_frag(const int32_t* h, bool fwd, double* S, 
       const double* u = S + R[R_SCR] + R[R_S];
       for (int a = lane; a < R[R_M]; a += 32) __stcg(A.upd + h[H_TOP_UPD] + a, u[a]);
     }
+    stamp(14);
+    if (pt && lane == 0) pt[15] = nlev;
   } else {
     {  // one batched gather: y at the columns + x of the external ancestor rows
       const int32_t* ex = h + h[H_EXTX];
@@ -404,6 +421,7 @@ __device__ __forceinline__ void run_col(const int32_t* h, double* S, const DagAr
 }
 
 // ================================================================ kernel
+template <int WPB>
 __global__ void __launch_bounds__(WPB * 32) k_dag(DagArgs A) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bars[WPB];
@@ -437,10 +455,19 @@ __global__ void __launch_bounds__(WPB * 32) k_dag(DagArgs A) {
       mbar_expect_tx(bar, (uint32_t)T.copy_bytes);
       bulk_g2s(smem + (size_t)warp * A.slot_bytes, A.blobs + T.blob_off, (uint32_t)T.copy_bytes, bar);
       if (T.wait_idx >= 0) {
+        // relaxed polling (no L1 invalidation per poll), one acquire at the end
         unsigned ns = 32;
-        while (ld_acquire(A.ctr + T.wait_idx) < T.wait_target) {
-          __nanosleep(ns);
-          ns = ns < 256 ? 2 * ns : 256;
+        if (A.mode & 1) {
+          while (ld_acquire(A.ctr + T.wait_idx) < T.wait_target) {
+            __nanosleep(ns);
+            ns = ns < 256 ? 2 * ns : 256;
+          }
+        } else {
+          while (ld_relaxed(A.ctr + T.wait_idx) < T.wait_target) {
+            __nanosleep(ns);
+            ns = ns < 256 ? 2 * ns : 256;
+          }
+          (void)ld_acquire(A.ctr + T.wait_idx);
         }
       }
       if (tr) tr[2] = gtimer();
@@ -452,10 +479,10 @@ __global__ void __launch_bounds__(WPB * 32) k_dag(DagArgs A) {
     const FactorDev F = A.factors[T.factor];
     switch (T.kind) {
       case TK_FRAG_FWD:
-        run_frag(h, true, S, A, F, lane);
+        run_frag(h, true, S, A, F, lane, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr);
         break;
       case TK_FRAG_BWD:
-        run_frag(h, false, S, A, F, lane);
+        run_frag(h, false, S, A, F, lane, nullptr);
         break;
       case TK_ROW_FWD:
         run_row(h, S, A, F, lane);
@@ -466,7 +493,8 @@ __global__ void __launch_bounds__(WPB * 32) k_dag(DagArgs A) {
     }
     __syncwarp();
     if (lane == 0) {
-      __threadfence();  // cumulative over the warp's writes (ordered by __syncwarp)
+      // release: cumulative over the warp's writes (ordered before it by __syncwarp)
+      if (A.mode & 2) __threadfence();
       red_release_add(A.ctr + T.signal_idx, 1);
       if (tr) tr[4] = gtimer();
     }
@@ -484,7 +512,13 @@ DagSolver::DagSolver(const DevicePlan& plan, int device, int64_t extra_xy) : dev
   host_tasks = plan.tasks;
   blob_max_ = round128(plan.blob_max);
   slot_bytes_ = blob_max_ + round128(8 * (int64_t)std::max(plan.max_scratch, 16));
-  smem_ = WPB * slot_bytes_;
+  // worker warps per CTA (2, 4 or 8; SFCDD_WPB overrides the default 4)
+  wpb_ = 4;
+  if (const char* e = std::getenv("SFCDD_WPB")) wpb_ = std::atoi(e);
+  SFCDD_REQUIRE(wpb_ == 2 || wpb_ == 4 || wpb_ == 8, SFCDD_EVALUE, "SFCDD_WPB must be 2, 4 or 8");
+  kern_ = wpb_ == 2 ? (const void*)k_dag<2> : wpb_ == 4 ? (const void*)k_dag<4> : (const void*)k_dag<8>;
+  if (const char* e = std::getenv("SFCDD_DAG_MODE")) mode_ = std::atoi(e);
+  smem_ = wpb_ * slot_bytes_;
   SFCDD_REQUIRE(smem_ <= 227 * 1024, SFCDD_EINTERNAL, "DAG shared-memory footprint exceeds 227 KB");
   auto up = [&](void** dst, const void* src, size_t bytes) {
     CUDA_CHECK(cudaMalloc(dst, std::max<size_t>(bytes, 16)));
@@ -504,18 +538,18 @@ DagSolver::DagSolver(const DevicePlan& plan, int device, int64_t extra_xy) : dev
     // the attribute is per function: only ever raise it, so every live
     // solver (several handles per process in shard emulation) can launch
     static std::mutex mu;
-    static int max_smem = 0;
+    static int max_smem[9] = {0};
     std::lock_guard<std::mutex> g(mu);
-    if (smem_ > max_smem) {
-      CUDA_CHECK(cudaFuncSetAttribute(k_dag, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
-      max_smem = smem_;
+    if (smem_ > max_smem[wpb_]) {
+      CUDA_CHECK(cudaFuncSetAttribute(kern_, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
+      max_smem[wpb_] = smem_;
     }
   }
   int per_sm = 0, sms = 0;
-  CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dag, WPB * 32, smem_));
+  CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern_, wpb_ * 32, smem_));
   CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   SFCDD_REQUIRE(per_sm >= 1, SFCDD_EINTERNAL, "DAG kernel cannot be resident");
-  grid_ = std::max(1, std::min(per_sm * sms, (ntask_ + WPB - 1) / WPB));
+  grid_ = std::max(1, std::min(per_sm * sms, (ntask_ + wpb_ - 1) / wpb_));
 }
 
 DagSolver::~DagSolver() {
@@ -543,8 +577,10 @@ void DagSolver::solve(const double* rhs, cudaStream_t st, const int32_t* skip) {
   a.ctr = ctr_;
   a.skip = skip;
   a.trace = trace_;
-  k_dag<<<grid_, WPB * 32, smem_, st>>>(a);
-  CUDA_CHECK(cudaGetLastError());
+  a.ptrace = trace_ ? trace_ + 5 * (size_t)ntask_ : nullptr;
+  a.mode = mode_;
+  void* params[] = {&a};
+  CUDA_CHECK(cudaLaunchKernel(kern_, dim3(grid_), dim3(wpb_ * 32), params, smem_, st));
 }
 
 void DagSolver::set_trace(unsigned long long* dev_buf) { trace_ = dev_buf; }

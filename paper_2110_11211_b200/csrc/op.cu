@@ -978,15 +978,15 @@ extern "C" int sfcdd_op_trace(sfcdd_op* op, const double* g_dev, uint64_t* out_h
   if (!out_host) return SFCDD_OK;
   CUDA_CHECK(cudaSetDevice(op->device));
   unsigned long long* buf = nullptr;
-  CUDA_CHECK(cudaMalloc(&buf, nt * 5 * 8));
-  CUDA_CHECK(cudaMemset(buf, 0, nt * 5 * 8));
+  CUDA_CHECK(cudaMalloc(&buf, nt * 21 * 8));
+  CUDA_CHECK(cudaMemset(buf, 0, nt * 21 * 8));
   op->dag->solve(g_dev, nullptr);  // warm
   op->dag->set_trace(buf);
   op->dag->solve(g_dev, nullptr);
   op->dag->set_trace(nullptr);
   CUDA_CHECK(cudaDeviceSynchronize());
-  std::vector<unsigned long long> h(nt * 5);
-  CUDA_CHECK(cudaMemcpy(h.data(), buf, nt * 5 * 8, cudaMemcpyDeviceToHost));
+  std::vector<unsigned long long> h(nt * 21);
+  CUDA_CHECK(cudaMemcpy(h.data(), buf, nt * 21 * 8, cudaMemcpyDeviceToHost));
   CUDA_CHECK(cudaFree(buf));
   for (int64_t t = 0; t < nt; ++t) {
     const TaskDev& T = op->dag->host_tasks[t];
@@ -999,6 +999,10 @@ extern "C" int sfcdd_op_trace(sfcdd_op* op, const double* g_dev, uint64_t* out_h
     out_host[24 * t + 10] = (uint64_t)T.wait_target;
     out_host[24 * t + 11] = (uint64_t)T.signal_idx;
     for (int j = 12; j < 24; ++j) out_host[24 * t + j] = 0;
+    // FRAG forward phase stamps (clock64): [0] start [1] prologue done
+    // [2+2l, 3+2l] level l assembly / rows done (l < 4) [10] end [11] nlev
+    if (T.kind == TK_FRAG_FWD)
+      for (int j = 0; j < 12; ++j) out_host[24 * t + 12 + j] = h[5 * nt + 16 * t + (j < 10 ? j : j + 4)];
   }
   SFCDD_API_END
 }

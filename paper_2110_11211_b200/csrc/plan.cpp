@@ -64,6 +64,7 @@ inline int64_t blob_size(int64_t ints, int64_t vals) { return align16(4 * ints) 
 PlanOptions::PlanOptions() {
   if (const char* e = std::getenv("SFCDD_BLOB_MAX")) blob_max = std::atoi(e);
   if (const char* e = std::getenv("SFCDD_SCRATCH_MAX")) scratch_max = std::atoi(e);
+  if (const char* e = std::getenv("SFCDD_WORKERS")) workers = std::atoi(e);
 }
 
 DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::vector<int64_t>& gstart,
@@ -287,7 +288,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         int32_t bytes = 0;
         const int64_t off = emit_blob(P, ints, RW_VAL_OFF, vals, bytes);
         P.max_scratch = std::max<int32_t>(P.max_scratch, C + NB);
-        add_task(g, TK_ROW_FWD, off, bytes, (int64_t)R * C, 1.5 + (double)R * C / 1500.0);
+        add_task(g, TK_ROW_FWD, off, bytes, (int64_t)R * C, 2.5 + 0.0045 * R * C);
         r0 += R;
       }
       // backward: column blocks
@@ -314,7 +315,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         int32_t bytes = 0;
         const int64_t off = emit_blob(P, ints, CL_VAL_OFF, vals, bytes);
         P.max_scratch = std::max<int32_t>(P.max_scratch, s - k0 + m);
-        add_task(g, TK_COL_BWD, off, bytes, nv, 1.5 + (double)nv / 1500.0);
+        add_task(g, TK_COL_BWD, off, bytes, nv, 3.5 + 0.0049 * nv);
         k0 = k1;
       }
       continue;
@@ -503,9 +504,9 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
     const int64_t off = emit_blob(P, ints, H_VAL_OFF, vals, bytes);
     SFCDD_REQUIRE(bytes <= opt.blob_max, SFCDD_EINTERNAL, "fragment blob exceeds the slot budget");
     P.max_scratch = std::max(P.max_scratch, scratch_used);
-    const double w = 1.5 + 0.3 * nlev + (double)nvals / 1500.0;
-    add_task(g, TK_FRAG_FWD, off, bytes, nvals, w);
-    add_task(g, TK_FRAG_BWD, off, bytes, nvals, w);
+    // task time model (us), fitted to traced C2 launches (tools/trace_dag.py)
+    add_task(g, TK_FRAG_FWD, off, bytes, nvals, 2.1 + 0.0035 * nvals + 0.76 * nlev);
+    add_task(g, TK_FRAG_BWD, off, bytes, nvals, 2.5 + 0.0086 * nvals + 0.8 * nlev);
   }
 
   // ---- 3. dependencies
@@ -553,9 +554,58 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
     const bool fwd = tl[t].kind == TK_FRAG_FWD || tl[t].kind == TK_ROW_FWD;
     rank[t] = tw[t] + (fwd ? succ_f[g] : succ_b[g]);
   }
-  std::vector<int32_t> order(tl.size());
-  std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return rank[a] > rank[b]; });
+  // queue = start order of a simulated list schedule on opt.workers warps:
+  // whenever a warp is free it takes the highest-rank READY task.  At run
+  // time warps dequeue in this order, so a task is (nearly) ready when it is
+  // dequeued instead of pinning a warp while it waits.
+  std::vector<int32_t> order;
+  order.reserve(tl.size());
+  {
+    const int32_t nctr = 1 + 3 * G;
+    std::vector<int32_t> ctr(nctr, 0);
+    std::vector<std::vector<int32_t>> waiters(nctr);
+    auto cmp_rank = [&](int32_t a, int32_t b) { return rank[a] < rank[b] || (rank[a] == rank[b] && a > b); };
+    std::vector<int32_t> ready;  // max-heap by rank
+    for (size_t t = 0; t < tl.size(); ++t) {
+      if (tl[t].wait_idx < 0) {
+        ready.push_back((int32_t)t);
+      } else {
+        waiters[tl[t].wait_idx].push_back((int32_t)t);
+      }
+    }
+    std::make_heap(ready.begin(), ready.end(), cmp_rank);
+    using Ev = std::pair<double, int32_t>;
+    std::vector<Ev> ev;  // min-heap of (end time, task)
+    auto ev_cmp = [](const Ev& a, const Ev& b) { return a.first > b.first; };
+    int64_t free_w = std::max(1, opt.workers);
+    double now = 0.0;
+    while (order.size() < tl.size()) {
+      while (free_w > 0 && !ready.empty()) {
+        std::pop_heap(ready.begin(), ready.end(), cmp_rank);
+        const int32_t t = ready.back();
+        ready.pop_back();
+        order.push_back(t);
+        --free_w;
+        ev.emplace_back(now + tw[t], t);
+        std::push_heap(ev.begin(), ev.end(), ev_cmp);
+      }
+      if (order.size() == tl.size()) break;
+      SFCDD_REQUIRE(!ev.empty(), SFCDD_EINTERNAL, "task graph has a cycle");
+      std::pop_heap(ev.begin(), ev.end(), ev_cmp);
+      const Ev e = ev.back();
+      ev.pop_back();
+      now = e.first;
+      ++free_w;
+      const int32_t c = tl[e.second].signal_idx;
+      ++ctr[c];
+      for (int32_t w : waiters[c])
+        if (ctr[c] == tl[w].wait_target) {
+          ready.push_back(w);
+          std::push_heap(ready.begin(), ready.end(), cmp_rank);
+        }
+    }
+    P.sim_us = now;
+  }
   P.tasks.resize(tl.size());
   for (size_t t = 0; t < order.size(); ++t) P.tasks[t] = tl[order[t]];
 
@@ -578,11 +628,12 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
     for (const Group& gr : groups) maxh = std::max(maxh, gr.height);
     std::fprintf(stderr,
                  "[plan] groups=%d frag=%d big=%d (%.1f%% of values; %lld row + %lld col tasks) frag avg: %.1f "
-                 "supernodes, %.1f levels, %.1f values; max group height %d; blobs %.1f MB; max scratch %d\n",
+                 "supernodes, %.1f levels, %.1f values; max group height %d; blobs %.1f MB; max scratch %d; "
+                 "simulated schedule %.1f us on %d warps\n",
                  G, P.nfrag, P.nbig, 100.0 * big_vals / std::max<int64_t>(1, big_vals + small_vals),
                  (long long)nrow, (long long)ncol, (double)sn_sum / std::max(1, P.nfrag),
                  (double)lev_sum / std::max(1, P.nfrag), (double)small_vals / std::max(1, P.nfrag), maxh,
-                 P.blobs.size() / 1e6, P.max_scratch);
+                 P.blobs.size() / 1e6, P.max_scratch, P.sim_us, opt.workers);
   }
   return P;
 }

@@ -136,9 +136,10 @@ enum ColHdr {
 constexpr int SMALL_MAX_S = 64;  // wider supernodes are always BIG
 
 struct PlanOptions {
-  int32_t blob_max = 12 * 1024;  // bytes of a task blob (slot blob area)
-  int32_t scratch_max = 768;     // doubles of FRAG scratch (< 65536)
+  int32_t blob_max = 8 * 1024;   // bytes of a task blob (slot blob area)
+  int32_t scratch_max = 512;     // doubles of FRAG scratch (< 65536)
   int32_t big_scratch_max = 8192;  // doubles of scratch a BIG task may use
+  int32_t workers = 148 * 16;      // warps assumed by the queue-order simulation (SFCDD_WORKERS)
   PlanOptions();                 // environment overrides SFCDD_BLOB_MAX, SFCDD_SCRATCH_MAX
 };
 
@@ -156,6 +157,7 @@ struct DevicePlan {
   int32_t max_scratch = 0;  // doubles, over all tasks
   int32_t max_copy = 0;     // bytes
   int32_t blob_max = 0;
+  double sim_us = 0.0;  // makespan of the simulated schedule (model time)
 };
 
 DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::vector<int64_t>& gstart,
