@@ -15,7 +15,8 @@ from pathlib import Path
 
 import numpy as np
 
-_LIB_PATH = Path(__file__).resolve().parent / "libsfcdd_b200.so"
+# SFCDD_LIB: alternative build of the same library (A/B timing of kernel variants)
+_LIB_PATH = Path(os.environ.get("SFCDD_LIB") or Path(__file__).resolve().parent / "libsfcdd_b200.so")
 
 SFCDD_OK = 0
 SFCDD_EVALUE = -1
