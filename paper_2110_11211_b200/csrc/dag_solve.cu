@@ -44,7 +44,9 @@ struct DagArgs {
   const double* rhs;
   double* xy;
   double* upd;
-  int32_t* ctr;  // [0] queue head | per group: fin, bdone, rdone (plan.h)
+  int32_t* ctr;  // [0] unused | per group: fin, bdone, rdone (plan.h)
+  int32_t* qhead;  // nq queue heads, one per 128-byte line: queue j holds tasks j, j+nq, ...
+  int32_t nq;
   const int32_t* skip;  // optional: nonzero -> whole solve skipped (PCG done)
   unsigned long long* trace;  // optional: per task {sm, t_top, t_deps, t_data, t_end} (ns)
   unsigned long long* ptrace;  // optional: per task 16 clock64 stamps (FRAG phases)
@@ -153,15 +155,51 @@ __device__ __forceinline__ void warp_gather(int n, int lane, Load ld, Store st) 
   }
 }
 
-// gather-form assembly runs: S[dst] += sum S[src] over the run (fixed order)
+// one gather-form assembly run with its first contributions' loads issued
+// together: S[dst] + S[src_0] + S[src_1] + ... (fixed order)
+struct RunLoad {
+  int dst, p, p1;
+  double acc, v0, v1, v2;
+};
+__device__ __forceinline__ RunLoad run_load(const int32_t* runs, const int32_t* gp, int r, const double* S) {
+  RunLoad L;
+  const int p0 = runs[r];
+  L.p1 = runs[r + 1];
+  const int n = L.p1 - p0;
+  const int32_t g0 = gp[p0];
+  const int32_t g1 = n > 1 ? gp[p0 + 1] : g0;
+  const int32_t g2 = n > 2 ? gp[p0 + 2] : g0;
+  L.dst = lo16(g0);
+  L.acc = S[L.dst];
+  L.v0 = S[hi16(g0)];
+  L.v1 = n > 1 ? S[hi16(g1)] : 0.0;
+  L.v2 = n > 2 ? S[hi16(g2)] : 0.0;
+  L.p = p0 + 3;
+  return L;
+}
+__device__ __forceinline__ void run_finish(RunLoad& L, const int32_t* gp, double* S) {
+  const int n = L.p1 - (L.p - 3);
+  double acc = L.acc + L.v0;
+  if (n > 1) acc += L.v1;
+  if (n > 2) acc += L.v2;
+  for (int p = L.p; p < L.p1; ++p) acc += S[hi16(gp[p])];
+  S[L.dst] = acc;
+}
+
+// gather-form assembly runs: S[dst] += sum S[src] over the run (fixed order);
+// two runs per lane in flight
 __device__ __forceinline__ void gather_runs(const int32_t* runs, const int32_t* gp, int r0, int r1, double* S,
                                             int lane) {
-  for (int r = r0 + lane; r < r1; r += 32) {
-    const int p0 = runs[r], p1 = runs[r + 1];
-    const int dst = lo16(gp[p0]);
-    double acc = S[dst];
-    for (int p = p0; p < p1; ++p) acc += S[hi16(gp[p])];
-    S[dst] = acc;
+  int r = r0 + lane;
+  for (; r + 32 < r1; r += 64) {
+    RunLoad a = run_load(runs, gp, r, S);
+    RunLoad b = run_load(runs, gp, r + 32, S);
+    run_finish(a, gp, S);
+    run_finish(b, gp, S);
+  }
+  if (r < r1) {
+    RunLoad a = run_load(runs, gp, r, S);
+    run_finish(a, gp, S);
   }
 }
 
@@ -239,8 +277,9 @@ __device__ __forceinline__ void bwd_packed(const int32_t* recs, const double* va
   }
 }
 
+template <typename Ahead>
 __device__ __forceinline__ void run_frag(const int32_t* h, bool fwd, double* S, const DagArgs& A, const FactorDev& F,
-                                         int lane, unsigned long long* pt) {
+                                         int lane, unsigned long long* pt, Ahead ahead) {
   auto stamp = [&](int i) {
     if (pt && lane == 0 && i < 15) pt[i] = clock64();
   };
@@ -273,6 +312,7 @@ __device__ __forceinline__ void run_frag(const int32_t* h, bool fwd, double* S, 
     stamp(1);
     for (int lv = 0; lv < nlev; ++lv) {
       const int32_t* L = levtab + L_WORDS * lv;
+      if (lv == nlev - 1) ahead();
       if (L[L_RUN1] > L[L_RUN0]) {  // multifrontal assembly, gather form
         gather_runs(runs, gp, L[L_RUN0], L[L_RUN1], S, lane);
         __syncwarp();
@@ -310,6 +350,7 @@ __device__ __forceinline__ void run_frag(const int32_t* h, bool fwd, double* S, 
     __syncwarp();
     for (int lv = nlev - 1; lv >= 0; --lv) {
       const int32_t* L = levtab + L_WORDS * lv;
+      if (lv == 0) ahead();
       if (L[L_BP1] > L[L_BP0]) {  // v_B = -x(rows)
         for (int p = L[L_BP0] + lane; p < L[L_BP1]; p += 32) S[lo16(bp[p])] = -S[hi16(bp[p])];
         __syncwarp();
@@ -328,36 +369,46 @@ __device__ __forceinline__ void run_frag(const int32_t* h, bool fwd, double* S, 
 }
 
 // ====================================================== ROW (big forward)
-// J's assembly record (plan.h): cols[s] rows[m] ptr[s+m+1] src[nnz]
-struct AsmRec {
-  const int32_t* cols;
-  const int32_t* rows;
-  const int32_t* ptr;
-  const int32_t* src;
-};
-__device__ __forceinline__ AsmRec asm_rec(const DagArgs& A, int32_t asm16, int s, int m) {
-  AsmRec r;
-  r.cols = reinterpret_cast<const int32_t*>(A.blobs + 16 * (int64_t)asm16);
-  r.rows = r.cols + s;
-  r.ptr = r.rows + m;
-  r.src = r.ptr + s + m + 1;
-  return r;
-}
-
-// rows [r0, r0+R) of out = M f_J; lanes = (row, k-phase) for R < 32
+// rows [r0, r0+R) of out = M f_J; lanes = (row, k-phase) when R < 32
+template <typename Ahead>
 __device__ __forceinline__ void run_row(const int32_t* h, double* S, const DagArgs& A, const FactorDev& F,
-                                        int lane) {
-  const int s = h[RW_S], m = h[RW_M], R = h[RW_R], C = h[RW_C], r0 = h[RW_R0], NB = h[RW_NB];
+                                        int lane, Ahead ahead) {
+  const int s = h[RW_S], R = h[RW_R], C = h[RW_C], r0 = h[RW_R0], NB = h[RW_NB];
   const double* V = reinterpret_cast<const double*>(reinterpret_cast<const uint8_t*>(h) + h[RW_VAL_OFF]);
-  const AsmRec ar = asm_rec(A, h[RW_ASM16], s, m);
-  // f_J[0:C) and f_B of the block rows: base + child updates in fixed order
-  for (int q = lane; q < C + NB; q += 32) {
-    const int p = q < C ? q : r0 + (q - C);
-    const int e0 = __ldg(ar.ptr + p), e1 = __ldg(ar.ptr + p + 1);
-    double acc = q < C ? __ldg(A.rhs + gidx(F, __ldg(ar.cols + q))) : 0.0;
-    for (int e = e0; e < e1; ++e) acc += __ldcg(A.upd + __ldg(ar.src + e));
-    S[q] = acc;
+  const int nf = C + NB;
+  if (h[RW_ASM16] >= 0) {
+    // huge s: J's assembly record in global memory [s, m] cols ptr src
+    const int32_t* am = reinterpret_cast<const int32_t*>(A.blobs + 16 * (int64_t)h[RW_ASM16]);
+    const int32_t* cols = am + 2;
+    const int32_t* ptr = cols + s;
+    const int32_t* src = ptr + s + __ldg(am + 1) + 1;
+    for (int q = lane; q < nf; q += 32) {
+      const int p = q < C ? q : r0 + (q - C);
+      const int e0 = __ldg(ptr + p), e1 = __ldg(ptr + p + 1);
+      double acc = q < C ? __ldg(A.rhs + gidx(F, __ldg(cols + q))) : 0.0;
+      for (int e = e0; e < e1; ++e) acc += __ldcg(A.upd + __ldg(src + e));
+      S[q] = acc;
+    }
+  } else {
+    const int32_t* cols = h + h[RW_COLS];
+    const int32_t* ptr = h + h[RW_PTR];
+    const int32_t* src = h + h[RW_SRC];
+    // f = base + child updates in fixed order (base 0 for update rows); the
+    // metadata is in the slot, so every load below is one global round trip
+    for (int q = lane; q < nf; q += 32) {
+      const int e0 = ptr[q], e1 = ptr[q + 1];
+      double acc = q < C ? __ldg(A.rhs + gidx(F, cols[q])) : 0.0;
+      int e = e0;
+      for (; e + 2 <= e1; e += 2) {
+        const double u0 = __ldcg(A.upd + src[e]), u1 = __ldcg(A.upd + src[e + 1]);
+        acc += u0;
+        acc += u1;
+      }
+      if (e < e1) acc += __ldcg(A.upd + src[e]);
+      S[q] = acc;
+    }
   }
+  ahead();
   __syncwarp();
   const int RP = R >= 32 ? 32 : (R <= 1 ? 1 : 1 << (32 - __clz(R - 1)));  // lanes per phase
   const int P = 32 / RP;
@@ -389,34 +440,40 @@ __device__ __forceinline__ void run_row(const int32_t* h, double* S, const DagAr
 }
 
 // ===================================================== COL (big backward)
-// columns [k0, k1): x_k = M[:,k]^T [y_J ; -x_B]
+// columns [k0, k0+c): x_j = sum_r M[k0+r, k0+j] v[r]; lanes = (column, row-phase)
+template <typename Ahead>
 __device__ __forceinline__ void run_col(const int32_t* h, double* S, const DagArgs& A, const FactorDev& F,
-                                        int lane) {
-  const int s = h[CL_S], m = h[CL_M], k0 = h[CL_K0], k1 = h[CL_K1];
+                                        int lane, Ahead ahead) {
+  const int s = h[CL_S], m = h[CL_M], k0 = h[CL_K0], c = h[CL_C];
   const double* V = reinterpret_cast<const double*>(reinterpret_cast<const uint8_t*>(h) + h[CL_VAL_OFF]);
-  const AsmRec ar = asm_rec(A, h[CL_ASM16], s, m);
+  const int32_t* cols = h + h[CL_COLS];
+  const int32_t* rows = h + h[CL_ROWS];
   double* xy = A.xy + F.xy_off;
-  const int ny = s - k0;
+  const int ny = s - k0, L = ny + m;
   const double* yv = A.upd + h[CL_YOFF] + k0;
   warp_gather(
-      ny + m, lane, [&](int c) { return c < ny ? __ldcg(yv + c) : -__ldcg(xy + __ldg(ar.rows + c - ny)); },
-      [&](int c, double v) { S[c] = v; });
+      L, lane, [&](int q) { return q < ny ? __ldcg(yv + q) : -__ldcg(xy + rows[q - ny]); },
+      [&](int q, double v) { S[q] = v; });
+  ahead();
   __syncwarp();
-  int off = 0;
-  for (int k = k0; k < k1; ++k) {
-    const int len = s + m - k;
-    const double* col = V + off;
-    const double* v = S + (k - k0);
+  const int CP = c >= 32 ? 32 : (c <= 1 ? 1 : 1 << (32 - __clz(c - 1)));  // lanes per phase
+  const int P = 32 / CP;
+  const int j = lane & (CP - 1), ph = lane / CP;
+  for (int jb = 0; jb < c; jb += CP) {
+    const int jj = jb + j;
     double a0 = 0.0, a1 = 0.0;
-    int t = lane;
-    for (; t + 32 < len; t += 64) {
-      a0 = fma(col[t], v[t], a0);
-      a1 = fma(col[t + 32], v[t + 32], a1);
+    if (jj < c) {
+      const double* v = V + jj;
+      int r = ph;
+      for (; r + P < L; r += 2 * P) {
+        a0 = fma(v[r * c], S[r], a0);
+        a1 = fma(v[(r + P) * c], S[r + P], a1);
+      }
+      if (r < L) a0 = fma(v[r * c], S[r], a0);
     }
-    if (t < len) a0 = fma(col[t], v[t], a0);
-    const double x = warp_sum(a0 + a1);
-    if (lane == 0) __stcg(xy + __ldg(ar.cols + k), x);
-    off += len;
+    double acc = a0 + a1;
+    for (int o = CP; o < 32; o <<= 1) acc += __shfl_xor_sync(FULL, acc, o);
+    if (ph == 0 && jj < c) __stcg(xy + cols[jj], acc);
   }
 }
 
@@ -434,9 +491,17 @@ __global__ void __launch_bounds__(WPB * 32) k_dag(DagArgs A) {
   }
   __syncwarp();
   uint32_t phase = 0;
+  // queue of this warp (interleaved split of the global order: spreads the
+  // claim atomics over nq lines; deadlock-free, the smallest unfinished task
+  // is always claimable)
+  const int q = (int)((blockIdx.x * WPB + warp) % (unsigned)A.nq);
+  int32_t* qh = A.qhead + 32 * q;
+  // hook at a task's tail (claiming the next task there was measured slower:
+  // holding a claimed task for even ~1 us delays the critical path)
+  auto ahead = [&]() {};
   for (;;) {
     int t = 0;
-    if (lane == 0) t = atomicAdd(A.ctr, 1);
+    if (lane == 0) t = q + A.nq * atomicAdd(qh, 1);
     t = __shfl_sync(FULL, t, 0);
     if (t >= A.ntask) break;
     const TaskDev T = A.tasks[t];
@@ -479,16 +544,16 @@ __global__ void __launch_bounds__(WPB * 32) k_dag(DagArgs A) {
     const FactorDev F = A.factors[T.factor];
     switch (T.kind) {
       case TK_FRAG_FWD:
-        run_frag(h, true, S, A, F, lane, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr);
+        run_frag(h, true, S, A, F, lane, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);
         break;
       case TK_FRAG_BWD:
-        run_frag(h, false, S, A, F, lane, nullptr);
+        run_frag(h, false, S, A, F, lane, nullptr, ahead);
         break;
       case TK_ROW_FWD:
-        run_row(h, S, A, F, lane);
+        run_row(h, S, A, F, lane, ahead);
         break;
       default:
-        run_col(h, S, A, F, lane);
+        run_col(h, S, A, F, lane, ahead);
         break;
     }
     __syncwarp();
@@ -531,8 +596,13 @@ DagSolver::DagSolver(const DevicePlan& plan, int device, int64_t extra_xy) : dev
   CUDA_CHECK(cudaMalloc(&upd_, std::max<int64_t>(plan.upd_doubles, 2) * 8));
   CUDA_CHECK(cudaMalloc(&xy_, std::max<int64_t>(plan.xy_doubles + extra_xy, 2) * 8));
   xy_doubles_ = plan.xy_doubles + extra_xy;
-  ctr_words_ = 1 + 3 * (int64_t)ngroups_;
+  // counters (plan.h) then nq queue heads, one per 128-byte line; one memset per solve
+  nq_ = 16;
+  if (const char* e = std::getenv("SFCDD_QUEUES")) nq_ = std::max(1, std::atoi(e));
+  const int64_t cw = (1 + 3 * (int64_t)ngroups_ + 31) / 32 * 32;
+  ctr_words_ = cw + 32 * (int64_t)nq_;
   CUDA_CHECK(cudaMalloc(&ctr_, ctr_words_ * 4));
+  qhead_ = ctr_ + cw;
   bytes_ += std::max<int64_t>(plan.upd_doubles, 2) * 8 + std::max<int64_t>(xy_doubles_, 2) * 8 + ctr_words_ * 4;
   {
     // the attribute is per function: only ever raise it, so every live
@@ -549,6 +619,7 @@ DagSolver::DagSolver(const DevicePlan& plan, int device, int64_t extra_xy) : dev
   CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern_, wpb_ * 32, smem_));
   CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   SFCDD_REQUIRE(per_sm >= 1, SFCDD_EINTERNAL, "DAG kernel cannot be resident");
+  if (const char* e = std::getenv("SFCDD_CTAS_PER_SM")) per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
   grid_ = std::max(1, std::min(per_sm * sms, (ntask_ + wpb_ - 1) / wpb_));
 }
 
@@ -575,6 +646,8 @@ void DagSolver::solve(const double* rhs, cudaStream_t st, const int32_t* skip) {
   a.xy = xy_;
   a.upd = upd_;
   a.ctr = ctr_;
+  a.qhead = qhead_;
+  a.nq = nq_;
   a.skip = skip;
   a.trace = trace_;
   a.ptrace = trace_ ? trace_ + 5 * (size_t)ntask_ : nullptr;

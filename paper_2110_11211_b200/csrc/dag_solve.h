@@ -40,6 +40,8 @@ class DagSolver {
   double* upd_ = nullptr;
   double* xy_ = nullptr;
   int32_t* ctr_ = nullptr;
+  int32_t* qhead_ = nullptr;
+  int32_t nq_ = 16;
   unsigned long long* trace_ = nullptr;
 
  public:

@@ -8,6 +8,7 @@
 #include <cstring>
 #include <map>
 #include <numeric>
+#include <string>
 
 #include "common.h"
 
@@ -65,6 +66,8 @@ PlanOptions::PlanOptions() {
   if (const char* e = std::getenv("SFCDD_BLOB_MAX")) blob_max = std::atoi(e);
   if (const char* e = std::getenv("SFCDD_SCRATCH_MAX")) scratch_max = std::atoi(e);
   if (const char* e = std::getenv("SFCDD_WORKERS")) workers = std::atoi(e);
+  if (const char* e = std::getenv("SFCDD_ROW_MAX")) row_max = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("SFCDD_COL_MAX")) col_max = std::max(1, std::atoi(e));
 }
 
 DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::vector<int64_t>& gstart,
@@ -224,8 +227,8 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
       const Supernode& S = Top;
       const int32_t s = S.s, m = S.m;
       const double* Mv = F.val.data() + S.val_off;
-      // assembly record: CSR over the front positions of the child update
-      // indices summed into each (fixed order: children, then rows)
+      // child update indices summed into each front position (fixed order:
+      // children, then rows)
       std::vector<std::vector<int32_t>> contrib(s + m);
       for (int32_t q = F.child_ptr[gr.top]; q < F.child_ptr[gr.top + 1]; ++q) {
         const int32_t c = F.child_list[q];
@@ -233,31 +236,86 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         SFCDD_REQUIRE(upd_slot[gr.factor][c] >= 0, SFCDD_EINTERNAL, "big child without update slot");
         for (int32_t a = 0; a < K.m; ++a) contrib[F.rel[K.rel_off + a]].push_back(upd_slot[gr.factor][c] + a);
       }
-      ints.clear();
-      for (int32_t c = 0; c < s; ++c) ints.push_back(F.perm[S.col0 + c]);
-      for (int32_t a = 0; a < m; ++a) ints.push_back(F.perm[F.rows[S.rows_off + a]]);
-      int32_t nnz = 0;
-      for (int32_t p = 0; p <= s + m; ++p) {
-        ints.push_back(nnz);
-        if (p < s + m) nnz += (int32_t)contrib[p].size();
+      // huge s: the f_J assembly metadata goes to one global record shared by
+      // all of J's row tasks instead of every blob
+      int64_t fj_nnz = 0;
+      for (int32_t q = 0; q < s; ++q) fj_nnz += (int64_t)contrib[q].size();
+      const bool global_asm = 4 * (RW_WORDS + 2 * s + 1 + fj_nnz) > opt.blob_max / 2;
+      int32_t asm16 = -1;
+      if (global_asm) {
+        ints.assign({s, m});
+        for (int32_t c = 0; c < s; ++c) ints.push_back(F.perm[S.col0 + c]);
+        int32_t nnz = 0;
+        for (int32_t p = 0; p <= s + m; ++p) {
+          ints.push_back(nnz);
+          if (p < s + m) nnz += (int32_t)contrib[p].size();
+        }
+        for (int32_t p = 0; p < s + m; ++p) ints.insert(ints.end(), contrib[p].begin(), contrib[p].end());
+        const int64_t asm_off = (int64_t)P.blobs.size();
+        SFCDD_REQUIRE(asm_off % 16 == 0 && asm_off / 16 < (int64_t(1) << 31), SFCDD_EINTERNAL,
+                      "blob buffer too large");
+        P.blobs.resize(P.blobs.size() + align16(4 * (int64_t)ints.size()), 0);
+        std::memcpy(P.blobs.data() + asm_off, ints.data(), 4 * ints.size());
+        asm16 = (int32_t)(asm_off / 16);
       }
-      for (int32_t p = 0; p < s + m; ++p) ints.insert(ints.end(), contrib[p].begin(), contrib[p].end());
-      const int64_t asm_off = (int64_t)P.blobs.size();
-      SFCDD_REQUIRE(asm_off % 16 == 0 && asm_off / 16 < (int64_t(1) << 31), SFCDD_EINTERNAL, "blob buffer too large");
-      P.blobs.resize(P.blobs.size() + align16(4 * (int64_t)ints.size()), 0);
-      std::memcpy(P.blobs.data() + asm_off, ints.data(), 4 * ints.size());
-      const int32_t asm16 = (int32_t)(asm_off / 16);
       // forward: row blocks that never straddle s
+      auto row_meta = [&](int32_t r0, int32_t R, bool emit) -> int64_t {
+        const int32_t C = r0 < s ? r0 + R : s;
+        const int32_t NB = r0 < s ? 0 : R;
+        int64_t nnz = 0;
+        if (!global_asm)
+          for (int32_t q = 0; q < C + NB; ++q) nnz += (int64_t)contrib[q < C ? q : r0 + (q - C)].size();
+        if (!emit) return global_asm ? (int64_t)RW_WORDS : RW_WORDS + C + (C + NB + 1) + nnz;
+        ints.assign(RW_WORDS, 0);
+        ints[RW_ASM16] = asm16;
+        if (global_asm) {
+          ints[RW_S] = s;
+          ints[RW_R] = R;
+          ints[RW_C] = C;
+          ints[RW_R0] = r0;
+          ints[RW_NB] = NB;
+          ints[RW_YOFF] = (int32_t)gr.y_off;
+          ints[RW_UOFF] = upd_slot[gr.factor][gr.top];
+          ints[RW_SCRATCH] = C + NB;
+          return (int64_t)ints.size();
+        }
+        ints[RW_S] = s;
+        ints[RW_R] = R;
+        ints[RW_C] = C;
+        ints[RW_R0] = r0;
+        ints[RW_NB] = NB;
+        ints[RW_YOFF] = (int32_t)gr.y_off;
+        ints[RW_UOFF] = upd_slot[gr.factor][gr.top];
+        ints[RW_COLS] = (int32_t)ints.size();
+        for (int32_t c = 0; c < C; ++c) ints.push_back(F.perm[S.col0 + c]);
+        ints[RW_PTR] = (int32_t)ints.size();
+        int32_t e = 0;
+        for (int32_t q = 0; q <= C + NB; ++q) {
+          ints.push_back(e);
+          if (q < C + NB) e += (int32_t)contrib[q < C ? q : r0 + (q - C)].size();
+        }
+        ints[RW_SRC] = (int32_t)ints.size();
+        for (int32_t q = 0; q < C + NB; ++q) {
+          const auto& cl = contrib[q < C ? q : r0 + (q - C)];
+          ints.insert(ints.end(), cl.begin(), cl.end());
+        }
+        ints[RW_SCRATCH] = C + NB;
+        return (int64_t)ints.size();
+      };
       auto row_fits = [&](int32_t r0, int32_t R) {
         const int32_t C = r0 < s ? r0 + R : s;
         const int32_t NB = r0 < s ? 0 : R;
-        return blob_size(RW_WORDS, (int64_t)R * C) <= opt.blob_max && C + NB <= opt.big_scratch_max;
+        const int64_t nints = row_meta(r0, R, false);
+        const int64_t nnz = global_asm ? 0 : nints - (RW_WORDS + C + (C + NB + 1));
+        (void)nnz;
+        return blob_size(nints, (int64_t)R * C) <= opt.blob_max && C + NB <= opt.big_scratch_max;
       };
       static const int32_t cand[] = {256, 192, 128, 96, 64, 32, 16, 8, 4, 2, 1};
       for (int32_t r0 = 0; r0 < s + m;) {
         const int32_t lim = r0 < s ? s : s + m;
         int32_t R = 0;
         for (int32_t c : cand) {
+          if (c > opt.row_max && c > 1) continue;
           const int32_t Re = std::min(c, lim - r0);
           if (row_fits(r0, Re)) {
             R = Re;
@@ -267,18 +325,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         SFCDD_REQUIRE(R > 0, SFCDD_EINTERNAL,
                       "big supernode row does not fit a task blob (s = " + std::to_string(s) + ")");
         const int32_t C = r0 < s ? r0 + R : s;
-        const int32_t NB = r0 < s ? 0 : R;
-        ints.assign(RW_WORDS, 0);
-        ints[RW_S] = s;
-        ints[RW_M] = m;
-        ints[RW_R] = R;
-        ints[RW_C] = C;
-        ints[RW_R0] = r0;
-        ints[RW_NB] = NB;
-        ints[RW_YOFF] = (int32_t)gr.y_off;
-        ints[RW_UOFF] = upd_slot[gr.factor][gr.top];
-        ints[RW_ASM16] = asm16;
-        ints[RW_SCRATCH] = C + NB;
+        row_meta(r0, R, true);
         vals.assign((size_t)R * C, 0.0);
         for (int32_t k = 0; k < C; ++k)
           for (int32_t i = 0; i < R; ++i) {
@@ -286,37 +333,43 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
             if (k <= row) vals[(size_t)k * R + i] = Mv[packed_col_off(s, m, k) + (row - k)];
           }
         int32_t bytes = 0;
+        const int32_t scratch = ints[RW_SCRATCH];
         const int64_t off = emit_blob(P, ints, RW_VAL_OFF, vals, bytes);
-        P.max_scratch = std::max<int32_t>(P.max_scratch, C + NB);
+        P.max_scratch = std::max<int32_t>(P.max_scratch, scratch);
         add_task(g, TK_ROW_FWD, off, bytes, (int64_t)R * C, 2.5 + 0.0045 * R * C);
         r0 += R;
       }
-      // backward: column blocks
+      // backward: column blocks, dense row-major L x c (L = s+m-k0)
       for (int32_t k0 = 0; k0 < s;) {
-        int32_t k1 = k0;
-        int64_t nv = 0;
-        while (k1 < s) {
-          const int64_t nv2 = nv + (s + m - k1);
-          if (blob_size(CL_WORDS, nv2) > opt.blob_max) break;
-          nv = nv2;
-          ++k1;
-        }
-        SFCDD_REQUIRE(k1 > k0 && s - k0 + m <= opt.big_scratch_max, SFCDD_EINTERNAL,
+        const int32_t L = s + m - k0;
+        int32_t c = std::min<int32_t>(opt.col_max, s - k0);
+        while (c > 1 && blob_size(CL_WORDS + c + m, (int64_t)L * c) > opt.blob_max) --c;
+        SFCDD_REQUIRE(blob_size(CL_WORDS + c + m, (int64_t)L * c) <= opt.blob_max && L <= opt.big_scratch_max,
+                      SFCDD_EINTERNAL,
                       "big supernode column does not fit a task blob (s+m = " + std::to_string(s + m) + ")");
         ints.assign(CL_WORDS, 0);
         ints[CL_S] = s;
         ints[CL_M] = m;
         ints[CL_K0] = k0;
-        ints[CL_K1] = k1;
+        ints[CL_C] = c;
         ints[CL_YOFF] = (int32_t)gr.y_off;
-        ints[CL_ASM16] = asm16;
-        ints[CL_SCRATCH] = s - k0 + m;
-        vals.assign(Mv + packed_col_off(s, m, k0), Mv + packed_col_off(s, m, k1));
+        ints[CL_COLS] = (int32_t)ints.size();
+        for (int32_t j = 0; j < c; ++j) ints.push_back(F.perm[S.col0 + k0 + j]);
+        ints[CL_ROWS] = (int32_t)ints.size();
+        for (int32_t a = 0; a < m; ++a) ints.push_back(F.perm[F.rows[S.rows_off + a]]);
+        ints[CL_SCRATCH] = L;
+        vals.assign((size_t)L * c, 0.0);
+        int64_t nv = 0;
+        for (int32_t r = 0; r < L; ++r)
+          for (int32_t j = 0; j < c && j <= r; ++j) {
+            vals[(size_t)r * c + j] = Mv[packed_col_off(s, m, k0 + j) + (r - j)];
+            ++nv;
+          }
         int32_t bytes = 0;
         const int64_t off = emit_blob(P, ints, CL_VAL_OFF, vals, bytes);
-        P.max_scratch = std::max<int32_t>(P.max_scratch, s - k0 + m);
+        P.max_scratch = std::max<int32_t>(P.max_scratch, L);
         add_task(g, TK_COL_BWD, off, bytes, nv, 3.5 + 0.0049 * nv);
-        k0 = k1;
+        k0 += c;
       }
       continue;
     }
@@ -605,6 +658,37 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         }
     }
     P.sim_us = now;
+    P.crit_us = 0.0;
+    int32_t cur = -1;
+    for (size_t t = 0; t < tl.size(); ++t)
+      if (rank[t] > P.crit_us) {
+        P.crit_us = rank[t];
+        cur = (int32_t)t;
+      }
+    if (std::getenv("SFCDD_PLAN_DEBUG") && cur >= 0) {
+      // walk the critical path: successor with the largest rank
+      std::vector<std::vector<int32_t>> succ(nctr);
+      std::string path;
+      int hops[4] = {0, 0, 0, 0};
+      double wsum[4] = {0, 0, 0, 0};
+      while (cur >= 0) {
+        if (tl[cur].kind == TK_ROW_FWD) {
+          const Group& gr = groups[tl[cur].group];
+          const Supernode& S = factors[gr.factor]->sn[gr.top];
+          path += " " + std::to_string(S.s) + "/" + std::to_string(S.m) + "(" +
+                  std::to_string(groups[tl[cur].group].ftask.size()) + ")";
+        }
+        hops[tl[cur].kind]++;
+        wsum[tl[cur].kind] += tw[cur];
+        int32_t best = -1;
+        for (int32_t w : waiters[tl[cur].signal_idx])
+          if (best < 0 || rank[w] > rank[best]) best = w;
+        cur = best;
+      }
+      std::fprintf(stderr, "[plan] critical big chain s/m(row tasks):%s\n", path.c_str());
+      std::fprintf(stderr, "[plan] critical path: frag_f %d (%.0f us) frag_b %d (%.0f us) row %d (%.0f us) col %d (%.0f us)\n",
+                   hops[0], wsum[0], hops[1], wsum[1], hops[2], wsum[2], hops[3], wsum[3]);
+    }
   }
   P.tasks.resize(tl.size());
   for (size_t t = 0; t < order.size(); ++t) P.tasks[t] = tl[order[t]];
@@ -626,14 +710,40 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
       }
     }
     for (const Group& gr : groups) maxh = std::max(maxh, gr.height);
+    {  // per-level FRAG work profile
+      double nl = 0, runs = 0, pairs = 0, fi = 0, bi = 0, bpr = 0, ncol = 0, nxu = 0, nxx = 0, nf = 0, maxr = 0;
+      for (const TaskDev& T : P.tasks) {
+        if (T.kind != TK_FRAG_FWD) continue;
+        const int32_t* h = reinterpret_cast<const int32_t*>(P.blobs.data() + T.blob_off);
+        const int32_t* runs_a = h + h[H_RUNS];
+        nf += 1;
+        ncol += h[H_NCOL];
+        nxu += h[H_NEXTU];
+        nxx += h[H_NEXTX];
+        for (int32_t l = 0; l < h[H_NLEV]; ++l) {
+          const int32_t* L = h + h[H_LEVELS] + L_WORDS * l;
+          nl += 1;
+          runs += L[L_RUN1] - L[L_RUN0];
+          maxr = std::max<double>(maxr, L[L_RUN1] - L[L_RUN0]);
+          pairs += runs_a[L[L_RUN1]] - runs_a[L[L_RUN0]];
+          fi += L[L_FI1] - L[L_FI0];
+          bi += L[L_BI1] - L[L_BI0];
+          bpr += L[L_BP1] - L[L_BP0];
+        }
+      }
+      std::fprintf(stderr,
+                   "[plan] FRAG per level: %.1f runs (%.1f pairs, max %.0f), %.1f fwd items, %.1f bwd items, %.1f "
+                   "bwd pairs; per task: %.1f cols, %.1f ext updates, %.1f ext rows\n",
+                   runs / nl, pairs / nl, maxr, fi / nl, bi / nl, bpr / nl, ncol / nf, nxu / nf, nxx / nf);
+    }
     std::fprintf(stderr,
                  "[plan] groups=%d frag=%d big=%d (%.1f%% of values; %lld row + %lld col tasks) frag avg: %.1f "
                  "supernodes, %.1f levels, %.1f values; max group height %d; blobs %.1f MB; max scratch %d; "
-                 "simulated schedule %.1f us on %d warps\n",
+                 "simulated schedule %.1f us on %d warps (critical path %.1f us)\n",
                  G, P.nfrag, P.nbig, 100.0 * big_vals / std::max<int64_t>(1, big_vals + small_vals),
                  (long long)nrow, (long long)ncol, (double)sn_sum / std::max(1, P.nfrag),
                  (double)lev_sum / std::max(1, P.nfrag), (double)small_vals / std::max(1, P.nfrag), maxh,
-                 P.blobs.size() / 1e6, P.max_scratch, P.sim_us, opt.workers);
+                 P.blobs.size() / 1e6, P.max_scratch, P.sim_us, opt.workers, P.crit_us);
   }
   return P;
 }

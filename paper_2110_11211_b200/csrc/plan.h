@@ -93,41 +93,47 @@ enum LevField { L_REC0 = 0, L_REC1, L_RUN0, L_RUN1, L_BP0, L_BP1, L_FI0, L_FI1, 
 // per-supernode record (int32 words)
 enum SnRecField { R_S = 0, R_M, R_VAL, R_SCR, R_CPOS, R_WORDS };
 
-// ------------------------------------------------------ BIG supernode meta
-// Per big supernode J one read-only ASSEMBLY record lives in the blob buffer
-// (16-aligned, read through the cache by all of J's tasks, never staged):
-//   [ro of the s columns] [ro of the m below rows] [ptr (s+m+1)] [src (nnz)]
-// -- a CSR over J's front positions listing, in fixed order (children, then
-// rows), the global update indices summed into that position.
-//
-// ROW blob: forward rows [r0, r0+R) of J (either all < s: y rows, or all
-// >= s: update rows).  Values: R x C dense column-major (leading dim R),
-// entry (i, k) = M[r0+i, k] (zero where k > r0+i), C = min(r0+R, s).
-// Scratch: [f_J (C)] [f_B of the block rows (NB)].
+// ---------------------------------------------------------- BIG blobs
+// ROW blob: forward rows [r0, r0+R) of one big supernode J (either all < s:
+// y rows, or all >= s: update rows).  Self-contained unless J's assembly
+// metadata is too large for a blob (RW_ASM16):
+//   cols: ro of J's first C columns (rhs gather)
+//   ptr[C+NB+1] / src[nnz]: CSR over the task's front positions (f_J[0:C),
+//     then its NB update rows) of the child update indices summed into each,
+//     in fixed order (children, then rows)
+//   values: R x C dense column-major (leading dim R), entry (i, k) =
+//     M[r0+i, k] (zero where k > r0+i), C = min(r0+R, s).
+// Scratch: [f (C+NB)] [staged child updates (nnz)].
 enum RowHdr {
   RW_S = 0,
-  RW_M,
   RW_R,        // rows in the block
   RW_C,        // columns
   RW_R0,       // first front row
   RW_NB,       // block rows >= s (0 or R)
   RW_YOFF,     // global y slot of J (upd buffer)
   RW_UOFF,     // global update slot of J (-1: root)
-  RW_ASM16,    // byte offset / 16 of J's assembly record in the blob buffer
+  RW_COLS,     // int offset: ro[C]
+  RW_PTR,      // int offset: ptr[C+NB+1]
+  RW_SRC,      // int offset: src[nnz]
+  RW_ASM16,    // -1, or (huge s) byte offset / 16 of J's global assembly record
+               // [s, m] [cols (s)] [ptr (s+m+1)] [src] over FRONT positions;
+               // then RW_COLS / RW_PTR / RW_SRC are unused
   RW_VAL_OFF,  // byte offset of the values
   RW_SCRATCH,  // doubles of scratch used
   RW_WORDS
 };
 
-// COL blob: backward columns [k0, k1) of J.  Values: packed columns k0..k1-1
-// of M (column k holds rows k..s+m-1).  Scratch: v = [y_J[k0:s) ; -x_B].
+// COL blob: backward columns [k0, k0+c) of J.  Values: L x c dense row-major
+// block of M (L = s+m-k0 rows starting at row k0), entry (r, j) =
+// M[k0+r, k0+j] (zero where r < j).  Scratch: v = [y_J[k0:s) ; -x_B] (L).
 enum ColHdr {
   CL_S = 0,
   CL_M,
   CL_K0,
-  CL_K1,
+  CL_C,        // columns in the block
   CL_YOFF,     // global y slot of J
-  CL_ASM16,    // byte offset / 16 of J's assembly record
+  CL_COLS,     // int offset: ro of the c columns
+  CL_ROWS,     // int offset: ro of the m below rows
   CL_VAL_OFF,  // byte offset of the values
   CL_SCRATCH,
   CL_WORDS
@@ -140,6 +146,8 @@ struct PlanOptions {
   int32_t scratch_max = 512;     // doubles of FRAG scratch (< 65536)
   int32_t big_scratch_max = 8192;  // doubles of scratch a BIG task may use
   int32_t workers = 148 * 16;      // warps assumed by the queue-order simulation (SFCDD_WORKERS)
+  int32_t row_max = 32;            // rows per ROW task (SFCDD_ROW_MAX; latency vs task count)
+  int32_t col_max = 16;            // columns per COL task (SFCDD_COL_MAX)
   PlanOptions();                 // environment overrides SFCDD_BLOB_MAX, SFCDD_SCRATCH_MAX
 };
 
@@ -158,6 +166,7 @@ struct DevicePlan {
   int32_t max_copy = 0;     // bytes
   int32_t blob_max = 0;
   double sim_us = 0.0;  // makespan of the simulated schedule (model time)
+  double crit_us = 0.0; // critical path of the task graph (model time)
 };
 
 DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::vector<int64_t>& gstart,

@@ -35,49 +35,45 @@ void plan_exec_host(const DevicePlan& P, const double* rhs, double* xy) {
       return g;
     };
     double* x = xy + Fd.xy_off;
-    if (T.kind == TK_ROW_FWD || T.kind == TK_COL_BWD) {
-      const bool row = T.kind == TK_ROW_FWD;
-      const int32_t s = h[row ? RW_S : CL_S], m = h[row ? RW_M : CL_M];
-      const int32_t* am = reinterpret_cast<const int32_t*>(P.blobs.data() + 16 * (int64_t)h[row ? RW_ASM16 : CL_ASM16]);
-      const int32_t* cols = am;
-      const int32_t* rows = am + s;
-      const int32_t* ptr = rows + m;
-      const int32_t* src = ptr + s + m + 1;
-      if (row) {
-        const double* V = reinterpret_cast<const double*>(blob + h[RW_VAL_OFF]);
-        const int32_t R = h[RW_R], C = h[RW_C], r0 = h[RW_R0], NB = h[RW_NB];
-        scratch.assign(C + NB, 0.0);
-        double* S = scratch.data();
-        for (int32_t q = 0; q < C + NB; ++q) {
-          const int32_t p = q < C ? q : r0 + (q - C);
-          double acc = q < C ? rhs[gidx(cols[q])] : 0.0;
-          for (int32_t e = ptr[p]; e < ptr[p + 1]; ++e) acc += upd[src[e]];
-          S[q] = acc;
-        }
-        for (int32_t i = 0; i < R; ++i) {
-          double acc = 0.0;
-          for (int32_t k = 0; k < C; ++k) acc += V[(size_t)k * R + i] * S[k];
-          const int32_t rw = r0 + i;
-          if (rw < s)
-            upd[h[RW_YOFF] + rw] = acc;
-          else
-            upd[h[RW_UOFF] + rw - s] = S[C + i] - acc;
-        }
-      } else {
-        const double* V = reinterpret_cast<const double*>(blob + h[CL_VAL_OFF]);
-        const int32_t k0 = h[CL_K0], k1 = h[CL_K1];
-        scratch.assign(s - k0 + m, 0.0);
-        double* v = scratch.data();
-        for (int32_t i = k0; i < s; ++i) v[i - k0] = upd[h[CL_YOFF] + i];
-        for (int32_t a = 0; a < m; ++a) v[s - k0 + a] = -x[rows[a]];
-        int64_t off = 0;
-        for (int32_t k = k0; k < k1; ++k) {
-          const int32_t len = s + m - k;
-          double acc = 0.0;
-          for (int32_t q = 0; q < len; ++q) acc += V[off + q] * v[k - k0 + q];
-          x[cols[k]] = acc;
-          off += len;
-        }
+    if (T.kind == TK_ROW_FWD) {
+      const double* V = reinterpret_cast<const double*>(blob + h[RW_VAL_OFF]);
+      const int32_t s = h[RW_S], R = h[RW_R], C = h[RW_C], r0 = h[RW_R0], NB = h[RW_NB];
+      const bool ga = h[RW_ASM16] >= 0;  // global assembly record (huge s)
+      const int32_t* am = reinterpret_cast<const int32_t*>(P.blobs.data() + 16 * (int64_t)std::max(0, h[RW_ASM16]));
+      const int32_t* cols = ga ? am + 2 : h + h[RW_COLS];
+      const int32_t* ptr = ga ? am + 2 + am[0] : h + h[RW_PTR];
+      const int32_t* src = ga ? ptr + am[0] + am[1] + 1 : h + h[RW_SRC];
+      scratch.assign(C + NB, 0.0);
+      double* S = scratch.data();
+      for (int32_t q = 0; q < C + NB; ++q) {
+        const int32_t p = ga ? (q < C ? q : r0 + (q - C)) : q;
+        double acc = q < C ? rhs[gidx(cols[q])] : 0.0;
+        for (int32_t e = ptr[p]; e < ptr[p + 1]; ++e) acc += upd[src[e]];
+        S[q] = acc;
+      }
+      for (int32_t i = 0; i < R; ++i) {
+        double acc = 0.0;
+        for (int32_t k = 0; k < C; ++k) acc += V[(size_t)k * R + i] * S[k];
+        const int32_t rw = r0 + i;
+        if (rw < s)
+          upd[h[RW_YOFF] + rw] = acc;
+        else
+          upd[h[RW_UOFF] + rw - s] = S[C + i] - acc;
+      }
+    } else if (T.kind == TK_COL_BWD) {
+      const double* V = reinterpret_cast<const double*>(blob + h[CL_VAL_OFF]);
+      const int32_t s = h[CL_S], m = h[CL_M], k0 = h[CL_K0], c = h[CL_C];
+      const int32_t* cols = h + h[CL_COLS];
+      const int32_t* rows = h + h[CL_ROWS];
+      const int32_t L = s + m - k0;
+      scratch.assign(L, 0.0);
+      double* v = scratch.data();
+      for (int32_t i = k0; i < s; ++i) v[i - k0] = upd[h[CL_YOFF] + i];
+      for (int32_t a = 0; a < m; ++a) v[s - k0 + a] = -x[rows[a]];
+      for (int32_t j = 0; j < c; ++j) {
+        double acc = 0.0;
+        for (int32_t r = j; r < L; ++r) acc += V[(size_t)r * c + j] * v[r];
+        x[cols[j]] = acc;
       }
     } else {
       const bool fwd = T.kind == TK_FRAG_FWD;

@@ -25,5 +25,6 @@ _lib.check(_lib.lib().sfcdd_op_trace(op.handle, g.data_ptr(), None, ctypes.byref
 out = np.zeros(24 * nt.value, dtype=np.uint64)
 _lib.check(_lib.lib().sfcdd_op_trace(op.handle, g.data_ptr(), out.ctypes.data, ctypes.byref(nt)))
 (ROOT / "gpurun_out").mkdir(exist_ok=True)
-np.savez_compressed(ROOT / "gpurun_out" / f"trace_{name}.npz", trace=out.reshape(-1, 24), stats=str(op.stats()))
+tag = sys.argv[2] if len(sys.argv) > 2 else ""
+np.savez_compressed(ROOT / "gpurun_out" / f"trace_{name}{tag}.npz", trace=out.reshape(-1, 24), stats=str(op.stats()))
 print("traced", nt.value, "tasks")
