@@ -236,21 +236,30 @@ __device__ __forceinline__ void fwd_row(const int32_t* R, const double* vals, do
     f[i] -= acc;  // u = f_B - W f_J (only f[0:s) is read by other rows)
 }
 
-// backward column k of a supernode by the warp (lanes = rows, warp reduce)
-__device__ __forceinline__ void bwd_col(const int32_t* R, const double* vals, double* S, int k, int lane) {
+// backward columns [k0, k0+c) of a supernode (c <= 32): lanes = (column,
+// row-phase), partial dot products reduced over the phases
+__device__ __forceinline__ void bwd_cols(const int32_t* R, const double* vals, double* S, int k0, int c, int lane) {
   const int s = R[R_S], m = R[R_M];
   const double* v = S + R[R_SCR];
-  const double* col = vals + R[R_VAL] + coloff(s, m, k);
-  const int len = s + m - k;
+  const int CP = c <= 1 ? 1 : 1 << (32 - __clz(c - 1));  // lanes per phase
+  const int P = 32 / CP;
+  const int j = lane & (CP - 1), ph = lane / CP;
+  const int k = k0 + j;
   double a0 = 0.0, a1 = 0.0;
-  int t = lane;
-  for (; t + 32 < len; t += 64) {
-    a0 = fma(col[t], v[k + t], a0);
-    a1 = fma(col[t + 32], v[k + t + 32], a1);
+  if (j < c) {
+    const double* col = vals + R[R_VAL] + coloff(s, m, k);
+    const double* vk = v + k;
+    const int len = s + m - k;
+    int t = ph;
+    for (; t + P < len; t += 2 * P) {
+      a0 = fma(col[t], vk[t], a0);
+      a1 = fma(col[t + P], vk[t + P], a1);
+    }
+    if (t < len) a0 = fma(col[t], vk[t], a0);
   }
-  if (t < len) a0 = fma(col[t], v[k + t], a0);
-  const double x = warp_sum(a0 + a1);
-  if (lane == 0) S[R[R_CPOS] + k] = x;
+  double acc = a0 + a1;
+  for (int o = CP; o < 32; o <<= 1) acc += __shfl_xor_sync(FULL, acc, o);
+  if (ph == 0 && j < c) S[R[R_CPOS] + k] = acc;
 }
 
 // backward of packed small supernodes: lanes = rows, x_k by segmented scans
@@ -358,7 +367,7 @@ __device__ __forceinline__ void run_frag(const int32_t* h, bool fwd, double* S, 
       for (int it = L[L_BI0]; it < L[L_BI1]; ++it) {  // columns / packed small supernodes
         const int2 item = items[it];
         if ((item.x >> 16) == 0)
-          bwd_col(recs + R_WORDS * item.x, vals, S, item.y, lane);
+          bwd_cols(recs + R_WORDS * item.x, vals, S, item.y & 0xffff, item.y >> 16, lane);
         else
           bwd_packed(recs, vals, S, item.x & 0xffff, item.x >> 16, (unsigned)item.y, lane);
       }

@@ -532,7 +532,9 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
             for (int32_t b = 0; b < (S.s + S.m + 31) / 32; ++b) items.insert(items.end(), {j, b});
             ++j;
           } else {
-            for (int32_t k = 0; k < S.s; ++k) items.insert(items.end(), {j, k});
+            // backward: blocks of up to 32 columns; lanes = (column, row-phase)
+            for (int32_t k0 = 0; k0 < S.s; k0 += 32)
+              items.insert(items.end(), {j, k0 | (std::min<int32_t>(32, S.s - k0) << 16)});
             ++j;
           }
         }

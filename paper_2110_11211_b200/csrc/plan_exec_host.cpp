@@ -115,7 +115,7 @@ void plan_exec_host(const DevicePlan& P, const double* rhs, double* xy) {
           if (forward)
             for (int32_t i = 32 * y; i < std::min(32 * y + 32, R[R_S] + R[R_M]); ++i) fn(R, i);
           else
-            fn(R, y);
+            for (int32_t k = y & 0xffff; k < (y & 0xffff) + (y >> 16); ++k) fn(R, k);
         }
       };
       if (fwd) {
