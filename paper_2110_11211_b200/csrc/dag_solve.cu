@@ -488,7 +488,7 @@ __device__ __forceinline__ void run_col(const int32_t* h, double* S, const DagAr
 
 // ================================================================ kernel
 template <int WPB>
-__global__ void __launch_bounds__(WPB * 32) k_dag(DagArgs A) {
+__global__ void __launch_bounds__(WPB * 32, 1) k_dag(DagArgs A) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bars[WPB];
   if (A.skip && *A.skip) return;
