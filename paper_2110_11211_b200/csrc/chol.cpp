@@ -25,6 +25,8 @@ FactorOptions::FactorOptions() {
   if (const char* v = std::getenv("SFCDD_RELAX_SMALL")) relax_small = std::atoi(v);
   if (const char* v = std::getenv("SFCDD_RELAX_SMALL_FRAC")) relax_small_frac = std::atof(v);
   if (const char* v = std::getenv("SFCDD_RELAX_FRAC")) relax_frac = std::atof(v);
+  if (const char* v = std::getenv("SFCDD_ORDER")) ordering = std::string(v) == "amd" ? 0 : 1;
+  if (const char* v = std::getenv("SFCDD_ND_LEAF")) nd_leaf = std::atoi(v);
 }
 
 int hardware_threads() {
@@ -103,7 +105,7 @@ HostFactor analyze_host(const CsrMatrix& A, const FactorOptions& opt) {
   P.n = n;
   P.indptr = A.indptr;
   P.indices = A.indices;
-  std::vector<int32_t> order = amd_order(P);
+  std::vector<int32_t> order = opt.ordering == 1 ? nd_order(P, opt.nd_leaf) : amd_order(P);
   std::vector<int32_t> iperm(n);
   for (int64_t k = 0; k < n; ++k) iperm[order[k]] = (int32_t)k;
   std::vector<int32_t> parent;

@@ -22,6 +22,8 @@ struct CsrMatrix {
 };
 
 std::vector<int32_t> amd_order(const SymPattern& A);
+// hybrid nested dissection (BFS level-set separators, AMD on parts <= leaf)
+std::vector<int32_t> nd_order(const SymPattern& A, int32_t leaf);
 
 // One supernode of the block-inverse factor.  Columns col0..col0+s-1 of the
 // permuted matrix; m below rows.  The stored block is
@@ -70,6 +72,10 @@ struct FactorOptions {
   int32_t relax_small = 16;
   double relax_small_frac = 0.30;
   double relax_frac = 0.02;
+  // fill-reducing ordering: 0 = AMD, 1 = hybrid nested dissection (SFCDD_ORDER=amd|nd,
+  // SFCDD_ND_LEAF = part size below which AMD takes over)
+  int32_t ordering = 1;
+  int32_t nd_leaf = 64;
   FactorOptions();
 };
 

@@ -682,6 +682,7 @@ extern "C" int sfcdd_op_setup(sfcdd_op* op, void* stream) {
   }
   op->xy_off_host = xyoff;
   PlanOptions po;
+  CUDA_CHECK(cudaDeviceGetAttribute(&po.sms, cudaDevAttrMultiProcessorCount, op->device));
   DevicePlan plan = build_plan(ptrs, gs, gm, po);
   op->stats.factor_nnz = plan.stored;
   op->stats.factor_nnz_l = plan.nnz_l;
@@ -1455,6 +1456,7 @@ extern "C" int sfcdd_factor_create(int64_t n, const int64_t* indptr, const int32
   f->stored = F.stored;
   f->nsuper = F.sn.size();
   PlanOptions po;
+  CUDA_CHECK(cudaDeviceGetAttribute(&po.sms, cudaDevAttrMultiProcessorCount, device));
   DevicePlan plan = build_plan({&F}, {0}, {n}, po);
   CUDA_CHECK(cudaSetDevice(device));
   f->dag.reset(new DagSolver(plan, device));

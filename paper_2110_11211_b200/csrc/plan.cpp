@@ -336,7 +336,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         const int32_t scratch = ints[RW_SCRATCH];
         const int64_t off = emit_blob(P, ints, RW_VAL_OFF, vals, bytes);
         P.max_scratch = std::max<int32_t>(P.max_scratch, scratch);
-        add_task(g, TK_ROW_FWD, off, bytes, (int64_t)R * C, 2.5 + 0.0045 * R * C);
+        add_task(g, TK_ROW_FWD, off, bytes, (int64_t)R * C, 2.56 + 0.0017 * R * C);
         r0 += R;
       }
       // backward: column blocks, dense row-major L x c (L = s+m-k0)
@@ -368,7 +368,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         int32_t bytes = 0;
         const int64_t off = emit_blob(P, ints, CL_VAL_OFF, vals, bytes);
         P.max_scratch = std::max<int32_t>(P.max_scratch, L);
-        add_task(g, TK_COL_BWD, off, bytes, nv, 3.5 + 0.0049 * nv);
+        add_task(g, TK_COL_BWD, off, bytes, nv, 2.94 + 0.0014 * nv);
         k0 += c;
       }
       continue;
@@ -449,14 +449,15 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
     ints[H_EXTU_BASE] = extu_base;
     ints[H_EXTU] = (int32_t)ints.size();
     ints.insert(ints.end(), extu.begin(), extu.end());
+    while (ints.size() % 4) ints.push_back(0);  // int4 records
     ints[H_REC] = (int32_t)ints.size();
     ints.resize(ints.size() + (size_t)R_WORDS * nsn, 0);
     int64_t nvals = 0;
     for (int32_t i = 0; i < nsn; ++i) {
       const Supernode& S = sn_of(i);
       int32_t* R = &ints[ints[H_REC] + R_WORDS * i];
-      R[R_S] = S.s;
-      R[R_M] = S.m;
+      SFCDD_REQUIRE(S.s < 65536 && S.m < 32768, SFCDD_EINTERNAL, "supernode too large for a FRAG record");
+      R[R_SM] = S.s | (S.m << 16);
       R[R_VAL] = (int32_t)vals.size();
       R[R_SCR] = scr[i];
       R[R_CPOS] = cpos[i];
@@ -517,16 +518,18 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         while (j < L[L_REC1]) {
           const Supernode& S = sn_of(j);
           if (S.s + S.m <= 32) {
-            int32_t j1 = j, rows = 0;
+            int32_t j1 = j, rows = 0, smax = 0;
             uint32_t mask = 0;  // lane of each segment start, plus the end lane
             while (j1 < L[L_REC1] && rows + sn_of(j1).s + sn_of(j1).m <= 32) {
               mask |= 1u << rows;
               rows += sn_of(j1).s + sn_of(j1).m;
+              smax = std::max<int32_t>(smax, sn_of(j1).s);
               ++j1;
             }
             if (rows < 32) mask |= 1u << rows;
             SFCDD_REQUIRE(j < 65536 && j1 - j < 32768, SFCDD_EINTERNAL, "packed item index overflow");
-            items.insert(items.end(), {j | ((j1 - j) << 16), (int32_t)mask});
+            const uint32_t tiny = (pass == 0 && smax <= 4) ? 0x80000000u : 0u;
+            items.insert(items.end(), {(int32_t)((uint32_t)(j | ((j1 - j) << 16)) | tiny), (int32_t)mask});
             j = j1;
           } else if (pass == 0) {
             for (int32_t b = 0; b < (S.s + S.m + 31) / 32; ++b) items.insert(items.end(), {j, b});
@@ -560,8 +563,8 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
     SFCDD_REQUIRE(bytes <= opt.blob_max, SFCDD_EINTERNAL, "fragment blob exceeds the slot budget");
     P.max_scratch = std::max(P.max_scratch, scratch_used);
     // task time model (us), fitted to traced C2 launches (tools/trace_dag.py)
-    add_task(g, TK_FRAG_FWD, off, bytes, nvals, 2.1 + 0.0035 * nvals + 0.76 * nlev);
-    add_task(g, TK_FRAG_BWD, off, bytes, nvals, 2.5 + 0.0086 * nvals + 0.8 * nlev);
+    add_task(g, TK_FRAG_FWD, off, bytes, nvals, 2.31 + 0.0038 * nvals + 0.51 * nlev);
+    add_task(g, TK_FRAG_BWD, off, bytes, nvals, 2.5 + 0.005 * nvals + 0.5 * nlev);
   }
 
   // ---- 3. dependencies
@@ -632,7 +635,16 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
     using Ev = std::pair<double, int32_t>;
     std::vector<Ev> ev;  // min-heap of (end time, task)
     auto ev_cmp = [](const Ev& a, const Ev& b) { return a.first > b.first; };
-    int64_t free_w = std::max(1, opt.workers);
+    // resident warps of the kernel: slots of blob_max + scratch, 4-warp CTAs,
+    // <= 21 warps/SM by registers (dag_solve.cu)
+    int64_t workers = opt.workers;
+    if (workers <= 0) {
+      const int64_t slot = (opt.blob_max + 127) / 128 * 128 + (8 * std::max(P.max_scratch, 16) + 127) / 128 * 128;
+      const int64_t ctas = std::max<int64_t>(1, (227 * 1024) / (4 * slot));
+      workers = (int64_t)opt.sms * std::min<int64_t>(20, 4 * ctas);
+    }
+    P.workers = (int32_t)workers;
+    int64_t free_w = std::max<int64_t>(1, workers);
     double now = 0.0;
     while (order.size() < tl.size()) {
       while (free_w > 0 && !ready.empty()) {
@@ -745,7 +757,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
                  G, P.nfrag, P.nbig, 100.0 * big_vals / std::max<int64_t>(1, big_vals + small_vals),
                  (long long)nrow, (long long)ncol, (double)sn_sum / std::max(1, P.nfrag),
                  (double)lev_sum / std::max(1, P.nfrag), (double)small_vals / std::max(1, P.nfrag), maxh,
-                 P.blobs.size() / 1e6, P.max_scratch, P.sim_us, opt.workers, P.crit_us);
+                 P.blobs.size() / 1e6, P.max_scratch, P.sim_us, P.workers, P.crit_us);
   }
   return P;
 }

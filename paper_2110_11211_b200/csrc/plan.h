@@ -61,8 +61,10 @@ struct TaskDev {
 //   * backward row pairs: S[dst] = -S[src]  (dst = v_B slot, src = x slot);
 //   * forward / backward warp items (int2) {x, y}:
 //     x < 65536: row block y (forward) / column y (backward) of supernode x;
-//     x = j | cnt << 16: cnt consecutive small supernodes j.. packed into the
-//     32 lanes, y = bit mask of the lanes where each one starts (+ end lane).
+//     x = j | cnt << 16 (| 1 << 31 in forward items whose supernodes all have
+//     s <= 4: straight-line path): cnt consecutive small supernodes j..
+//     packed into the 32 lanes, y = bit mask of the lanes where each one
+//     starts (+ end lane).
 enum FragHdr {
   H_NSN = 0,
   H_NLEV,
@@ -77,7 +79,7 @@ enum FragHdr {
   H_EXTX,       // int offset of their ro[nextx]
   H_NEXTU,      // number of staged external update doubles (contiguous from H_EXTU_BASE)
   H_EXTU,       // int offset of their global update indices [nextu]
-  H_REC,        // int offset of SnRec[nsn] (level order)
+  H_REC,        // int offset (16-aligned) of the int4 supernode records (level order)
   H_LEVELS,     // int offset of the per-level table (L_WORDS per level)
   H_RUNS,       // int offset of gather run starts (int32, absolute pair index)
   H_GPAIRS,     // int offset of forward gather pairs (uint32)
@@ -90,8 +92,8 @@ enum FragHdr {
 // per-level table: record range, forward gather runs, backward row pairs,
 // forward items, backward items
 enum LevField { L_REC0 = 0, L_REC1, L_RUN0, L_RUN1, L_BP0, L_BP1, L_FI0, L_FI1, L_BI0, L_BI1, L_WORDS };
-// per-supernode record (int32 words)
-enum SnRecField { R_S = 0, R_M, R_VAL, R_SCR, R_CPOS, R_WORDS };
+// per-supernode record: int4 {s | m << 16, scratch slot, value offset, column slot}
+enum SnRecField { R_SM = 0, R_SCR, R_VAL, R_CPOS, R_WORDS };
 
 // ---------------------------------------------------------- BIG blobs
 // ROW blob: forward rows [r0, r0+R) of one big supernode J (either all < s:
@@ -145,7 +147,8 @@ struct PlanOptions {
   int32_t blob_max = 8 * 1024;   // bytes of a task blob (slot blob area)
   int32_t scratch_max = 512;     // doubles of FRAG scratch (< 65536)
   int32_t big_scratch_max = 8192;  // doubles of scratch a BIG task may use
-  int32_t workers = 148 * 16;      // warps assumed by the queue-order simulation (SFCDD_WORKERS)
+  int32_t workers = 0;             // warps assumed by the queue-order simulation (0: from the slot size; SFCDD_WORKERS)
+  int32_t sms = 148;               // SMs of the target device (set by the caller)
   int32_t row_max = 32;            // rows per ROW task (SFCDD_ROW_MAX; latency vs task count)
   int32_t col_max = 16;            // columns per COL task (SFCDD_COL_MAX)
   PlanOptions();                 // environment overrides SFCDD_BLOB_MAX, SFCDD_SCRATCH_MAX
@@ -166,6 +169,7 @@ struct DevicePlan {
   int32_t max_copy = 0;     // bytes
   int32_t blob_max = 0;
   double sim_us = 0.0;  // makespan of the simulated schedule (model time)
+  int32_t workers = 0;  // warps the schedule was simulated on
   double crit_us = 0.0; // critical path of the task graph (model time)
 };
 

@@ -90,8 +90,11 @@ void plan_exec_host(const DevicePlan& P, const double* rhs, double* xy) {
       const int32_t* gp = h + h[H_GPAIRS];
       const int32_t* bp = h + h[H_BPAIRS];
       const int32_t* items = h + h[H_ITEMS];
+      auto rs = [&](const int32_t* R) { return R[R_SM] & 0xffff; };
+      auto rm = [&](const int32_t* R) { return (int32_t)((uint32_t)R[R_SM] >> 16); };
       // rows handled by a warp item, in lane order (also checks the lane masks)
       auto item_rows = [&](int32_t x0, int32_t y, bool forward, auto&& fn) {
+        x0 &= 0x7fffffff;  // forward "tiny" flag
         const int32_t cnt = x0 >> 16;
         if (cnt > 0) {
           x0 &= 0xffff;
@@ -99,21 +102,21 @@ void plan_exec_host(const DevicePlan& P, const double* rhs, double* xy) {
           int32_t rows = 0;
           for (int32_t j = x0; j < x0 + cnt; ++j) {
             mask |= 1u << rows;
-            rows += recs[R_WORDS * j + R_S] + recs[R_WORDS * j + R_M];
+            rows += rs(recs + R_WORDS * j) + rm(recs + R_WORDS * j);
           }
           if (rows < 32) mask |= 1u << rows;
           SFCDD_REQUIRE(rows <= 32 && mask == (uint32_t)y, SFCDD_EINTERNAL, "packed item lane mask mismatch");
           for (int32_t j = x0; j < x0 + cnt; ++j) {
             const int32_t* R = recs + R_WORDS * j;
             if (forward)
-              for (int32_t i = 0; i < R[R_S] + R[R_M]; ++i) fn(R, i);
+              for (int32_t i = 0; i < rs(R) + rm(R); ++i) fn(R, i);
             else
-              for (int32_t k = 0; k < R[R_S]; ++k) fn(R, k);
+              for (int32_t k = 0; k < rs(R); ++k) fn(R, k);
           }
         } else {
           const int32_t* R = recs + R_WORDS * x0;
           if (forward)
-            for (int32_t i = 32 * y; i < std::min(32 * y + 32, R[R_S] + R[R_M]); ++i) fn(R, i);
+            for (int32_t i = 32 * y; i < std::min(32 * y + 32, rs(R) + rm(R)); ++i) fn(R, i);
           else
             for (int32_t k = y & 0xffff; k < (y & 0xffff) + (y >> 16); ++k) fn(R, k);
         }
@@ -132,7 +135,7 @@ void plan_exec_host(const DevicePlan& P, const double* rhs, double* xy) {
           }
           for (int32_t it = L[L_FI0]; it < L[L_FI1]; ++it)
             item_rows(items[2 * it], items[2 * it + 1], true, [&](const int32_t* R, int32_t i) {
-              const int32_t s = R[R_S], m = R[R_M];
+              const int32_t s = rs(R), m = rm(R);
               const double* M = vals + R[R_VAL];
               double* f = S + R[R_SCR];
               double acc = 0.0;
@@ -147,7 +150,7 @@ void plan_exec_host(const DevicePlan& P, const double* rhs, double* xy) {
         for (int32_t c = 0; c < ncol; ++c) x[cols[c]] = S[hi16(colpos[c])];
         if (h[H_TOP_UPD] >= 0) {
           const int32_t* R = recs + R_WORDS * h[H_TOP];
-          for (int32_t a = 0; a < R[R_M]; ++a) upd[h[H_TOP_UPD] + a] = S[R[R_SCR] + R[R_S] + a];
+          for (int32_t a = 0; a < rm(R); ++a) upd[h[H_TOP_UPD] + a] = S[R[R_SCR] + rs(R) + a];
         }
       } else {
         for (int32_t c = 0; c < ncol; ++c) S[lo16(colpos[c])] = x[cols[c]];
@@ -158,7 +161,7 @@ void plan_exec_host(const DevicePlan& P, const double* rhs, double* xy) {
           for (int32_t p = L[L_BP0]; p < L[L_BP1]; ++p) S[lo16(bp[p])] = -S[hi16(bp[p])];
           for (int32_t it = L[L_BI0]; it < L[L_BI1]; ++it)
             item_rows(items[2 * it], items[2 * it + 1], false, [&](const int32_t* R, int32_t k) {
-              const int32_t s = R[R_S], m = R[R_M];
+              const int32_t s = rs(R), m = rm(R);
               const double* col = vals + R[R_VAL] + packed_col_off(s, m, k);
               const double* v = S + R[R_SCR];
               double acc = 0.0;

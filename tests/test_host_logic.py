@@ -74,17 +74,36 @@ def random_spd(n, seed, density=0.05):
 
 
 @pytest.mark.parametrize("levels,p", [((7, 7), 16), ((4, 4, 4), 8)])
-def test_amd_is_a_permutation_with_mmd_quality_fill(oracle, levels, p):
+def test_amd_is_a_permutation_with_mmd_quality_fill(oracle, levels, p, monkeypatch):
     A = oracle.assemble_scaled_laplacian(levels)
     ov = oracle.enlarge(oracle.disjoint_partition(A.shape[0], p), 0.5)
     idx = ov[1].indices()
     As = A[idx][:, idx].tocsr()
     perm = host_amd(As)
     assert sorted(perm.tolist()) == list(range(len(idx)))
+    monkeypatch.setenv("SFCDD_ORDER", "amd")
     x, nnz_l, stored = host_solve(As, np.ones(len(idx)))
     lu = spla.splu(sp.csc_matrix(As), permc_spec="MMD_AT_PLUS_A", options={"SymmetricMode": True})
     assert nnz_l <= 1.10 * lu.L.nnz  # AMD within 10% of SuperLU's MMD fill
     assert stored >= nnz_l
+    np.testing.assert_allclose(As @ x, np.ones(len(idx)), atol=1e-10)
+
+
+@pytest.mark.parametrize("levels,p,bound", [((7, 7), 16, 1.35), ((10, 10), 64, 1.15), ((4, 4, 4), 8, 1.35)])
+def test_nested_dissection_fill(oracle, levels, p, bound, monkeypatch):
+    """The default ordering (hybrid nested dissection, nd.cpp) trades a little
+    fill for a shallow elimination tree; its fill stays within a bound of
+    SuperLU's MMD (the reference's ordering) and the factor solves exactly."""
+    A = oracle.assemble_scaled_laplacian(levels)
+    ov = oracle.enlarge(oracle.disjoint_partition(A.shape[0], p), 0.5)
+    idx = ov[1].indices()
+    As = A[idx][:, idx].tocsr()
+    monkeypatch.setenv("SFCDD_ORDER", "nd")
+    b = np.random.default_rng(1).standard_normal(len(idx))
+    x, nnz_l, stored = host_solve(As, b)
+    lu = spla.splu(sp.csc_matrix(As), permc_spec="MMD_AT_PLUS_A", options={"SymmetricMode": True})
+    assert nnz_l <= bound * lu.L.nnz
+    np.testing.assert_allclose(As @ x, b, atol=1e-10 * np.abs(b).max())
 
 
 @pytest.mark.parametrize("n,seed", [(1, 0), (2, 1), (7, 2), (60, 3), (300, 4)])
