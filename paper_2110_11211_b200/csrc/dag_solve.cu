@@ -50,7 +50,7 @@ struct DagArgs {
   const int32_t* skip;  // optional: nonzero -> whole solve skipped (PCG done)
   unsigned long long* trace;  // optional: per task {sm, t_top, t_deps, t_data, t_end} (ns)
   unsigned long long* ptrace;  // optional: per task 16 clock64 stamps (FRAG phases)
-  int32_t mode;  // tuning switches (SFCDD_DAG_MODE): 1 = acquire polling, 2 = fence before signal
+  int32_t mode;  // tuning switches (SFCDD_DAG_MODE): 1 = acquire polling, 2 = workers release directly
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -113,6 +113,24 @@ __device__ __forceinline__ int32_t ld_relaxed(const int32_t* p) {
   int32_t v;
   asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+
+__device__ __forceinline__ int32_t ld_acquire_cta(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.acquire.cta.shared::cta.s32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_cta(int32_t* p, int32_t v) {
+  asm volatile("st.release.cta.shared::cta.s32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void st_relaxed_cta(int32_t* p, int32_t v) {
+  asm volatile("st.relaxed.cta.shared::cta.s32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void red_relaxed_add(int32_t* p, int32_t v) {
+  asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ void red_release_add(int32_t* p, int32_t v) {
@@ -310,6 +328,45 @@ __device__ __forceinline__ void bwd_packed(const int4* recs, const double* vals,
   }
 }
 
+// backward of packed tiny supernodes (all s <= K <= 4): every lane forms its
+// row's products for the K columns, then ONE segmented inclusive scan over
+// the lanes (log2 of the longest segment steps) sums them per column
+template <int K>
+__device__ __forceinline__ void bwd_tiny(const int4* recs, const double* vals, double* S, int x, int cnt,
+                                         unsigned mask, int lane) {
+  const unsigned upto = mask & ((2u << lane) - 1u);
+  const int seg = __popc(upto) - 1;
+  const int seg_lo = 31 - __clz(upto);
+  const int i = lane - seg_lo;
+  const bool on = seg < cnt;
+  const int4 R = recs[x + (on ? seg : 0)];
+  const int s = rec_s(R), w = s + rec_m(R);
+  const bool ok = on && i < w;
+  const double vi = ok ? S[R.y + i] : 0.0;
+  const double* M = vals + R.z;
+  double p[K];
+  p[0] = ok ? M[i] * vi : 0.0;
+  if (K > 1) p[1] = ok && s > 1 && i >= 1 ? M[w + i - 1] * vi : 0.0;
+  if (K > 2) p[2] = ok && s > 2 && i >= 2 ? M[2 * w + i - 3] * vi : 0.0;
+  if (K > 3) p[3] = ok && s > 3 && i >= 3 ? M[3 * w + i - 6] * vi : 0.0;
+  const unsigned wmax = __reduce_max_sync(FULL, ok ? (unsigned)w : 1u);
+  const int span = 1 << (32 - __clz(wmax - 1 | 1));  // power of two >= longest segment
+  for (int d = 1; d < span; d <<= 1) {
+    double o[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) o[q] = __shfl_up_sync(FULL, p[q], d);
+    if (lane - d >= seg_lo) {
+#pragma unroll
+      for (int q = 0; q < K; ++q) p[q] += o[q];
+    }
+  }
+  if (ok && i == w - 1) {
+#pragma unroll
+    for (int q = 0; q < K; ++q)
+      if (q < s) S[R.w + q] = p[q];
+  }
+}
+
 template <typename Ahead>
 __device__ __forceinline__ void run_frag(const int32_t* h, bool fwd, double* S, const DagArgs& A, const FactorDev& F,
                                          int lane, unsigned long long* pt, Ahead ahead) {
@@ -397,10 +454,24 @@ __device__ __forceinline__ void run_frag(const int32_t* h, bool fwd, double* S, 
       }
       for (int it = L[L_BI0]; it < L[L_BI1]; ++it) {  // columns / packed small supernodes
         const int2 item = items[it];
-        if ((item.x >> 16) == 0)
-          bwd_cols(recs[item.x], vals, S, item.y & 0xffff, item.y >> 16, lane);
-        else
-          bwd_packed(recs, vals, S, item.x & 0xffff, item.x >> 16, (unsigned)item.y, lane);
+        const unsigned ix = (unsigned)item.x;
+        const int cnt = (int)((ix >> 16) & 0x7fffu);
+        if (cnt == 0) {
+          bwd_cols(recs[ix], vals, S, item.y & 0xffff, item.y >> 16, lane);
+        } else if (ix & 0x80000000u) {
+          const unsigned upto = (unsigned)item.y & ((2u << lane) - 1u);
+          const int seg = __popc(upto) - 1;
+          const int sl = seg < cnt ? rec_s(recs[(ix & 0xffffu) + seg]) : 0;
+          const int smax = (int)__reduce_max_sync(FULL, (unsigned)sl);
+          if (smax <= 1)
+            bwd_tiny<1>(recs, vals, S, ix & 0xffffu, cnt, (unsigned)item.y, lane);
+          else if (smax <= 2)
+            bwd_tiny<2>(recs, vals, S, ix & 0xffffu, cnt, (unsigned)item.y, lane);
+          else
+            bwd_tiny<4>(recs, vals, S, ix & 0xffffu, cnt, (unsigned)item.y, lane);
+        } else {
+          bwd_packed(recs, vals, S, ix & 0xffffu, cnt, (unsigned)item.y, lane);
+        }
       }
       __syncwarp();
     }
@@ -518,12 +589,61 @@ __device__ __forceinline__ void run_col(const int32_t* h, double* S, const DagAr
 }
 
 // ================================================================ kernel
+// Completion signaller (one thread per CTA, in an extra warp): workers post
+// the counter index of a finished task to their mailbox (st.release.cta) and
+// move on; the signaller acquires the mailboxes, issues ONE gpu-scope fence
+// for everything collected (cumulative over the workers' writes, which
+// happen-before it through the CTA-scope release/acquire) and then bumps the
+// counters.  The workers never stall on the ~1 us release fence.
 template <int WPB>
-__global__ void __launch_bounds__(WPB * 32, 20 / WPB) k_dag(DagArgs A) {
+__device__ __forceinline__ void signaller(const DagArgs& A, int32_t* mbox, int32_t* nexit) {
+  int32_t v[WPB];
+  for (;;) {
+    int np = 0;
+#pragma unroll
+    for (int w = 0; w < WPB; ++w) {
+      v[w] = ld_acquire_cta(mbox + w);
+      np += v[w] >= 0;
+    }
+    if (np == 0) {
+      if (ld_acquire_cta(nexit) == WPB) {  // workers done: drain once more
+        np = 0;
+#pragma unroll
+        for (int w = 0; w < WPB; ++w) {
+          v[w] = ld_acquire_cta(mbox + w);
+          np += v[w] >= 0;
+        }
+        if (np == 0) return;
+      } else {
+        __nanosleep(20);
+        continue;
+      }
+    }
+    __threadfence();
+#pragma unroll
+    for (int w = 0; w < WPB; ++w)
+      if (v[w] >= 0) {
+        red_relaxed_add(A.ctr + v[w], 1);
+        st_relaxed_cta(mbox + w, -1);
+      }
+  }
+}
+
+template <int WPB>
+__global__ void __launch_bounds__((WPB + 1) * 32, 20 / WPB) k_dag(DagArgs A) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bars[WPB];
+  __shared__ int32_t mbox[WPB];
+  __shared__ int32_t nexit;
   if (A.skip && *A.skip) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x < WPB) mbox[threadIdx.x] = -1;
+  if (threadIdx.x == 0) nexit = 0;
+  __syncthreads();
+  if (warp == WPB) {
+    if (lane == 0) signaller<WPB>(A, mbox, &nexit);
+    return;
+  }
   uint64_t* bar = &bars[warp];
   if (lane == 0) {
     mbar_init(bar, 1);
@@ -543,7 +663,11 @@ __global__ void __launch_bounds__(WPB * 32, 20 / WPB) k_dag(DagArgs A) {
     int t = 0;
     if (lane == 0) t = q + A.nq * atomicAdd(qh, 1);
     t = __shfl_sync(FULL, t, 0);
-    if (t >= A.ntask) break;
+    if (t >= A.ntask) {
+      if (lane == 0)  // release: ordered after this warp's last mailbox post
+        asm volatile("red.release.cta.shared::cta.add.s32 [%0], 1;" ::"r"(smem_u32(&nexit)) : "memory");
+      break;
+    }
     const TaskDev T = A.tasks[t];
     // slot addresses computed from the shared base so the compiler keeps the
     // shared state space (LDS, not generic loads) for every blob/scratch access
@@ -599,8 +723,12 @@ __global__ void __launch_bounds__(WPB * 32, 20 / WPB) k_dag(DagArgs A) {
     __syncwarp();
     if (lane == 0) {
       // release: cumulative over the warp's writes (ordered before it by __syncwarp)
-      if (A.mode & 2) __threadfence();
-      red_release_add(A.ctr + T.signal_idx, 1);
+      if (A.mode & 2) {  // direct release by the worker (old path)
+        red_release_add(A.ctr + T.signal_idx, 1);
+      } else {
+        while (ld_acquire_cta(&mbox[warp]) >= 0) __nanosleep(20);  // signaller still busy with the last one
+        st_release_cta(&mbox[warp], T.signal_idx);
+      }
       if (tr) tr[4] = gtimer();
     }
   }
@@ -656,7 +784,7 @@ DagSolver::DagSolver(const DevicePlan& plan, int device, int64_t extra_xy) : dev
     }
   }
   int per_sm = 0, sms = 0;
-  CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern_, wpb_ * 32, smem_));
+  CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern_, (wpb_ + 1) * 32, smem_));
   CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   SFCDD_REQUIRE(per_sm >= 1, SFCDD_EINTERNAL, "DAG kernel cannot be resident");
   if (const char* e = std::getenv("SFCDD_CTAS_PER_SM")) per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
@@ -693,7 +821,7 @@ void DagSolver::solve(const double* rhs, cudaStream_t st, const int32_t* skip) {
   a.ptrace = trace_ ? trace_ + 5 * (size_t)ntask_ : nullptr;
   a.mode = mode_;
   void* params[] = {&a};
-  CUDA_CHECK(cudaLaunchKernel(kern_, dim3(grid_), dim3(wpb_ * 32), params, smem_, st));
+  CUDA_CHECK(cudaLaunchKernel(kern_, dim3(grid_), dim3((wpb_ + 1) * 32), params, smem_, st));
 }
 
 void DagSolver::set_trace(unsigned long long* dev_buf) { trace_ = dev_buf; }

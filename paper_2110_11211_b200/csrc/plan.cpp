@@ -528,7 +528,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
             }
             if (rows < 32) mask |= 1u << rows;
             SFCDD_REQUIRE(j < 65536 && j1 - j < 32768, SFCDD_EINTERNAL, "packed item index overflow");
-            const uint32_t tiny = (pass == 0 && smax <= 4) ? 0x80000000u : 0u;
+            const uint32_t tiny = smax <= 4 ? 0x80000000u : 0u;
             items.insert(items.end(), {(int32_t)((uint32_t)(j | ((j1 - j) << 16)) | tiny), (int32_t)mask});
             j = j1;
           } else if (pass == 0) {

@@ -61,8 +61,8 @@ struct TaskDev {
 //   * backward row pairs: S[dst] = -S[src]  (dst = v_B slot, src = x slot);
 //   * forward / backward warp items (int2) {x, y}:
 //     x < 65536: row block y (forward) / column y (backward) of supernode x;
-//     x = j | cnt << 16 (| 1 << 31 in forward items whose supernodes all have
-//     s <= 4: straight-line path): cnt consecutive small supernodes j..
+//     x = j | cnt << 16 (| 1 << 31 when the packed supernodes all have
+//     s <= 4: straight-line paths): cnt consecutive small supernodes j..
 //     packed into the 32 lanes, y = bit mask of the lanes where each one
 //     starts (+ end lane).
 enum FragHdr {
