@@ -173,52 +173,33 @@ __device__ __forceinline__ void warp_gather(int n, int lane, Load ld, Store st) 
   }
 }
 
-// one gather-form assembly run with its first contributions' loads issued
-// together: S[dst] + S[src_0] + S[src_1] + ... (fixed order)
-struct RunLoad {
-  int dst, p, p1;
-  double acc, v0, v1, v2;
-};
-__device__ __forceinline__ RunLoad run_load(const int32_t* runs, const int32_t* gp, int r, const double* S) {
-  RunLoad L;
-  const int p0 = runs[r];
-  L.p1 = runs[r + 1];
-  const int n = L.p1 - p0;
+// one gather-form assembly run: S[dst] + S[src_0] + S[src_1] + ... in fixed
+// order.  Runs of <= 3 sources (nearly all) are straight-line: every load is
+// unconditional (indices clamped into the run), the adds are selects.
+__device__ __forceinline__ void run_apply(const int32_t* runs, const int32_t* gp, int r, double* S) {
+  const int p0 = runs[r], p1 = runs[r + 1];
+  const int n = p1 - p0;
   const int32_t g0 = gp[p0];
-  const int32_t g1 = n > 1 ? gp[p0 + 1] : g0;
-  const int32_t g2 = n > 2 ? gp[p0 + 2] : g0;
-  L.dst = lo16(g0);
-  L.acc = S[L.dst];
-  L.v0 = S[hi16(g0)];
-  L.v1 = n > 1 ? S[hi16(g1)] : 0.0;
-  L.v2 = n > 2 ? S[hi16(g2)] : 0.0;
-  L.p = p0 + 3;
-  return L;
-}
-__device__ __forceinline__ void run_finish(RunLoad& L, const int32_t* gp, double* S) {
-  const int n = L.p1 - (L.p - 3);
-  double acc = L.acc + L.v0;
-  if (n > 1) acc += L.v1;
-  if (n > 2) acc += L.v2;
-  for (int p = L.p; p < L.p1; ++p) acc += S[hi16(gp[p])];
-  S[L.dst] = acc;
+  const int32_t g1 = gp[p0 + (n > 1 ? 1 : 0)];
+  const int32_t g2 = gp[p0 + (n > 2 ? 2 : 0)];
+  const int dst = lo16(g0);
+  const double d = S[dst], v0 = S[hi16(g0)], v1 = S[hi16(g1)], v2 = S[hi16(g2)];
+  double acc = d + v0;
+  acc = n > 1 ? acc + v1 : acc;
+  acc = n > 2 ? acc + v2 : acc;
+  for (int p = p0 + 3; p < p1; ++p) acc += S[hi16(gp[p])];
+  S[dst] = acc;
 }
 
-// gather-form assembly runs: S[dst] += sum S[src] over the run (fixed order);
-// two runs per lane in flight
+// gather-form assembly runs of one level; two runs per lane in flight
 __device__ __forceinline__ void gather_runs(const int32_t* runs, const int32_t* gp, int r0, int r1, double* S,
                                             int lane) {
   int r = r0 + lane;
   for (; r + 32 < r1; r += 64) {
-    RunLoad a = run_load(runs, gp, r, S);
-    RunLoad b = run_load(runs, gp, r + 32, S);
-    run_finish(a, gp, S);
-    run_finish(b, gp, S);
+    run_apply(runs, gp, r, S);
+    run_apply(runs, gp, r + 32, S);
   }
-  if (r < r1) {
-    RunLoad a = run_load(runs, gp, r, S);
-    run_finish(a, gp, S);
-  }
+  if (r < r1) run_apply(runs, gp, r, S);
 }
 
 // ===================================================== FRAG (small subtree)
