@@ -51,6 +51,7 @@ struct DagArgs {
   unsigned long long* trace;  // optional: per task {sm, t_top, t_deps, t_data, t_end} (ns)
   unsigned long long* ptrace;  // optional: per task 16 clock64 stamps (FRAG phases)
   int32_t mode;  // tuning switches (SFCDD_DAG_MODE): 1 = acquire polling, 2 = workers release directly
+  int32_t sig_ns;  // signaller idle sleep (ns, SFCDD_SIG_NS)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -596,7 +597,7 @@ __device__ __forceinline__ void signaller(const DagArgs& A, int32_t* mbox, int32
         }
         if (np == 0) return;
       } else {
-        __nanosleep(20);
+        __nanosleep(A.sig_ns);
         continue;
       }
     }
@@ -732,6 +733,7 @@ DagSolver::DagSolver(const DevicePlan& plan, int device, int64_t extra_xy) : dev
   SFCDD_REQUIRE(wpb_ == 2 || wpb_ == 4 || wpb_ == 8, SFCDD_EVALUE, "SFCDD_WPB must be 2, 4 or 8");
   kern_ = wpb_ == 2 ? (const void*)k_dag<2> : wpb_ == 4 ? (const void*)k_dag<4> : (const void*)k_dag<8>;
   if (const char* e = std::getenv("SFCDD_DAG_MODE")) mode_ = std::atoi(e);
+  if (const char* e = std::getenv("SFCDD_SIG_NS")) sig_ns_ = std::atoi(e);
   smem_ = wpb_ * slot_bytes_;
   SFCDD_REQUIRE(smem_ <= 227 * 1024, SFCDD_EINTERNAL, "DAG shared-memory footprint exceeds 227 KB");
   auto up = [&](void** dst, const void* src, size_t bytes) {
@@ -801,6 +803,7 @@ void DagSolver::solve(const double* rhs, cudaStream_t st, const int32_t* skip) {
   a.trace = trace_;
   a.ptrace = trace_ ? trace_ + 5 * (size_t)ntask_ : nullptr;
   a.mode = mode_;
+  a.sig_ns = sig_ns_;
   void* params[] = {&a};
   CUDA_CHECK(cudaLaunchKernel(kern_, dim3(grid_), dim3((wpb_ + 1) * 32), params, smem_, st));
 }

@@ -724,6 +724,32 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
       }
     }
     for (const Group& gr : groups) maxh = std::max(maxh, gr.height);
+    {  // copied bytes vs factor value bytes per task kind
+      double cb[4] = {0, 0, 0, 0}, vb[4] = {0, 0, 0, 0}, nt[4] = {0, 0, 0, 0};
+      for (const TaskDev& T : P.tasks) {
+        cb[T.kind] += T.copy_bytes;
+        vb[T.kind] += 8.0 * T.values;
+        nt[T.kind] += 1;
+      }
+      double dense = 0, sparse = 0, hist[8] = {0};
+      for (const TaskDev& T : P.tasks) {
+        if (T.kind != TK_FRAG_FWD) continue;
+        const int32_t* h = reinterpret_cast<const int32_t*>(P.blobs.data() + T.blob_off);
+        const int32_t* rec = h + h[H_REC] + 4 * h[H_TOP];
+        const double sc = h[H_NCOL], mt = (double)((unsigned)rec[0] >> 16);
+        const double dv = sc * (sc + 1) / 2 + sc * mt;
+        dense += dv;
+        sparse += T.values;
+        const double r = dv / std::max(1, T.values);
+        hist[r < 1.25 ? 0 : r < 1.5 ? 1 : r < 2 ? 2 : r < 3 ? 3 : 4] += 1;
+      }
+      std::fprintf(stderr, "[plan] flattened FRAG values %.1f MB vs sparse %.1f MB (%.2fx); ratio hist <1.25 %.0f <1.5 %.0f <2 %.0f <3 %.0f >=3 %.0f\n",
+                   8 * dense / 1e6, 8 * sparse / 1e6, dense / sparse, hist[0], hist[1], hist[2], hist[3], hist[4]);
+      const char* nm[4] = {"frag_f", "frag_b", "row", "col"};
+      for (int k = 0; k < 4; ++k)
+        std::fprintf(stderr, "[plan] %s: %.0f tasks, copied %.1f MB, values %.1f MB (%.2fx), %.0f B/task\n", nm[k],
+                     nt[k], cb[k] / 1e6, vb[k] / 1e6, cb[k] / std::max(1.0, vb[k]), cb[k] / std::max(1.0, nt[k]));
+    }
     {  // per-level FRAG work profile
       double nl = 0, runs = 0, pairs = 0, fi = 0, bi = 0, bpr = 0, ncol = 0, nxu = 0, nxx = 0, nf = 0, maxr = 0;
       for (const TaskDev& T : P.tasks) {

@@ -1,0 +1,23 @@
+import numpy as np, sys
+d = np.load(sys.argv[1])
+T = d['trace'].astype(np.int64)
+sm, t0, tdep, tdat, tend = T[:,0], T[:,1], T[:,2], T[:,3], T[:,4]
+kind = T[:,5]; cb = T[:,6]; vals = T[:,8]; wait = T[:,9]
+base = t0.min(); 
+print("makespan us", (tend.max()-base)/1e3)
+names = ["frag_f","frag_b","row","col"]
+for k in range(4):
+    m = kind==k
+    print(f"{names[k]:7s} n={m.sum():6d} claim->deps {np.mean(tdep[m]-t0[m])/1e3:6.2f}us  deps->data {np.mean(np.maximum(tdat[m]-tdep[m],0))/1e3:6.2f}  data->end {np.mean(tend[m]-tdat[m])/1e3:6.2f}  total {np.mean(tend[m]-t0[m])/1e3:6.2f}  bytes {cb[m].mean():.0f}")
+# per-warp idle: gaps between consecutive tasks of same warp unknown (no warp id); utilisation over time
+edges = np.linspace(0, (tend.max()-base), 21)
+act = []
+for a,b in zip(edges[:-1], edges[1:]):
+    s = np.clip(np.minimum(tend-base, b) - np.maximum(t0-base, a), 0, None).sum()
+    act.append(s/(b-a))
+print("avg busy warps per 5% window:", [int(x) for x in act])
+byt = []
+for a,b in zip(edges[:-1], edges[1:]):
+    m = (tdat-base>=a)&(tdat-base<b)
+    byt.append(cb[m].sum()/((b-a)*1e-9)/1e9)
+print("GB/s of blob data arriving per window:", [int(x) for x in byt])
