@@ -50,7 +50,8 @@ struct DagArgs {
   const int32_t* skip;  // optional: nonzero -> whole solve skipped (PCG done)
   unsigned long long* trace;  // optional: per task {sm, t_top, t_deps, t_data, t_end} (ns)
   unsigned long long* ptrace;  // optional: per task 16 clock64 stamps (FRAG phases)
-  int32_t mode;  // tuning switches (SFCDD_DAG_MODE): 1 = acquire polling, 2 = workers release directly
+  int32_t mode;  // tuning switches (SFCDD_DAG_MODE): 1 = acquire polling, 2 = workers release directly,
+                 // 4 = blob copies without the L2 evict_first hint
   int32_t sig_ns;  // signaller idle sleep (ns, SFCDD_SIG_NS)
 };
 
@@ -98,6 +99,23 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+
+// the same with an L2 cache policy (evict_first for the streamed factor blobs,
+// so the work vectors the gathers read stay resident in L2)
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 
 __device__ __forceinline__ void fence_proxy_async() {
@@ -664,7 +682,11 @@ __global__ void __launch_bounds__((WPB + 1) * 32, 20 / WPB) k_dag(DagArgs A) {
       // the blob does not depend on other tasks: copy it while waiting
       fence_proxy_async();
       mbar_expect_tx(bar, (uint32_t)T.copy_bytes);
-      bulk_g2s(smem + (size_t)warp * A.slot_bytes, A.blobs + T.blob_off, (uint32_t)T.copy_bytes, bar);
+      if (A.mode & 4)
+        bulk_g2s(smem + (size_t)warp * A.slot_bytes, A.blobs + T.blob_off, (uint32_t)T.copy_bytes, bar);
+      else
+        bulk_g2s_hint(smem + (size_t)warp * A.slot_bytes, A.blobs + T.blob_off, (uint32_t)T.copy_bytes, bar,
+                      policy_evict_first());
       if (T.wait_idx >= 0) {
         // relaxed polling (no L1 invalidation per poll), one acquire at the end
         unsigned ns = 32;

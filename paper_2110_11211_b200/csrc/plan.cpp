@@ -743,6 +743,29 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         const double r = dv / std::max(1, T.values);
         hist[r < 1.25 ? 0 : r < 1.5 ? 1 : r < 2 ? 2 : r < 3 ? 3 : 4] += 1;
       }
+      {
+        double sp_sum = 0, nc_sum = 0, runs_sum = 0, nfr = 0, spx = 0, nx = 0;
+        for (const TaskDev& T : P.tasks) {
+          if (T.kind != TK_FRAG_FWD) continue;
+          const int32_t* h = reinterpret_cast<const int32_t*>(P.blobs.data() + T.blob_off);
+          const int32_t* cl = h + h[H_COLS];
+          std::vector<int32_t> c(cl, cl + h[H_NCOL]);
+          std::sort(c.begin(), c.end());
+          int runs = c.empty() ? 0 : 1;
+          for (size_t i = 1; i < c.size(); ++i) runs += c[i] != c[i - 1] + 1;
+          if (!c.empty()) sp_sum += c.back() - c.front() + 1;
+          nc_sum += c.size();
+          runs_sum += runs;
+          nfr += 1;
+          const int32_t* ex = h + h[H_EXTX];
+          std::vector<int32_t> e(ex, ex + h[H_NEXTX]);
+          std::sort(e.begin(), e.end());
+          if (!e.empty()) spx += e.back() - e.front() + 1;
+          nx += e.size();
+        }
+        std::fprintf(stderr, "[plan] FRAG cols: avg %.1f, ro span %.1f (%.2fx), %.1f runs; ext rows %.1f span %.1f\n",
+                     nc_sum / nfr, sp_sum / nfr, sp_sum / nc_sum, runs_sum / nfr, nx / nfr, spx / nfr);
+      }
       std::fprintf(stderr, "[plan] flattened FRAG values %.1f MB vs sparse %.1f MB (%.2fx); ratio hist <1.25 %.0f <1.5 %.0f <2 %.0f <3 %.0f >=3 %.0f\n",
                    8 * dense / 1e6, 8 * sparse / 1e6, dense / sparse, hist[0], hist[1], hist[2], hist[3], hist[4]);
       const char* nm[4] = {"frag_f", "frag_b", "row", "col"};
