@@ -222,7 +222,8 @@ __device__ __forceinline__ void gather_runs(const int32_t* runs, const int32_t* 
 }
 
 // ===================================================== FRAG (small subtree)
-__device__ __forceinline__ int rec_s(const int4& r) { return r.x & 0xffff; }
+__device__ __forceinline__ int rec_s(const int4& r) { return r.x & 0xfff; }
+__device__ __forceinline__ int rec_lp(const int4& r) { return (r.x >> 12) & 7; }
 __device__ __forceinline__ int rec_m(const int4& r) { return (int)((unsigned)r.x >> 16); }
 
 // forward row i of a supernode: y_i (i < s) or u_i = f_i - (W f_J)_i.
@@ -303,68 +304,40 @@ __device__ __forceinline__ void bwd_cols(const int4 R, const double* vals, doubl
   if (ph == 0 && j < c) S[R.w + k] = acc;
 }
 
-// backward of packed small supernodes: lanes = rows, x_k by segmented scans
-__device__ __forceinline__ void bwd_packed(const int4* recs, const double* vals, double* S, int x, int cnt,
-                                           unsigned mask, int lane) {
+// backward of packed supernodes (s <= 32 each), lanes = (supernode, column
+// k, row phase): 2^lp lanes per column each sum every 2^lp-th row of column
+// k of M against v = [y_J ; -x_B], then a butterfly over the phases (groups
+// are aligned to 2^lp).  Supernodes are in descending record order.
+__device__ __forceinline__ void bwd_lanes(const int4* recs, const double* vals, double* S, int x, int cnt,
+                                          unsigned mask, int lane) {
   const unsigned upto = mask & ((2u << lane) - 1u);
   const int seg = __popc(upto) - 1;
   const int seg_lo = 31 - __clz(upto);
-  const int i = lane - seg_lo;
   const bool on = seg < cnt;
-  const int4 R = recs[x + (on ? seg : 0)];
-  const int s = on ? rec_s(R) : 0, m = rec_m(R);
-  const int smax = (int)__reduce_max_sync(FULL, (unsigned)s);
-  const double vi = on ? S[R.y + i] : 0.0;
-  const double* M = vals + R.z;
-  const bool seg_end = on && i == s + m - 1;
-  for (int k = 0; k < smax; ++k) {
-    double val = (on && k < s && i >= k) ? M[coloff(s, m, k) + (i - k)] * vi : 0.0;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const double o = __shfl_up_sync(FULL, val, d);
-      if (lane - d >= seg_lo) val += o;
+  const int4 R = recs[x + cnt - 1 - (on ? seg : 0)];
+  const int s = rec_s(R), m = rec_m(R), lp = rec_lp(R);
+  const int local = lane - seg_lo;
+  const int k = local >> lp, P = 1 << lp;
+  const bool act = on && k < s;
+  double a0 = 0.0, a1 = 0.0;
+  if (act) {
+    const double* col = vals + R.z + coloff(s, m, k);
+    const double* v = S + R.y + k;
+    const int len = s + m - k;
+    int t = local & (P - 1);
+    for (; t + P < len; t += 2 * P) {
+      a0 = fma(col[t], v[t], a0);
+      a1 = fma(col[t + P], v[t + P], a1);
     }
-    if (seg_end && k < s) S[R.w + k] = val;
+    if (t < len) a0 = fma(col[t], v[t], a0);
   }
-}
-
-// backward of packed tiny supernodes (all s <= K <= 4): every lane forms its
-// row's products for the K columns, then ONE segmented inclusive scan over
-// the lanes (log2 of the longest segment steps) sums them per column
-template <int K>
-__device__ __forceinline__ void bwd_tiny(const int4* recs, const double* vals, double* S, int x, int cnt,
-                                         unsigned mask, int lane) {
-  const unsigned upto = mask & ((2u << lane) - 1u);
-  const int seg = __popc(upto) - 1;
-  const int seg_lo = 31 - __clz(upto);
-  const int i = lane - seg_lo;
-  const bool on = seg < cnt;
-  const int4 R = recs[x + (on ? seg : 0)];
-  const int s = rec_s(R), w = s + rec_m(R);
-  const bool ok = on && i < w;
-  const double vi = ok ? S[R.y + i] : 0.0;
-  const double* M = vals + R.z;
-  double p[K];
-  p[0] = ok ? M[i] * vi : 0.0;
-  if (K > 1) p[1] = ok && s > 1 && i >= 1 ? M[w + i - 1] * vi : 0.0;
-  if (K > 2) p[2] = ok && s > 2 && i >= 2 ? M[2 * w + i - 3] * vi : 0.0;
-  if (K > 3) p[3] = ok && s > 3 && i >= 3 ? M[3 * w + i - 6] * vi : 0.0;
-  const unsigned wmax = __reduce_max_sync(FULL, ok ? (unsigned)w : 1u);
-  const int span = 1 << (32 - __clz(wmax - 1 | 1));  // power of two >= longest segment
-  for (int d = 1; d < span; d <<= 1) {
-    double o[K];
-#pragma unroll
-    for (int q = 0; q < K; ++q) o[q] = __shfl_up_sync(FULL, p[q], d);
-    if (lane - d >= seg_lo) {
-#pragma unroll
-      for (int q = 0; q < K; ++q) p[q] += o[q];
-    }
+  double acc = a0 + a1;
+  const int pmax = (int)__reduce_max_sync(FULL, act ? (unsigned)P : 1u);
+  for (int d = 1; d < pmax; d <<= 1) {
+    const double o = __shfl_xor_sync(FULL, acc, d);
+    if (d < P) acc += o;
   }
-  if (ok && i == w - 1) {
-#pragma unroll
-    for (int q = 0; q < K; ++q)
-      if (q < s) S[R.w + q] = p[q];
-  }
+  if (act && (local & (P - 1)) == 0) S[R.w + k] = acc;
 }
 
 template <typename Ahead>
@@ -438,6 +411,7 @@ __device__ __forceinline__ void run_frag(const int32_t* h, bool fwd, double* S, 
     stamp(14);
     if (pt && lane == 0) pt[15] = nlev;
   } else {
+    stamp(0);
     {  // one batched gather: y at the columns + x of the external ancestor rows
       const int32_t* ex = h + h[H_EXTX];
       const int nx = h[H_NEXTX], xb = h[H_EXTX_BASE];
@@ -445,6 +419,7 @@ __device__ __forceinline__ void run_frag(const int32_t* h, bool fwd, double* S, 
                   [&](int c, double v) { S[c < ncol ? lo16(colpos[c]) : xb + (c - ncol)] = v; });
     }
     __syncwarp();
+    stamp(1);
     for (int lv = nlev - 1; lv >= 0; --lv) {
       const int32_t* L = levtab + L_WORDS * lv;
       if (lv == 0) ahead();
@@ -452,30 +427,23 @@ __device__ __forceinline__ void run_frag(const int32_t* h, bool fwd, double* S, 
         for (int p = L[L_BP0] + lane; p < L[L_BP1]; p += 32) S[lo16(bp[p])] = -S[hi16(bp[p])];
         __syncwarp();
       }
+      const int ls = nlev - 1 - lv;
+      if (ls < 4) stamp(2 + 2 * ls);
       for (int it = L[L_BI0]; it < L[L_BI1]; ++it) {  // columns / packed small supernodes
         const int2 item = items[it];
         const unsigned ix = (unsigned)item.x;
         const int cnt = (int)((ix >> 16) & 0x7fffu);
-        if (cnt == 0) {
+        if (cnt == 0)
           bwd_cols(recs[ix], vals, S, item.y & 0xffff, item.y >> 16, lane);
-        } else if (ix & 0x80000000u) {
-          const unsigned upto = (unsigned)item.y & ((2u << lane) - 1u);
-          const int seg = __popc(upto) - 1;
-          const int sl = seg < cnt ? rec_s(recs[(ix & 0xffffu) + seg]) : 0;
-          const int smax = (int)__reduce_max_sync(FULL, (unsigned)sl);
-          if (smax <= 1)
-            bwd_tiny<1>(recs, vals, S, ix & 0xffffu, cnt, (unsigned)item.y, lane);
-          else if (smax <= 2)
-            bwd_tiny<2>(recs, vals, S, ix & 0xffffu, cnt, (unsigned)item.y, lane);
-          else
-            bwd_tiny<4>(recs, vals, S, ix & 0xffffu, cnt, (unsigned)item.y, lane);
-        } else {
-          bwd_packed(recs, vals, S, ix & 0xffffu, cnt, (unsigned)item.y, lane);
-        }
+        else
+          bwd_lanes(recs, vals, S, ix & 0xffffu, cnt, (unsigned)item.y, lane);
       }
       __syncwarp();
+      if (ls < 4) stamp(3 + 2 * ls);
     }
     for (int c = lane; c < ncol; c += 32) __stcg(xy + cols[c], S[hi16(colpos[c])]);
+    stamp(14);
+    if (pt && lane == 0) pt[15] = nlev;
   }
 }
 
@@ -715,7 +683,7 @@ __global__ void __launch_bounds__((WPB + 1) * 32, 20 / WPB) k_dag(DagArgs A) {
         run_frag(h, true, S, A, F, lane, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);
         break;
       case TK_FRAG_BWD:
-        run_frag(h, false, S, A, F, lane, nullptr, ahead);
+        run_frag(h, false, S, A, F, lane, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);
         break;
       case TK_ROW_FWD:
         run_row(h, S, A, F, lane, ahead);

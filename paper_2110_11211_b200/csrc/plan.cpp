@@ -456,7 +456,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
     for (int32_t i = 0; i < nsn; ++i) {
       const Supernode& S = sn_of(i);
       int32_t* R = &ints[ints[H_REC] + R_WORDS * i];
-      SFCDD_REQUIRE(S.s < 65536 && S.m < 32768, SFCDD_EINTERNAL, "supernode too large for a FRAG record");
+      SFCDD_REQUIRE(S.s < 4096 && S.m < 32768, SFCDD_EINTERNAL, "supernode too large for a FRAG record");
       R[R_SM] = S.s | (S.m << 16);
       R[R_VAL] = (int32_t)vals.size();
       R[R_SCR] = scr[i];
@@ -465,6 +465,76 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
       vals.insert(vals.end(), v, v + packed_size(S.s, S.m));
       nvals += packed_size(S.s, S.m);
     }
+    // Backward items of one level.  Supernodes with s <= 32 are packed into
+    // column-lane items: lanes = (supernode, column k, row phase) with 2^lp
+    // phases per column (lp in bits 12-14 of the record's s|m word), each
+    // lane summing every 2^lp-th row of column k, then a shuffle reduction
+    // over the phases.  Lane order is DESCENDING record order (larger fronts,
+    // hence more phases, first, so segment starts stay aligned to their phase
+    // count); the item is {lo | cnt << 16, mask of segment start lanes (+ the
+    // end lane)} over records [lo, lo + cnt).  Wider supernodes: blocks of up
+    // to 32 columns, lanes = (column, row phase) (bwd_cols).
+    auto emit_bwd_items = [&](int32_t* L, std::vector<int32_t>& its) {
+      L[L_BI0] = (int32_t)its.size() / 2;
+      int32_t j = L[L_REC1] - 1;
+      while (j >= L[L_REC0]) {
+        const Supernode& S = sn_of(j);
+        if (S.s > 32) {
+          for (int32_t k0 = 0; k0 < S.s; k0 += 32)
+            its.insert(its.end(), {j, k0 | (std::min<int32_t>(32, S.s - k0) << 16)});
+          --j;
+          continue;
+        }
+        const int32_t hi = j;
+        int32_t lo = j, lanes = 0;
+        while (lo >= L[L_REC0] && sn_of(lo).s <= 32 && lanes + sn_of(lo).s <= 32 && hi - lo < 31) {
+          lanes += sn_of(lo).s;
+          --lo;
+        }
+        ++lo;
+        const int32_t cnt = hi - lo + 1;
+        std::vector<int32_t> lp(cnt, 0);
+        std::vector<char> frozen(cnt, 0);
+        auto layout = [&](uint32_t* mask_out) -> int32_t {
+          int32_t off = 0;
+          uint32_t mask = 0;
+          for (int32_t q = 0; q < cnt; ++q) {
+            const int32_t Pq = 1 << lp[q];
+            off = (off + Pq - 1) / Pq * Pq;
+            if (off >= 32) return 33;
+            mask |= 1u << off;
+            off += sn_of(hi - q).s * Pq;
+          }
+          if (off < 32) mask |= 1u << off;
+          if (mask_out) *mask_out = mask;
+          return off;
+        };
+        for (;;) {  // give more row phases to the longest columns while the lanes last
+          int32_t best = -1;
+          double bw = 0.0;
+          for (int32_t q = 0; q < cnt; ++q) {
+            const Supernode& T = sn_of(hi - q);
+            const double w = (double)(T.s + T.m) / (1 << lp[q]);
+            if (!frozen[q] && w > bw) {
+              bw = w;
+              best = q;
+            }
+          }
+          if (best < 0 || bw <= 2.0) break;
+          ++lp[best];
+          if (lp[best] > 5 || layout(nullptr) > 32) {
+            --lp[best];
+            frozen[best] = 1;
+          }
+        }
+        uint32_t mask = 0;
+        SFCDD_REQUIRE(layout(&mask) <= 32, SFCDD_EINTERNAL, "backward item lane overflow");
+        for (int32_t q = 0; q < cnt; ++q) ints[ints[H_REC] + R_WORDS * (hi - q) + R_SM] |= lp[q] << 12;
+        its.insert(its.end(), {(int32_t)((uint32_t)lo | ((uint32_t)cnt << 16)), (int32_t)mask});
+        j = lo - 1;
+      }
+      L[L_BI1] = (int32_t)its.size() / 2;
+    };
     std::vector<int32_t> levtab((size_t)L_WORDS * nlev, 0), runs, gpairs, bpairs, items;
     std::vector<std::pair<int32_t, int32_t>> jp;
     int32_t i = 0;
@@ -513,6 +583,10 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
       L[L_BP1] = (int32_t)bpairs.size();
       // warp items: forward (row blocks / packed) then backward (columns / packed)
       for (int pass = 0; pass < 2; ++pass) {
+        if (pass == 1) {
+          emit_bwd_items(L, items);
+          continue;
+        }
         L[pass == 0 ? L_FI0 : L_BI0] = (int32_t)items.size() / 2;
         int32_t j = L[L_REC0];
         while (j < L[L_REC1]) {
@@ -765,6 +839,46 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         }
         std::fprintf(stderr, "[plan] FRAG cols: avg %.1f, ro span %.1f (%.2fx), %.1f runs; ext rows %.1f span %.1f\n",
                      nc_sum / nfr, sp_sum / nfr, sp_sum / nc_sum, runs_sum / nfr, nx / nfr, spx / nfr);
+      }
+      {  // backward item mix
+        double n_tiny = 0, n_pack = 0, n_cols = 0, w_tiny = 0, w_pack = 0, w_cols = 0, smax_pack = 0;
+        for (const TaskDev& T : P.tasks) {
+          if (T.kind != TK_FRAG_BWD) continue;
+          const int32_t* h = reinterpret_cast<const int32_t*>(P.blobs.data() + T.blob_off);
+          const int32_t* lv = h + h[H_LEVELS];
+          const int32_t* it = h + h[H_ITEMS];
+          const int32_t* rc = h + h[H_REC];
+          for (int l = 0; l < h[H_NLEV]; ++l)
+            for (int q = lv[L_WORDS * l + L_BI0]; q < lv[L_WORDS * l + L_BI1]; ++q) {
+              const uint32_t ix = (uint32_t)it[2 * q];
+              const int cnt = (int)((ix >> 16) & 0x7fffu);
+              auto work = [&](int j) {
+                const int s_ = rc[4 * j] & 0xfff, m_ = (int)((unsigned)rc[4 * j] >> 16);
+                return (double)s_ * (s_ + m_) - 0.5 * s_ * (s_ - 1);
+              };
+              if (cnt == 0) {
+                n_cols += 1;
+                w_cols += work(ix);
+              } else {
+                double w = 0, sm = 0;
+                for (int j = 0; j < cnt; ++j) {
+                  w += work((ix & 0xffff) + j);
+                  sm = std::max<double>(sm, rc[4 * ((ix & 0xffff) + j)] & 0xfff);
+                }
+                if (ix & 0x80000000u) {
+                  n_tiny += 1;
+                  w_tiny += w;
+                } else {
+                  n_pack += 1;
+                  w_pack += w;
+                  smax_pack += sm;
+                }
+              }
+            }
+        }
+        std::fprintf(stderr, "[plan] FRAG bwd items: tiny %.0f (%.0f fma each), packed %.0f (%.0f fma, smax %.1f), cols %.0f (%.0f fma)\n",
+                     n_tiny, w_tiny / std::max(1.0, n_tiny), n_pack, w_pack / std::max(1.0, n_pack),
+                     smax_pack / std::max(1.0, n_pack), n_cols, w_cols / std::max(1.0, n_cols));
       }
       std::fprintf(stderr, "[plan] flattened FRAG values %.1f MB vs sparse %.1f MB (%.2fx); ratio hist <1.25 %.0f <1.5 %.0f <2 %.0f <3 %.0f >=3 %.0f\n",
                    8 * dense / 1e6, 8 * sparse / 1e6, dense / sparse, hist[0], hist[1], hist[2], hist[3], hist[4]);

@@ -60,11 +60,15 @@ struct TaskDev {
 //     all with the same dst: S[dst] += sum S[src];
 //   * backward row pairs: S[dst] = -S[src]  (dst = v_B slot, src = x slot);
 //   * forward / backward warp items (int2) {x, y}:
-//     x < 65536: row block y (forward) / column y (backward) of supernode x;
-//     x = j | cnt << 16 (| 1 << 31 when the packed supernodes all have
-//     s <= 4: straight-line paths): cnt consecutive small supernodes j..
-//     packed into the 32 lanes, y = bit mask of the lanes where each one
-//     starts (+ end lane).
+//     x < 65536: row block y (forward) / column block y = k0 | c << 16
+//     (backward) of supernode x;
+//     forward x = j | cnt << 16 (| 1 << 31 when the packed supernodes all
+//     have s <= 4: straight-line paths): cnt consecutive small supernodes
+//     j.. packed into the 32 lanes (lanes = rows), y = bit mask of the lanes
+//     where each one starts (+ end lane);
+//     backward x = j | cnt << 16: supernodes j..j+cnt-1 (s <= 32) packed in
+//     DESCENDING order, lanes = (column, row phase), 2^lp phases (record),
+//     segment starts aligned to 2^lp, y = start mask (+ end lane).
 enum FragHdr {
   H_NSN = 0,
   H_NLEV,
@@ -92,7 +96,9 @@ enum FragHdr {
 // per-level table: record range, forward gather runs, backward row pairs,
 // forward items, backward items
 enum LevField { L_REC0 = 0, L_REC1, L_RUN0, L_RUN1, L_BP0, L_BP1, L_FI0, L_FI1, L_BI0, L_BI1, L_WORDS };
-// per-supernode record: int4 {s | m << 16, scratch slot, value offset, column slot}
+// per-supernode record: int4 {s | lp << 12 | m << 16, scratch slot, value
+// offset, column slot}; lp = log2 of the row phases per column in the
+// supernode's backward column-lane item (s < 4096)
 enum SnRecField { R_SM = 0, R_SCR, R_VAL, R_CPOS, R_WORDS };
 
 // ---------------------------------------------------------- BIG blobs

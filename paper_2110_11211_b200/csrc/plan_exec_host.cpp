@@ -90,13 +90,29 @@ void plan_exec_host(const DevicePlan& P, const double* rhs, double* xy) {
       const int32_t* gp = h + h[H_GPAIRS];
       const int32_t* bp = h + h[H_BPAIRS];
       const int32_t* items = h + h[H_ITEMS];
-      auto rs = [&](const int32_t* R) { return R[R_SM] & 0xffff; };
+      auto rs = [&](const int32_t* R) { return R[R_SM] & 0xfff; };
+      auto rlp = [&](const int32_t* R) { return (R[R_SM] >> 12) & 7; };
       auto rm = [&](const int32_t* R) { return (int32_t)((uint32_t)R[R_SM] >> 16); };
       // rows handled by a warp item, in lane order (also checks the lane masks)
       auto item_rows = [&](int32_t x0, int32_t y, bool forward, auto&& fn) {
         x0 &= 0x7fffffff;  // forward "tiny" flag
         const int32_t cnt = x0 >> 16;
-        if (cnt > 0) {
+        if (cnt > 0 && !forward) {  // column lanes, descending records, segments aligned to 2^lp
+          x0 &= 0xffff;
+          uint32_t mask = 0;
+          int32_t off = 0;
+          for (int32_t q = 0; q < cnt; ++q) {
+            const int32_t* R = recs + R_WORDS * (x0 + cnt - 1 - q);
+            const int32_t Pq = 1 << rlp(R);
+            off = (off + Pq - 1) / Pq * Pq;
+            mask |= 1u << off;
+            off += rs(R) * Pq;
+          }
+          if (off < 32) mask |= 1u << off;
+          SFCDD_REQUIRE(off <= 32 && mask == (uint32_t)y, SFCDD_EINTERNAL, "backward item lane mask mismatch");
+          for (int32_t j = x0; j < x0 + cnt; ++j)
+            for (int32_t k = 0; k < rs(recs + R_WORDS * j); ++k) fn(recs + R_WORDS * j, k);
+        } else if (cnt > 0) {
           x0 &= 0xffff;
           uint32_t mask = 0;
           int32_t rows = 0;

@@ -21,3 +21,21 @@ for a,b in zip(edges[:-1], edges[1:]):
     m = (tdat-base>=a)&(tdat-base<b)
     byt.append(cb[m].sum()/((b-a)*1e-9)/1e9)
 print("GB/s of blob data arriving per window:", [int(x) for x in byt])
+# FRAG phase stamps (clock64): [0] start [1] prologue done [2+2l, 3+2l] level l
+# (assembly / v_B rows, then items) [10] end [11] nlev
+for kind, nm in ((0, "frag_f"), (1, "frag_b")):
+    m = T[:, 5] == kind
+    Pp = T[m][:, 12:24]
+    ok = (Pp[:, 0] > 0) & (Pp[:, 10] > 0)
+    Pp = Pp[ok]
+    if not len(Pp):
+        continue
+    nl = Pp[:, 11]
+    print(f"{nm}: {len(Pp)} tasks, {nl.mean():.2f} levels, {np.mean(Pp[:, 10] - Pp[:, 0]):.0f} cycles; prologue {np.mean(Pp[:, 1] - Pp[:, 0]):.0f}")
+    for l in range(4):
+        sel = nl > l
+        a = np.mean(Pp[sel, 2 + 2 * l] - (Pp[sel, 1] if l == 0 else Pp[sel, 1 + 2 * l]))
+        r = np.mean(Pp[sel, 3 + 2 * l] - Pp[sel, 2 + 2 * l])
+        print(f"   level {l}: n={sel.sum()} first phase {a:.0f} items {r:.0f}")
+    last = np.array([Pp[i, min(3 + 2 * (nl[i] - 1), 9)] for i in range(len(Pp))])
+    print(f"   epilogue {np.mean(Pp[:, 10] - last):.0f}")
