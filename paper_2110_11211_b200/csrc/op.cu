@@ -12,6 +12,8 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -82,6 +84,29 @@ __device__ __forceinline__ double block_sum(double v) {
   return total;
 }
 
+// two deterministic block-wide sums at once (one set of barriers)
+__device__ __forceinline__ double2 block_sum2(double a, double b) {
+  __shared__ double2 red2[VEC_THREADS / 32];
+  __shared__ double2 total2;
+  a = warp_sum(a);
+  b = warp_sum(b);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) red2[warp] = make_double2(a, b);
+  __syncthreads();
+  if (warp == 0) {
+    double2 t = lane < VEC_THREADS / 32 ? red2[lane] : make_double2(0.0, 0.0);
+    t.x = warp_sum(t.x);
+    t.y = warp_sum(t.y);
+    if (lane == 0) total2 = t;
+  }
+  __syncthreads();
+  return total2;
+}
+
+// points of a reduction chunk are processed PT per thread per round, every
+// load of a round issued before any use (memory-level parallelism)
+constexpr int PT = 4;
+
 // last-block election; the last block must reset *ticket
 __device__ __forceinline__ bool last_block(uint32_t* ticket) {
   __shared__ bool am_last;
@@ -140,31 +165,73 @@ __global__ void k_fill_agg(const int64_t* __restrict__ agg_start, int32_t n0, in
 __global__ void k_chunk_sum(const double* __restrict__ v, Chunks C, double* __restrict__ part) {
   const int ch = blockIdx.x;
   double s = 0.0;
-  for (int64_t g = C.start[ch] + threadIdx.x; g < C.start[ch + 1]; g += VEC_THREADS) s += v[g];
+  const int64_t c_end = C.start[ch + 1];
+  for (int64_t g = C.start[ch] + threadIdx.x; g < c_end; g += VEC_THREADS) s += v[g];
   s = block_sum(s);
   if (threadIdx.x == 0) part[ch] = s;
 }
 
-// y0 = A0^{-1} c with c[a] = sum of the chunk partials of aggregate a
+// y0 = A0^{-1} c with c[a] = sum of the chunk partials of aggregate a.
+// Dense GEMV over the redundant coarse inverse (Bank-Holst copy):
+// GEMV_WPR warps per row, 8 independent loads per lane in flight, partial
+// sums combined in a fixed order (bitwise reproducible).  When every
+// aggregate is one chunk (`direct`), c is the partial array itself;
+// otherwise each CTA sums the partials into shared memory first.
+constexpr int GEMV_WPR = 4;
+constexpr int GEMV_ROWS = VEC_THREADS / 32 / GEMV_WPR;
 __global__ void k_coarse_gemv(const double* __restrict__ ainv, const double* __restrict__ part,
                               const int32_t* __restrict__ agg_ptr, int32_t n0, double* __restrict__ y,
-                              const DevState* st) {
+                              const DevState* st, bool direct) {
   if (skip(st)) return;
-  extern __shared__ double c[];
-  for (int a = threadIdx.x; a < n0; a += VEC_THREADS) {
-    double s = 0.0;
-    for (int ch = agg_ptr[a]; ch < agg_ptr[a + 1]; ++ch) s += __ldcg(part + ch);
-    c[a] = s;
+  extern __shared__ double csm[];
+  __shared__ double red[VEC_THREADS / 32];
+  const double* c = part;
+  if (!direct) {
+    for (int a = threadIdx.x; a < n0; a += VEC_THREADS) {
+      double s = 0.0;
+      for (int ch = agg_ptr[a]; ch < agg_ptr[a + 1]; ++ch) s += __ldcg(part + ch);
+      csm[a] = s;
+    }
+    __syncthreads();
+    c = csm;
   }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int row = blockIdx.x * GEMV_ROWS + warp / GEMV_WPR;
+  const int pw = warp % GEMV_WPR;
+  const int span = (n0 + GEMV_WPR - 1) / GEMV_WPR;
+  const int j0 = pw * span, j1 = min(n0, j0 + span);
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  if (row < n0) {
+    const double* ar = ainv + (int64_t)row * n0;
+    int j = j0 + lane;
+    for (; j + 7 * 32 < j1; j += 8 * 32) {
+      double v[8], cv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        v[u] = __ldg(ar + j + 32 * u);
+        cv[u] = direct ? __ldcg(c + j + 32 * u) : c[j + 32 * u];
+      }
+      a0 = fma(v[0], cv[0], a0);
+      a1 = fma(v[1], cv[1], a1);
+      a2 = fma(v[2], cv[2], a2);
+      a3 = fma(v[3], cv[3], a3);
+      a0 = fma(v[4], cv[4], a0);
+      a1 = fma(v[5], cv[5], a1);
+      a2 = fma(v[6], cv[6], a2);
+      a3 = fma(v[7], cv[7], a3);
+    }
+    for (; j < j1; j += 32) a0 = fma(__ldg(ar + j), direct ? __ldcg(c + j) : c[j], a0);
+  }
+  const double acc = warp_sum((a0 + a1) + (a2 + a3));
+  if (lane == 0) red[warp] = acc;
   __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int row = blockIdx.x * (VEC_THREADS / 32) + (threadIdx.x >> 5);
-  if (row >= n0) return;
-  const double* ar = ainv + (int64_t)row * n0;
-  double acc = 0.0;
-  for (int j = lane; j < n0; j += 32) acc = fma(__ldg(ar + j), c[j], acc);
-  acc = warp_sum(acc);
-  if (lane == 0) y[row] = acc;
+  if (threadIdx.x < GEMV_ROWS) {
+    const int r = blockIdx.x * GEMV_ROWS + threadIdx.x;
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < GEMV_WPR; ++k) t += red[threadIdx.x * GEMV_WPR + k];
+    if (r < n0) y[r] = t;
+  }
 }
 
 // t = g - Â R0^T y0   (schwarz.py:116: g - A @ F(g))
@@ -226,6 +293,42 @@ __global__ void k_combine(CombineArgs C, double* __restrict__ w, const DevState*
   w[g] = acc;
 }
 
+// The same combination, one CTA per reduction chunk: the chunk's candidate
+// subdomains (every overlapped range meeting the chunk, ascending index =
+// the reference's accumulation order) are staged in shared memory once, so
+// a point costs one range test and one load per covering subdomain.
+constexpr int COMBINE_MAXC = 32;
+__global__ void k_combine_chunk(CombineArgs C, const int64_t* __restrict__ cstart,
+                                const int32_t* __restrict__ ccand_ptr, const int32_t* __restrict__ ccand,
+                                double* __restrict__ w, const DevState* st) {
+  if (skip(st)) return;
+  __shared__ int64_t s_start[COMBINE_MAXC], s_len[COMBINE_MAXC], s_off[COMBINE_MAXC];
+  __shared__ double s_w[COMBINE_MAXC];
+  const int ch = blockIdx.x;
+  const int c0 = ccand_ptr[ch], nc = ccand_ptr[ch + 1] - c0;
+  const bool faulty = C.fault != nullptr && *C.apply_calls == C.fault_index;
+  if (threadIdx.x < nc) {
+    const int i = ccand[c0 + threadIdx.x];
+    s_start[threadIdx.x] = C.ov_start[i];
+    // a faulted subdomain contributes nothing in the fault apply
+    s_len[threadIdx.x] = (faulty && C.fault[i]) ? 0 : C.ov_len[i];
+    s_off[threadIdx.x] = C.xy_off[i];
+    s_w[threadIdx.x] = C.wgt[i];
+  }
+  __syncthreads();
+  const int64_t g1 = cstart[ch + 1];
+  for (int64_t g = cstart[ch] + threadIdx.x; g < g1; g += VEC_THREADS) {
+    const double dw = C.count ? 1.0 / (double)C.count[g] : 0.0;
+    double acc = 0.0;
+    for (int c = 0; c < nc; ++c) {
+      int64_t off = g - s_start[c];
+      if (off < 0) off += C.n;
+      if (off < s_len[c]) acc = __dadd_rn(acc, __dmul_rn(C.count ? dw : s_w[c], __ldcg(C.xy + s_off[c] + off)));
+    }
+    w[g] = acc;
+  }
+}
+
 // per-chunk partials of sum (Â w) -> R0 Â w  (coarse.py:84 project_transpose)
 __global__ void k_matvec_chunk(const double* __restrict__ w, Stencil S, Chunks C, double* __restrict__ part,
                                const DevState* st) {
@@ -249,12 +352,27 @@ __global__ void k_finalize(const double* __restrict__ w, const double* __restric
   const double c0 = (mode >= 1 && a >= 0) ? y0[a] : 0.0;
   const double c1 = (mode >= 2 && a >= 0) ? y0b[a] : 0.0;
   double s = 0.0;
-  for (int64_t g = C.start[ch] + threadIdx.x; g < C.start[ch + 1]; g += VEC_THREADS) {
-    double v = w[g];
-    if (mode == 1) v = v + c0;
-    if (mode == 2) v = (v - c1) + c0;
-    h[g] = v;
-    if (rdot) s = fma(rdot[g], v, s);
+  const int64_t e1 = C.start[ch + 1];
+  for (int64_t b = C.start[ch] + threadIdx.x; b < e1; b += PT * VEC_THREADS) {
+    double wv[PT], rv[PT];
+#pragma unroll
+    for (int u = 0; u < PT; ++u) {
+      const int64_t g = b + (int64_t)u * VEC_THREADS;
+      const bool ok = g < e1;
+      wv[u] = ok ? w[g] : 0.0;
+      rv[u] = ok && rdot ? rdot[g] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < PT; ++u) {
+      const int64_t g = b + (int64_t)u * VEC_THREADS;
+      if (g < e1) {
+        double v = wv[u];
+        if (mode == 1) v = v + c0;
+        if (mode == 2) v = (v - c1) + c0;
+        h[g] = v;
+        if (rdot) s = fma(rv[u], v, s);
+      }
+    }
   }
   if (rdot) {
     s = block_sum(s);
@@ -285,7 +403,8 @@ __global__ void k_residual0(const double* __restrict__ b, const double* __restri
                             double* __restrict__ part_c, DevState* st, double* hist) {
   const int ch = blockIdx.x;
   double rr = 0.0, cs = 0.0;
-  for (int64_t g = C.start[ch] + threadIdx.x; g < C.start[ch + 1]; g += VEC_THREADS) {
+  const int64_t c_end = C.start[ch + 1];
+  for (int64_t g = C.start[ch] + threadIdx.x; g < c_end; g += VEC_THREADS) {
     const double v = b[g] - stencil_at(S, x, g);
     r[g] = v;
     rr = fma(v, v, rr);
@@ -356,19 +475,35 @@ __global__ void k_update(double* __restrict__ x, double* __restrict__ r, const d
   if (skip(st)) return;
   const double alpha = st->alpha;
   const int ch = blockIdx.x;
+  const int64_t c0 = C.start[ch], c1 = C.start[ch + 1];
   double rr = 0.0, cs = 0.0;
-  for (int64_t g = C.start[ch] + threadIdx.x; g < C.start[ch + 1]; g += VEC_THREADS) {
-    x[g] = __dadd_rn(x[g], __dmul_rn(alpha, p[g]));
-    const double v = __dsub_rn(r[g], __dmul_rn(alpha, ap[g]));
-    r[g] = v;
-    rr = fma(v, v, rr);
-    cs += v;
+  for (int64_t b = c0 + threadIdx.x; b < c1; b += PT * VEC_THREADS) {
+    double xv[PT], pv[PT], rv[PT], av[PT];
+#pragma unroll
+    for (int u = 0; u < PT; ++u) {
+      const int64_t g = b + (int64_t)u * VEC_THREADS;
+      const bool ok = g < c1;
+      xv[u] = ok ? x[g] : 0.0;
+      pv[u] = ok ? p[g] : 0.0;
+      rv[u] = ok ? r[g] : 0.0;
+      av[u] = ok ? ap[g] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < PT; ++u) {
+      const int64_t g = b + (int64_t)u * VEC_THREADS;
+      if (g < c1) {
+        x[g] = __dadd_rn(xv[u], __dmul_rn(alpha, pv[u]));
+        const double v = __dsub_rn(rv[u], __dmul_rn(alpha, av[u]));
+        r[g] = v;
+        rr = fma(v, v, rr);
+        cs += v;
+      }
+    }
   }
-  rr = block_sum(rr);
-  cs = block_sum(cs);
+  const double2 red = block_sum2(rr, cs);
   if (threadIdx.x == 0) {
-    part_rr[ch] = rr;
-    part_c[ch] = cs;
+    part_rr[ch] = red.x;
+    part_c[ch] = red.y;
   }
   if (last_block(&st->ticket[2])) {
     const double tot = reduce_partials(part_rr, gridDim.x);
@@ -429,6 +564,35 @@ static T* dev_upload(sfcdd_op* op, const std::vector<T>& v) {
   return p;
 }
 
+// optional per-kernel timing (sfcdd_op_profile with SFCDD_PROFILE_KERNELS=1):
+// an event after every launch of apply_device / pcg_iteration
+struct KernelTimer {
+  std::vector<cudaEvent_t> ev;
+  std::vector<const char*> name;
+  std::vector<double> ms;
+  size_t idx = 0;
+};
+static KernelTimer* g_ktimer = nullptr;
+static void kmark(cudaStream_t st, const char* name) {
+  KernelTimer* k = g_ktimer;
+  if (!k) return;
+  if (k->idx == k->ev.size()) {
+    cudaEvent_t e;
+    CUDA_CHECK(cudaEventCreate(&e));
+    k->ev.push_back(e);
+    k->name.push_back(name);
+    k->ms.push_back(0.0);
+  }
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  CUDA_CHECK(cudaStreamIsCapturing(st, &cap));
+  if (cap == cudaStreamCaptureStatusActive)  // an event-record node of the graph
+    CUDA_CHECK(cudaEventRecordWithFlags(k->ev[k->idx], st, cudaEventRecordExternal));
+  else
+    CUDA_CHECK(cudaEventRecord(k->ev[k->idx], st));
+  k->name[k->idx] = name;
+  ++k->idx;
+}
+
 static int mode_of(int variant) {
   switch (variant) {
     case SFCDD_VARIANT_ONE_LEVEL: return 0;
@@ -448,18 +612,24 @@ static void apply_device(sfcdd_op* op, const double* g, double* h, cudaStream_t 
   const DevState* sk = pcg ? op->st : nullptr;
   const int v = op->variant;
   const bool coarse = v != SFCDD_VARIANT_ONE_LEVEL;
-  const size_t csm = (size_t)op->n0 * sizeof(double);
-  const unsigned cgrid = nblocks(op->n0, VEC_THREADS / 32);
+  const bool direct = op->nch == op->n0;  // one chunk per aggregate: c = partials
+  const size_t csm = direct ? 0 : (size_t)op->n0 * sizeof(double);
+  const unsigned cgrid = nblocks(op->n0, GEMV_ROWS);
   if (coarse) {
     if (!partials_ready) k_chunk_sum<<<op->nch, VEC_THREADS, 0, st>>>(g, C, op->part_c);
-    k_coarse_gemv<<<cgrid, VEC_THREADS, csm, st>>>(op->ainv, op->part_c, op->agg_ptr, op->n0, op->y0, sk);
+    if (!partials_ready) kmark(st, "chunk_sum");
+    k_coarse_gemv<<<cgrid, VEC_THREADS, csm, st>>>(op->ainv, op->part_c, op->agg_ptr, op->n0, op->y0, sk,
+                                                   direct);
+    kmark(st, "coarse_gemv");
   }
   const double* rhs = g;
   if (v == SFCDD_VARIANT_BALANCED) {
     k_tvec<<<nblocks(op->n, VEC_THREADS), VEC_THREADS, 0, st>>>(g, op->y0, op->agg, S, op->t, sk);
+    kmark(st, "tvec");
     rhs = op->t;
   }
   op->dag->solve(rhs, st, sk ? &op->st->done : nullptr);
+  kmark(st, "dag");
   CombineArgs ca;
   ca.xy = op->dag->xy();
   ca.ov_start = op->d_ov_start;
@@ -475,14 +645,19 @@ static void apply_device(sfcdd_op* op, const double* g, double* h, cudaStream_t 
   ca.fault_index = op->stats.reserved[0];
   ca.p = op->p;
   ca.n = op->n;
-  k_combine<<<nblocks(op->n, VEC_THREADS), VEC_THREADS, 0, st>>>(ca, op->w, sk);
+  k_combine_chunk<<<op->nch, VEC_THREADS, 0, st>>>(ca, op->chunk_start, op->ccand_ptr, op->ccand, op->w, sk);
+  kmark(st, "combine");
   const int mode = mode_of(v);
   if (mode == 2) {
     k_matvec_chunk<<<op->nch, VEC_THREADS, 0, st>>>(op->w, S, C, op->part_b, sk);
-    k_coarse_gemv<<<cgrid, VEC_THREADS, csm, st>>>(op->ainv, op->part_b, op->agg_ptr, op->n0, op->y0b, sk);
+    kmark(st, "matvec_chunk");
+    k_coarse_gemv<<<cgrid, VEC_THREADS, csm, st>>>(op->ainv, op->part_b, op->agg_ptr, op->n0, op->y0b, sk,
+                                                   direct);
+    kmark(st, "coarse_gemv2");
   }
   k_finalize<<<op->nch, VEC_THREADS, 0, st>>>(op->w, op->y0, op->y0b, C, mode, h, pcg ? op->r : nullptr,
                                               op->part_a, dst, pcg);
+  kmark(st, "finalize");
   CUDA_CHECK(cudaGetLastError());
 }
 
@@ -491,8 +666,10 @@ static void pcg_iteration(sfcdd_op* op, double* x, const double* pold, double* p
   const Stencil S = stencil_of(op);
   const Chunks C = chunks_of(op);
   k_pm<<<op->nch, VEC_THREADS, 0, st>>>(op->z, pold, S, C, pnew, op->ap, op->part_a, op->st);
+  kmark(st, "pm");
   k_update<<<op->nch, VEC_THREADS, 0, st>>>(x, op->r, pnew, op->ap, C, op->part_b, op->part_c, op->st,
                                             op->hist);
+  kmark(st, "update");
   apply_device(op, op->r, op->z, st, true, true);
 }
 
@@ -712,6 +889,34 @@ extern "C" int sfcdd_op_setup(sfcdd_op* op, void* stream) {
   }
   op->cand_ptr = dev_upload(op, cptr);
   op->cand = dev_upload(op, cand);
+  {  // per reduction chunk: the subdomains meeting it, ascending (k_combine_chunk)
+    std::vector<int64_t> cs((size_t)op->nch + 1);
+    CUDA_CHECK(cudaMemcpy(cs.data(), op->chunk_start, cs.size() * 8, cudaMemcpyDeviceToHost));
+    std::vector<int32_t> qptr{0}, qc;
+    std::vector<int32_t> tmp;
+    for (int32_t ch = 0; ch < op->nch; ++ch) {
+      const int64_t c0 = cs[ch], c1 = cs[ch + 1];
+      // owners of the chunk's points: disjoint ranges k with [dj_k) meeting [c0, c1)
+      int k0 = (int)(std::upper_bound(op->dj_start.begin(), op->dj_start.end(), c0) - op->dj_start.begin()) - 1;
+      tmp.clear();
+      for (int k = std::max(k0, 0); k < op->p && op->dj_start[k] < c1; ++k)
+        for (int e = cptr[k]; e < cptr[k + 1]; ++e) {
+          const int i = cand[e];
+          const int64_t st0 = op->ov_start[i], l = op->ov_len[i];
+          int64_t off = c0 - st0;  // does cyclic range i meet [c0, c1)?
+          if (off < 0) off += n;
+          const bool hit = off < l || (st0 >= c0 && st0 < c1);
+          if (hit) tmp.push_back(i);
+        }
+      std::sort(tmp.begin(), tmp.end());
+      tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+      SFCDD_REQUIRE((int)tmp.size() <= COMBINE_MAXC, SFCDD_EINTERNAL, "too many subdomains meet one chunk");
+      qc.insert(qc.end(), tmp.begin(), tmp.end());
+      qptr.push_back((int32_t)qc.size());
+    }
+    op->ccand_ptr = dev_upload(op, qptr);
+    op->ccand = dev_upload(op, qc);
+  }
   op->d_ov_start = dev_upload(op, op->ov_start);
   op->d_ov_len = dev_upload(op, op->ov_len);
   op->d_xy_off = dev_upload(op, xyoff);
@@ -959,6 +1164,85 @@ extern "C" int sfcdd_op_profile(sfcdd_op* op, const double* g_dev, double* scrat
   CUDA_CHECK(cudaEventSynchronize(op->ev1));
   CUDA_CHECK(cudaEventElapsedTime(&t, op->ev0, op->ev1));
   ms[2] = t / reps;
+  if (std::getenv("SFCDD_PROFILE_KERNELS")) {
+    // one PCG iteration's kernels, each timed by the events between launches
+    // (warm, back to back on the stream; the solver state is reset per rep so
+    // no kernel early-exits)
+    KernelTimer kt;
+    if (op->hist_cap < 2) {  // k_update records the residual history
+      if (op->hist) CUDA_CHECK(cudaFree(op->hist));
+      op->hist = (double*)dev_alloc(op, 2 * 8);
+      op->hist_cap = 2;
+    }
+    double* xs = (double*)dev_alloc(op, op->n * 8);
+    CUDA_CHECK(cudaMemsetAsync(xs, 0, op->n * 8, st));
+    CUDA_CHECK(cudaMemsetAsync(op->p0, 0, op->n * 8, st));
+    CUDA_CHECK(cudaMemcpyAsync(op->r, g_dev, op->n * 8, cudaMemcpyDeviceToDevice, st));
+    CUDA_CHECK(cudaMemcpyAsync(op->z, g_dev, op->n * 8, cudaMemcpyDeviceToDevice, st));
+    // captured as a CUDA graph (event-record nodes between the kernels), as
+    // the PCG loop runs it, so host launch latency is not measured
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    cudaGraph_t graph;
+    cudaGraphExec_t gexec;
+    cudaStream_t cs = op->own_stream;
+    CUDA_CHECK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    k_zero_state_pcg<<<1, 1, 0, cs>>>(op->st, 1e-300, 1 << 30);
+    g_ktimer = &kt;
+    kt.idx = 0;
+    kmark(cs, "start");
+    pcg_iteration(op, xs, op->p0, op->p1, cs);
+    g_ktimer = nullptr;
+    CUDA_CHECK(cudaStreamEndCapture(cs, &graph));
+    CUDA_CHECK(cudaGraphInstantiate(&gexec, graph, 0));
+    CUDA_CHECK(cudaGraphDestroy(graph));
+    for (int i = 0; i < reps + 1; ++i) {
+      CUDA_CHECK(cudaGraphLaunch(gexec, st));
+      CUDA_CHECK(cudaStreamSynchronize(st));
+      if (i == 0) continue;  // warm-up
+      for (size_t e = 1; e < kt.idx; ++e) {
+        float dt = 0.f;
+        CUDA_CHECK(cudaEventElapsedTime(&dt, kt.ev[e - 1], kt.ev[e]));
+        kt.ms[e] += dt / reps;
+      }
+    }
+    double tot = 0.0;
+    for (size_t e = 1; e < kt.idx; ++e) tot += kt.ms[e];
+    for (size_t e = 1; e < kt.idx; ++e)
+      std::fprintf(stderr, "[kernels] %-14s %8.1f us\n", kt.name[e], 1e3 * kt.ms[e]);
+    std::fprintf(stderr, "[kernels] %-14s %8.1f us\n", "total", 1e3 * tot);
+    CUDA_CHECK(cudaGraphExecDestroy(gexec));
+    {  // each vector kernel alone, 20 back-to-back launches
+      const Stencil S = stencil_of(op);
+      const Chunks C = chunks_of(op);
+      const bool direct = op->nch == op->n0;
+      const size_t csm = direct ? 0 : (size_t)op->n0 * sizeof(double);
+      const unsigned cgrid = nblocks(op->n0, GEMV_ROWS);
+      auto iso = [&](const char* name, auto fn) {
+        fn();
+        CUDA_CHECK(cudaEventRecord(op->ev0, st));
+        for (int i = 0; i < 20; ++i) fn();
+        CUDA_CHECK(cudaEventRecord(op->ev1, st));
+        CUDA_CHECK(cudaEventSynchronize(op->ev1));
+        float dt = 0.f;
+        CUDA_CHECK(cudaEventElapsedTime(&dt, op->ev0, op->ev1));
+        std::fprintf(stderr, "[isolated] %-14s %8.1f us\n", name, 1e3 * dt / 20);
+      };
+      iso("gemv", [&] {
+        k_coarse_gemv<<<cgrid, VEC_THREADS, csm, st>>>(op->ainv, op->part_c, op->agg_ptr, op->n0, op->y0, nullptr,
+                                                       direct);
+      });
+      iso("tvec", [&] {
+        k_tvec<<<nblocks(op->n, VEC_THREADS), VEC_THREADS, 0, st>>>(op->r, op->y0, op->agg, S, op->t, nullptr);
+      });
+      iso("matvec_chunk", [&] { k_matvec_chunk<<<op->nch, VEC_THREADS, 0, st>>>(op->w, S, C, op->part_b, nullptr); });
+      iso("matvec", [&] { k_matvec<<<nblocks(op->n, VEC_THREADS), VEC_THREADS, 0, st>>>(op->w, S, op->t); });
+      iso("chunk_sum", [&] { k_chunk_sum<<<op->nch, VEC_THREADS, 0, st>>>(op->w, C, op->part_c); });
+      iso("copy", [&] { CUDA_CHECK(cudaMemcpyAsync(op->t, op->w, op->n * 8, cudaMemcpyDeviceToDevice, st)); });
+    }
+    for (cudaEvent_t e : kt.ev) cudaEventDestroy(e);
+    CUDA_CHECK(cudaFree(xs));
+    op->dev_bytes -= op->n * 8;
+  }
   long long zero = 0;
   CUDA_CHECK(cudaMemcpy(&op->st->apply_calls, &zero, sizeof(zero), cudaMemcpyHostToDevice));
   if (launches) {
@@ -1054,7 +1338,8 @@ extern "C" void sfcdd_op_destroy(sfcdd_op* op) {
   cudaSetDevice(op->device);
   if (op->pcg_graph) cudaGraphExecDestroy(op->pcg_graph);
   void* ptrs[] = {op->nbr, op->agg, op->chunk_start, op->chunk_agg, op->agg_ptr, op->ainv, op->d_ov_start,
-                  op->d_ov_len, op->d_xy_off, op->d_dj_start, op->cand_ptr, op->cand, op->d_wgt, op->d_count,
+                  op->d_ov_len, op->d_xy_off, op->d_dj_start, op->cand_ptr, op->cand, op->ccand_ptr, op->ccand,
+                  op->d_wgt, op->d_count,
                   op->d_fault, op->st, op->hist, op->t, op->w, op->y0, op->y0b, op->part_a, op->part_b,
                   op->part_c, op->r, op->z, op->p0, op->p1, op->ap};
   for (void* p : ptrs)
@@ -1079,7 +1364,8 @@ __global__ void k_sh_residual(const double* __restrict__ b, const double* __rest
                               int ch0, double* __restrict__ r, double* __restrict__ prr, double* __restrict__ pc) {
   const int ch = ch0 + blockIdx.x;
   double rr = 0.0, cs = 0.0;
-  for (int64_t g = C.start[ch] + threadIdx.x; g < C.start[ch + 1]; g += VEC_THREADS) {
+  const int64_t c_end = C.start[ch + 1];
+  for (int64_t g = C.start[ch] + threadIdx.x; g < c_end; g += VEC_THREADS) {
     const double v = b[g] - stencil_at(S, x, g);
     r[g] = v;
     rr = fma(v, v, rr);
@@ -1098,7 +1384,8 @@ __global__ void k_sh_pm(const double* __restrict__ z, const double* __restrict__
                         double* __restrict__ part) {
   const int ch = ch0 + blockIdx.x;
   double s = 0.0;
-  for (int64_t g = C.start[ch] + threadIdx.x; g < C.start[ch + 1]; g += VEC_THREADS) {
+  const int64_t c_end = C.start[ch + 1];
+  for (int64_t g = C.start[ch] + threadIdx.x; g < c_end; g += VEC_THREADS) {
     const double pg = __dadd_rn(z[g], __dmul_rn(beta, pold[g]));
     double acc = S.dhat * pg;
     for (int a = 0; a < 2 * S.d; ++a) {
@@ -1118,7 +1405,8 @@ __global__ void k_sh_update(double* __restrict__ x, double* __restrict__ r, cons
                             double* __restrict__ prr, double* __restrict__ pc) {
   const int ch = ch0 + blockIdx.x;
   double rr = 0.0, cs = 0.0;
-  for (int64_t g = C.start[ch] + threadIdx.x; g < C.start[ch + 1]; g += VEC_THREADS) {
+  const int64_t c_end = C.start[ch + 1];
+  for (int64_t g = C.start[ch] + threadIdx.x; g < c_end; g += VEC_THREADS) {
     x[g] = __dadd_rn(x[g], __dmul_rn(alpha, p[g]));
     const double v = __dsub_rn(r[g], __dmul_rn(alpha, ap[g]));
     r[g] = v;
@@ -1137,7 +1425,8 @@ __global__ void k_sh_stencil_chunks(const double* __restrict__ w, Stencil S, Chu
                                     double* __restrict__ part) {
   const int ch = ch0 + blockIdx.x;
   double s = 0.0;
-  for (int64_t g = C.start[ch] + threadIdx.x; g < C.start[ch + 1]; g += VEC_THREADS) s += stencil_at(S, w, g);
+  const int64_t c_end = C.start[ch + 1];
+  for (int64_t g = C.start[ch] + threadIdx.x; g < c_end; g += VEC_THREADS) s += stencil_at(S, w, g);
   s = block_sum(s);
   if (threadIdx.x == 0) part[ch] = s;
 }
@@ -1150,7 +1439,8 @@ __global__ void k_sh_finalize(const double* __restrict__ w, const double* __rest
   const double c0 = mode >= 1 ? y0[a] : 0.0;
   const double c1 = mode >= 2 ? y0b[a] : 0.0;
   double s = 0.0;
-  for (int64_t g = C.start[ch] + threadIdx.x; g < C.start[ch + 1]; g += VEC_THREADS) {
+  const int64_t c_end = C.start[ch + 1];
+  for (int64_t g = C.start[ch] + threadIdx.x; g < c_end; g += VEC_THREADS) {
     double v = w[g];
     if (mode == 1) v = v + c0;
     if (mode == 2) v = (v - c1) + c0;

@@ -69,6 +69,8 @@ struct sfcdd_op {
   int64_t* d_dj_start = nullptr;  // p + 1
   int32_t* cand_ptr = nullptr;
   int32_t* cand = nullptr;
+  int32_t* ccand_ptr = nullptr;  // per reduction chunk (nch + 1)
+  int32_t* ccand = nullptr;
   double* d_wgt = nullptr;     // per subdomain weight (omega / 1)
   int32_t* d_count = nullptr;  // per point cover count (d_matrix weighting)
   int8_t* d_fault = nullptr;   // per subdomain fault mask

@@ -1,6 +1,6 @@
 """Per-CUDA-line stall samples / instructions from an ncu report.
 
-    python tools/ncu_lines.py report.ncu-rep [top]
+    python tools/ncu_lines.py report.ncu-rep [top] [kernel filter, e.g. regex:k_update]
 """
 import csv
 import io
@@ -9,7 +9,8 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass,cuda"],
+kern = ["-k", sys.argv[3]] if len(sys.argv) > 3 else []  # e.g. regex:k_update
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass,cuda", *kern],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr = None
