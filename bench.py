@@ -46,7 +46,9 @@ CONFIGS = {
     "c1": ((7, 7), 16, 0.5, 4, "C1: 2D 127^2 interior (l=(7,7)), P=16, gamma=0.5, q=4"),
     "c2": ((10, 10), 64, 0.5, 16, "C2: 2D 1023^2 interior (l=(10,10)), P=64, gamma=0.5 (delta=H/4), q=16 (32x32 coarse)"),
     "c3": ((7, 7, 7), 512, 0.5, 8, "C3: 3D 127^3 interior (l=(7,7,7)), P=512, gamma=0.5, q=8 (16^3 coarse)"),
-    "c4": ((12, 12), 256, 0.5, 16, "C4: 2D 4095^2 interior (l=(12,12)), P=256, gamma=0.5, q=16 (64x64 coarse)"),
+    "c4": ((12, 12), 256, 0.5, 16, "C4: 2D 4095^2 interior (l=(12,12)), P=256, gamma=0.5, q=16 (64x64 coarse); "
+                                   "fault mode: apply 5 of every solve zeroes the local pieces of "
+                                   "default_rng(42).choice(256, 26) (SURVEY §8(d))"),
 }
 METRIC = "PCG DOF-iterations/s (SFC two-level Schwarz, Poisson)"
 UNIT = "DOF-it/s"
@@ -322,6 +324,8 @@ def run_gpu(args, cfg):
     op = sf.setup(Ah, part, sf.build_coarse(part, Ah, q), sf.SchwarzConfig("balanced", "omega", gamma, q))
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t0
+    if args.config == "c4":  # BASELINE configs[3]: fault-tolerance mode
+        op.set_fault(5, np.random.default_rng(42).choice(p, size=int(round(0.1 * p)), replace=False))
     stats = op.stats()
     log(f"setup {setup_s:.2f}s stats={stats}")
     dev = torch.device("cuda", local)

@@ -530,6 +530,7 @@ __global__ void k_zero_state_pcg(DevState* st, double tol, int32_t max_iters) {
   st->rz = st->beta = st->pap = st->alpha = 0;
   st->k = st->converged = st->breakdown = st->exhausted = st->have_rz = st->done = 0;
   st->max_iters = max_iters;
+  st->apply_calls = 0;  // fault mode counts preconditioner calls per solve
   for (int i = 0; i < 8; ++i) st->ticket[i] = 0;
 }
 
