@@ -124,6 +124,22 @@ int sfcdd_op_matvec(sfcdd_op* op, const double* x_dev, double* y_dev, void* stre
 int sfcdd_op_pcg(sfcdd_op* op, const double* b_dev, double* x_dev, double tol,
                  int32_t max_iters, double* res_hist_host, int32_t* iters,
                  int32_t* converged, void* stream);
+/* PCG with the reference tracker's full semantics (krylov.py:171-200):
+ * exact_dev (nullable) = the exact solution; when given, energy_hist_host
+ * receives ||x_k - x*||_A = sqrt(max(e.(b - r - A x*), 0)) per iteration
+ * (krylov.py:189-193).  tol_kind 0 = relative_residual, 1 =
+ * energy_error_reduction (needs exact_dev; stopping metric <= tol * metric_0,
+ * krylov.py:194-200).  sfcdd_op_pcg == sfcdd_op_pcg_ex(..., NULL, 0, NULL).  */
+int sfcdd_op_pcg_ex(sfcdd_op* op, const double* b_dev, double* x_dev, const double* exact_dev,
+                    int32_t tol_kind, double tol, int32_t max_iters, double* res_hist_host,
+                    double* energy_hist_host, int32_t* iters, int32_t* converged, void* stream);
+/* ------------------------------------------------------- vector kernels --
+ * Deterministic fp64 BLAS-1 on device vectors for the non-PCG solvers
+ * (Richardson + Lanczos, flexible CG: krylov.py:102-168, 219-254, 294-326);
+ * the dot is summed in a fixed order (bitwise repeatable).                 */
+int sfcdd_vec_dot(const double* x_dev, const double* y_dev, int64_t n, double* out_host, void* stream);
+/* y = a x + b y */
+int sfcdd_vec_axpby(double a, const double* x_dev, double b, double* y_dev, int64_t n, void* stream);
 /* Config-4 fault mode: in apply call number apply_index the
  * local contributions of the listed subdomains are zeroed.  n = 0 clears. */
 int sfcdd_op_set_fault(sfcdd_op* op, int64_t apply_index, const int32_t* ids_host, int32_t n);

@@ -19,6 +19,8 @@ to /root/reference/pkg/src/sfcdd/):
   coarse_c1.npz      A0 of config 1 (coarse.py:56-59)
   solve_*.npz        PCG residual histories / solutions (krylov.py:257-291)
   apply_c1.npz       SchwarzOperator.apply on seeded vectors (schwarz.py:103-118)
+  solvers.npz        Richardson (optimal / fixed damping), Lanczos estimates, flexible
+                     CG (full / windowed) and energy-error PCG (krylov.py:102-326)
 """
 
 from __future__ import annotations
@@ -218,6 +220,60 @@ def make_solve(ref, name, levels, p, gamma, q, full_solution, fault_iter=None):
     print(f"solve {name}: {rep.iterations} its, {time.time() - t0:.1f}s", flush=True)
 
 
+def make_solvers(ref):
+    """the reference's Richardson (optimal damping via
+    Lanczos, krylov.py:102-168, 219-254), flexible CG (krylov.py:294-326) and
+    the energy-error tracker (krylov.py:171-213) on small balanced / deflated
+    operators.  x* = the exact discrete solution (scipy spsolve of Â x = b̂)."""
+    import scipy.sparse.linalg as spla
+
+    K = ref.krylov
+    out = {}
+
+    def store(tag, rep, extra=None):
+        out[f"{tag}_iterations"] = rep.iterations
+        out[f"{tag}_converged"] = rep.converged
+        out[f"{tag}_residual_history"] = np.asarray(rep.residual_history)
+        out[f"{tag}_energy_history"] = np.asarray(rep.energy_history)
+        out[f"{tag}_solution"] = rep.solution
+        for k in ("lambda_min", "lambda_max", "damping"):
+            v = getattr(rep, k)
+            out[f"{tag}_{k}"] = np.nan if v is None else v
+        for k, v in (extra or {}).items():
+            out[f"{tag}_{k}"] = v
+
+    for tag, levels, p, gamma, q, variant in [("b66", (6, 6), 8, 0.5, 4, "balanced"),
+                                              ("b44", (4, 4), 4, 0.5, 2, "balanced"),
+                                              ("d55", (5, 5), 6, 0.5, 2, "deflated")]:
+        A = ref.grid.assemble_laplacian(levels)
+        n = A.shape[0]
+        b = np.random.default_rng(42).uniform(-1.0, 1.0, size=n)
+        Ah, bh, t = ref.grid.symmetrize_diag(A, b)
+        part = ref.partition.build_partition(n, p, gamma)
+        cs = ref.coarse.build_coarse(part, Ah, q)
+        op = ref.schwarz.setup(Ah, part, cs, ref.schwarz.SchwarzConfig(variant, "omega", gamma, q))
+        exact = spla.spsolve(Ah.tocsc(), bh)
+        out[f"{tag}_exact"] = exact
+        x0 = np.zeros(n)
+        if variant == "balanced":
+            store(f"{tag}_pcg_energy", K.run(Ah, bh, op, K.SolverConfig(method="pcg", tolerance=1e-8), x0, exact))
+            store(f"{tag}_pcg_rel", K.run(Ah, bh, op, K.SolverConfig(
+                method="pcg", tolerance=1e-8, tolerance_kind="relative_residual"), x0, exact))
+            store(f"{tag}_rich_opt", K.run(Ah, bh, op, K.SolverConfig(
+                method="richardson", tolerance=1e-6, tolerance_kind="relative_residual"), x0, exact))
+            store(f"{tag}_rich_fixed", K.run(Ah, bh, op, K.SolverConfig(
+                method="richardson", damping=0.5, tolerance=1e-6), x0, exact))
+            lam = K.estimate_extremal_eigs(lambda v: op.apply(Ah @ v), n, seed=42, a_matvec=lambda v: Ah @ v,
+                                           force_iterative=True)
+            out[f"{tag}_lanczos_forced"] = np.asarray(lam)
+        store(f"{tag}_fcg", K.run(Ah, bh, op, K.SolverConfig(method="fcg", tolerance=1e-8,
+                                                            tolerance_kind="relative_residual"), x0, exact))
+        store(f"{tag}_fcg_w2", K.run(Ah, bh, op, K.SolverConfig(method="fcg", tolerance=1e-8, fcg_window=2),
+                                     x0, exact))
+        print(f"solvers {tag}: n={n}", flush=True)
+    np.savez_compressed(OUT / "solvers.npz", **out)
+
+
 def make_dense_operator(ref):
     """Small operator matrices via apply() (cf. test_schwarz.py:14-22)."""
     out = {}
@@ -244,6 +300,7 @@ def main():
     make_perms(ref, args.big)
     make_partitions(ref)
     make_dense_operator(ref)
+    make_solvers(ref)
     make_solve(ref, "c1_g05", (7, 7), 16, 0.5, 4, True)
     make_solve(ref, "c1_g025", (7, 7), 16, 0.25, 4, True)
     make_solve(ref, "small_3d", (4, 4, 4), 8, 0.5, 4, True)

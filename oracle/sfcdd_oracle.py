@@ -413,3 +413,183 @@ def solve_config(levels, p, gamma, q, seed=42, tol=1e-8, fault_iter=None, max_st
     op = BalancedSchwarz(A, n, p, gamma, q, fault=fault)
     res = pcg(A, b, op, tol=tol, max_steps=max_steps)
     return A, b, op, res
+
+
+# ------------------------------------------- other outer solvers
+class Tracker:
+    """krylov.py:171-213: residual (and, with an exact solution, energy-error)
+    histories and the stopping test metric <= tol * metric_0."""
+
+    def __init__(self, A, b, tol, kind, exact):
+        if kind == "energy_error_reduction" and exact is None:
+            raise ValueError("energy stopping needs the exact solution")
+        self.A, self.b, self.tol, self.kind, self.exact = A, b, tol, kind, exact
+        self.a_exact = A @ exact if exact is not None else None
+        self.energy, self.residual = [], []
+        self.base = None
+
+    def record(self, x, r) -> bool:
+        self.residual.append(float(np.linalg.norm(r)))
+        if self.exact is not None:                       # krylov.py:189-193
+            e = x - self.exact
+            self.energy.append(float(np.sqrt(max(e @ (self.b - r - self.a_exact), 0.0))))
+        metric = self.energy[-1] if self.kind == "energy_error_reduction" else self.residual[-1]
+        if self.base is None:
+            self.base = metric
+        return metric <= self.tol * self.base
+
+    def diverged(self) -> bool:                           # krylov.py:205-213
+        if self.base is None or self.base == 0.0:
+            return False
+        hist = self.energy if self.kind == "energy_error_reduction" else self.residual
+        return hist[-1] > 10.0 * self.base
+
+
+@dataclass
+class SolverResult:
+    iterations: int
+    converged: bool
+    residual_history: list
+    energy_history: list
+    solution: np.ndarray
+    lambda_min: float | None = None
+    lambda_max: float | None = None
+    damping: float | None = None
+
+
+def pcg_tracked(A, b, precond, tol=1e-8, kind="relative_residual", exact=None, max_iters=20000):
+    """krylov.py:257-291 with the full tracker (energy errors when exact is given)."""
+    tr = Tracker(A, b, tol, kind, exact)
+    x = np.zeros_like(b)
+    r = b - A @ x
+    if tr.record(x, r):
+        return SolverResult(0, True, tr.residual, tr.energy, x)
+    z = precond.apply(r)
+    p = z.copy()
+    rz = float(r @ z)
+    it, conv = 0, False
+    for k in range(1, max_iters + 1):
+        Ap = A @ p
+        pAp = float(p @ Ap)
+        if pAp <= 0.0:
+            raise RuntimeError(f"nonpositive curvature at iteration {k}")
+        alpha = rz / pAp
+        x += alpha * p
+        r -= alpha * Ap
+        it = k
+        if tr.record(x, r):
+            conv = True
+            break
+        z = precond.apply(r)
+        rz_new = float(r @ z)
+        p = z + (rz_new / rz) * p
+        rz = rz_new
+    return SolverResult(it, conv, tr.residual, tr.energy, x)
+
+
+def estimate_extremal_eigs(apply_ca, n, iters=None, seed=0, a_matvec=None, force_iterative=False,
+                           stagnation_tol=2e-5, min_iters=40):
+    """krylov.py:102-168: dense eigenvalues for n <= 300, else Lanczos in the
+    a_matvec inner product with full (CGS2) reorthogonalization and
+    stagnation stopping."""
+    if n <= 300 and not force_iterative:
+        M = np.empty((n, n))
+        e = np.zeros(n)
+        for j in range(n):
+            e[j] = 1.0
+            M[:, j] = apply_ca(e)
+            e[j] = 0.0
+        lam = np.real(sla.eigvals(M))
+        return float(lam.min()), float(lam.max())
+    if iters is None:
+        iters = min(200, n)
+    rng = np.random.default_rng((seed, 0xE16))
+    mv = a_matvec if a_matvec is not None else (lambda v: v)
+    q = rng.standard_normal(n)
+    q /= np.sqrt(float(q @ mv(q)))
+    basis, alphas, betas = [q], [], []
+    prev, stable, lo, hi = None, 0, None, None
+    for k in range(iters):
+        w = apply_ca(basis[k])
+        alpha = float(mv(w) @ basis[k])
+        alphas.append(alpha)
+        w = w - alpha * basis[k]
+        if k > 0:
+            w = w - betas[k - 1] * basis[k - 1]
+        for _ in range(2):
+            aw = mv(w)
+            coeffs = [float(aw @ qj) for qj in basis]
+            for c, qj in zip(coeffs, basis):
+                w = w - c * qj
+        lam = sla.eigvalsh_tridiagonal(alphas, betas)
+        lo, hi = float(lam[0]), float(lam[-1])
+        if prev is not None:
+            d = max(abs(lo - prev[0]) / max(abs(lo), 1e-30), abs(hi - prev[1]) / max(abs(hi), 1e-30))
+            stable = stable + 1 if d < stagnation_tol else 0
+        prev = (lo, hi)
+        if k + 1 >= min_iters and stable >= 5:
+            break
+        beta = np.sqrt(max(float(w @ mv(w)), 0.0))
+        if beta <= 1e-14 * max(abs(alpha), 1.0):
+            break
+        betas.append(beta)
+        basis.append(w / beta)
+    return lo, hi
+
+
+def richardson(A, b, precond, tol=1e-6, kind="relative_residual", exact=None, damping="optimal", seed=42,
+               eig_iters=None, max_iters=20000):
+    """krylov.py:219-254: x += xi C^-1 (b - A x); xi = 2/(lmin+lmax) for 'optimal'."""
+    lam = (None, None)
+    if damping == "optimal":
+        lam = estimate_extremal_eigs(lambda v: precond.apply(A @ v), b.shape[0], iters=eig_iters, seed=seed,
+                                     a_matvec=lambda v: A @ v)
+        xi = 2.0 / (lam[0] + lam[1])
+    else:
+        xi = float(damping)
+    tr = Tracker(A, b, tol, kind, exact)
+    x = np.zeros_like(b)
+    it, conv = 0, False
+    for k in range(max_iters + 1):
+        r = b - A @ x
+        if tr.record(x, r):
+            it, conv = k, True
+            break
+        if tr.diverged():
+            raise RuntimeError(f"error grew 10x after {k} iterations")
+        if k == max_iters:
+            it = k
+            break
+        x += xi * precond.apply(r)
+    return SolverResult(it, conv, tr.residual, tr.energy, x, lam[0], lam[1], xi)
+
+
+def fcg(A, b, precond, tol=1e-8, kind="relative_residual", exact=None, window=None, max_iters=20000):
+    """krylov.py:294-326: directions explicitly A-orthogonalized against the
+    stored ones (the last `window`, or all)."""
+    tr = Tracker(A, b, tol, kind, exact)
+    x = np.zeros_like(b)
+    r = b - A @ x
+    if tr.record(x, r):
+        return SolverResult(0, True, tr.residual, tr.energy, x)
+    dirs = []
+    it, conv = 0, False
+    for k in range(1, max_iters + 1):
+        p = precond.apply(r)
+        for pj, Apj, pApj in dirs:
+            p = p - (float(p @ Apj) / pApj) * pj
+        Ap = A @ p
+        pAp = float(p @ Ap)
+        if pAp <= 0.0:
+            raise RuntimeError(f"nonpositive curvature at iteration {k}")
+        alpha = float(p @ r) / pAp
+        x += alpha * p
+        r -= alpha * Ap
+        dirs.append((p, Ap, pAp))
+        if window is not None and len(dirs) > window:
+            dirs.pop(0)
+        it = k
+        if tr.record(x, r):
+            conv = True
+            break
+    return SolverResult(it, conv, tr.residual, tr.energy, x)

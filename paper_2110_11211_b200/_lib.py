@@ -89,7 +89,8 @@ class Stats(ctypes.Structure):
 EXPORTS = [
     "sfcdd_last_error", "sfcdd_version", "sfcdd_sfc_encode", "sfcdd_sfc_decode",
     "sfcdd_sfc_perm", "sfcdd_op_create", "sfcdd_op_setup", "sfcdd_op_apply",
-    "sfcdd_op_matvec", "sfcdd_op_pcg", "sfcdd_op_set_fault", "sfcdd_op_reset_calls",
+    "sfcdd_op_matvec", "sfcdd_op_pcg", "sfcdd_op_pcg_ex", "sfcdd_vec_dot", "sfcdd_vec_axpby",
+    "sfcdd_op_set_fault", "sfcdd_op_reset_calls",
     "sfcdd_op_stats", "sfcdd_op_stencil", "sfcdd_op_coarse_dense", "sfcdd_op_destroy",
     "sfcdd_op_profile", "sfcdd_op_trace",
     "sfcdd_shard_info", "sfcdd_op_neighbors", "sfcdd_shard_xy", "sfcdd_shard_residual", "sfcdd_shard_pm", "sfcdd_shard_update",
@@ -123,6 +124,9 @@ def lib() -> ctypes.CDLL:
         "sfcdd_op_apply": [vp, vp, vp, vp],
         "sfcdd_op_matvec": [vp, vp, vp, vp],
         "sfcdd_op_pcg": [vp, vp, vp, dbl, i32, vp, ctypes.POINTER(i32), ctypes.POINTER(i32), vp],
+        "sfcdd_op_pcg_ex": [vp, vp, vp, vp, i32, dbl, i32, vp, vp, ctypes.POINTER(i32), ctypes.POINTER(i32), vp],
+        "sfcdd_vec_dot": [vp, vp, i64, ctypes.POINTER(dbl), vp],
+        "sfcdd_vec_axpby": [dbl, vp, dbl, vp, i64, vp],
         "sfcdd_op_set_fault": [vp, i64, vp, i32],
         "sfcdd_op_reset_calls": [vp],
         "sfcdd_op_stats": [vp, ctypes.POINTER(Stats)],

@@ -424,7 +424,7 @@ __global__ void k_residual0(const double* __restrict__ b, const double* __restri
       hist[0] = nrm;
       st->hist0 = nrm;
       st->k = 0;
-      if (nrm <= st->tol * nrm) {  // krylov.py:268-270 (only for r0 == 0)
+      if (!st->energy_mode && nrm <= st->tol * nrm) {  // krylov.py:268-270 (only for r0 == 0)
         st->converged = 1;
         st->done = 1;
       }
@@ -513,18 +513,60 @@ __global__ void k_update(double* __restrict__ x, double* __restrict__ r, const d
       st->k = k;
       const double nrm = sqrt(tot);
       hist[k] = nrm;
-      if (nrm <= st->tol * st->hist0) {  // krylov.py:283-286
-        st->converged = 1;
-        st->done = 1;
-      } else if (k >= st->max_iters) {
-        st->exhausted = 1;
-        st->done = 1;
+      if (!st->energy_mode) {  // else k_energy decides (after the energy error is known)
+        if (nrm <= st->tol * st->hist0) {  // krylov.py:283-286
+          st->converged = 1;
+          st->done = 1;
+        } else if (k >= st->max_iters) {
+          st->exhausted = 1;
+          st->done = 1;
+        }
       }
     }
   }
 }
 
-__global__ void k_zero_state_pcg(DevState* st, double tol, int32_t max_iters) {
+// energy error of iterate k: ||x - x*||_A = sqrt(max(e.(b - r - A x*), 0)),
+// e = x - x* (krylov.py:189-193: A e = (b - r) - A x* needs no matvec); with
+// energy stopping it decides convergence / exhaustion (krylov.py:194-200)
+__global__ void k_energy(const double* __restrict__ x, const double* __restrict__ ex,
+                         const double* __restrict__ b, const double* __restrict__ r,
+                         const double* __restrict__ aex, Chunks C, double* __restrict__ part, DevState* st,
+                         double* ehist, bool initial) {
+  if (!initial && skip(st)) return;
+  const int ch = blockIdx.x;
+  const int64_t c1 = C.start[ch + 1];
+  double s = 0.0;
+  for (int64_t g = C.start[ch] + threadIdx.x; g < c1; g += VEC_THREADS)
+    s = fma(__dsub_rn(x[g], ex[g]), __dsub_rn(__dsub_rn(b[g], r[g]), aex[g]), s);
+  s = block_sum(s);
+  if (threadIdx.x == 0) part[ch] = s;
+  if (last_block(&st->ticket[4])) {
+    const double tot = reduce_partials(part, gridDim.x);
+    if (threadIdx.x == 0) {
+      st->ticket[4] = 0;
+      const int k = st->k;
+      const double en = sqrt(fmax(tot, 0.0));
+      ehist[k] = en;
+      if (initial) st->ehist0 = en;
+      if (st->energy_mode && !st->breakdown) {
+        if (en <= st->tol * st->ehist0) {
+          st->converged = 1;
+          st->done = 1;
+        } else if (!initial && k >= st->max_iters) {
+          st->exhausted = 1;
+          st->done = 1;
+        }
+      }
+    }
+  }
+}
+
+__global__ void k_zero_state_pcg(DevState* st, double tol, int32_t max_iters, int32_t track_energy,
+                                 int32_t energy_mode) {
+  st->track_energy = track_energy;
+  st->energy_mode = energy_mode;
+  st->ehist0 = 0;
   st->tol = tol;
   st->hist0 = 0;
   st->rz = st->beta = st->pap = st->alpha = 0;
@@ -671,6 +713,9 @@ static void pcg_iteration(sfcdd_op* op, double* x, const double* pold, double* p
   k_update<<<op->nch, VEC_THREADS, 0, st>>>(x, op->r, pnew, op->ap, C, op->part_b, op->part_c, op->st,
                                             op->hist);
   kmark(st, "update");
+  if (op->pcg_exact)
+    k_energy<<<op->nch, VEC_THREADS, 0, st>>>(x, op->pcg_exact, op->pcg_b, op->r, op->aex, C, op->part_e, op->st,
+                                              op->ehist, false);
   apply_device(op, op->r, op->z, st, true, true);
 }
 
@@ -1040,23 +1085,51 @@ extern "C" int sfcdd_op_matvec(sfcdd_op* op, const double* x_dev, double* y_dev,
 
 extern "C" int sfcdd_op_pcg(sfcdd_op* op, const double* b_dev, double* x_dev, double tol, int32_t max_iters,
                             double* res_hist_host, int32_t* iters, int32_t* converged, void* stream) {
+  return sfcdd_op_pcg_ex(op, b_dev, x_dev, nullptr, 0, tol, max_iters, res_hist_host, nullptr, iters, converged,
+                         stream);
+}
+
+extern "C" int sfcdd_op_pcg_ex(sfcdd_op* op, const double* b_dev, double* x_dev, const double* exact_dev,
+                               int32_t tol_kind, double tol, int32_t max_iters, double* res_hist_host,
+                               double* energy_hist_host, int32_t* iters, int32_t* converged, void* stream) {
   SFCDD_API_BEGIN
   SFCDD_REQUIRE(op && op->ready, SFCDD_EVALUE, "operator not set up");
   SFCDD_REQUIRE(tol > 0, SFCDD_EVALUE, "tolerance must be positive");
   SFCDD_REQUIRE(max_iters >= 0, SFCDD_EVALUE, "max_iters must be nonnegative");
+  SFCDD_REQUIRE(tol_kind == 0 || tol_kind == 1, SFCDD_EVALUE, "unknown tolerance kind");
+  SFCDD_REQUIRE(tol_kind == 0 || exact_dev, SFCDD_EVALUE, "energy stopping needs the exact solution");
   CUDA_CHECK(cudaSetDevice(op->device));
   cudaStream_t st = (cudaStream_t)stream;  // NULL = legacy default stream
   if (op->hist_cap < max_iters + 1) {
     if (op->hist) CUDA_CHECK(cudaFree(op->hist));
+    if (op->ehist) CUDA_CHECK(cudaFree(op->ehist));
     op->hist = (double*)dev_alloc(op, (size_t)(max_iters + 1) * 8);
+    op->ehist = (double*)dev_alloc(op, (size_t)(max_iters + 1) * 8);
     op->hist_cap = max_iters + 1;
   }
   const Stencil S = stencil_of(op);
   const Chunks C = chunks_of(op);
-  k_zero_state_pcg<<<1, 1, 0, st>>>(op->st, tol, max_iters);
+  if (exact_dev) {
+    if (!op->aex) {
+      op->aex = (double*)dev_alloc(op, op->n * 8);
+      op->part_e = (double*)dev_alloc(op, op->nch * 8);
+    }
+    k_matvec<<<nblocks(op->n, VEC_THREADS), VEC_THREADS, 0, st>>>(exact_dev, S, op->aex);  // A x*
+  }
+  // the captured iteration graph reads b / x* only for the energy error
+  if (op->pcg_b != (exact_dev ? b_dev : nullptr) || op->pcg_exact != exact_dev) {
+    if (op->pcg_graph) CUDA_CHECK(cudaGraphExecDestroy(op->pcg_graph));
+    op->pcg_graph = nullptr;
+  }
+  op->pcg_b = exact_dev ? b_dev : nullptr;
+  op->pcg_exact = exact_dev;
+  k_zero_state_pcg<<<1, 1, 0, st>>>(op->st, tol, max_iters, exact_dev ? 1 : 0, tol_kind);
   CUDA_CHECK(cudaMemsetAsync(op->p0, 0, op->n * 8, st));
   k_residual0<<<op->nch, VEC_THREADS, 0, st>>>(b_dev, x_dev, S, C, op->r, op->part_b, op->part_c, op->st,
                                                op->hist);
+  if (exact_dev)
+    k_energy<<<op->nch, VEC_THREADS, 0, st>>>(x_dev, exact_dev, b_dev, op->r, op->aex, C, op->part_e, op->st,
+                                              op->ehist, true);
   // z = C^{-1} r (krylov.py:272); skipped on device if r0 == 0
   apply_device(op, op->r, op->z, st, true, true);
   if (max_iters > 0) {
@@ -1105,6 +1178,8 @@ extern "C" int sfcdd_op_pcg(sfcdd_op* op, const double* b_dev, double* x_dev, do
   }
   const int k = hs.k;
   if (res_hist_host) CUDA_CHECK(cudaMemcpy(res_hist_host, op->hist, (size_t)(k + 1) * 8, cudaMemcpyDeviceToHost));
+  if (energy_hist_host && exact_dev)
+    CUDA_CHECK(cudaMemcpy(energy_hist_host, op->ehist, (size_t)(k + 1) * 8, cudaMemcpyDeviceToHost));
   *iters = k;
   *converged = hs.converged;
   if (hs.breakdown) throw Error(SFCDD_EBREAKDOWN, "nonpositive curvature at iteration " + std::to_string(k + 1));
@@ -1170,9 +1245,14 @@ extern "C" int sfcdd_op_profile(sfcdd_op* op, const double* g_dev, double* scrat
     // (warm, back to back on the stream; the solver state is reset per rep so
     // no kernel early-exits)
     KernelTimer kt;
+    if (op->pcg_graph) CUDA_CHECK(cudaGraphExecDestroy(op->pcg_graph));
+    op->pcg_graph = nullptr;
+    op->pcg_exact = op->pcg_b = nullptr;
     if (op->hist_cap < 2) {  // k_update records the residual history
       if (op->hist) CUDA_CHECK(cudaFree(op->hist));
+      if (op->ehist) CUDA_CHECK(cudaFree(op->ehist));
       op->hist = (double*)dev_alloc(op, 2 * 8);
+      op->ehist = (double*)dev_alloc(op, 2 * 8);
       op->hist_cap = 2;
     }
     double* xs = (double*)dev_alloc(op, op->n * 8);
@@ -1187,7 +1267,7 @@ extern "C" int sfcdd_op_profile(sfcdd_op* op, const double* g_dev, double* scrat
     cudaGraphExec_t gexec;
     cudaStream_t cs = op->own_stream;
     CUDA_CHECK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-    k_zero_state_pcg<<<1, 1, 0, cs>>>(op->st, 1e-300, 1 << 30);
+    k_zero_state_pcg<<<1, 1, 0, cs>>>(op->st, 1e-300, 1 << 30, 0, 0);
     g_ktimer = &kt;
     kt.idx = 0;
     kmark(cs, "start");
@@ -1342,7 +1422,7 @@ extern "C" void sfcdd_op_destroy(sfcdd_op* op) {
                   op->d_ov_len, op->d_xy_off, op->d_dj_start, op->cand_ptr, op->cand, op->ccand_ptr, op->ccand,
                   op->d_wgt, op->d_count,
                   op->d_fault, op->st, op->hist, op->t, op->w, op->y0, op->y0b, op->part_a, op->part_b,
-                  op->part_c, op->r, op->z, op->p0, op->p1, op->ap};
+                  op->part_c, op->r, op->z, op->p0, op->p1, op->ap, op->aex, op->part_e, op->ehist};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   op->dag.reset();
@@ -1779,4 +1859,58 @@ extern "C" void sfcdd_factor_destroy(sfcdd_factor* f) {
   cudaSetDevice(f->device);
   f->dag.reset();
   delete f;
+}
+
+// ------------------------------------------------------------ BLAS-1 API
+namespace sfcdd {
+namespace {
+constexpr int DOT_BLOCKS = 592;  // 4 x 148 SMs; fixed -> fixed summation order
+__global__ void k_dot_part(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
+                           double* __restrict__ part) {
+  double s = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * VEC_THREADS + threadIdx.x; i < n; i += (int64_t)DOT_BLOCKS * VEC_THREADS)
+    s = fma(x[i], y[i], s);
+  s = block_sum(s);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+__global__ void k_dot_final(const double* __restrict__ part, double* __restrict__ out) {
+  const double s = reduce_partials(part, DOT_BLOCKS);
+  if (threadIdx.x == 0) *out = s;
+}
+__global__ void k_axpby(double a, const double* __restrict__ x, double b, double* __restrict__ y, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = b == 0.0 ? a * x[i] : fma(a, x[i], b * y[i]);
+}
+}  // namespace
+}  // namespace sfcdd
+
+extern "C" int sfcdd_vec_dot(const double* x_dev, const double* y_dev, int64_t n, double* out_host, void* stream) {
+  using namespace sfcdd;
+  SFCDD_API_BEGIN
+  SFCDD_REQUIRE(n >= 0 && out_host, SFCDD_EVALUE, "bad dot arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  static thread_local double* buf = nullptr;  // DOT_BLOCKS partials + result (per thread, per process)
+  static thread_local int buf_dev = -1;
+  int dev = 0;
+  CUDA_CHECK(cudaGetDevice(&dev));
+  if (!buf || buf_dev != dev) {
+    CUDA_CHECK(cudaMalloc(&buf, (DOT_BLOCKS + 1) * 8));
+    buf_dev = dev;
+  }
+  k_dot_part<<<DOT_BLOCKS, VEC_THREADS, 0, st>>>(x_dev, y_dev, n, buf);
+  k_dot_final<<<1, VEC_THREADS, 0, st>>>(buf, buf + DOT_BLOCKS);
+  CUDA_CHECK(cudaMemcpyAsync(out_host, buf + DOT_BLOCKS, 8, cudaMemcpyDeviceToHost, st));
+  CUDA_CHECK(cudaStreamSynchronize(st));
+  SFCDD_API_END
+}
+
+extern "C" int sfcdd_vec_axpby(double a, const double* x_dev, double b, double* y_dev, int64_t n, void* stream) {
+  using namespace sfcdd;
+  SFCDD_API_BEGIN
+  SFCDD_REQUIRE(n >= 0, SFCDD_EVALUE, "bad axpby arguments");
+  if (n == 0) return SFCDD_OK;
+  const unsigned blocks = (unsigned)std::min<int64_t>(4 * 148, (n + VEC_THREADS - 1) / VEC_THREADS);
+  k_axpby<<<blocks, VEC_THREADS, 0, (cudaStream_t)stream>>>(a, x_dev, b, y_dev, n);
+  CUDA_CHECK(cudaGetLastError());
+  SFCDD_API_END
 }

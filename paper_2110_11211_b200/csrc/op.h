@@ -30,6 +30,9 @@ struct DevState {
   uint32_t ticket[8];
   long long apply_calls;
   long long fault_index;
+  double ehist0;         // energy error at k = 0 (energy tracking)
+  int32_t track_energy;  // an exact solution was given: record energy errors
+  int32_t energy_mode;   // the energy error decides convergence (else ||r||)
 };
 
 struct Chunks {
@@ -80,6 +83,9 @@ struct sfcdd_op {
   double *t = nullptr, *w = nullptr, *y0 = nullptr, *y0b = nullptr;
   double *part_a = nullptr, *part_b = nullptr, *part_c = nullptr;
   double *r = nullptr, *z = nullptr, *p0 = nullptr, *p1 = nullptr, *ap = nullptr;
+  double *aex = nullptr, *part_e = nullptr, *ehist = nullptr;  // energy tracking (A x*, partials, history)
+  const double* pcg_b = nullptr;                                // b / x* the captured graph reads
+  const double* pcg_exact = nullptr;
   std::unique_ptr<sfcdd::DagSolver> dag;
   std::vector<double> a0_dense;  // host copy (diagnostics)
   sfcdd_stats stats{};

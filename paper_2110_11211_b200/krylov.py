@@ -1,6 +1,9 @@
-"""Preconditioned CG on the device (mirrors sfcdd.krylov).
+"""Outer solvers on the device (mirrors sfcdd.krylov).
 
-Reference: /root/reference/pkg/src/sfcdd/krylov.py:29-334.  ``pcg`` with a
+Reference: /root/reference/pkg/src/sfcdd/krylov.py:29-334.  Richardson with
+Lanczos-optimal damping and flexible CG compose the device
+apply / stencil with deterministic BLAS-1 kernels of the C ABI; their
+control flow is the reference's, step for step.  ``pcg`` with a
 device SchwarzOperator runs the whole iteration on the B200 (csrc/op.cu:
 fused matvec + p-update + p.Ap, fused x/r update + ||r|| + R0 r, the
 balanced apply, r.z), captured as a CUDA graph and replayed until the
@@ -84,25 +87,133 @@ class SolveReport:
         return out
 
 
-def pcg_device(op, b, x0=None, tol: float = 1e-8, max_iters: int = 20000):
-    """Device-resident PCG on CUDA tensors: returns (x, iterations, converged, history)."""
+def pcg_device(op, b, x0=None, tol: float = 1e-8, max_iters: int = 20000, exact=None,
+               tolerance_kind: str = "relative_residual"):
+    """Device-resident PCG on CUDA tensors.
+
+    Returns (x, iterations, converged, residual_history); with ``exact`` the
+    energy-error history is appended as a fifth element (krylov.py:189-193).
+    """
     import torch
 
     dev = _lib.device()
     b = b.to(dev, torch.float64).contiguous()
     x = torch.zeros_like(b) if x0 is None else x0.to(dev, torch.float64).clone().contiguous()
+    ex = None if exact is None else exact.to(dev, torch.float64).contiguous()
     hist = np.zeros(max_iters + 1)
+    ehist = np.zeros(max_iters + 1)
     its = ctypes.c_int32()
     conv = ctypes.c_int32()
-    _lib.check(_lib.lib().sfcdd_op_pcg(op.handle, b.data_ptr(), x.data_ptr(), float(tol), int(max_iters),
-                                       hist.ctypes.data, ctypes.byref(its), ctypes.byref(conv),
-                                       _lib.stream_ptr()))
+    kind = 1 if tolerance_kind == "energy_error_reduction" else 0
+    _lib.check(_lib.lib().sfcdd_op_pcg_ex(op.handle, b.data_ptr(), x.data_ptr(),
+                                          None if ex is None else ex.data_ptr(), kind, float(tol),
+                                          int(max_iters), hist.ctypes.data, ehist.ctypes.data,
+                                          ctypes.byref(its), ctypes.byref(conv), _lib.stream_ptr()))
     k = its.value
-    return x, k, bool(conv.value), hist[:k + 1].tolist()
+    if ex is None:
+        return x, k, bool(conv.value), hist[:k + 1].tolist()
+    return x, k, bool(conv.value), hist[:k + 1].tolist(), ehist[:k + 1].tolist()
+
+
+def _check_device_operands(A, precond):
+    from .schwarz import SchwarzOperator
+
+    if not isinstance(A, GridLaplacian) or not A.scaled:
+        raise NotImplementedError("the device solvers need the scaled grid Laplacian")
+    if precond is not None and not isinstance(precond, SchwarzOperator):
+        raise NotImplementedError("the device solvers need a device SchwarzOperator (or None)")
+
+
+def _to_device(v):
+    import torch
+
+    if isinstance(v, np.ndarray) or not hasattr(v, "data_ptr"):
+        return torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64)).to(_lib.device())
+    return v.to(_lib.device(), torch.float64).contiguous()
+
+
+class _Vec:
+    """Deterministic BLAS-1 on device vectors through the C ABI (csrc/op.cu)."""
+
+    def __init__(self, n):
+        self.n = n
+
+    def dot(self, x, y) -> float:
+        out = ctypes.c_double()
+        _lib.check(_lib.lib().sfcdd_vec_dot(x.data_ptr(), y.data_ptr(), self.n, ctypes.byref(out),
+                                            _lib.stream_ptr()))
+        return out.value
+
+    def axpby(self, a, x, b, y):
+        """y = a x + b y (in place)."""
+        _lib.check(_lib.lib().sfcdd_vec_axpby(float(a), x.data_ptr(), float(b), y.data_ptr(), self.n,
+                                              _lib.stream_ptr()))
+        return y
+
+    def new(self):
+        import torch
+
+        return torch.empty(self.n, dtype=torch.float64, device=_lib.device())
+
+    def copy(self, x):
+        return self.axpby(1.0, x, 0.0, self.new())
+
+    def lin(self, a, x, b, y):
+        """a x + b y as a new vector."""
+        return self.axpby(a, x, b, self.copy(y))
+
+
+class _DeviceTracker:
+    """krylov.py:171-213 on device vectors: ||r||, and with an exact solution
+    the energy error sqrt(max(e.(b - r - A x*), 0)), e = x - x*."""
+
+    def __init__(self, A, b, cfg: SolverConfig, exact, vec: _Vec):
+        if cfg.tolerance_kind == "energy_error_reduction" and exact is None:
+            raise ValueError("energy stopping needs the exact solution")
+        self.vec = vec
+        self.b = b
+        self.cfg = cfg
+        self.exact = exact
+        self.a_exact = A @ exact if exact is not None else None
+        self.energy_history: list[float] = []
+        self.residual_history: list[float] = []
+        self._baseline = None
+
+    def record(self, x, r) -> bool:
+        v = self.vec
+        res = float(np.sqrt(max(v.dot(r, r), 0.0)))
+        self.residual_history.append(res)
+        if self.exact is not None:
+            e = v.lin(1.0, x, -1.0, self.exact)            # x - x*
+            ae = v.axpby(-1.0, self.a_exact, 1.0, v.lin(1.0, self.b, -1.0, r))  # (b - r) - A x*
+            self.energy_history.append(float(np.sqrt(max(v.dot(e, ae), 0.0))))
+        metric = self.energy_history[-1] if self.cfg.tolerance_kind == "energy_error_reduction" else res
+        if self._baseline is None:
+            self._baseline = metric
+        return metric <= self.cfg.tolerance * self._baseline
+
+    def diverged(self) -> bool:
+        if self._baseline is None or self._baseline == 0.0:
+            return False
+        hist = (self.energy_history if self.cfg.tolerance_kind == "energy_error_reduction"
+                else self.residual_history)
+        return hist[-1] > 10.0 * self._baseline
+
+
+def _finish(rep: SolveReport, t0: float, x, tracker: _DeviceTracker, to_numpy: bool) -> SolveReport:
+    rep.wall_time = time.perf_counter() - t0
+    rep.solution = x.cpu().numpy() if to_numpy else x
+    rep.energy_history = tracker.energy_history
+    rep.residual_history = tracker.residual_history
+    return rep
 
 
 def pcg(A, b, precond, cfg: SolverConfig, x0, exact=None) -> SolveReport:
-    """Preconditioned CG; refuses non-symmetric preconditioners (krylov.py:257-291)."""
+    """Preconditioned CG; refuses non-symmetric preconditioners (krylov.py:257-291).
+
+    Runs entirely on the device (csrc/op.cu, CUDA-graph iteration) with the
+    reference tracker: residual history always, energy-error history when
+    ``exact`` is given, stopping on ``cfg.tolerance_kind``."""
     from .schwarz import SchwarzOperator
 
     t0 = time.perf_counter()
@@ -113,29 +224,156 @@ def pcg(A, b, precond, cfg: SolverConfig, x0, exact=None) -> SolveReport:
         raise ValueError("energy stopping needs the exact solution")
     if not isinstance(precond, SchwarzOperator) or not isinstance(A, GridLaplacian) or not A.scaled:
         raise NotImplementedError("device PCG needs the scaled grid Laplacian and a device SchwarzOperator")
-    if cfg.tolerance_kind != "relative_residual":
-        raise NotImplementedError("device PCG implements the relative_residual stopping rule")
-    import torch
-
-    bt = torch.from_numpy(np.ascontiguousarray(b, dtype=np.float64))
-    xt = torch.from_numpy(np.ascontiguousarray(x0, dtype=np.float64))
-    x, k, conv, hist = pcg_device(precond, bt, xt, cfg.tolerance, cfg.max_iters)
-    rep = SolveReport("pcg", k, conv, [], hist)
-    rep.solution = x.cpu().numpy()
+    to_numpy = isinstance(b, np.ndarray)
+    out = pcg_device(precond, _to_device(b), _to_device(x0), cfg.tolerance, cfg.max_iters,
+                     exact=None if exact is None else _to_device(exact), tolerance_kind=cfg.tolerance_kind)
+    x, k, conv, hist = out[:4]
+    rep = SolveReport("pcg", k, conv, out[4] if len(out) > 4 else [], hist)
+    rep.solution = x.cpu().numpy() if to_numpy else x
     rep.wall_time = time.perf_counter() - t0
     return rep
 
 
-def _not_on_device(name):
-    def fn(*args, **kwargs):
-        raise NotImplementedError(f"{name} is not part of the device hot path (SURVEY §8(f))")
-    fn.__name__ = name
-    return fn
+def estimate_extremal_eigs(apply_ca, n: int, *, iters: int | None = None, seed: int = 0, a_matvec=None,
+                           force_iterative: bool = False, stagnation_tol: float = 2e-5, min_iters: int = 40):
+    """Extremal eigenvalues of a preconditioned SPD operator (krylov.py:102-168).
+
+    ``apply_ca`` and ``a_matvec`` map CUDA tensors to CUDA tensors (device
+    apply / stencil).  n <= 300: dense eigenvalues of the operator matrix built
+    column by column; otherwise Lanczos in the a_matvec inner product with full
+    CGS2 reorthogonalization, stopping once both Ritz values stagnate.  The
+    start vector is the reference's numpy draw (default_rng((seed, 0xE16)))."""
+    import torch
+
+    vec = _Vec(n)
+    if n <= 300 and not force_iterative:
+        M = np.empty((n, n))
+        e = torch.zeros(n, dtype=torch.float64, device=_lib.device())
+        for j in range(n):
+            e.zero_()
+            e[j] = 1.0
+            M[:, j] = apply_ca(e).cpu().numpy()
+        lam = np.real(np.linalg.eigvals(M))
+        return float(lam.min()), float(lam.max())
+    if iters is None:
+        iters = min(200, n)
+    rng = np.random.default_rng((seed, 0xE16))
+    mv = a_matvec if a_matvec is not None else (lambda v: v)
+    q = _to_device(rng.standard_normal(n))
+    vec.axpby(1.0 / np.sqrt(vec.dot(q, mv(q))), q, 0.0, q)
+    basis = [q]
+    alphas: list[float] = []
+    betas: list[float] = []
+    prev = None
+    stable = 0
+    lam_lo = lam_hi = None
+    for k in range(iters):
+        w = apply_ca(basis[k])
+        alpha = vec.dot(mv(w), basis[k])
+        alphas.append(alpha)
+        vec.axpby(-alpha, basis[k], 1.0, w)
+        if k > 0:
+            vec.axpby(-betas[k - 1], basis[k - 1], 1.0, w)
+        for _ in range(2):  # CGS2 against the whole basis
+            aw = mv(w)
+            coeffs = [vec.dot(aw, qj) for qj in basis]
+            for c, qj in zip(coeffs, basis):
+                vec.axpby(-c, qj, 1.0, w)
+        T = np.diag(alphas) + np.diag(betas[:len(alphas) - 1], 1) + np.diag(betas[:len(alphas) - 1], -1)
+        lam = np.linalg.eigvalsh(T)
+        lam_lo, lam_hi = float(lam[0]), float(lam[-1])
+        if prev is not None:
+            d_lo = abs(lam_lo - prev[0]) / max(abs(lam_lo), 1e-30)
+            d_hi = abs(lam_hi - prev[1]) / max(abs(lam_hi), 1e-30)
+            stable = stable + 1 if max(d_lo, d_hi) < stagnation_tol else 0
+        prev = (lam_lo, lam_hi)
+        if k + 1 >= min_iters and stable >= 5:
+            break
+        beta = float(np.sqrt(max(vec.dot(w, mv(w)), 0.0)))
+        if beta <= 1e-14 * max(abs(alpha), 1.0):
+            break
+        betas.append(beta)
+        basis.append(vec.axpby(1.0 / beta, w, 0.0, w))
+    return lam_lo, lam_hi
 
 
-richardson = _not_on_device("richardson")
-fcg = _not_on_device("fcg")
-estimate_extremal_eigs = _not_on_device("estimate_extremal_eigs")
+def richardson(A, b, precond, cfg: SolverConfig, x0, exact=None) -> SolveReport:
+    """Damped preconditioned Richardson x += xi C^-1 (b - A x) (krylov.py:219-254).
+
+    ``damping="optimal"``: xi = 2/(lambda_min + lambda_max) of C^-1 A from
+    estimate_extremal_eigs.  Every product runs on the device."""
+    t0 = time.perf_counter()
+    _check_device_operands(A, precond)
+    n = b.shape[0]
+    vec = _Vec(n)
+    apply_c = precond.apply_device if precond is not None else vec.copy
+    lam = (None, None)
+    if cfg.damping == "optimal":
+        if precond is not None and not getattr(precond, "symmetric", True):
+            raise ValueError("optimal damping requires a symmetric preconditioner")
+        lam = estimate_extremal_eigs(lambda v: apply_c(A @ v), n, iters=cfg.eig_iters, seed=cfg.seed,
+                                     a_matvec=lambda v: A @ v)
+        xi = 2.0 / (lam[0] + lam[1])
+    else:
+        xi = float(cfg.damping)
+    to_numpy = isinstance(b, np.ndarray)
+    bd = _to_device(b)
+    tracker = _DeviceTracker(A, bd, cfg, None if exact is None else _to_device(exact), vec)
+    x = vec.copy(_to_device(x0))
+    report = SolveReport("richardson", 0, False, [], [], lambda_min=lam[0], lambda_max=lam[1], damping=xi)
+    for k in range(cfg.max_iters + 1):
+        r = vec.axpby(1.0, bd, -1.0, A @ x)  # b - A x
+        if tracker.record(x, r):
+            report.iterations, report.converged = k, True
+            break
+        if tracker.diverged():
+            raise DivergenceError(f"error grew 10x after {k} iterations")
+        if k == cfg.max_iters:
+            report.iterations = k
+            break
+        vec.axpby(xi, apply_c(r), 1.0, x)
+    return _finish(report, t0, x, tracker, to_numpy)
+
+
+def fcg(A, b, precond, cfg: SolverConfig, x0, exact=None) -> SolveReport:
+    """Flexible CG (krylov.py:294-326): each new direction is A-orthogonalized
+    against the stored ones (the last ``cfg.fcg_window``, or all), so
+    non-symmetric preconditioners (e.g. the deflated variant) are admissible."""
+    t0 = time.perf_counter()
+    _check_device_operands(A, precond)
+    n = b.shape[0]
+    vec = _Vec(n)
+    apply_c = precond.apply_device if precond is not None else vec.copy
+    to_numpy = isinstance(b, np.ndarray)
+    bd = _to_device(b)
+    tracker = _DeviceTracker(A, bd, cfg, None if exact is None else _to_device(exact), vec)
+    x = vec.copy(_to_device(x0))
+    r = vec.axpby(1.0, bd, -1.0, A @ x)
+    report = SolveReport("fcg", 0, False, [], [])
+    if tracker.record(x, r):
+        report.converged = True
+        return _finish(report, t0, x, tracker, to_numpy)
+    directions = []
+    for k in range(1, cfg.max_iters + 1):
+        p = vec.copy(apply_c(r))
+        for pj, Apj, pApj in directions:
+            vec.axpby(-(vec.dot(p, Apj) / pApj), pj, 1.0, p)
+        Ap = A @ p
+        pAp = vec.dot(p, Ap)
+        if pAp <= 0.0:
+            raise BreakdownError(f"nonpositive curvature at iteration {k}")
+        alpha = vec.dot(p, r) / pAp
+        vec.axpby(alpha, p, 1.0, x)
+        vec.axpby(-alpha, Ap, 1.0, r)
+        directions.append((p, Ap, pAp))
+        if cfg.fcg_window is not None and len(directions) > cfg.fcg_window:
+            directions.pop(0)
+        report.iterations = k
+        if tracker.record(x, r):
+            report.converged = True
+            break
+    return _finish(report, t0, x, tracker, to_numpy)
+
 
 _METHODS = {"richardson": richardson, "pcg": pcg, "fcg": fcg}
 
