@@ -179,9 +179,17 @@ __global__ void k_chunk_sum(const double* __restrict__ v, Chunks C, double* __re
 // otherwise each CTA sums the partials into shared memory first.
 constexpr int GEMV_WPR = 4;
 constexpr int GEMV_ROWS = VEC_THREADS / 32 / GEMV_WPR;
+struct PcgFin {           // fused PCG epilogue of the second coarse GEMV
+  const double* part_rw;  // per-chunk r.w partials (k_combine_chunk)
+  const double* part_rc;  // per-chunk R0 r partials (k_update / k_residual0)
+  const double* y0;       // A0^{-1} R0 r
+  int32_t nch;
+  DevState* st;           // null: no epilogue
+};
+
 __global__ void k_coarse_gemv(const double* __restrict__ ainv, const double* __restrict__ part,
                               const int32_t* __restrict__ agg_ptr, int32_t n0, double* __restrict__ y,
-                              const DevState* st, bool direct) {
+                              const DevState* st, bool direct, PcgFin fin) {
   if (skip(st)) return;
   extern __shared__ double csm[];
   __shared__ double red[VEC_THREADS / 32];
@@ -231,6 +239,36 @@ __global__ void k_coarse_gemv(const double* __restrict__ ainv, const double* __r
 #pragma unroll
     for (int k = 0; k < GEMV_WPR; ++k) t += red[threadIdx.x * GEMV_WPR + k];
     if (r < n0) y[r] = t;
+  }
+  if (fin.st && last_block(&fin.st->ticket[5])) {
+    // r.z without materialising z = (w - R0^T y0b) + R0^T y0 (schwarz.py:117-118):
+    // r.z = r.w + (R0 r).(y0 - y0b); then beta (krylov.py:288-289)
+    double rw = 0.0, cd = 0.0;
+#pragma unroll 4
+    for (int i = threadIdx.x; i < fin.nch; i += VEC_THREADS) rw += __ldcg(fin.part_rw + i);
+    if (direct) {  // aggregate a = chunk a
+#pragma unroll 4
+      for (int a = threadIdx.x; a < n0; a += VEC_THREADS)
+        cd = fma(__ldcg(fin.part_rc + a), __ldcg(fin.y0 + a) - __ldcg(y + a), cd);
+    } else {
+      for (int a = threadIdx.x; a < n0; a += VEC_THREADS) {
+        double ra = 0.0;
+        for (int ch = agg_ptr[a]; ch < agg_ptr[a + 1]; ++ch) ra += __ldcg(fin.part_rc + ch);
+        cd = fma(ra, __ldcg(fin.y0 + a) - __ldcg(y + a), cd);
+      }
+    }
+    const double2 tot = block_sum2(rw, cd);
+    rw = tot.x;
+    cd = tot.y;
+    if (threadIdx.x == 0) {
+      DevState* S = fin.st;
+      S->ticket[5] = 0;
+      S->apply_calls += 1;
+      const double rz = rw + cd;
+      S->beta = S->have_rz ? rz / S->rz : 0.0;
+      S->have_rz = 1;
+      S->rz = rz;
+    }
   }
 }
 
@@ -300,7 +338,8 @@ __global__ void k_combine(CombineArgs C, double* __restrict__ w, const DevState*
 constexpr int COMBINE_MAXC = 32;
 __global__ void k_combine_chunk(CombineArgs C, const int64_t* __restrict__ cstart,
                                 const int32_t* __restrict__ ccand_ptr, const int32_t* __restrict__ ccand,
-                                double* __restrict__ w, const DevState* st) {
+                                double* __restrict__ w, const DevState* st, const double* __restrict__ rdot,
+                                double* __restrict__ part) {
   if (skip(st)) return;
   __shared__ int64_t s_start[COMBINE_MAXC], s_len[COMBINE_MAXC], s_off[COMBINE_MAXC];
   __shared__ double s_w[COMBINE_MAXC];
@@ -317,6 +356,7 @@ __global__ void k_combine_chunk(CombineArgs C, const int64_t* __restrict__ cstar
   }
   __syncthreads();
   const int64_t g1 = cstart[ch + 1];
+  double rw = 0.0;
   for (int64_t g = cstart[ch] + threadIdx.x; g < g1; g += VEC_THREADS) {
     const double dw = C.count ? 1.0 / (double)C.count[g] : 0.0;
     double acc = 0.0;
@@ -326,6 +366,11 @@ __global__ void k_combine_chunk(CombineArgs C, const int64_t* __restrict__ cstar
       if (off < s_len[c]) acc = __dadd_rn(acc, __dmul_rn(C.count ? dw : s_w[c], __ldcg(C.xy + s_off[c] + off)));
     }
     w[g] = acc;
+    if (rdot) rw = fma(rdot[g], acc, rw);
+  }
+  if (rdot) {  // r.w partials of the fused PCG epilogue (k_coarse_gemv, fin)
+    rw = block_sum(rw);
+    if (threadIdx.x == 0) part[ch] = rw;
   }
 }
 
@@ -446,6 +491,52 @@ __global__ void k_pm(const double* __restrict__ z, const double* __restrict__ po
     for (int a = 0; a < 2 * S.d; ++a) {
       const int32_t nb = __ldg(S.nbr + (int64_t)a * S.n + g);
       if (nb >= 0) acc = fma(S.off[a >> 1], __dadd_rn(z[nb], __dmul_rn(beta, pold[nb])), acc);
+    }
+    pnew[g] = pg;
+    ap[g] = acc;
+    s = fma(pg, acc, s);
+  }
+  s = block_sum(s);
+  if (threadIdx.x == 0) part[ch] = s;
+  if (last_block(&st->ticket[1])) {
+    const double pap = reduce_partials(part, gridDim.x);
+    if (threadIdx.x == 0) {
+      st->ticket[1] = 0;
+      st->pap = pap;
+      if (!(pap > 0.0)) {
+        st->breakdown = 1;
+        st->done = 1;
+      } else {
+        st->alpha = st->rz / pap;
+      }
+    }
+  }
+}
+
+// the same with z = (w - R0^T y0b) + R0^T y0 formed on the fly (fused PCG
+// path of the balanced / deflated variants: k_finalize is not launched);
+// bitwise the same p and Ap as k_pm over the materialised z
+__global__ void k_pm_w(const double* __restrict__ w, const double* __restrict__ y0,
+                       const double* __restrict__ y0b, const int32_t* __restrict__ agg,
+                       const double* __restrict__ pold, Stencil S, Chunks C, double* __restrict__ pnew,
+                       double* __restrict__ ap, double* __restrict__ part, DevState* st) {
+  if (skip(st)) return;
+  const double beta = st->beta;
+  const int ch = blockIdx.x;
+  const int a0 = C.agg[ch];
+  const double zc = y0[a0], zb = y0b[a0];
+  auto zv = [&](int64_t i, double cb, double c0) { return (w[i] - cb) + c0; };
+  double s = 0.0;
+  for (int64_t g = C.start[ch] + threadIdx.x; g < C.start[ch + 1]; g += VEC_THREADS) {
+    const double pg = __dadd_rn(zv(g, zb, zc), __dmul_rn(beta, pold[g]));
+    double acc = S.dhat * pg;
+    for (int a = 0; a < 2 * S.d; ++a) {
+      const int32_t nb = __ldg(S.nbr + (int64_t)a * S.n + g);
+      if (nb >= 0) {
+        const int32_t an = __ldg(agg + nb);
+        acc = fma(S.off[a >> 1], __dadd_rn(zv(nb, __ldg(y0b + an), __ldg(y0 + an)), __dmul_rn(beta, pold[nb])),
+                  acc);
+      }
     }
     pnew[g] = pg;
     ap[g] = acc;
@@ -662,7 +753,7 @@ static void apply_device(sfcdd_op* op, const double* g, double* h, cudaStream_t 
     if (!partials_ready) k_chunk_sum<<<op->nch, VEC_THREADS, 0, st>>>(g, C, op->part_c);
     if (!partials_ready) kmark(st, "chunk_sum");
     k_coarse_gemv<<<cgrid, VEC_THREADS, csm, st>>>(op->ainv, op->part_c, op->agg_ptr, op->n0, op->y0, sk,
-                                                   direct);
+                                                   direct, PcgFin{});
     kmark(st, "coarse_gemv");
   }
   const double* rhs = g;
@@ -688,19 +779,26 @@ static void apply_device(sfcdd_op* op, const double* g, double* h, cudaStream_t 
   ca.fault_index = op->stats.reserved[0];
   ca.p = op->p;
   ca.n = op->n;
-  k_combine_chunk<<<op->nch, VEC_THREADS, 0, st>>>(ca, op->chunk_start, op->ccand_ptr, op->ccand, op->w, sk);
-  kmark(st, "combine");
   const int mode = mode_of(v);
+  // PCG with a two-sided coarse correction: z is never materialised; r.z and
+  // beta come from the second GEMV's epilogue and k_pm_w forms z on the fly
+  const bool fused = pcg && mode == 2;
+  k_combine_chunk<<<op->nch, VEC_THREADS, 0, st>>>(ca, op->chunk_start, op->ccand_ptr, op->ccand, op->w, sk,
+                                                   fused ? op->r : nullptr, op->part_a);
+  kmark(st, "combine");
   if (mode == 2) {
     k_matvec_chunk<<<op->nch, VEC_THREADS, 0, st>>>(op->w, S, C, op->part_b, sk);
     kmark(st, "matvec_chunk");
+    PcgFin fin{op->part_a, op->part_c, op->y0, op->nch, fused ? dst : nullptr};
     k_coarse_gemv<<<cgrid, VEC_THREADS, csm, st>>>(op->ainv, op->part_b, op->agg_ptr, op->n0, op->y0b, sk,
-                                                   direct);
+                                                   direct, fin);
     kmark(st, "coarse_gemv2");
   }
-  k_finalize<<<op->nch, VEC_THREADS, 0, st>>>(op->w, op->y0, op->y0b, C, mode, h, pcg ? op->r : nullptr,
-                                              op->part_a, dst, pcg);
-  kmark(st, "finalize");
+  if (!fused) {
+    k_finalize<<<op->nch, VEC_THREADS, 0, st>>>(op->w, op->y0, op->y0b, C, mode, h, pcg ? op->r : nullptr,
+                                                op->part_a, dst, pcg);
+    kmark(st, "finalize");
+  }
   CUDA_CHECK(cudaGetLastError());
 }
 
@@ -708,7 +806,11 @@ static void apply_device(sfcdd_op* op, const double* g, double* h, cudaStream_t 
 static void pcg_iteration(sfcdd_op* op, double* x, const double* pold, double* pnew, cudaStream_t st) {
   const Stencil S = stencil_of(op);
   const Chunks C = chunks_of(op);
-  k_pm<<<op->nch, VEC_THREADS, 0, st>>>(op->z, pold, S, C, pnew, op->ap, op->part_a, op->st);
+  if (mode_of(op->variant) == 2)
+    k_pm_w<<<op->nch, VEC_THREADS, 0, st>>>(op->w, op->y0, op->y0b, op->agg, pold, S, C, pnew, op->ap, op->part_a,
+                                            op->st);
+  else
+    k_pm<<<op->nch, VEC_THREADS, 0, st>>>(op->z, pold, S, C, pnew, op->ap, op->part_a, op->st);
   kmark(st, "pm");
   k_update<<<op->nch, VEC_THREADS, 0, st>>>(x, op->r, pnew, op->ap, C, op->part_b, op->part_c, op->st,
                                             op->hist);
@@ -1172,9 +1274,12 @@ extern "C" int sfcdd_op_pcg_ex(sfcdd_op* op, const double* b_dev, double* x_dev,
   {
     // kernel launches of this call: init (zero, residual, apply) + 2 iterations per graph
     const int v = op->variant;
+    // DAG + combine [+ GEMV] [+ t] [+ R0 Â w + GEMV (finalize fused away)] [+ finalize]
     const int64_t per_apply = 1 + 1 + (v != SFCDD_VARIANT_ONE_LEVEL ? 1 : 0) + (v == SFCDD_VARIANT_BALANCED) +
-                              (mode_of(v) == 2 ? 2 : 0) + 1;
-    op->stats.reserved[2] = 2 + per_apply + op->stats.reserved[3] * (2 + per_apply);
+                              (mode_of(v) == 2 ? 2 : 1);
+    // per iteration: p-update/matvec, x/r update [+ energy error]
+    const int64_t per_it = 2 + (exact_dev ? 1 : 0);
+    op->stats.reserved[2] = 2 + (exact_dev ? 2 : 0) + per_apply + op->stats.reserved[3] * (per_it + per_apply);
   }
   const int k = hs.k;
   if (res_hist_host) CUDA_CHECK(cudaMemcpy(res_hist_host, op->hist, (size_t)(k + 1) * 8, cudaMemcpyDeviceToHost));
@@ -1310,7 +1415,7 @@ extern "C" int sfcdd_op_profile(sfcdd_op* op, const double* g_dev, double* scrat
       };
       iso("gemv", [&] {
         k_coarse_gemv<<<cgrid, VEC_THREADS, csm, st>>>(op->ainv, op->part_c, op->agg_ptr, op->n0, op->y0, nullptr,
-                                                       direct);
+                                                       direct, PcgFin{});
       });
       iso("tvec", [&] {
         k_tvec<<<nblocks(op->n, VEC_THREADS), VEC_THREADS, 0, st>>>(op->r, op->y0, op->agg, S, op->t, nullptr);
