@@ -68,6 +68,7 @@ PlanOptions::PlanOptions() {
   if (const char* e = std::getenv("SFCDD_WORKERS")) workers = std::atoi(e);
   if (const char* e = std::getenv("SFCDD_ROW_MAX")) row_max = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("SFCDD_COL_MAX")) col_max = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("SFCDD_SLACK_US")) slack_us = std::atof(e);
 }
 
 DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::vector<int64_t>& gstart,
@@ -336,7 +337,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         const int32_t scratch = ints[RW_SCRATCH];
         const int64_t off = emit_blob(P, ints, RW_VAL_OFF, vals, bytes);
         P.max_scratch = std::max<int32_t>(P.max_scratch, scratch);
-        add_task(g, TK_ROW_FWD, off, bytes, (int64_t)R * C, 2.56 + 0.0017 * R * C);
+        add_task(g, TK_ROW_FWD, off, bytes, (int64_t)R * C, 2.36 + 0.0013 * R * C);
         r0 += R;
       }
       // backward: column blocks, dense row-major L x c (L = s+m-k0)
@@ -368,7 +369,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         int32_t bytes = 0;
         const int64_t off = emit_blob(P, ints, CL_VAL_OFF, vals, bytes);
         P.max_scratch = std::max<int32_t>(P.max_scratch, L);
-        add_task(g, TK_COL_BWD, off, bytes, nv, 2.94 + 0.0014 * nv);
+        add_task(g, TK_COL_BWD, off, bytes, nv, 2.24 + 0.0013 * nv);
         k0 += c;
       }
       continue;
@@ -637,8 +638,8 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
     SFCDD_REQUIRE(bytes <= opt.blob_max, SFCDD_EINTERNAL, "fragment blob exceeds the slot budget");
     P.max_scratch = std::max(P.max_scratch, scratch_used);
     // task time model (us), fitted to traced C2 launches (tools/trace_dag.py)
-    add_task(g, TK_FRAG_FWD, off, bytes, nvals, 2.31 + 0.0038 * nvals + 0.51 * nlev);
-    add_task(g, TK_FRAG_BWD, off, bytes, nvals, 2.5 + 0.005 * nvals + 0.5 * nlev);
+    add_task(g, TK_FRAG_FWD, off, bytes, nvals, 2.13 + 0.0041 * nvals + 0.57 * nlev);
+    add_task(g, TK_FRAG_BWD, off, bytes, nvals, 1.11 + 0.0021 * nvals + 0.68 * nlev);
   }
 
   // ---- 3. dependencies
@@ -736,13 +737,26 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
       const Ev e = ev.back();
       ev.pop_back();
       now = e.first;
+      if (e.second < 0) {  // a waiter's release delay has passed: it is ready
+        ready.push_back(-e.second - 1);
+        std::push_heap(ready.begin(), ready.end(), cmp_rank);
+        continue;
+      }
       ++free_w;
       const int32_t c = tl[e.second].signal_idx;
       ++ctr[c];
       for (int32_t w : waiters[c])
         if (ctr[c] == tl[w].wait_target) {
-          ready.push_back(w);
-          std::push_heap(ready.begin(), ready.end(), cmp_rank);
+          // modelled durations are means: a dependent task enters the queue
+          // opt.slack_us after its last predecessor's modelled end, so at run
+          // time its warp rarely finds the dependency still unfinished
+          if (opt.slack_us > 0.0) {
+            ev.emplace_back(now + opt.slack_us, -w - 1);
+            std::push_heap(ev.begin(), ev.end(), ev_cmp);
+          } else {
+            ready.push_back(w);
+            std::push_heap(ready.begin(), ready.end(), cmp_rank);
+          }
         }
     }
     P.sim_us = now;

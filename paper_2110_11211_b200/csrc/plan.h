@@ -157,6 +157,7 @@ struct PlanOptions {
   int32_t sms = 148;               // SMs of the target device (set by the caller)
   int32_t row_max = 32;            // rows per ROW task (SFCDD_ROW_MAX; latency vs task count)
   int32_t col_max = 16;            // columns per COL task (SFCDD_COL_MAX)
+  double slack_us = 4.0;           // queue-order simulation: dependents become ready this late (SFCDD_SLACK_US)
   PlanOptions();                 // environment overrides SFCDD_BLOB_MAX, SFCDD_SCRATCH_MAX
 };
 
