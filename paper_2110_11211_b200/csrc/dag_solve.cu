@@ -447,21 +447,77 @@ __device__ __forceinline__ void run_frag(const int32_t* h, bool fwd, double* S, 
   }
 }
 
+// ====================================================== ASM (big forward)
+// front positions [q0, q0+nq) of J: f[q] = (q < s ? rhs[col] : 0) + child
+// updates in fixed order; 2 positions per lane, their first 3 update loads
+// all in flight (nearly every position has <= 3 contributions)
+__device__ __noinline__ void run_asm(const int32_t* h, const DagArgs& A, const FactorDev& F, int lane) {
+  const int s = h[AS_S], q0 = h[AS_Q0], nq = h[AS_NQ];
+  const int32_t* cols = h + h[AS_COLS];
+  const int32_t* ptr = h + h[AS_PTR];
+  const int32_t* src = h + h[AS_SRC];
+  double* f = A.upd + h[AS_FOFF] + q0;
+  constexpr int U = 2;
+  for (int base = 0; base < nq; base += 32 * U) {
+    double acc[U], v0[U], v1[U], v2[U];
+    int e0[U], e1[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + lane + 32 * u;
+      const bool ok = i < nq;
+      e0[u] = ok ? ptr[i] : 0;
+      e1[u] = ok ? ptr[i + 1] : 0;
+      const int n = e1[u] - e0[u];
+      acc[u] = (ok && q0 + i < s) ? __ldg(A.rhs + gidx(F, cols[i])) : 0.0;
+      v0[u] = n > 0 ? __ldcg(A.upd + src[e0[u]]) : 0.0;
+      v1[u] = n > 1 ? __ldcg(A.upd + src[e0[u] + 1]) : 0.0;
+      v2[u] = n > 2 ? __ldcg(A.upd + src[e0[u] + 2]) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + lane + 32 * u;
+      if (i >= nq) continue;
+      const int n = e1[u] - e0[u];
+      double a = acc[u];
+      if (n > 0) a += v0[u];
+      if (n > 1) a += v1[u];
+      if (n > 2) a += v2[u];
+      for (int e = e0[u] + 3; e < e1[u]; ++e) a += __ldcg(A.upd + src[e]);
+      __stcg(f + i, a);
+    }
+  }
+}
+
+// ======================================================= XB (big backward)
+// vb[a] = -x(rows[a]) for J's below rows [a0, a0+na)
+__device__ __noinline__ void run_xb(const int32_t* h, const DagArgs& A, const FactorDev& F, int lane) {
+  const int a0 = h[XB_A0], na = h[XB_NA];
+  const int32_t* rows = h + h[XB_ROWS];
+  const double* xy = A.xy + F.xy_off;
+  double* vb = A.upd + h[XB_XOFF] + a0;
+  warp_gather(na, lane, [&](int q) { return -__ldcg(xy + rows[q]); }, [&](int q, double v) { __stcg(vb + q, v); });
+}
+
 // ====================================================== ROW (big forward)
-// rows [r0, r0+R) of out = M f_J; lanes = (row, k-phase) when R < 32
-template <typename Ahead>
+// rows [r0, r0+R) of out = M f_J; lanes = (row, k-phase) when R < 32; the
+// assembled front f = [f_J ; f_B] is read contiguously (ASM tasks)
+template <bool SPLIT, typename Ahead>
 __device__ __forceinline__ void run_row(const int32_t* h, double* S, const DagArgs& A, const FactorDev& F,
                                         int lane, Ahead ahead) {
   const int s = h[RW_S], R = h[RW_R], C = h[RW_C], r0 = h[RW_R0], NB = h[RW_NB];
   const double* V = reinterpret_cast<const double*>(reinterpret_cast<const uint8_t*>(h) + h[RW_VAL_OFF]);
-  const int nf = C + NB;
-  if (h[RW_ASM16] >= 0) {
+  if (SPLIT && h[RW_FOFF] >= 0) {  // front assembled by J's ASM tasks
+    const double* f = A.upd + h[RW_FOFF];
+    warp_gather(
+        C + NB, lane, [&](int q) { return __ldcg(f + (q < C ? q : r0 + (q - C))); },
+        [&](int q, double v) { S[q] = v; });
+  } else if (h[RW_ASM16] >= 0) {
     // huge s: J's assembly record in global memory [s, m] cols ptr src
     const int32_t* am = reinterpret_cast<const int32_t*>(A.blobs + 16 * (int64_t)h[RW_ASM16]);
     const int32_t* cols = am + 2;
     const int32_t* ptr = cols + s;
     const int32_t* src = ptr + s + __ldg(am + 1) + 1;
-    for (int q = lane; q < nf; q += 32) {
+    for (int q = lane; q < C + NB; q += 32) {
       const int p = q < C ? q : r0 + (q - C);
       const int e0 = __ldg(ptr + p), e1 = __ldg(ptr + p + 1);
       double acc = q < C ? __ldg(A.rhs + gidx(F, __ldg(cols + q))) : 0.0;
@@ -469,12 +525,12 @@ __device__ __forceinline__ void run_row(const int32_t* h, double* S, const DagAr
       S[q] = acc;
     }
   } else {
+    // f = base + child updates in fixed order (base 0 for update rows); the
+    // metadata is in the slot, so every load below is one global round trip
     const int32_t* cols = h + h[RW_COLS];
     const int32_t* ptr = h + h[RW_PTR];
     const int32_t* src = h + h[RW_SRC];
-    // f = base + child updates in fixed order (base 0 for update rows); the
-    // metadata is in the slot, so every load below is one global round trip
-    for (int q = lane; q < nf; q += 32) {
+    for (int q = lane; q < C + NB; q += 32) {
       const int e0 = ptr[q], e1 = ptr[q + 1];
       double acc = q < C ? __ldg(A.rhs + gidx(F, cols[q])) : 0.0;
       int e = e0;
@@ -520,19 +576,25 @@ __device__ __forceinline__ void run_row(const int32_t* h, double* S, const DagAr
 
 // ===================================================== COL (big backward)
 // columns [k0, k0+c): x_j = sum_r M[k0+r, k0+j] v[r]; lanes = (column, row-phase)
-template <typename Ahead>
+template <bool SPLIT, typename Ahead>
 __device__ __forceinline__ void run_col(const int32_t* h, double* S, const DagArgs& A, const FactorDev& F,
                                         int lane, Ahead ahead) {
   const int s = h[CL_S], m = h[CL_M], k0 = h[CL_K0], c = h[CL_C];
   const double* V = reinterpret_cast<const double*>(reinterpret_cast<const uint8_t*>(h) + h[CL_VAL_OFF]);
   const int32_t* cols = h + h[CL_COLS];
-  const int32_t* rows = h + h[CL_ROWS];
   double* xy = A.xy + F.xy_off;
   const int ny = s - k0, L = ny + m;
   const double* yv = A.upd + h[CL_YOFF] + k0;
-  warp_gather(
-      L, lane, [&](int q) { return q < ny ? __ldcg(yv + q) : -__ldcg(xy + rows[q - ny]); },
-      [&](int q, double v) { S[q] = v; });
+  if (SPLIT && h[CL_XOFF] >= 0) {
+    const double* vb = A.upd + h[CL_XOFF];  // -x_B (XB tasks)
+    warp_gather(
+        L, lane, [&](int q) { return __ldcg(q < ny ? yv + q : vb + (q - ny)); }, [&](int q, double v) { S[q] = v; });
+  } else {
+    const int32_t* rows = h + h[CL_ROWS];
+    warp_gather(
+        L, lane, [&](int q) { return q < ny ? __ldcg(yv + q) : -__ldcg(xy + rows[q - ny]); },
+        [&](int q, double v) { S[q] = v; });
+  }
   ahead();
   __syncwarp();
   const int CP = c >= 32 ? 32 : (c <= 1 ? 1 : 1 << (32 - __clz(c - 1)));  // lanes per phase
@@ -597,7 +659,9 @@ __device__ __forceinline__ void signaller(const DagArgs& A, int32_t* mbox, int32
   }
 }
 
-template <int WPB>
+// SPLIT: the plan has ASM / XB tasks (many-subdomain configurations); the
+// kernel without them keeps the smaller code of the common case
+template <int WPB, bool SPLIT>
 __global__ void __launch_bounds__((WPB + 1) * 32, 20 / WPB) k_dag(DagArgs A) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bars[WPB];
@@ -686,10 +750,20 @@ __global__ void __launch_bounds__((WPB + 1) * 32, 20 / WPB) k_dag(DagArgs A) {
         run_frag(h, false, S, A, F, lane, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);
         break;
       case TK_ROW_FWD:
-        run_row(h, S, A, F, lane, ahead);
+        run_row<SPLIT>(h, S, A, F, lane, ahead);
         break;
       default:
-        run_col(h, S, A, F, lane, ahead);
+        if constexpr (SPLIT) {
+          if (T.kind == TK_ASM_FWD) {
+            run_asm(h, A, F, lane);
+            break;
+          }
+          if (T.kind == TK_XB_BWD) {
+            run_xb(h, A, F, lane);
+            break;
+          }
+        }
+        run_col<SPLIT>(h, S, A, F, lane, ahead);
         break;
     }
     __syncwarp();
@@ -721,7 +795,13 @@ DagSolver::DagSolver(const DevicePlan& plan, int device, int64_t extra_xy) : dev
   wpb_ = 4;
   if (const char* e = std::getenv("SFCDD_WPB")) wpb_ = std::atoi(e);
   SFCDD_REQUIRE(wpb_ == 2 || wpb_ == 4 || wpb_ == 8, SFCDD_EVALUE, "SFCDD_WPB must be 2, 4 or 8");
-  kern_ = wpb_ == 2 ? (const void*)k_dag<2> : wpb_ == 4 ? (const void*)k_dag<4> : (const void*)k_dag<8>;
+  bool split = false;
+  for (const TaskDev& T : plan.tasks) split = split || T.kind == TK_ASM_FWD || T.kind == TK_XB_BWD;
+  kern_ = split ? (wpb_ == 2 ? (const void*)k_dag<2, true> : wpb_ == 4 ? (const void*)k_dag<4, true>
+                                                                      : (const void*)k_dag<8, true>)
+                : (wpb_ == 2 ? (const void*)k_dag<2, false> : wpb_ == 4 ? (const void*)k_dag<4, false>
+                                                                       : (const void*)k_dag<8, false>);
+  split_ = split;
   if (const char* e = std::getenv("SFCDD_DAG_MODE")) mode_ = std::atoi(e);
   if (const char* e = std::getenv("SFCDD_SIG_NS")) sig_ns_ = std::atoi(e);
   smem_ = wpb_ * slot_bytes_;
@@ -740,7 +820,7 @@ DagSolver::DagSolver(const DevicePlan& plan, int device, int64_t extra_xy) : dev
   // counters (plan.h) then nq queue heads, one per 128-byte line; one memset per solve
   nq_ = 16;
   if (const char* e = std::getenv("SFCDD_QUEUES")) nq_ = std::max(1, std::atoi(e));
-  const int64_t cw = (1 + 3 * (int64_t)ngroups_ + 31) / 32 * 32;
+  const int64_t cw = (1 + CTR_PER_GROUP * (int64_t)ngroups_ + 31) / 32 * 32;
   ctr_words_ = cw + 32 * (int64_t)nq_;
   CUDA_CHECK(cudaMalloc(&ctr_, ctr_words_ * 4));
   qhead_ = ctr_ + cw;
@@ -749,11 +829,12 @@ DagSolver::DagSolver(const DevicePlan& plan, int device, int64_t extra_xy) : dev
     // the attribute is per function: only ever raise it, so every live
     // solver (several handles per process in shard emulation) can launch
     static std::mutex mu;
-    static int max_smem[9] = {0};
+    static int max_smem[18] = {0};
     std::lock_guard<std::mutex> g(mu);
-    if (smem_ > max_smem[wpb_]) {
+    const int mi = wpb_ + (split_ ? 9 : 0);
+    if (smem_ > max_smem[mi]) {
       CUDA_CHECK(cudaFuncSetAttribute(kern_, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
-      max_smem[wpb_] = smem_;
+      max_smem[mi] = smem_;
     }
   }
   int per_sm = 0, sms = 0;

@@ -24,7 +24,10 @@ struct Group {
   int32_t parent = -1;  // parent group
   std::vector<int32_t> kids;
   std::vector<int32_t> ftask, btask;  // indices into the unordered task list
+  std::vector<int32_t> atask, xtask;  // BIG: assembly / -x_B gather tasks
   int64_t y_off = -1;                 // BIG: global y slot
+  int64_t f_off = -1;                 // BIG: assembled front [f_J ; f_B] (s + m)
+  int64_t xb_off = -1;                // BIG: -x_B (m)
   int32_t height = 0;
 };
 
@@ -47,7 +50,7 @@ void put_pair(std::vector<int32_t>& v, int32_t lo, int32_t hi) {
 int64_t emit_blob(DevicePlan& P, std::vector<int32_t>& ints, int32_t val_off_word, const std::vector<double>& vals,
                   int32_t& copy_bytes) {
   const int64_t meta_bytes = align16(4 * (int64_t)ints.size());
-  ints[val_off_word] = (int32_t)meta_bytes;
+  if (val_off_word >= 0) ints[val_off_word] = (int32_t)meta_bytes;
   const int64_t val_bytes = align16(8 * (int64_t)vals.size());
   const int64_t off = (int64_t)P.blobs.size();
   copy_bytes = (int32_t)(meta_bytes + val_bytes);
@@ -69,6 +72,10 @@ PlanOptions::PlanOptions() {
   if (const char* e = std::getenv("SFCDD_ROW_MAX")) row_max = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("SFCDD_COL_MAX")) col_max = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("SFCDD_SLACK_US")) slack_us = std::atof(e);
+  if (const char* e = std::getenv("SFCDD_ASM_MAX")) asm_max = std::max(32, std::atoi(e));
+  if (const char* e = std::getenv("SFCDD_ASM_RED")) asm_redundancy = std::atof(e);
+  if (const char* e = std::getenv("SFCDD_XB_MIN")) xb_min_tasks = std::atoi(e);
+  if (const char* e = std::getenv("SFCDD_SPLIT_MIN")) split_min_factors = std::atoi(e);
 }
 
 DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::vector<int64_t>& gstart,
@@ -182,14 +189,14 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
     gr.parent = p < 0 ? -1 : group_of[gr.factor][p];
     if (gr.parent >= 0) groups[gr.parent].kids.push_back(g);
     if (gr.big) {
+      const Supernode& J = F.sn[gr.top];
       gr.y_off = P.upd_doubles;
-      P.upd_doubles += F.sn[gr.top].s;
+      P.upd_doubles += J.s;
       ++P.nbig;
     } else {
       ++P.nfrag;
     }
   }
-  SFCDD_REQUIRE(P.upd_doubles < (int64_t(1) << 31), SFCDD_EINTERNAL, "update buffer too large");
   for (int32_t g = 0; g < G; ++g)  // children have smaller ids than parents
     if (groups[g].parent >= 0)
       groups[groups[g].parent].height = std::max(groups[groups[g].parent].height, groups[g].height + 1);
@@ -217,10 +224,15 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
     T.values = (int32_t)nvals;
     tl.push_back(T);
     tw.push_back(w);
-    ((kind == TK_FRAG_FWD || kind == TK_ROW_FWD) ? groups[g].ftask : groups[g].btask).push_back((int32_t)tl.size() - 1);
+    Group& G_ = groups[g];
+    std::vector<int32_t>& lst = kind == TK_ASM_FWD ? G_.atask
+                                : kind == TK_XB_BWD ? G_.xtask
+                                : (kind == TK_FRAG_FWD || kind == TK_ROW_FWD) ? G_.ftask
+                                                                                : G_.btask;
+    lst.push_back((int32_t)tl.size() - 1);
   };
   for (int32_t g = 0; g < G; ++g) {
-    const Group& gr = groups[g];
+    Group& gr = groups[g];
     const HostFactor& F = *factors[gr.factor];
     const Supernode& Top = F.sn[gr.top];
     if (gr.big) {
@@ -237,11 +249,51 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         SFCDD_REQUIRE(upd_slot[gr.factor][c] >= 0, SFCDD_EINTERNAL, "big child without update slot");
         for (int32_t a = 0; a < K.m; ++a) contrib[F.rel[K.rel_off + a]].push_back(upd_slot[gr.factor][c] + a);
       }
-      // huge s: the f_J assembly metadata goes to one global record shared by
-      // all of J's row tasks instead of every blob
+      // forward row blocks that never straddle s.  ASM mode: values only;
+      // inline mode: + the assembly CSR of the task's front positions
+      auto row_nnz = [&](int32_t r0, int32_t C, int32_t NB) {
+        int64_t nnz = 0;
+        for (int32_t q = 0; q < C + NB; ++q) nnz += (int64_t)contrib[q < C ? q : r0 + (q - C)].size();
+        return nnz;
+      };
+      auto row_split = [&](bool inl, std::vector<std::pair<int32_t, int32_t>>& out) {
+        static const int32_t cand[] = {256, 192, 128, 96, 64, 32, 16, 8, 4, 2, 1};
+        out.clear();
+        for (int32_t r0 = 0; r0 < s + m;) {
+          const int32_t lim = r0 < s ? s : s + m;
+          int32_t R = 0;
+          for (int32_t cnd : cand) {
+            if (cnd > opt.row_max && cnd > 1) continue;
+            const int32_t Re = std::min(cnd, lim - r0);
+            const int32_t C = r0 < s ? r0 + Re : s, NB = r0 < s ? 0 : Re;
+            const int64_t meta = inl ? RW_WORDS + C + (C + NB + 1) + row_nnz(r0, C, NB) : RW_WORDS;
+            if (blob_size(meta, (int64_t)Re * C) <= opt.blob_max && C + NB <= opt.big_scratch_max) {
+              R = Re;
+              break;
+            }
+          }
+          if (R == 0) return false;
+          out.emplace_back(r0, R);
+          r0 += R;
+        }
+        return true;
+      };
+      std::vector<std::pair<int32_t, int32_t>> split_a, split_i;
+      SFCDD_REQUIRE(row_split(false, split_a), SFCDD_EINTERNAL,
+                    "big supernode row does not fit a task blob (s = " + std::to_string(s) + ")");
+      double gathered = 0.0;
+      for (const auto& rb : split_a) gathered += rb.first < s ? rb.first + rb.second : s + rb.second;
+      // three ways to assemble f_J for the ROW tasks: ASM tasks (once, one
+      // extra dependency hop), a global assembly record shared by the ROW
+      // tasks (huge s: the metadata would crowd the values out of the blobs),
+      // or inline metadata in every ROW blob
       int64_t fj_nnz = 0;
       for (int32_t q = 0; q < s; ++q) fj_nnz += (int64_t)contrib[q].size();
-      const bool global_asm = 4 * (RW_WORDS + 2 * s + 1 + fj_nnz) > opt.blob_max / 2;
+      const bool huge = 4 * (RW_WORDS + 2 * s + 1 + fj_nnz) > opt.blob_max / 2;
+      const bool split_ok = (int64_t)factors.size() >= opt.split_min_factors;
+      const bool use_asm = split_ok && gathered >= opt.asm_redundancy * (s + m);
+      const bool global_asm = !use_asm && (huge || !row_split(true, split_i));
+      const auto& split = (use_asm || global_asm) ? split_a : split_i;
       int32_t asm16 = -1;
       if (global_asm) {
         ints.assign({s, m});
@@ -259,27 +311,53 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         std::memcpy(P.blobs.data() + asm_off, ints.data(), 4 * ints.size());
         asm16 = (int32_t)(asm_off / 16);
       }
-      // forward: row blocks that never straddle s
-      auto row_meta = [&](int32_t r0, int32_t R, bool emit) -> int64_t {
+      if (use_asm) {  // the assembled front [f_J ; f_B]
+        gr.f_off = P.upd_doubles;
+        P.upd_doubles += s + m;
+      }
+      if (use_asm) {
+        // forward assembly: f = [f_J ; f_B] in chunks of front positions
+        for (int32_t q0 = 0; q0 < s + m;) {
+          int32_t nq = 0;
+          int64_t nnz = 0, ncol = 0;
+          while (q0 + nq < s + m && nq < opt.asm_max) {
+            const int32_t q = q0 + nq;
+            const int64_t nnz2 = nnz + (int64_t)contrib[q].size(), ncol2 = ncol + (q < s);
+            if (blob_size(AS_WORDS + ncol2 + (nq + 2) + nnz2, 0) > opt.blob_max) break;
+            nnz = nnz2;
+            ncol = ncol2;
+            ++nq;
+          }
+          SFCDD_REQUIRE(nq > 0, SFCDD_EINTERNAL, "assembly position does not fit a task blob");
+          ints.assign(AS_WORDS, 0);
+          ints[AS_S] = s;
+          ints[AS_Q0] = q0;
+          ints[AS_NQ] = nq;
+          ints[AS_FOFF] = (int32_t)gr.f_off;
+          ints[AS_COLS] = (int32_t)ints.size();
+          for (int32_t q = q0; q < q0 + nq && q < s; ++q) ints.push_back(F.perm[S.col0 + q]);
+          ints[AS_PTR] = (int32_t)ints.size();
+          int32_t e = 0;
+          for (int32_t q = q0; q <= q0 + nq; ++q) {
+            ints.push_back(e);
+            if (q < q0 + nq) e += (int32_t)contrib[q].size();
+          }
+          ints[AS_SRC] = (int32_t)ints.size();
+          for (int32_t q = q0; q < q0 + nq; ++q) ints.insert(ints.end(), contrib[q].begin(), contrib[q].end());
+          while (ints.size() % 4) ints.push_back(0);
+          vals.clear();
+          int32_t bytes = 0;
+          const int64_t off = emit_blob(P, ints, -1, vals, bytes);  // metadata only
+          ints.clear();
+          add_task(g, TK_ASM_FWD, off, bytes, 0, 1.2 + 0.004 * (nq + (double)e));
+          q0 += nq;
+        }
+      }
+      for (const auto& rb : split) {
+        const int32_t r0 = rb.first, R = rb.second;
         const int32_t C = r0 < s ? r0 + R : s;
         const int32_t NB = r0 < s ? 0 : R;
-        int64_t nnz = 0;
-        if (!global_asm)
-          for (int32_t q = 0; q < C + NB; ++q) nnz += (int64_t)contrib[q < C ? q : r0 + (q - C)].size();
-        if (!emit) return global_asm ? (int64_t)RW_WORDS : RW_WORDS + C + (C + NB + 1) + nnz;
         ints.assign(RW_WORDS, 0);
-        ints[RW_ASM16] = asm16;
-        if (global_asm) {
-          ints[RW_S] = s;
-          ints[RW_R] = R;
-          ints[RW_C] = C;
-          ints[RW_R0] = r0;
-          ints[RW_NB] = NB;
-          ints[RW_YOFF] = (int32_t)gr.y_off;
-          ints[RW_UOFF] = upd_slot[gr.factor][gr.top];
-          ints[RW_SCRATCH] = C + NB;
-          return (int64_t)ints.size();
-        }
         ints[RW_S] = s;
         ints[RW_R] = R;
         ints[RW_C] = C;
@@ -287,46 +365,24 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         ints[RW_NB] = NB;
         ints[RW_YOFF] = (int32_t)gr.y_off;
         ints[RW_UOFF] = upd_slot[gr.factor][gr.top];
-        ints[RW_COLS] = (int32_t)ints.size();
-        for (int32_t c = 0; c < C; ++c) ints.push_back(F.perm[S.col0 + c]);
-        ints[RW_PTR] = (int32_t)ints.size();
-        int32_t e = 0;
-        for (int32_t q = 0; q <= C + NB; ++q) {
-          ints.push_back(e);
-          if (q < C + NB) e += (int32_t)contrib[q < C ? q : r0 + (q - C)].size();
-        }
-        ints[RW_SRC] = (int32_t)ints.size();
-        for (int32_t q = 0; q < C + NB; ++q) {
-          const auto& cl = contrib[q < C ? q : r0 + (q - C)];
-          ints.insert(ints.end(), cl.begin(), cl.end());
-        }
-        ints[RW_SCRATCH] = C + NB;
-        return (int64_t)ints.size();
-      };
-      auto row_fits = [&](int32_t r0, int32_t R) {
-        const int32_t C = r0 < s ? r0 + R : s;
-        const int32_t NB = r0 < s ? 0 : R;
-        const int64_t nints = row_meta(r0, R, false);
-        const int64_t nnz = global_asm ? 0 : nints - (RW_WORDS + C + (C + NB + 1));
-        (void)nnz;
-        return blob_size(nints, (int64_t)R * C) <= opt.blob_max && C + NB <= opt.big_scratch_max;
-      };
-      static const int32_t cand[] = {256, 192, 128, 96, 64, 32, 16, 8, 4, 2, 1};
-      for (int32_t r0 = 0; r0 < s + m;) {
-        const int32_t lim = r0 < s ? s : s + m;
-        int32_t R = 0;
-        for (int32_t c : cand) {
-          if (c > opt.row_max && c > 1) continue;
-          const int32_t Re = std::min(c, lim - r0);
-          if (row_fits(r0, Re)) {
-            R = Re;
-            break;
+        ints[RW_FOFF] = use_asm ? (int32_t)gr.f_off : -1;
+        ints[RW_ASM16] = asm16;
+        if (!use_asm && !global_asm) {
+          ints[RW_COLS] = (int32_t)ints.size();
+          for (int32_t c = 0; c < C; ++c) ints.push_back(F.perm[S.col0 + c]);
+          ints[RW_PTR] = (int32_t)ints.size();
+          int32_t e = 0;
+          for (int32_t q = 0; q <= C + NB; ++q) {
+            ints.push_back(e);
+            if (q < C + NB) e += (int32_t)contrib[q < C ? q : r0 + (q - C)].size();
+          }
+          ints[RW_SRC] = (int32_t)ints.size();
+          for (int32_t q = 0; q < C + NB; ++q) {
+            const auto& cl = contrib[q < C ? q : r0 + (q - C)];
+            ints.insert(ints.end(), cl.begin(), cl.end());
           }
         }
-        SFCDD_REQUIRE(R > 0, SFCDD_EINTERNAL,
-                      "big supernode row does not fit a task blob (s = " + std::to_string(s) + ")");
-        const int32_t C = r0 < s ? r0 + R : s;
-        row_meta(r0, R, true);
+        ints[RW_SCRATCH] = C + NB;
         vals.assign((size_t)R * C, 0.0);
         for (int32_t k = 0; k < C; ++k)
           for (int32_t i = 0; i < R; ++i) {
@@ -334,18 +390,49 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
             if (k <= row) vals[(size_t)k * R + i] = Mv[packed_col_off(s, m, k) + (row - k)];
           }
         int32_t bytes = 0;
-        const int32_t scratch = ints[RW_SCRATCH];
         const int64_t off = emit_blob(P, ints, RW_VAL_OFF, vals, bytes);
-        P.max_scratch = std::max<int32_t>(P.max_scratch, scratch);
-        add_task(g, TK_ROW_FWD, off, bytes, (int64_t)R * C, 2.36 + 0.0013 * R * C);
-        r0 += R;
+        P.max_scratch = std::max<int32_t>(P.max_scratch, C + NB);
+        add_task(g, TK_ROW_FWD, off, bytes, (int64_t)R * C, (use_asm ? 1.8 : 2.36) + 0.0013 * R * C);
       }
-      // backward: column blocks, dense row-major L x c (L = s+m-k0)
-      for (int32_t k0 = 0; k0 < s;) {
+      // backward column blocks, dense row-major L x c (L = s+m-k0); -x_B is
+      // gathered once by XB tasks when J has many column blocks
+      auto col_width = [&](int32_t k0, bool inl) {
         const int32_t L = s + m - k0;
         int32_t c = std::min<int32_t>(opt.col_max, s - k0);
-        while (c > 1 && blob_size(CL_WORDS + c + m, (int64_t)L * c) > opt.blob_max) --c;
-        SFCDD_REQUIRE(blob_size(CL_WORDS + c + m, (int64_t)L * c) <= opt.blob_max && L <= opt.big_scratch_max,
+        while (c > 1 && blob_size(CL_WORDS + c + (inl ? m : 0), (int64_t)L * c) > opt.blob_max) --c;
+        return c;
+      };
+      int32_t ncol_tasks = 0;
+      for (int32_t k0 = 0; k0 < s; k0 += col_width(k0, false)) ++ncol_tasks;
+      const bool use_xb = split_ok && m > 0 && ncol_tasks >= opt.xb_min_tasks;
+      if (use_xb) {  // -x_B
+        gr.xb_off = P.upd_doubles;
+        P.upd_doubles += m;
+      }
+      if (use_xb) {
+        for (int32_t a0 = 0; a0 < m;) {
+          int32_t na = std::min<int32_t>(m - a0, opt.asm_max);
+          while (na > 1 && blob_size(XB_WORDS + na, 0) > opt.blob_max) --na;
+          ints.assign(XB_WORDS, 0);
+          ints[XB_A0] = a0;
+          ints[XB_NA] = na;
+          ints[XB_XOFF] = (int32_t)gr.xb_off;
+          ints[XB_ROWS] = (int32_t)ints.size();
+          for (int32_t a = a0; a < a0 + na; ++a) ints.push_back(F.perm[F.rows[S.rows_off + a]]);
+          while (ints.size() % 4) ints.push_back(0);
+          vals.clear();
+          int32_t bytes = 0;
+          const int64_t off = emit_blob(P, ints, -1, vals, bytes);  // metadata only
+          ints.clear();
+          add_task(g, TK_XB_BWD, off, bytes, 0, 1.2 + 0.003 * na);
+          a0 += na;
+        }
+      }
+      for (int32_t k0 = 0; k0 < s;) {
+        const int32_t L = s + m - k0;
+        const int32_t c = col_width(k0, !use_xb);
+        SFCDD_REQUIRE(blob_size(CL_WORDS + c + (use_xb ? 0 : m), (int64_t)L * c) <= opt.blob_max &&
+                          L <= opt.big_scratch_max,
                       SFCDD_EINTERNAL,
                       "big supernode column does not fit a task blob (s+m = " + std::to_string(s + m) + ")");
         ints.assign(CL_WORDS, 0);
@@ -354,10 +441,13 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         ints[CL_K0] = k0;
         ints[CL_C] = c;
         ints[CL_YOFF] = (int32_t)gr.y_off;
+        ints[CL_XOFF] = use_xb ? (int32_t)gr.xb_off : -1;
         ints[CL_COLS] = (int32_t)ints.size();
         for (int32_t j = 0; j < c; ++j) ints.push_back(F.perm[S.col0 + k0 + j]);
-        ints[CL_ROWS] = (int32_t)ints.size();
-        for (int32_t a = 0; a < m; ++a) ints.push_back(F.perm[F.rows[S.rows_off + a]]);
+        if (!use_xb) {
+          ints[CL_ROWS] = (int32_t)ints.size();
+          for (int32_t a = 0; a < m; ++a) ints.push_back(F.perm[F.rows[S.rows_off + a]]);
+        }
         ints[CL_SCRATCH] = L;
         vals.assign((size_t)L * c, 0.0);
         int64_t nv = 0;
@@ -369,7 +459,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         int32_t bytes = 0;
         const int64_t off = emit_blob(P, ints, CL_VAL_OFF, vals, bytes);
         P.max_scratch = std::max<int32_t>(P.max_scratch, L);
-        add_task(g, TK_COL_BWD, off, bytes, nv, 2.24 + 0.0013 * nv);
+        add_task(g, TK_COL_BWD, off, bytes, nv, (use_xb ? 1.8 : 2.24) + 0.0013 * nv);
         k0 += c;
       }
       continue;
@@ -642,50 +732,86 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
     add_task(g, TK_FRAG_BWD, off, bytes, nvals, 1.11 + 0.0021 * nvals + 0.68 * nlev);
   }
 
-  // ---- 3. dependencies
+  SFCDD_REQUIRE(P.upd_doubles < (int64_t(1) << 31), SFCDD_EINTERNAL, "update buffer too large");
+
+  // ---- 3. dependencies (counters: plan.h)
+  auto FIN = [&](int32_t g) { return 1 + g; };
+  auto BDONE = [&](int32_t g) { return 1 + G + g; };
+  auto RDONE = [&](int32_t g) { return 1 + 2 * G + g; };
+  auto ADONE = [&](int32_t g) { return 1 + 3 * G + g; };
+  auto XDONE = [&](int32_t g) { return 1 + 4 * G + g; };
   for (int32_t g = 0; g < G; ++g) {
     const Group& gr = groups[g];
     int32_t kids_f = 0;
     for (int32_t c : gr.kids) kids_f += (int32_t)groups[c].ftask.size();
-    for (int32_t t : gr.ftask) {
-      tl[t].wait_idx = kids_f > 0 ? 1 + g : -1;
+    // children's forward -> (BIG: assembly ->) forward rows
+    for (int32_t t : gr.atask) {
+      tl[t].wait_idx = kids_f > 0 ? FIN(g) : -1;
       tl[t].wait_target = kids_f;
-      tl[t].signal_idx = gr.parent >= 0 ? 1 + gr.parent : 1 + 2 * G + g;
+      tl[t].signal_idx = ADONE(g);
+    }
+    for (int32_t t : gr.ftask) {
+      if (!gr.atask.empty()) {
+        tl[t].wait_idx = ADONE(g);
+        tl[t].wait_target = (int32_t)gr.atask.size();
+      } else {
+        tl[t].wait_idx = kids_f > 0 ? FIN(g) : -1;
+        tl[t].wait_target = kids_f;
+      }
+      tl[t].signal_idx = gr.parent >= 0 ? FIN(gr.parent) : RDONE(g);
+    }
+    // parent's backward (root: own forward) -> (BIG: -x_B gather ->) backward
+    for (int32_t t : gr.xtask) {
+      SFCDD_REQUIRE(gr.parent >= 0, SFCDD_EINTERNAL, "root supernode with below rows");
+      tl[t].wait_idx = BDONE(gr.parent);
+      tl[t].wait_target = (int32_t)groups[gr.parent].btask.size();
+      tl[t].signal_idx = XDONE(g);
     }
     for (int32_t t : gr.btask) {
-      if (gr.parent >= 0) {
-        tl[t].wait_idx = 1 + G + gr.parent;
+      if (!gr.xtask.empty()) {
+        tl[t].wait_idx = XDONE(g);
+        tl[t].wait_target = (int32_t)gr.xtask.size();
+      } else if (gr.parent >= 0) {
+        tl[t].wait_idx = BDONE(gr.parent);
         tl[t].wait_target = (int32_t)groups[gr.parent].btask.size();
       } else {
-        tl[t].wait_idx = 1 + 2 * G + g;
+        tl[t].wait_idx = RDONE(g);
         tl[t].wait_target = (int32_t)gr.ftask.size();
       }
-      tl[t].signal_idx = 1 + G + g;
+      tl[t].signal_idx = BDONE(g);
     }
   }
 
   // ---- 4. queue order: decreasing critical-path rank (HLFET) over the
   // combined forward/backward DAG -- a topological order (weights > 0)
-  std::vector<double> wf(G, 0.0), wb(G, 0.0), rank_f(G, 0.0), rank_b(G, 0.0), succ_f(G, 0.0), succ_b(G, 0.0);
+  std::vector<double> wf(G, 0.0), wb(G, 0.0), wa(G, 0.0), wx(G, 0.0), rank_f(G, 0.0), rank_b(G, 0.0),
+      succ_f(G, 0.0), succ_b(G, 0.0);
   for (int32_t g = 0; g < G; ++g) {
     for (int32_t t : groups[g].ftask) wf[g] = std::max(wf[g], tw[t]);
     for (int32_t t : groups[g].btask) wb[g] = std::max(wb[g], tw[t]);
+    for (int32_t t : groups[g].atask) wa[g] = std::max(wa[g], tw[t]);
+    for (int32_t t : groups[g].xtask) wx[g] = std::max(wx[g], tw[t]);
   }
   for (int32_t g = 0; g < G; ++g) {  // children before parents
     double mx = 0.0;
     for (int32_t c : groups[g].kids) mx = std::max(mx, rank_b[c]);
     succ_b[g] = mx;
-    rank_b[g] = wb[g] + mx;
+    rank_b[g] = wx[g] + wb[g] + mx;
   }
   for (int32_t g = G - 1; g >= 0; --g) {  // parents before children
     succ_f[g] = groups[g].parent >= 0 ? rank_f[groups[g].parent] : rank_b[g];
-    rank_f[g] = wf[g] + succ_f[g];
+    rank_f[g] = wa[g] + wf[g] + succ_f[g];
   }
   std::vector<double> rank(tl.size());
   for (size_t t = 0; t < tl.size(); ++t) {
     const int32_t g = tl[t].group;
-    const bool fwd = tl[t].kind == TK_FRAG_FWD || tl[t].kind == TK_ROW_FWD;
-    rank[t] = tw[t] + (fwd ? succ_f[g] : succ_b[g]);
+    switch (tl[t].kind) {
+      case TK_ASM_FWD: rank[t] = tw[t] + wf[g] + succ_f[g]; break;
+      case TK_XB_BWD: rank[t] = tw[t] + wb[g] + succ_b[g]; break;
+      case TK_FRAG_FWD:
+      case TK_ROW_FWD: rank[t] = tw[t] + succ_f[g]; break;
+      default: rank[t] = tw[t] + succ_b[g]; break;
+    }
   }
   // queue = start order of a simulated list schedule on opt.workers warps:
   // whenever a warp is free it takes the highest-rank READY task.  At run
@@ -694,7 +820,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
   std::vector<int32_t> order;
   order.reserve(tl.size());
   {
-    const int32_t nctr = 1 + 3 * G;
+    const int32_t nctr = 1 + CTR_PER_GROUP * G;
     std::vector<int32_t> ctr(nctr, 0);
     std::vector<std::vector<int32_t>> waiters(nctr);
     auto cmp_rank = [&](int32_t a, int32_t b) { return rank[a] < rank[b] || (rank[a] == rank[b] && a > b); };
@@ -771,8 +897,8 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
       // walk the critical path: successor with the largest rank
       std::vector<std::vector<int32_t>> succ(nctr);
       std::string path;
-      int hops[4] = {0, 0, 0, 0};
-      double wsum[4] = {0, 0, 0, 0};
+      int hops[TK_KINDS] = {0};
+      double wsum[TK_KINDS] = {0};
       while (cur >= 0) {
         if (tl[cur].kind == TK_ROW_FWD) {
           const Group& gr = groups[tl[cur].group];
@@ -788,8 +914,11 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         cur = best;
       }
       std::fprintf(stderr, "[plan] critical big chain s/m(row tasks):%s\n", path.c_str());
-      std::fprintf(stderr, "[plan] critical path: frag_f %d (%.0f us) frag_b %d (%.0f us) row %d (%.0f us) col %d (%.0f us)\n",
-                   hops[0], wsum[0], hops[1], wsum[1], hops[2], wsum[2], hops[3], wsum[3]);
+      std::fprintf(stderr,
+                   "[plan] critical path: frag_f %d (%.0f us) frag_b %d (%.0f us) row %d (%.0f us) col %d (%.0f us) "
+                   "asm %d (%.0f us) xb %d (%.0f us)\n",
+                   hops[0], wsum[0], hops[1], wsum[1], hops[2], wsum[2], hops[3], wsum[3], hops[4], wsum[4], hops[5],
+                   wsum[5]);
     }
   }
   P.tasks.resize(tl.size());
@@ -813,7 +942,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
     }
     for (const Group& gr : groups) maxh = std::max(maxh, gr.height);
     {  // copied bytes vs factor value bytes per task kind
-      double cb[4] = {0, 0, 0, 0}, vb[4] = {0, 0, 0, 0}, nt[4] = {0, 0, 0, 0};
+      double cb[TK_KINDS] = {0}, vb[TK_KINDS] = {0}, nt[TK_KINDS] = {0};
       for (const TaskDev& T : P.tasks) {
         cb[T.kind] += T.copy_bytes;
         vb[T.kind] += 8.0 * T.values;
@@ -896,8 +1025,8 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
       }
       std::fprintf(stderr, "[plan] flattened FRAG values %.1f MB vs sparse %.1f MB (%.2fx); ratio hist <1.25 %.0f <1.5 %.0f <2 %.0f <3 %.0f >=3 %.0f\n",
                    8 * dense / 1e6, 8 * sparse / 1e6, dense / sparse, hist[0], hist[1], hist[2], hist[3], hist[4]);
-      const char* nm[4] = {"frag_f", "frag_b", "row", "col"};
-      for (int k = 0; k < 4; ++k)
+      const char* nm[TK_KINDS] = {"frag_f", "frag_b", "row", "col", "asm", "xb"};
+      for (int k = 0; k < TK_KINDS; ++k)
         std::fprintf(stderr, "[plan] %s: %.0f tasks, copied %.1f MB, values %.1f MB (%.2fx), %.0f B/task\n", nm[k],
                      nt[k], cb[k] / 1e6, vb[k] / 1e6, cb[k] / std::max(1.0, vb[k]), cb[k] / std::max(1.0, nt[k]));
     }

@@ -28,13 +28,24 @@ struct FactorDev {
   int64_t n;
 };
 
-enum TaskKind : int32_t { TK_FRAG_FWD = 0, TK_FRAG_BWD = 1, TK_ROW_FWD = 2, TK_COL_BWD = 3 };
+enum TaskKind : int32_t {
+  TK_FRAG_FWD = 0,
+  TK_FRAG_BWD = 1,
+  TK_ROW_FWD = 2,
+  TK_COL_BWD = 3,
+  TK_ASM_FWD = 4,  // BIG forward assembly: f = [f_J ; f_B] once per supernode
+  TK_XB_BWD = 5,   // BIG backward gather: -x_B once per supernode
+  TK_KINDS = 6
+};
 
 // One warp task.  The queue holds all tasks in decreasing critical-path rank
 // (HLFET), a topological order: a task only waits on tasks earlier in the
 // queue.  Counters (int32, zeroed per solve): ctr[0] = queue head; per group
 // g of G: fin = 1+g (forward arrivals of g's children), bdone = 1+G+g
-// (g's backward tasks done), rdone = 1+2G+g (a root group's forward done).
+// (g's backward tasks done), rdone = 1+2G+g (a root group's forward done),
+// adone = 1+3G+g (BIG: assembly tasks done), xdone = 1+4G+g (BIG: -x_B
+// gathered).
+constexpr int CTR_PER_GROUP = 5;
 struct TaskDev {
   int64_t blob_off;     // byte offset of the task blob (16-byte aligned)
   int32_t copy_bytes;   // bytes bulk-copied into the slot (multiple of 16)
@@ -102,16 +113,27 @@ enum LevField { L_REC0 = 0, L_REC1, L_RUN0, L_RUN1, L_BP0, L_BP1, L_FI0, L_FI1, 
 enum SnRecField { R_SM = 0, R_SCR, R_VAL, R_CPOS, R_WORDS };
 
 // ---------------------------------------------------------- BIG blobs
-// ROW blob: forward rows [r0, r0+R) of one big supernode J (either all < s:
-// y rows, or all >= s: update rows).  Self-contained unless J's assembly
-// metadata is too large for a blob (RW_ASM16):
-//   cols: ro of J's first C columns (rhs gather)
-//   ptr[C+NB+1] / src[nnz]: CSR over the task's front positions (f_J[0:C),
-//     then its NB update rows) of the child update indices summed into each,
-//     in fixed order (children, then rows)
-//   values: R x C dense column-major (leading dim R), entry (i, k) =
-//     M[r0+i, k] (zero where k > r0+i), C = min(r0+R, s).
-// Scratch: [f (C+NB)] [staged child updates (nnz)].
+// A BIG group is one supernode J too large for a slot.  Its dense block
+// M = [L_JJ^-1 ; L_BJ L_JJ^-1] is cut into ROW tasks (forward) and COL tasks
+// (backward); the gathers of the sweeps are done ONCE per supernode by
+// ASM / XB tasks into contiguous global vectors (update buffer):
+//   f  [s+m] at AS_FOFF: f_J = rhs + child updates, f_B = child updates
+//   vb [m]   at XB_XOFF: -x_B
+// so ROW / COL blobs carry values only (plus the column ids COL stores to).
+// The split costs one dependency hop, so it is used only where the inline
+// gathers would be repeated by many tasks (PlanOptions::asm_redundancy,
+// xb_min_tasks); otherwise ROW / COL tasks gather for themselves.
+//
+// ASM blob: front positions [q0, q0+nq) of J: cols (ro of the positions < s),
+// ptr[nq+1] / src[nnz] = CSR of the child update indices summed into each
+// position (fixed order: children, then rows).
+enum AsmHdr { AS_S = 0, AS_Q0, AS_NQ, AS_FOFF, AS_COLS, AS_PTR, AS_SRC, AS_WORDS };
+// XB blob: rows [a0, a0+na) of J's m below-rows: vb[a] = -x(rows[a]).
+enum XbHdr { XB_A0 = 0, XB_NA, XB_XOFF, XB_ROWS, XB_WORDS };
+// ROW blob: forward rows [r0, r0+R) of J (all < s: y rows, or all >= s:
+// update rows).  Values: R x C dense column-major (leading dim R), entry
+// (i, k) = M[r0+i, k] (zero where k > r0+i), C = min(r0+R, s).  Scratch:
+// [f_J[0:C) ; f_B[r0 : r0+NB)] loaded from f.
 enum RowHdr {
   RW_S = 0,
   RW_R,        // rows in the block
@@ -120,17 +142,16 @@ enum RowHdr {
   RW_NB,       // block rows >= s (0 or R)
   RW_YOFF,     // global y slot of J (upd buffer)
   RW_UOFF,     // global update slot of J (-1: root)
-  RW_COLS,     // int offset: ro[C]
-  RW_PTR,      // int offset: ptr[C+NB+1]
-  RW_SRC,      // int offset: src[nnz]
-  RW_ASM16,    // -1, or (huge s) byte offset / 16 of J's global assembly record
-               // [s, m] [cols (s)] [ptr (s+m+1)] [src] over FRONT positions;
-               // then RW_COLS / RW_PTR / RW_SRC are unused
+  RW_FOFF,     // f slot of J (ASM mode), or -1: the task assembles f itself from
+  RW_COLS,     //   int offset: ro[C] (rhs gather)
+  RW_PTR,      //   int offset: ptr[C+NB+1] / src[nnz]: CSR over the task's front
+  RW_SRC,      //   positions (f_J[0:C), then its NB update rows) of child update indices
+  RW_ASM16,    // or (huge s, >= 0): byte offset / 16 of J's global assembly record
+               // [s, m] [cols (s)] [ptr (s+m+1)] [src] over FRONT positions
   RW_VAL_OFF,  // byte offset of the values
   RW_SCRATCH,  // doubles of scratch used
   RW_WORDS
 };
-
 // COL blob: backward columns [k0, k0+c) of J.  Values: L x c dense row-major
 // block of M (L = s+m-k0 rows starting at row k0), entry (r, j) =
 // M[k0+r, k0+j] (zero where r < j).  Scratch: v = [y_J[k0:s) ; -x_B] (L).
@@ -140,8 +161,9 @@ enum ColHdr {
   CL_K0,
   CL_C,        // columns in the block
   CL_YOFF,     // global y slot of J
+  CL_XOFF,     // vb slot of J (-x_B, XB mode), or -1: the task gathers -x_B itself
   CL_COLS,     // int offset: ro of the c columns
-  CL_ROWS,     // int offset: ro of the m below rows
+  CL_ROWS,     // (CL_XOFF < 0) int offset: ro of the m below rows
   CL_VAL_OFF,  // byte offset of the values
   CL_SCRATCH,
   CL_WORDS
@@ -157,6 +179,12 @@ struct PlanOptions {
   int32_t sms = 148;               // SMs of the target device (set by the caller)
   int32_t row_max = 32;            // rows per ROW task (SFCDD_ROW_MAX; latency vs task count)
   int32_t col_max = 16;            // columns per COL task (SFCDD_COL_MAX)
+  int32_t asm_max = 256;           // front positions per ASM task (SFCDD_ASM_MAX)
+  double asm_redundancy = 4.0;     // ASM when ROW tasks would gather the front >= this often (SFCDD_ASM_RED)
+  int32_t xb_min_tasks = 4;        // XB when J has >= this many COL tasks (SFCDD_XB_MIN)
+  int32_t split_min_factors = 256; // ASM / XB only in plans of >= this many factors: with few
+                                   // subdomains the top of the trees is latency bound and the
+                                   // extra dependency hop costs more than it saves (SFCDD_SPLIT_MIN)
   double slack_us = 4.0;           // queue-order simulation: dependents become ready this late (SFCDD_SLACK_US)
   PlanOptions();                 // environment overrides SFCDD_BLOB_MAX, SFCDD_SCRATCH_MAX
 };

@@ -21,7 +21,7 @@ inline int32_t hi16(int32_t v) { return (int32_t)((uint32_t)v >> 16); }
 void plan_exec_host(const DevicePlan& P, const double* rhs, double* xy) {
   std::vector<double> upd(P.upd_doubles, 0.0);
   std::vector<double> scratch;
-  std::vector<int64_t> ctr(1 + 3 * (size_t)P.ngroups, 0);
+  std::vector<int64_t> ctr(1 + CTR_PER_GROUP * (size_t)P.ngroups, 0);
   for (size_t t = 0; t < P.tasks.size(); ++t) {
     const TaskDev& T = P.tasks[t];
     SFCDD_REQUIRE(T.wait_idx < 0 || ctr[T.wait_idx] >= T.wait_target, SFCDD_EINTERNAL,
@@ -35,21 +35,41 @@ void plan_exec_host(const DevicePlan& P, const double* rhs, double* xy) {
       return g;
     };
     double* x = xy + Fd.xy_off;
-    if (T.kind == TK_ROW_FWD) {
+    if (T.kind == TK_ASM_FWD) {
+      const int32_t s = h[AS_S], q0 = h[AS_Q0], nq = h[AS_NQ];
+      const int32_t* cols = h + h[AS_COLS];
+      const int32_t* ptr = h + h[AS_PTR];
+      const int32_t* src = h + h[AS_SRC];
+      for (int32_t i = 0; i < nq; ++i) {
+        const int32_t q = q0 + i;
+        double acc = q < s ? rhs[gidx(cols[i])] : 0.0;
+        for (int32_t e = ptr[i]; e < ptr[i + 1]; ++e) acc += upd[src[e]];
+        upd[h[AS_FOFF] + q] = acc;
+      }
+    } else if (T.kind == TK_XB_BWD) {
+      const int32_t* rows = h + h[XB_ROWS];
+      for (int32_t i = 0; i < h[XB_NA]; ++i) upd[h[XB_XOFF] + h[XB_A0] + i] = -x[rows[i]];
+    } else if (T.kind == TK_ROW_FWD) {
       const double* V = reinterpret_cast<const double*>(blob + h[RW_VAL_OFF]);
       const int32_t s = h[RW_S], R = h[RW_R], C = h[RW_C], r0 = h[RW_R0], NB = h[RW_NB];
-      const bool ga = h[RW_ASM16] >= 0;  // global assembly record (huge s)
-      const int32_t* am = reinterpret_cast<const int32_t*>(P.blobs.data() + 16 * (int64_t)std::max(0, h[RW_ASM16]));
-      const int32_t* cols = ga ? am + 2 : h + h[RW_COLS];
-      const int32_t* ptr = ga ? am + 2 + am[0] : h + h[RW_PTR];
-      const int32_t* src = ga ? ptr + am[0] + am[1] + 1 : h + h[RW_SRC];
       scratch.assign(C + NB, 0.0);
       double* S = scratch.data();
-      for (int32_t q = 0; q < C + NB; ++q) {
-        const int32_t p = ga ? (q < C ? q : r0 + (q - C)) : q;
-        double acc = q < C ? rhs[gidx(cols[q])] : 0.0;
-        for (int32_t e = ptr[p]; e < ptr[p + 1]; ++e) acc += upd[src[e]];
-        S[q] = acc;
+      if (h[RW_FOFF] >= 0) {
+        const double* f = upd.data() + h[RW_FOFF];
+        for (int32_t q = 0; q < C; ++q) S[q] = f[q];
+        for (int32_t i = 0; i < NB; ++i) S[C + i] = f[r0 + i];
+      } else {
+        const bool ga = h[RW_ASM16] >= 0;  // global assembly record (huge s)
+        const int32_t* am = reinterpret_cast<const int32_t*>(P.blobs.data() + 16 * (int64_t)std::max(0, h[RW_ASM16]));
+        const int32_t* cols = ga ? am + 2 : h + h[RW_COLS];
+        const int32_t* ptr = ga ? am + 2 + am[0] : h + h[RW_PTR];
+        const int32_t* src = ga ? ptr + am[0] + am[1] + 1 : h + h[RW_SRC];
+        for (int32_t q = 0; q < C + NB; ++q) {
+          const int32_t p = ga ? (q < C ? q : r0 + (q - C)) : q;
+          double acc = q < C ? rhs[gidx(cols[q])] : 0.0;
+          for (int32_t e = ptr[p]; e < ptr[p + 1]; ++e) acc += upd[src[e]];
+          S[q] = acc;
+        }
       }
       for (int32_t i = 0; i < R; ++i) {
         double acc = 0.0;
@@ -64,12 +84,12 @@ void plan_exec_host(const DevicePlan& P, const double* rhs, double* xy) {
       const double* V = reinterpret_cast<const double*>(blob + h[CL_VAL_OFF]);
       const int32_t s = h[CL_S], m = h[CL_M], k0 = h[CL_K0], c = h[CL_C];
       const int32_t* cols = h + h[CL_COLS];
-      const int32_t* rows = h + h[CL_ROWS];
       const int32_t L = s + m - k0;
       scratch.assign(L, 0.0);
       double* v = scratch.data();
       for (int32_t i = k0; i < s; ++i) v[i - k0] = upd[h[CL_YOFF] + i];
-      for (int32_t a = 0; a < m; ++a) v[s - k0 + a] = -x[rows[a]];
+      for (int32_t a = 0; a < m; ++a)
+        v[s - k0 + a] = h[CL_XOFF] >= 0 ? upd[h[CL_XOFF] + a] : -x[h[h[CL_ROWS] + a]];
       for (int32_t j = 0; j < c; ++j) {
         double acc = 0.0;
         for (int32_t r = j; r < L; ++r) acc += V[(size_t)r * c + j] * v[r];

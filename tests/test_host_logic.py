@@ -123,8 +123,14 @@ def test_host_factor_rejects_non_spd():
 @pytest.mark.parametrize("levels,p,gamma,blob", [((7, 7), 16, 0.5, 0), ((7, 7), 16, 0.25, 4096),
                                                   ((4, 4, 4), 8, 0.5, 0), ((4, 4, 4), 8, 1.0, 2048),
                                                   ((6, 5), 6, 0.75, 0)])
-def test_device_plan_host_interpreter(oracle, levels, p, gamma, blob):
-    """The fragment/blob layout the DAG kernel executes, run on the host."""
+@pytest.mark.parametrize("split", [False, True])
+def test_device_plan_host_interpreter(oracle, levels, p, gamma, blob, split, monkeypatch):
+    """The fragment/blob layout the DAG kernel executes, run on the host;
+    ``split`` forces the ASM / XB task path of big supernodes (plan.h)."""
+    if split:
+        monkeypatch.setenv("SFCDD_SPLIT_MIN", "1")
+        monkeypatch.setenv("SFCDD_ASM_RED", "1")
+        monkeypatch.setenv("SFCDD_XB_MIN", "1")
     A = oracle.assemble_scaled_laplacian(levels)
     n = A.shape[0]
     ov = oracle.enlarge(oracle.disjoint_partition(n, p), gamma)
