@@ -360,8 +360,8 @@ __device__ __forceinline__ void run_frag(const int32_t* h, bool fwd, double* S, 
   double* xy = A.xy + F.xy_off;
   if (fwd) {
     stamp(0);
-    const int nscr = h[H_SCRATCH];
-    for (int i = lane; i < nscr; i += 32) S[i] = 0.0;
+    const int nzero = h[H_ZERO];
+    for (int i = lane; i < nzero; i += 32) S[i] = 0.0;
     __syncwarp();
     {  // one batched gather: right-hand side at the columns + external child updates
       const int32_t* eu = h + h[H_EXTU];

@@ -722,6 +722,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
     ints[H_ITEMS] = (int32_t)ints.size();
     ints.insert(ints.end(), items.begin(), items.end());
     ints[H_SCRATCH] = scratch_used;
+    ints[H_ZERO] = nsn > 0 ? cpos[0] : 0;  // frontal slots [0, cpos[0])
     SFCDD_REQUIRE(scratch_used <= opt.scratch_max, SFCDD_EINTERNAL, "fragment scratch exceeds budget");
     int32_t bytes = 0;
     const int64_t off = emit_blob(P, ints, H_VAL_OFF, vals, bytes);

@@ -102,6 +102,8 @@ enum FragHdr {
   H_ITEMS,      // int offset of items (int2)
   H_EXTX_BASE,  // scratch position of the first ext_x slot
   H_EXTU_BASE,  // scratch position of the first ext_u slot
+  H_ZERO,       // doubles zeroed before the forward gather: the frontal slots
+                // (their f_B rows accumulate child updates); the rest is written
   H_WORDS
 };
 // per-level table: record range, forward gather runs, backward row pairs,

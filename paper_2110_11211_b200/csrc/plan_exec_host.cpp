@@ -6,6 +6,7 @@
 // suite validate plan layouts without a GPU); not on the product path.
 #include <algorithm>
 #include <cstring>
+#include <limits>
 #include <vector>
 
 #include "common.h"
@@ -100,7 +101,10 @@ void plan_exec_host(const DevicePlan& P, const double* rhs, double* xy) {
       const double* vals = reinterpret_cast<const double*>(blob + h[H_VAL_OFF]);
       const int32_t* recs = h + h[H_REC];
       const int32_t* cols = h + h[H_COLS];
-      scratch.assign(h[H_SCRATCH], 0.0);
+      // like the kernel: only the frontal slots are zeroed; everything else
+      // must be written before it is read (NaN poison catches a miss)
+      scratch.assign(h[H_SCRATCH], std::numeric_limits<double>::quiet_NaN());
+      if (fwd) std::fill(scratch.begin(), scratch.begin() + h[H_ZERO], 0.0);
       double* S = scratch.data();
       const int32_t ncol = h[H_NCOL];
       const int32_t* colpos = h + h[H_COLPOS];
