@@ -16,12 +16,13 @@ for w in $WHAT; do
     c4) timeout 1500 python bench.py --config c4 --steps 3 --warmup 3 --no-cpu-baseline > $OUT/bench_c4.json 2> $OUT/bench_c4.err ;;
     ref) timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_reference_c2.json 2> $OUT/bench_reference_c2.err ;;
     ncu)
-      timeout 300 python tools/profile_apply.py c2 3 > $OUT/plain.log 2>&1 &&
+      timeout 300 python tools/profile_pcg.py c2 6 > $OUT/plain.log 2>&1 &&
       timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-          --log-file $OUT/launches_c2.csv python tools/profile_apply.py c2 3 > $OUT/ncu_launch.log 2>&1 &&
-      timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_dag -s 1 -c 1 \
-          -o $OUT/dag_c2 python tools/profile_apply.py c2 3 > $OUT/ncu_full.log 2>&1
+          --log-file $OUT/launches_c2.csv python tools/profile_pcg.py c2 6 > $OUT/ncu_launch.log 2>&1 &&
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_dag -s 2 -c 1 \
+          -o $OUT/dag_c2 python tools/profile_pcg.py c2 6 > $OUT/ncu_full.log 2>&1
       echo "ncu exit $?" >> $OUT/ncu_full.log ;;
+    trace) timeout 300 python tools/trace_dag.py c2 > $OUT/trace.log 2>&1; mv gpurun_out/trace_c2.npz $OUT/ ;;
   esac
 done
 echo done
