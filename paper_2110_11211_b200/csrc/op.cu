@@ -21,6 +21,7 @@
 
 #include "op.h"
 #include "plan.h"
+#include "tiles.h"
 
 namespace sfcdd {
 
@@ -372,6 +373,221 @@ __global__ void k_combine_chunk(CombineArgs C, const int64_t* __restrict__ cstar
     rw = block_sum(rw);
     if (threadIdx.x == 0) part[ch] = rw;
   }
+}
+
+// ------------------------------------------------ index-free stencil tiles
+// One CTA per tile (tiles.h): own values -> box in shared memory through the
+// tile's rank->box table (entries = packed box coordinates), face neighbours
+// through the halo rank list, then the stencil in the box.  Same summation
+// order as stencil_at (dhat x, then axis 0 -/+, axis 1 -/+, ...; absent
+// neighbours skipped): bitwise equal.  PER points per thread, all loads of a
+// phase issued before their uses.
+template <int D>
+__device__ __forceinline__ void tile_coords(uint32_t e, int& u0, int& u1, int& u2) {
+  if (D == 3) {
+    u0 = e & 31;
+    u1 = (e >> 5) & 31;
+    u2 = (e >> 10) & 31;
+  } else {
+    u0 = e & 255;
+    u1 = e >> 8;
+    u2 = 0;
+  }
+}
+
+template <int D, int PER, typename Val, typename Epi>
+__device__ __forceinline__ void tile_stencil(const Tiles& T, const Stencil& S, int tile, double* Lx, double* H,
+                                             Val val, Epi epi) {
+  const int r0 = T.r0[tile], np = T.r0[tile + 1] - r0;
+  const int n0 = T.dims[3 * tile], n1 = T.dims[3 * tile + 1], n2 = T.dims[3 * tile + 2];
+  const uint16_t* tab = T.tab + T.tab_off[tile];
+  const int h0 = T.halo_off[tile], nh = T.halo_off[tile + 1] - h0;
+  const int32_t* hr = T.halo + h0;
+  const int st0 = D == 3 ? n1 * n2 : n1, st1 = D == 3 ? n2 : 1;
+  uint32_t e[PER];
+  int bl[PER];
+  double v[PER];
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int k = threadIdx.x + u * VEC_THREADS;
+    e[u] = k < np ? __ldg(tab + k) : 0u;
+  }
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int k = threadIdx.x + u * VEC_THREADS;
+    v[u] = k < np ? val(r0 + k) : 0.0;
+  }
+  for (int h = threadIdx.x; h < nh; h += VEC_THREADS) {
+    const int32_t rk = __ldg(hr + h);
+    H[h] = rk >= 0 ? val(rk) : 0.0;
+  }
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    int u0, u1, u2;
+    tile_coords<D>(e[u], u0, u1, u2);
+    bl[u] = u0 * st0 + u1 * st1 + u2;
+    if (threadIdx.x + u * VEC_THREADS < np) Lx[bl[u]] = v[u];
+  }
+  __syncthreads();
+  // face f = 2 axis + side; face sizes: axis 0 n1 n2, axis 1 n0 n2, axis 2 n0 n1
+  const int fs0 = D == 3 ? n1 * n2 : n1, fs1 = D == 3 ? n0 * n2 : n0, fs2 = D == 3 ? n0 * n1 : 0;
+  double acc[PER];
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    int u0, u1, u2;
+    tile_coords<D>(e[u], u0, u1, u2);
+    const int b = bl[u];
+    double a = S.dhat * v[u];
+    {  // axis 0: face index over (u1[, u2])
+      const int fi = D == 3 ? u1 * n2 + u2 : u1;
+      if (u0 > 0) a = fma(S.off[0], Lx[b - st0], a);
+      else if (__ldg(hr + fi) >= 0) a = fma(S.off[0], H[fi], a);
+      if (u0 < n0 - 1) a = fma(S.off[0], Lx[b + st0], a);
+      else if (__ldg(hr + fs0 + fi) >= 0) a = fma(S.off[0], H[fs0 + fi], a);
+    }
+    {  // axis 1: face index over (u0[, u2])
+      const int fb = 2 * fs0;
+      const int fi = D == 3 ? u0 * n2 + u2 : u0;
+      if (u1 > 0) a = fma(S.off[1], Lx[b - st1], a);
+      else if (__ldg(hr + fb + fi) >= 0) a = fma(S.off[1], H[fb + fi], a);
+      if (u1 < n1 - 1) a = fma(S.off[1], Lx[b + st1], a);
+      else if (__ldg(hr + fb + fs1 + fi) >= 0) a = fma(S.off[1], H[fb + fs1 + fi], a);
+    }
+    if (D == 3) {  // axis 2: face index over (u0, u1)
+      const int fb = 2 * fs0 + 2 * fs1;
+      const int fi = u0 * n1 + u1;
+      if (u2 > 0) a = fma(S.off[2], Lx[b - 1], a);
+      else if (__ldg(hr + fb + fi) >= 0) a = fma(S.off[2], H[fb + fi], a);
+      if (u2 < n2 - 1) a = fma(S.off[2], Lx[b + 1], a);
+      else if (__ldg(hr + fb + fs2 + fi) >= 0) a = fma(S.off[2], H[fb + fs2 + fi], a);
+    }
+    acc[u] = a;
+  }
+  epi(r0, np, v, acc);
+}
+
+// per-thread points of a tile (PER template argument of the launches)
+template <int PER>
+__device__ __forceinline__ bool tile_pt(int u, int np) {
+  return (int)threadIdx.x + u * VEC_THREADS < np;
+}
+
+template <int D, int PER>
+__global__ void k_tile_matvec(const double* __restrict__ x, Stencil S, Tiles T, double* __restrict__ y) {
+  extern __shared__ double tsm[];
+  tile_stencil<D, PER>(T, S, blockIdx.x, tsm, tsm + T.max_points, [&](int64_t i) { return x[i]; },
+                       [&](int r0, int np, const double*, const double* acc) {
+#pragma unroll
+                         for (int u = 0; u < PER; ++u)
+                           if (tile_pt<PER>(u, np)) y[r0 + threadIdx.x + u * VEC_THREADS] = acc[u];
+                       });
+}
+
+// t = g - Â R0^T y0 (k_tvec on tiles)
+template <int D, int PER>
+__global__ void k_tile_tvec(const double* __restrict__ gv, const double* __restrict__ y0,
+                            const int32_t* __restrict__ agg, Stencil S, Tiles T, double* __restrict__ t,
+                            const DevState* st) {
+  if (skip(st)) return;
+  extern __shared__ double tsm[];
+  tile_stencil<D, PER>(T, S, blockIdx.x, tsm, tsm + T.max_points, [&](int64_t i) { return __ldg(y0 + agg[i]); },
+                       [&](int r0, int np, const double*, const double* acc) {
+                         double g[PER];
+#pragma unroll
+                         for (int u = 0; u < PER; ++u)
+                           g[u] = tile_pt<PER>(u, np) ? gv[r0 + threadIdx.x + u * VEC_THREADS] : 0.0;
+#pragma unroll
+                         for (int u = 0; u < PER; ++u)
+                           if (tile_pt<PER>(u, np)) t[r0 + threadIdx.x + u * VEC_THREADS] = g[u] - acc[u];
+                       });
+}
+
+// p = z + beta p_old with z = (w - R0^T y0b) + R0^T y0, Ap, p.Ap (k_pm_w on tiles)
+template <int D, int PER>
+__global__ void k_tile_pm_w(const double* __restrict__ w, const double* __restrict__ y0,
+                            const double* __restrict__ y0b, const int32_t* __restrict__ agg,
+                            const double* __restrict__ pold, Stencil S, Tiles T, double* __restrict__ pnew,
+                            double* __restrict__ ap, double* __restrict__ part, DevState* st) {
+  if (skip(st)) return;
+  extern __shared__ double tsm[];
+  const double beta = st->beta;
+  double s = 0.0;
+  tile_stencil<D, PER>(
+      T, S, blockIdx.x, tsm, tsm + T.max_points,
+      [&](int64_t i) {
+        const int32_t a = agg[i];
+        return __dadd_rn((w[i] - __ldg(y0b + a)) + __ldg(y0 + a), __dmul_rn(beta, pold[i]));
+      },
+      [&](int r0, int np, const double* pg, const double* acc) {
+#pragma unroll
+        for (int u = 0; u < PER; ++u)
+          if (tile_pt<PER>(u, np)) {
+            const int g = r0 + threadIdx.x + u * VEC_THREADS;
+            pnew[g] = pg[u];
+            ap[g] = acc[u];
+            s = fma(pg[u], acc[u], s);
+          }
+      });
+  s = block_sum(s);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+  if (last_block(&st->ticket[1])) {
+    const double pap = reduce_partials(part, gridDim.x);
+    if (threadIdx.x == 0) {
+      st->ticket[1] = 0;
+      st->pap = pap;
+      if (!(pap > 0.0)) {
+        st->breakdown = 1;
+        st->done = 1;
+      } else {
+        st->alpha = st->rz / pap;
+      }
+    }
+  }
+}
+
+// R0 Â w per (tile, aggregate met) slot (coarse.py:84; aggregates are
+// contiguous rank ranges, so a tile's slots are in aggregate order)
+template <int D, int PER>
+__global__ void k_tile_agg_matvec(const double* __restrict__ w, const int64_t* __restrict__ agg_start,
+                                  const int32_t* __restrict__ agg, Stencil S, Tiles T, double* __restrict__ part,
+                                  const DevState* sk) {
+  if (skip(sk)) return;
+  extern __shared__ double tsm[];
+  const int tile = blockIdx.x;
+  const int r0 = T.r0[tile], np = T.r0[tile + 1] - r0;
+  const int a_first = agg[r0], nseg = agg[r0 + np - 1] - a_first + 1;
+  int64_t bnd[TILE_MAX_SEGS];  // segment q = ranks [start of a_first+q, start of a_first+q+1)
+#pragma unroll
+  for (int q = 0; q < TILE_MAX_SEGS; ++q) bnd[q] = q < nseg ? agg_start[a_first + q + 1] : INT64_MAX;
+  double loc[TILE_MAX_SEGS];
+#pragma unroll
+  for (int q = 0; q < TILE_MAX_SEGS; ++q) loc[q] = 0.0;
+  tile_stencil<D, PER>(T, S, tile, tsm, tsm + T.max_points, [&](int64_t i) { return w[i]; },
+                       [&](int r, int n, const double*, const double* acc) {
+#pragma unroll
+                         for (int u = 0; u < PER; ++u)
+                           if (tile_pt<PER>(u, n)) {
+                             const int64_t g = r + threadIdx.x + u * VEC_THREADS;
+#pragma unroll
+                             for (int q = 0; q < TILE_MAX_SEGS; ++q)
+                               if (g < bnd[q] && (q == 0 || g >= bnd[q - 1])) loc[q] += acc[u];
+                           }
+                       });
+  for (int q = 0; q < TILE_MAX_SEGS && q < nseg; ++q) {
+    const double v = block_sum(loc[q]);
+    if (threadIdx.x == 0) part[T.slot0[tile] + q] = v;
+  }
+}
+
+// c[a] = sum of aggregate a's tile slots, in tile order
+__global__ void k_slot_sums(const double* __restrict__ part, const int32_t* __restrict__ sptr, int32_t n0,
+                            double* __restrict__ c, const DevState* sk) {
+  if (skip(sk)) return;
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= n0) return;
+  double v = 0.0;
+  for (int q = sptr[a]; q < sptr[a + 1]; ++q) v += __ldcg(part + q);
+  c[a] = v;
 }
 
 // per-chunk partials of sum (Â w) -> R0 Â w  (coarse.py:84 project_transpose)
@@ -735,6 +951,29 @@ static int mode_of(int variant) {
   }
 }
 
+// stencil-tile launches (d = 2 or 3)
+#define TILE_LAUNCH(KERNEL, OP, ST, ...)                                                                  \
+  do {                                                                                                   \
+    const size_t smem_ = (size_t)(OP)->tiles.smem_doubles * 8;                                           \
+    const int per_ = ((OP)->tiles.max_points + VEC_THREADS - 1) / VEC_THREADS;                           \
+    const unsigned g_ = (unsigned)(OP)->tiles.ntiles;                                                    \
+    if ((OP)->d == 2 && per_ <= 4)                                                                        \
+      KERNEL<2, 4><<<g_, VEC_THREADS, smem_, ST>>>(__VA_ARGS__);                                         \
+    else if ((OP)->d == 2)                                                                                \
+      KERNEL<2, 16><<<g_, VEC_THREADS, smem_, ST>>>(__VA_ARGS__);                                        \
+    else if (per_ <= 2)                                                                                   \
+      KERNEL<3, 2><<<g_, VEC_THREADS, smem_, ST>>>(__VA_ARGS__);                                         \
+    else                                                                                                  \
+      KERNEL<3, 16><<<g_, VEC_THREADS, smem_, ST>>>(__VA_ARGS__);                                        \
+  } while (0)
+
+static void launch_matvec(sfcdd_op* op, const double* x, double* y, cudaStream_t st) {
+  if (op->tiled)
+    TILE_LAUNCH(k_tile_matvec, op, st, x, stencil_of(op), op->tiles, y);
+  else
+    k_matvec<<<nblocks(op->n, VEC_THREADS), VEC_THREADS, 0, st>>>(x, stencil_of(op), y);
+}
+
 // the preconditioner apply on device: h = C^{-1} g.  If `pcg`, the R0 g
 // partials are already in part_c (fused into k_update) and r.h partials are
 // produced for the PCG scalars.
@@ -758,7 +997,10 @@ static void apply_device(sfcdd_op* op, const double* g, double* h, cudaStream_t 
   }
   const double* rhs = g;
   if (v == SFCDD_VARIANT_BALANCED) {
-    k_tvec<<<nblocks(op->n, VEC_THREADS), VEC_THREADS, 0, st>>>(g, op->y0, op->agg, S, op->t, sk);
+    if (op->tiled)
+      TILE_LAUNCH(k_tile_tvec, op, st, g, op->y0, op->agg, S, op->tiles, op->t, sk);
+    else
+      k_tvec<<<nblocks(op->n, VEC_THREADS), VEC_THREADS, 0, st>>>(g, op->y0, op->agg, S, op->t, sk);
     kmark(st, "tvec");
     rhs = op->t;
   }
@@ -787,11 +1029,20 @@ static void apply_device(sfcdd_op* op, const double* g, double* h, cudaStream_t 
                                                    fused ? op->r : nullptr, op->part_a);
   kmark(st, "combine");
   if (mode == 2) {
-    k_matvec_chunk<<<op->nch, VEC_THREADS, 0, st>>>(op->w, S, C, op->part_b, sk);
-    kmark(st, "matvec_chunk");
     PcgFin fin{op->part_a, op->part_c, op->y0, op->nch, fused ? dst : nullptr};
-    k_coarse_gemv<<<cgrid, VEC_THREADS, csm, st>>>(op->ainv, op->part_b, op->agg_ptr, op->n0, op->y0b, sk,
-                                                   direct, fin);
+    if (op->tile_agg) {  // c = R0 Â w per aggregate from the tile slots
+      TILE_LAUNCH(k_tile_agg_matvec, op, st, op->w, op->d_agg_start, op->agg, S, op->tiles, op->part_t, sk);
+      k_slot_sums<<<nblocks(op->n0, VEC_THREADS), VEC_THREADS, 0, st>>>(op->part_t, op->tiles.sptr, op->n0,
+                                                                       op->cvec, sk);
+      kmark(st, "matvec_chunk");
+      k_coarse_gemv<<<cgrid, VEC_THREADS, 0, st>>>(op->ainv, op->cvec, op->agg_ptr, op->n0, op->y0b, sk, true,
+                                                   fin);
+    } else {
+      k_matvec_chunk<<<op->nch, VEC_THREADS, 0, st>>>(op->w, S, C, op->part_b, sk);
+      kmark(st, "matvec_chunk");
+      k_coarse_gemv<<<cgrid, VEC_THREADS, csm, st>>>(op->ainv, op->part_b, op->agg_ptr, op->n0, op->y0b, sk,
+                                                     direct, fin);
+    }
     kmark(st, "coarse_gemv2");
   }
   if (!fused) {
@@ -806,7 +1057,10 @@ static void apply_device(sfcdd_op* op, const double* g, double* h, cudaStream_t 
 static void pcg_iteration(sfcdd_op* op, double* x, const double* pold, double* pnew, cudaStream_t st) {
   const Stencil S = stencil_of(op);
   const Chunks C = chunks_of(op);
-  if (mode_of(op->variant) == 2)
+  if (mode_of(op->variant) == 2 && op->tiled)
+    TILE_LAUNCH(k_tile_pm_w, op, st, op->w, op->y0, op->y0b, op->agg, pold, S, op->tiles, pnew, op->ap, op->part_t,
+                op->st);
+  else if (mode_of(op->variant) == 2)
     k_pm_w<<<op->nch, VEC_THREADS, 0, st>>>(op->w, op->y0, op->y0b, op->agg, pold, S, C, pnew, op->ap, op->part_a,
                                             op->st);
   else
@@ -896,6 +1150,13 @@ extern "C" int sfcdd_op_create(const sfcdd_op_desc* desc, sfcdd_op** out) {
   k_nbr<<<nblocks(op->n, 256), 256, 0, st>>>(g, perm, rank, op->nbr);
   CUDA_CHECK(cudaGetLastError());
   CUDA_CHECK(cudaStreamSynchronize(st));
+  // stencil tiles (2-D / 3-D, single-GPU operator; SFCDD_NO_TILES=1 keeps the
+  // neighbour-table kernels)
+  std::vector<int64_t> perm_host;
+  if ((op->d == 2 || op->d == 3) && op->shard_count == 0 && !std::getenv("SFCDD_NO_TILES")) {
+    perm_host.resize(op->n);
+    CUDA_CHECK(cudaMemcpy(perm_host.data(), perm, op->n * 8, cudaMemcpyDeviceToHost));
+  }
   CUDA_CHECK(cudaFree(perm));
   CUDA_CHECK(cudaFree(rank));
   op->dev_bytes -= 2 * std::max<int64_t>(op->n * 8, 16);
@@ -931,6 +1192,63 @@ extern "C" int sfcdd_op_create(const sfcdd_op_desc* desc, sfcdd_op** out) {
   op->chunk_start = dev_upload(op.get(), cstart);
   op->chunk_agg = dev_upload(op.get(), cagg);
   op->agg_ptr = dev_upload(op.get(), aptr);
+  if (!perm_host.empty()) {
+    int lshift[MAX_GRID_DIM];
+    int lmax = 0;
+    for (int j = 0; j < op->d; ++j) lmax = std::max(lmax, op->levels[j]);
+    for (int j = 0; j < op->d; ++j) lshift[j] = lmax - op->levels[j];
+    HostTiles ht = build_tiles(op->d, g.shape, lshift, perm_host);
+    perm_host.clear();
+    perm_host.shrink_to_fit();
+    // R0 Â w slots: one per (tile, aggregate met), in rank order
+    std::vector<int32_t> slot0{0}, sptr;
+    int max_seg = 0;
+    if (coarse) {
+      sptr.assign(op->n0 + 1, 0);
+      for (int32_t t = 0; t < ht.ntiles; ++t) {
+        const int64_t a = ht.r0[t], b = ht.r0[t + 1] - 1;  // first/last rank of the tile
+        const int32_t fa = (int32_t)(std::upper_bound(op->agg_start.begin(), op->agg_start.end(), a) -
+                                     op->agg_start.begin()) - 1;
+        const int32_t la = (int32_t)(std::upper_bound(op->agg_start.begin(), op->agg_start.end(), b) -
+                                     op->agg_start.begin()) - 1;
+        max_seg = std::max(max_seg, la - fa + 1);
+        for (int32_t q = fa; q <= la; ++q) ++sptr[q + 1];
+        slot0.push_back(slot0.back() + (la - fa + 1));
+      }
+      for (int32_t q = 0; q < op->n0; ++q) sptr[q + 1] += sptr[q];
+    }
+    Tiles& T = op->tiles;
+    T.d = op->d;
+    T.ntiles = ht.ntiles;
+    T.r0 = dev_upload(op.get(), ht.r0);
+    T.dims = dev_upload(op.get(), ht.dims);
+    T.tab_off = dev_upload(op.get(), ht.tab_off);
+    T.tab = dev_upload(op.get(), ht.tab);
+    T.halo_off = dev_upload(op.get(), ht.halo_off);
+    T.halo = dev_upload(op.get(), ht.halo);
+    int32_t maxp = 0;
+    for (int32_t t = 0; t < ht.ntiles; ++t) maxp = std::max(maxp, ht.r0[t + 1] - ht.r0[t]);
+    T.max_points = maxp;
+    T.smem_doubles = maxp + ht.max_halo;
+    op->tiled = true;
+    op->tile_agg = coarse && max_seg <= TILE_MAX_SEGS;
+    if (op->tile_agg) {
+      T.slot0 = dev_upload(op.get(), slot0);
+      T.sptr = dev_upload(op.get(), sptr);
+      op->cvec = (double*)dev_alloc(op.get(), (size_t)op->n0 * 8);
+      op->d_agg_start = dev_upload(op.get(), op->agg_start);
+    }
+    op->part_t = (double*)dev_alloc(op.get(), (size_t)std::max<int64_t>(slot0.back(), ht.ntiles) * 8);
+    const int smem = T.smem_doubles * 8;
+    SFCDD_REQUIRE(smem <= 227 * 1024, SFCDD_EINTERNAL, "stencil tile exceeds shared memory");
+    if (smem > 48 * 1024) {
+      const void* ks[] = {(const void*)k_tile_matvec<2, 16>,     (const void*)k_tile_matvec<3, 16>,
+                          (const void*)k_tile_tvec<2, 16>,       (const void*)k_tile_tvec<3, 16>,
+                          (const void*)k_tile_pm_w<2, 16>,       (const void*)k_tile_pm_w<3, 16>,
+                          (const void*)k_tile_agg_matvec<2, 16>, (const void*)k_tile_agg_matvec<3, 16>};
+      for (const void* k : ks) CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    }
+  }
   *out = op.release();
   SFCDD_API_END
 }
@@ -1180,7 +1498,7 @@ extern "C" int sfcdd_op_matvec(sfcdd_op* op, const double* x_dev, double* y_dev,
   SFCDD_REQUIRE(op, SFCDD_EVALUE, "null handle");
   CUDA_CHECK(cudaSetDevice(op->device));
   cudaStream_t st = (cudaStream_t)stream;  // NULL = legacy default stream
-  k_matvec<<<nblocks(op->n, VEC_THREADS), VEC_THREADS, 0, st>>>(x_dev, stencil_of(op), y_dev);
+  launch_matvec(op, x_dev, y_dev, st);
   CUDA_CHECK(cudaGetLastError());
   SFCDD_API_END
 }
@@ -1216,7 +1534,7 @@ extern "C" int sfcdd_op_pcg_ex(sfcdd_op* op, const double* b_dev, double* x_dev,
       op->aex = (double*)dev_alloc(op, op->n * 8);
       op->part_e = (double*)dev_alloc(op, op->nch * 8);
     }
-    k_matvec<<<nblocks(op->n, VEC_THREADS), VEC_THREADS, 0, st>>>(exact_dev, S, op->aex);  // A x*
+    launch_matvec(op, exact_dev, op->aex, st);  // A x*
   }
   // the captured iteration graph reads b / x* only for the energy error
   if (op->pcg_b != (exact_dev ? b_dev : nullptr) || op->pcg_exact != exact_dev) {
@@ -1340,7 +1658,7 @@ extern "C" int sfcdd_op_profile(sfcdd_op* op, const double* g_dev, double* scrat
   // matvec
   CUDA_CHECK(cudaEventRecord(op->ev0, st));
   for (int i = 0; i < reps; ++i)
-    k_matvec<<<nblocks(op->n, VEC_THREADS), VEC_THREADS, 0, st>>>(g_dev, stencil_of(op), scratch_dev);
+    launch_matvec(op, g_dev, scratch_dev, st);
   CUDA_CHECK(cudaEventRecord(op->ev1, st));
   CUDA_CHECK(cudaEventSynchronize(op->ev1));
   CUDA_CHECK(cudaEventElapsedTime(&t, op->ev0, op->ev1));
@@ -1421,7 +1739,7 @@ extern "C" int sfcdd_op_profile(sfcdd_op* op, const double* g_dev, double* scrat
         k_tvec<<<nblocks(op->n, VEC_THREADS), VEC_THREADS, 0, st>>>(op->r, op->y0, op->agg, S, op->t, nullptr);
       });
       iso("matvec_chunk", [&] { k_matvec_chunk<<<op->nch, VEC_THREADS, 0, st>>>(op->w, S, C, op->part_b, nullptr); });
-      iso("matvec", [&] { k_matvec<<<nblocks(op->n, VEC_THREADS), VEC_THREADS, 0, st>>>(op->w, S, op->t); });
+      iso("matvec", [&] { launch_matvec(op, op->w, op->t, st); });
       iso("chunk_sum", [&] { k_chunk_sum<<<op->nch, VEC_THREADS, 0, st>>>(op->w, C, op->part_c); });
       iso("copy", [&] { CUDA_CHECK(cudaMemcpyAsync(op->t, op->w, op->n * 8, cudaMemcpyDeviceToDevice, st)); });
     }
@@ -1527,7 +1845,10 @@ extern "C" void sfcdd_op_destroy(sfcdd_op* op) {
                   op->d_ov_len, op->d_xy_off, op->d_dj_start, op->cand_ptr, op->cand, op->ccand_ptr, op->ccand,
                   op->d_wgt, op->d_count,
                   op->d_fault, op->st, op->hist, op->t, op->w, op->y0, op->y0b, op->part_a, op->part_b,
-                  op->part_c, op->r, op->z, op->p0, op->p1, op->ap, op->aex, op->part_e, op->ehist};
+                  op->part_c, op->r, op->z, op->p0, op->p1, op->ap, op->aex, op->part_e, op->ehist,
+                  (void*)op->tiles.r0, (void*)op->tiles.dims, (void*)op->tiles.tab_off, (void*)op->tiles.tab,
+                  (void*)op->tiles.halo_off, (void*)op->tiles.halo, (void*)op->tiles.slot0, (void*)op->tiles.sptr,
+                  op->part_t, op->cvec, op->d_agg_start};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   op->dag.reset();

@@ -35,6 +35,23 @@ struct DevState {
   int32_t energy_mode;   // the energy error decides convergence (else ||r||)
 };
 
+// index-free stencil tiles (tiles.h), device copy
+struct Tiles {
+  int d;
+  int32_t ntiles;
+  const int32_t* r0;        // ntiles + 1
+  const int32_t* dims;      // 3 per tile
+  const int32_t* tab_off;   // ntiles
+  const uint16_t* tab;
+  const int32_t* halo_off;  // ntiles + 1
+  const int32_t* halo;
+  const int32_t* slot0;     // ntiles + 1: first R0 Â w partial slot of each tile (one per aggregate met)
+  const int32_t* sptr;      // n0 + 1: slots of each aggregate (contiguous, tile order)
+  int32_t max_points;       // points of the largest tile (box area in shared memory)
+  int32_t smem_doubles;     // box + halo doubles of the largest tile
+};
+constexpr int TILE_MAX_SEGS = 4;  // aggregates one tile may meet for the tiled R0 Â w
+
 struct Chunks {
   const int64_t* start;       // nch + 1
   const int32_t* agg;         // aggregate of each chunk (or -1)
@@ -72,6 +89,12 @@ struct sfcdd_op {
   int64_t* d_dj_start = nullptr;  // p + 1
   int32_t* cand_ptr = nullptr;
   int32_t* cand = nullptr;
+  bool tiled = false;             // stencils run on SFC tiles (2-D / 3-D, single GPU)
+  bool tile_agg = false;          // ... including R0 Â w (every tile meets <= TILE_MAX_SEGS aggregates)
+  sfcdd::Tiles tiles{};
+  double* part_t = nullptr;       // per-tile partials (p.Ap; R0 Â w slots)
+  double* cvec = nullptr;         // n0: R0 Â w summed per aggregate
+  int64_t* d_agg_start = nullptr; // n0 + 1 (tiled R0 Â w)
   int32_t* ccand_ptr = nullptr;  // per reduction chunk (nch + 1)
   int32_t* ccand = nullptr;
   double* d_wgt = nullptr;     // per subdomain weight (omega / 1)

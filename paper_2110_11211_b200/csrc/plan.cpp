@@ -404,7 +404,9 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
       };
       int32_t ncol_tasks = 0;
       for (int32_t k0 = 0; k0 < s; k0 += col_width(k0, false)) ++ncol_tasks;
-      const bool use_xb = split_ok && m > 0 && ncol_tasks >= opt.xb_min_tasks;
+      // XB also when a column block with its inline row list cannot fit a blob
+      const bool inline_fits = blob_size(CL_WORDS + 1 + m, (int64_t)(s + m)) <= opt.blob_max;
+      const bool use_xb = m > 0 && ((split_ok && ncol_tasks >= opt.xb_min_tasks) || !inline_fits);
       if (use_xb) {  // -x_B
         gr.xb_off = P.upd_doubles;
         P.upd_doubles += m;

@@ -255,3 +255,35 @@ def test_factorization_rejects_non_spd(sfcdd):
 
     with pytest.raises(sfcdd.FactorizationError):
         sfcdd.Factorization(sp.csr_matrix(np.array([[1.0, 2.0], [2.0, 1.0]])))
+
+
+@pytest.mark.parametrize("levels", [(7, 7), (6, 7), (10, 10), (4, 4, 4), (5, 6, 5), (7, 7, 7)])
+def test_tiled_stencil_bitwise_equals_neighbour_table(sfcdd, levels, monkeypatch):
+    """The index-free SFC-tile stencil (csrc/tiles.cpp) against the
+    neighbour-table stencil on the same vector: bitwise equal."""
+    n = sfcdd.num_dofs(levels)
+    part = sfcdd.build_partition(n, max(4, n // 8000), 0.5)  # blocks a COL blob can hold
+
+    def op_for(env):
+        if env:
+            monkeypatch.setenv("SFCDD_NO_TILES", "1")
+        else:
+            monkeypatch.delenv("SFCDD_NO_TILES", raising=False)
+        A = sfcdd.assemble_laplacian(levels)
+        Ah, _, _ = sfcdd.symmetrize_diag(A, np.zeros(n))
+        return sfcdd.schwarz.SchwarzOperator(Ah, part, sfcdd.build_coarse(part, Ah, 1),
+                                             sfcdd.SchwarzConfig("balanced", "omega", 0.5, 1))
+
+    x = torch.from_numpy(np.random.default_rng(9).standard_normal(n)).cuda()
+    outs = []
+    for env in (True, False):
+        op = op_for(env)
+        y = torch.empty_like(x)
+        from paper_2110_11211_b200 import _lib
+
+        _lib.check(_lib.lib().sfcdd_op_matvec(op.handle, x.data_ptr(), y.data_ptr(), _lib.stream_ptr()))
+        outs.append(y.cpu().numpy())
+        a = op.apply(x.cpu().numpy())
+        outs.append(a)
+    np.testing.assert_array_equal(outs[0], outs[2])
+    np.testing.assert_allclose(outs[1], outs[3], rtol=1e-12, atol=1e-14 * np.abs(outs[1]).max())
