@@ -290,12 +290,24 @@ def make_dense_operator(ref):
     np.savez_compressed(OUT / "dense_operators.npz", **out)
 
 
+# extra solve fixtures: name -> (levels, p, gamma, q, full_solution)
+SOLVES = {
+    # aggregates of 16320 points = 8 reduction chunks each (the R0 r partials
+    # are per chunk, not per aggregate: pins the fused PCG epilogue's sums)
+    "multichunk": ((9, 9), 8, 0.5, 2, False),
+}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
+    ap.add_argument("--only", default=None, help="regenerate one solve fixture (name of SOLVES)")
     args = ap.parse_args()
     OUT.mkdir(parents=True, exist_ok=True)
     ref = load_reference()
+    if args.only:
+        make_solve(ref, args.only, *SOLVES[args.only])
+        return
     make_sfc(ref)
     make_perms(ref, args.big)
     make_partitions(ref)
@@ -307,6 +319,7 @@ def main():
     make_solve(ref, "aniso", (6, 7), 12, 0.5, 3, True)
     make_solve(ref, "fault_88", (8, 8), 256, 0.5, 16, False, fault_iter=5)
     make_solve(ref, "nofault_88", (8, 8), 256, 0.5, 16, False)
+    make_solve(ref, "multichunk", *SOLVES["multichunk"])
     if args.big:
         make_solve(ref, "c2", (10, 10), 64, 0.5, 16, False)
         make_solve(ref, "c3", (7, 7, 7), 512, 0.5, 8, False)

@@ -220,6 +220,20 @@ def test_pcg_c3_matches_reference(sfcdd, golden):
     assert np.linalg.norm(rep.solution[idx] - ref) <= 1e-10 * np.linalg.norm(ref)
 
 
+def test_pcg_multichunk_aggregates_match_reference(sfcdd, golden):
+    """Aggregates spanning several reduction chunks: the fused PCG epilogue
+    sums the per-chunk R0 r partials per aggregate (op.cu pcg_fin_epilogue)."""
+    g = golden.npz("solve_multichunk.npz")
+    rep, _ = _pcg(sfcdd, (9, 9), 8, 0.5, 2)
+    assert abs(rep.iterations - int(g["iterations"])) <= 1
+    h = g["residual_history"]
+    k = min(len(h), len(rep.residual_history))
+    assert (np.abs(np.asarray(rep.residual_history[:k]) - h[:k]) / h[:k]).max() <= 1e-10
+    idx = g["solution_sample_idx"]
+    ref = g["solution_sample"]
+    assert np.linalg.norm(rep.solution[idx] - ref) <= 1e-10 * np.linalg.norm(ref)
+
+
 def test_pcg_fault_mode_matches_reference(sfcdd, golden):
     g = golden.npz("solve_fault_88.npz")
     dead = np.random.default_rng(42).choice(256, size=int(round(0.1 * 256)), replace=False)
