@@ -380,10 +380,6 @@ __global__ void k_combine(CombineArgs C, double* __restrict__ w, const DevState*
   w[g] = acc;
 }
 
-// The same combination, one CTA per reduction chunk: the chunk's candidate
-// subdomains (every overlapped range meeting the chunk, ascending index =
-// the reference's accumulation order) are staged in shared memory once, so
-// a point costs one range test and one load per covering subdomain.
 constexpr int COMBINE_MAXC = 32;
 
 // the points [g0, g1) of one reduction chunk: w[g] = sum over the chunk's
@@ -405,60 +401,6 @@ __device__ __forceinline__ double combine_points(const CombineArgs& C, const int
     }
     w[g] = acc;
     if (rdot) rw = fma(rdot[g], acc, rw);
-  }
-  return rw;
-}
-
-// The same combination, one CTA per reduction chunk: the chunk's candidate
-// subdomains (every overlapped range meeting the chunk, ascending index =
-// the reference's accumulation order) are staged in shared memory once, so
-// a point costs one range test and one load per covering subdomain.
-constexpr int COMBINE_MAXC = 32;
-
-// the points [g0, g1) of one reduction chunk: w[g] = sum over the chunk's
-// candidate subdomains c (staged in shared memory, ascending) covering g of
-// wt_c * xy_c[g - start_c], in candidate order; PT points per thread with the
-// loads of their first CK candidates (and of r) in flight together.
-// Returns this thread's share of r.w (rdot != null).
-__device__ __forceinline__ double combine_points(const CombineArgs& C, const int64_t* s_start, const int64_t* s_len,
-                                                 const int64_t* s_off, const double* s_w, int nc, int64_t g0,
-                                                 int64_t g1, double* __restrict__ w, const double* rdot) {
-  constexpr int CK = 3;
-  double rw = 0.0;
-  for (int64_t b = g0 + threadIdx.x; b < g1; b += PT * VEC_THREADS) {
-    double v[PT][CK], rv[PT];
-#pragma unroll
-    for (int u = 0; u < PT; ++u) {
-      const int64_t g = b + (int64_t)u * VEC_THREADS;
-      const bool ok = g < g1;
-#pragma unroll
-      for (int c = 0; c < CK; ++c) {
-        int64_t off = g - s_start[c];
-        if (off < 0) off += C.n;
-        v[u][c] = (ok && c < nc && off < s_len[c]) ? __ldcg(C.xy + s_off[c] + off) : 0.0;
-      }
-      rv[u] = (ok && rdot) ? rdot[g] : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < PT; ++u) {
-      const int64_t g = b + (int64_t)u * VEC_THREADS;
-      if (g >= g1) continue;
-      const double dw = C.count ? 1.0 / (double)C.count[g] : 0.0;
-      double acc = 0.0;
-#pragma unroll
-      for (int c = 0; c < CK; ++c) {
-        int64_t off = g - s_start[c];
-        if (off < 0) off += C.n;
-        if (c < nc && off < s_len[c]) acc = __dadd_rn(acc, __dmul_rn(C.count ? dw : s_w[c], v[u][c]));
-      }
-      for (int c = CK; c < nc; ++c) {
-        int64_t off = g - s_start[c];
-        if (off < 0) off += C.n;
-        if (off < s_len[c]) acc = __dadd_rn(acc, __dmul_rn(C.count ? dw : s_w[c], __ldcg(C.xy + s_off[c] + off)));
-      }
-      w[g] = acc;
-      rw = fma(rv[u], acc, rw);
-    }
   }
   return rw;
 }
