@@ -290,6 +290,68 @@ def make_dense_operator(ref):
     np.savez_compressed(OUT / "dense_operators.npz", **out)
 
 
+# harness / combination-technique runs of the reference
+HARNESS_SPECS = {
+    "weak_d2": dict(kind="weak", dim=2, s=6, p_values=(1, 2, 4, 8, 16, 32, 64)),
+    "gamma_d1": dict(kind="gamma_sweep", dim=1, s=6, gamma_values=(0.25, 0.5, 1.0, 2.0), p_values=(2, 4, 8, 16)),
+    "dim_sweep": dict(kind="dim_sweep", dims=(1, 2, 3), s=6, p_values=(4, 8, 16)),
+    "strong_d1": dict(kind="strong", dim=1, level=10, p_values=(2, 4, 8, 16, 32)),
+    "weak_d2_richardson": dict(kind="weak", dim=2, s=5, p_values=(4, 16), method="richardson"),
+    "weak_d2_fcg_deflated": dict(kind="weak", dim=2, s=5, p_values=(4, 16), method="fcg", variant="deflated"),
+    "weak_d3_additive": dict(kind="weak", dim=3, s=6, p_values=(8, 64), variant="additive_two_level"),
+    "weak_d2_s10": dict(kind="weak", dim=2, s=10, p_values=(4, 16, 64, 256)),
+    "weak_d3_s9": dict(kind="weak", dim=3, s=9, p_values=(8, 64)),
+}
+COMBINE_SPECS = {
+    "combine_d2_l6": dict(kind="combine", dim=2, level=6, p_hat=2, sample_count=500),
+    "combine_d3_l4": dict(kind="combine", dim=3, level=4, p_hat=1, sample_count=500),
+    "combine_d2_l11": dict(kind="combine", dim=2, level=11, p_hat=8, sample_count=2000),
+}
+
+
+def make_harness(ref):
+    """Rows (CSV text without timings) of small sweeps and combination runs."""
+    import io
+    import tempfile
+
+    out = {}
+    for name, kw in HARNESS_SPECS.items():
+        t0 = time.time()
+        spec = ref.harness.ExperimentSpec(**kw)
+        runner = {"weak": ref.harness.run_weak_scaling, "strong": ref.harness.run_strong_scaling,
+                  "gamma_sweep": ref.harness.run_gamma_sweep, "dim_sweep": ref.harness.run_dim_sweep}[spec.kind]
+        rows = runner(spec)
+        with tempfile.TemporaryDirectory() as td:
+            ref.harness.write_rows_csv(Path(td) / "rows.csv", rows)
+            csv_text = (Path(td) / "rows.csv").read_text(encoding="utf-8")
+        out[name] = {"spec": {k: list(v) if isinstance(v, tuple) else v for k, v in kw.items()}, "csv": csv_text}
+        print(f"harness {name}: {len(rows)} rows, {time.time() - t0:.1f}s", flush=True)
+    for name, kw in COMBINE_SPECS.items():
+        t0 = time.time()
+        spec = ref.harness.ExperimentSpec(**kw)
+        rows, summary = ref.harness.run_combine_experiment(spec)
+        with tempfile.TemporaryDirectory() as td:
+            ref.harness.write_rows_csv(Path(td) / "rows.csv", rows)
+            csv_text = (Path(td) / "rows.csv").read_text(encoding="utf-8")
+        plan = ref.combine.enumerate_plan(spec.dim, spec.level, spec.p_hat)
+        res = ref.combine.run_combination(plan, seed=spec.seed)
+        pts = np.random.default_rng(11).uniform(0.0, 1.0, size=(64, spec.dim))
+        out[name] = {"spec": kw, "csv": csv_text, "summary": summary,
+                     "points": pts.tolist(), "values": res.evaluator(pts).tolist()}
+        print(f"combine {name}: {len(rows)} rows, err {summary['max_error']:.3e}, {time.time() - t0:.1f}s", flush=True)
+    mp = {}
+    for d in (1, 2, 3):
+        prob = ref.grid.manufactured_poisson((3,) * d)
+        pts = np.random.default_rng(20 + d).uniform(0.01, 0.99, size=(20, d))
+        mp[str(d)] = {"points": pts.tolist(), "rhs": prob.rhs(pts).tolist(),
+                      "exact": prob.exact_solution(pts).tolist()}
+    out["manufactured"] = mp
+    x0 = ref.krylov.initial_iterate(225, 42, ref.grid.symmetrize_diag(
+        ref.grid.assemble_laplacian((4, 4)), np.zeros(225))[0])
+    out["initial_iterate_4x4"] = x0.tolist()
+    (OUT / "harness.json").write_text(json.dumps(out, indent=1) + "\n")
+
+
 # extra solve fixtures: name -> (levels, p, gamma, q, full_solution)
 SOLVES = {
     # aggregates of 16320 points = 8 reduction chunks each (the R0 r partials
@@ -305,6 +367,9 @@ def main():
     args = ap.parse_args()
     OUT.mkdir(parents=True, exist_ok=True)
     ref = load_reference()
+    if args.only == "harness":
+        make_harness(ref)
+        return
     if args.only:
         make_solve(ref, args.only, *SOLVES[args.only])
         return
@@ -320,6 +385,7 @@ def main():
     make_solve(ref, "fault_88", (8, 8), 256, 0.5, 16, False, fault_iter=5)
     make_solve(ref, "nofault_88", (8, 8), 256, 0.5, 16, False)
     make_solve(ref, "multichunk", *SOLVES["multichunk"])
+    make_harness(ref)
     if args.big:
         make_solve(ref, "c2", (10, 10), 64, 0.5, 16, False)
         make_solve(ref, "c3", (7, 7, 7), 512, 0.5, 8, False)

@@ -321,6 +321,27 @@ __global__ void k_coarse_gemv(const double* __restrict__ ainv, const double* __r
   if (fin.st && last_block(&fin.st->ticket[5])) pcg_fin_epilogue(fin, n0, y);
 }
 
+// c[a] = sum of the chunk partials of aggregate a (sparse coarse path)
+__global__ void k_seg_sum(const double* __restrict__ part, const int32_t* __restrict__ ptr, int32_t n0,
+                          double* __restrict__ c, const DevState* st) {
+  if (skip(st)) return;
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= n0) return;
+  double s = 0.0;
+  for (int ch = ptr[a]; ch < ptr[a + 1]; ++ch) s += __ldcg(part + ch);
+  c[a] = s;
+}
+
+// y = the coarse DAG solution (sparse coarse path), then the fused PCG
+// epilogue in the last block (as k_coarse_gemv)
+__global__ void k_coarse_out(const double* __restrict__ xy, int32_t n0, double* __restrict__ y, const DevState* st,
+                             PcgFin fin) {
+  if (skip(st)) return;
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a < n0) y[a] = __ldcg(xy + a);
+  if (fin.st && last_block(&fin.st->ticket[5])) pcg_fin_epilogue(fin, n0, y);
+}
+
 // t = g - Â R0^T y0   (schwarz.py:116: g - A @ F(g))
 __global__ void k_tvec(const double* __restrict__ gv, const double* __restrict__ y0,
                        const int32_t* __restrict__ agg, Stencil S, double* __restrict__ t,
@@ -1054,6 +1075,27 @@ static CombineArgs combine_args(sfcdd_op* op) {
   return ca;
 }
 
+// y = A0^{-1} c, c[a] = sum of part[ptr[a]] .. part[ptr[a+1]-1] (ptr ignored
+// when `direct`: c = part).  Dense redundant inverse (GEMV) up to
+// COARSE_DENSE_MAX coarse DOFs, else the sparse supernodal factor of A0
+// through its own DAG solve; optional fused PCG epilogue (fin).
+static void coarse_solve(sfcdd_op* op, const double* part, const int32_t* ptr, bool direct, double* y,
+                         const DevState* sk, const PcgFin& fin, cudaStream_t st) {
+  if (op->ainv) {
+    const size_t csm = direct ? 0 : (size_t)op->n0 * sizeof(double);
+    k_coarse_gemv<<<nblocks(op->n0, GEMV_ROWS), VEC_THREADS, csm, st>>>(op->ainv, part, ptr, op->n0, y, sk, direct,
+                                                                       fin);
+    return;
+  }
+  const double* c = part;
+  if (!direct) {
+    k_seg_sum<<<nblocks(op->n0, VEC_THREADS), VEC_THREADS, 0, st>>>(part, ptr, op->n0, op->cvec0, sk);
+    c = op->cvec0;
+  }
+  op->coarse_dag->solve(c, st, sk ? &op->st->done : nullptr);
+  k_coarse_out<<<nblocks(op->n0, VEC_THREADS), VEC_THREADS, 0, st>>>(op->coarse_dag->xy(), op->n0, y, sk, fin);
+}
+
 // the preconditioner apply on device: h = C^{-1} g.  If `pcg`, the R0 g
 // partials are already in part_c (fused into k_update) and r.h partials are
 // produced for the PCG scalars.
@@ -1066,13 +1108,10 @@ static void apply_device(sfcdd_op* op, const double* g, double* h, cudaStream_t 
   const int v = op->variant;
   const bool coarse = v != SFCDD_VARIANT_ONE_LEVEL;
   const bool direct = op->nch == op->n0;  // one chunk per aggregate: c = partials
-  const size_t csm = direct ? 0 : (size_t)op->n0 * sizeof(double);
-  const unsigned cgrid = nblocks(op->n0, GEMV_ROWS);
   if (coarse) {
     if (!partials_ready) k_chunk_sum<<<op->nch, VEC_THREADS, 0, st>>>(g, C, op->part_c);
     if (!partials_ready) kmark(st, "chunk_sum");
-    k_coarse_gemv<<<cgrid, VEC_THREADS, csm, st>>>(op->ainv, op->part_c, op->agg_ptr, op->n0, op->y0, sk,
-                                                   direct, PcgFin{});
+    coarse_solve(op, op->part_c, op->agg_ptr, direct, op->y0, sk, PcgFin{}, st);
     kmark(st, "coarse_gemv");
   }
   const double* rhs = g;
@@ -1101,13 +1140,11 @@ static void apply_device(sfcdd_op* op, const double* g, double* h, cudaStream_t 
       k_slot_sums<<<nblocks(op->n0, VEC_THREADS), VEC_THREADS, 0, st>>>(op->part_t, op->tiles.sptr, op->n0,
                                                                        op->cvec, sk);
       kmark(st, "matvec_chunk");
-      k_coarse_gemv<<<cgrid, VEC_THREADS, 0, st>>>(op->ainv, op->cvec, op->agg_ptr, op->n0, op->y0b, sk, true,
-                                                   fin);
+      coarse_solve(op, op->cvec, op->agg_ptr, true, op->y0b, sk, fin, st);
     } else {
       k_matvec_chunk<<<op->nch, VEC_THREADS, 0, st>>>(op->w, S, C, op->part_b, sk);
       kmark(st, "matvec_chunk");
-      k_coarse_gemv<<<cgrid, VEC_THREADS, csm, st>>>(op->ainv, op->part_b, op->agg_ptr, op->n0, op->y0b, sk,
-                                                     direct, fin);
+      coarse_solve(op, op->part_b, op->agg_ptr, direct, op->y0b, sk, fin, st);
     }
     kmark(st, "coarse_gemv2");
   }
@@ -1258,14 +1295,23 @@ extern "C" int sfcdd_op_create(const sfcdd_op_desc* desc, sfcdd_op** out) {
   op->chunk_start = dev_upload(op.get(), cstart);
   op->chunk_agg = dev_upload(op.get(), cagg);
   op->agg_ptr = dev_upload(op.get(), aptr);
+  HostTiles ht;
   if (!perm_host.empty()) {
     int lshift[MAX_GRID_DIM];
     int lmax = 0;
     for (int j = 0; j < op->d; ++j) lmax = std::max(lmax, op->levels[j]);
     for (int j = 0; j < op->d; ++j) lshift[j] = lmax - op->levels[j];
-    HostTiles ht = build_tiles(op->d, g.shape, lshift, perm_host);
+    try {
+      ht = build_tiles(op->d, g.shape, lshift, perm_host);
+    } catch (const Error&) {
+      // blocks the packed tile tables cannot describe (e.g. grids of extreme
+      // anisotropy such as levels (1, 11)): keep the neighbour-table stencil
+      ht.ntiles = 0;
+    }
     perm_host.clear();
     perm_host.shrink_to_fit();
+  }
+  if (ht.ntiles > 0) {
     // R0 Â w slots: one per (tile, aggregate met), in rank order
     std::vector<int32_t> slot0{0}, sptr;
     int max_seg = 0;
@@ -1473,7 +1519,6 @@ extern "C" int sfcdd_op_setup(sfcdd_op* op, void* stream) {
   (void)fault;
   // coarse problem A0 = R0 Â R0^T, symmetrized (linalg.py:83-91), dense inverse
   if (op->n0 > 0) {
-    SFCDD_REQUIRE(op->n0 <= 8192, SFCDD_EVALUE, "coarse problems above 8192 dofs are not supported yet");
     const int32_t n0 = op->n0;
     std::vector<int32_t> aggh(n);
     for (int32_t a = 0; a < n0; ++a)
@@ -1497,34 +1542,46 @@ extern "C" int sfcdd_op_setup(sfcdd_op* op, void* stream) {
         sym[a][e.first] += 0.5 * e.second;
         sym[e.first][a] += 0.5 * e.second;
       }
-    CsrMatrix A0;
+    CsrMatrix& A0 = op->a0;
     A0.n = n0;
     A0.indptr.assign(n0 + 1, 0);
-    op->a0_dense.assign((size_t)n0 * n0, 0.0);
     for (int32_t a = 0; a < n0; ++a) {
       for (auto& e : sym[a]) {
         A0.indices.push_back(e.first);
         A0.data.push_back(e.second);
-        op->a0_dense[(size_t)a * n0 + e.first] = e.second;
       }
       A0.indptr[a + 1] = A0.indices.size();
     }
     op->stats.coarse_nnz = A0.indices.size();
     HostFactor F0 = factorize_host(A0, fo);
-    std::vector<double> ainv((size_t)n0 * n0);
-    parallel_for(n0, op->threads, [&](int64_t j) {
-      std::vector<double> e(n0, 0.0), col(n0);
-      e[j] = 1.0;
-      host_block_solve(F0, e.data(), col.data());
-      for (int32_t i = 0; i < n0; ++i) ainv[(size_t)j * n0 + i] = col[i];  // symmetric: row j
-    });
-    op->ainv = dev_upload(op, ainv);
+    int dense_max = COARSE_DENSE_MAX;  // SFCDD_COARSE_DENSE_MAX lowers it (tests of the sparse path)
+    if (const char* e = std::getenv("SFCDD_COARSE_DENSE_MAX")) dense_max = std::min(dense_max, std::atoi(e));
+    if (n0 <= dense_max) {
+      // Bank-Holst redundant copy as a dense inverse: one GEMV per coarse solve
+      std::vector<double> ainv((size_t)n0 * n0);
+      parallel_for(n0, op->threads, [&](int64_t j) {
+        std::vector<double> e(n0, 0.0), col(n0);
+        e[j] = 1.0;
+        host_block_solve(F0, e.data(), col.data());
+        for (int32_t i = 0; i < n0; ++i) ainv[(size_t)j * n0 + i] = col[i];  // symmetric: row j
+      });
+      op->ainv = dev_upload(op, ainv);
+    } else {
+      // large coarse problems: supernodal factor of A0 solved by the DAG kernel
+      PlanOptions pc;
+      CUDA_CHECK(cudaDeviceGetAttribute(&pc.sms, cudaDevAttrMultiProcessorCount, op->device));
+      DevicePlan cplan = build_plan({&F0}, {0}, {(int64_t)n0}, pc);
+      op->coarse_dag.reset(new DagSolver(cplan, op->device));
+      op->dev_bytes += op->coarse_dag->device_bytes();
+      op->cvec0 = (double*)dev_alloc(op, (size_t)n0 * 8);
+    }
     op->y0 = (double*)dev_alloc(op, n0 * 8);
     op->y0b = (double*)dev_alloc(op, n0 * 8);
     CUDA_CHECK(cudaMemset(op->y0, 0, n0 * 8));
     CUDA_CHECK(cudaMemset(op->y0b, 0, n0 * 8));
-    if ((size_t)n0 * 8 > 48 * 1024)  // per-function attribute: always the maximum (n0 <= 8192)
-      CUDA_CHECK(cudaFuncSetAttribute(k_coarse_gemv, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8));
+    if (op->ainv && (size_t)n0 * 8 > 48 * 1024)  // per-function attribute: always the maximum
+      CUDA_CHECK(cudaFuncSetAttribute(k_coarse_gemv, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      COARSE_DENSE_MAX * 8));
   }
   // work vectors
   op->t = (double*)dev_alloc(op, n * 8);
@@ -1786,8 +1843,6 @@ extern "C" int sfcdd_op_profile(sfcdd_op* op, const double* g_dev, double* scrat
       const Stencil S = stencil_of(op);
       const Chunks C = chunks_of(op);
       const bool direct = op->nch == op->n0;
-      const size_t csm = direct ? 0 : (size_t)op->n0 * sizeof(double);
-      const unsigned cgrid = nblocks(op->n0, GEMV_ROWS);
       auto iso = [&](const char* name, auto fn) {
         fn();
         CUDA_CHECK(cudaEventRecord(op->ev0, st));
@@ -1798,10 +1853,7 @@ extern "C" int sfcdd_op_profile(sfcdd_op* op, const double* g_dev, double* scrat
         CUDA_CHECK(cudaEventElapsedTime(&dt, op->ev0, op->ev1));
         std::fprintf(stderr, "[isolated] %-14s %8.1f us\n", name, 1e3 * dt / 20);
       };
-      iso("gemv", [&] {
-        k_coarse_gemv<<<cgrid, VEC_THREADS, csm, st>>>(op->ainv, op->part_c, op->agg_ptr, op->n0, op->y0, nullptr,
-                                                       direct, PcgFin{});
-      });
+      iso("coarse_solve", [&] { coarse_solve(op, op->part_c, op->agg_ptr, direct, op->y0, nullptr, PcgFin{}, st); });
       iso("tvec", [&] {
         k_tvec<<<nblocks(op->n, VEC_THREADS), VEC_THREADS, 0, st>>>(op->r, op->y0, op->agg, S, op->t, nullptr);
       });
@@ -1899,8 +1951,11 @@ extern "C" int sfcdd_op_stencil(sfcdd_op* op, double* diag, double* off, double*
 extern "C" int sfcdd_op_coarse_dense(sfcdd_op* op, double* a0_host) {
   SFCDD_API_BEGIN
   SFCDD_REQUIRE(op && op->ready, SFCDD_EVALUE, "operator not set up");
-  SFCDD_REQUIRE(!op->a0_dense.empty(), SFCDD_EVALUE, "no coarse space");
-  std::memcpy(a0_host, op->a0_dense.data(), op->a0_dense.size() * 8);
+  SFCDD_REQUIRE(op->a0.n > 0, SFCDD_EVALUE, "no coarse space");
+  const int64_t n0 = op->a0.n;
+  std::fill(a0_host, a0_host + n0 * n0, 0.0);
+  for (int64_t a = 0; a < n0; ++a)
+    for (int64_t e = op->a0.indptr[a]; e < op->a0.indptr[a + 1]; ++e) a0_host[a * n0 + op->a0.indices[e]] = op->a0.data[e];
   SFCDD_API_END
 }
 
@@ -2212,9 +2267,15 @@ extern "C" int sfcdd_shard_update(sfcdd_op* op, double* x, double* r, const doub
 extern "C" int sfcdd_shard_coarse(sfcdd_op* op, const double* c, double* y, void* stream) {
   SFCDD_API_BEGIN
   cudaStream_t st = (cudaStream_t)stream;
+  if (!op->ainv) {  // sparse coarse factor
+    op->coarse_dag->solve(c, st);
+    CUDA_CHECK(cudaMemcpyAsync(y, op->coarse_dag->xy(), (size_t)op->n0 * 8, cudaMemcpyDeviceToDevice, st));
+    CUDA_CHECK(cudaGetLastError());
+    return SFCDD_OK;
+  }
   const size_t smem = (size_t)op->n0 * 8;
   if (smem > 48 * 1024)
-    CUDA_CHECK(cudaFuncSetAttribute(k_gemv_c, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8));
+    CUDA_CHECK(cudaFuncSetAttribute(k_gemv_c, cudaFuncAttributeMaxDynamicSharedMemorySize, COARSE_DENSE_MAX * 8));
   k_gemv_c<<<nblocks(op->n0, VEC_THREADS / 32), VEC_THREADS, smem, st>>>(op->ainv, c, op->n0, y);
   CUDA_CHECK(cudaGetLastError());
   SFCDD_API_END

@@ -13,7 +13,8 @@
 namespace sfcdd {
 
 constexpr int VEC_THREADS = 256;
-constexpr int CHUNK = 2048;  // points per reduction chunk (never crosses an aggregate)
+constexpr int CHUNK = 2048;
+constexpr int COARSE_DENSE_MAX = 8192;  // coarse DOFs up to which A0^{-1} is held dense (GEMV solve)  // points per reduction chunk (never crosses an aggregate)
 
 struct Stencil {
   int d;
@@ -110,7 +111,9 @@ struct sfcdd_op {
   const double* pcg_b = nullptr;                                // b / x* the captured graph reads
   const double* pcg_exact = nullptr;
   std::unique_ptr<sfcdd::DagSolver> dag;
-  std::vector<double> a0_dense;  // host copy (diagnostics)
+  sfcdd::CsrMatrix a0;           // host copy of A0 (diagnostics)
+  std::unique_ptr<sfcdd::DagSolver> coarse_dag;  // sparse A0 factor (n0 > COARSE_DENSE_MAX)
+  double* cvec0 = nullptr;       // n0: coarse right-hand side of the sparse path
   sfcdd_stats stats{};
   int64_t dev_bytes = 0;
   cudaStream_t own_stream = nullptr;

@@ -10,13 +10,25 @@ diagnostics and needs scipy.
 from __future__ import annotations
 
 import ctypes
+from dataclasses import dataclass
 from functools import lru_cache
+from typing import Callable
 
 import numpy as np
 
 from . import _lib
 
 MAX_DOFS = 2**62
+
+
+@dataclass(frozen=True)
+class Problem:
+    """Right-hand side and optional exact solution on a grid (grid.py:26-36):
+    vectorized callables mapping (m, d) points of the open unit cube to (m,)."""
+
+    levels: tuple[int, ...]
+    rhs: Callable[[np.ndarray], np.ndarray]
+    exact_solution: Callable[[np.ndarray], np.ndarray] | None = None
 
 
 def as_levels(levels) -> tuple[int, ...]:
@@ -241,3 +253,39 @@ def symmetrize_diag(A, b):
     A_hat = sp.csr_matrix(T @ A @ T)
     A_hat.sort_indices()
     return A_hat, t * np.asarray(b, dtype=np.float64), t
+
+
+def manufactured_poisson(levels) -> Problem:
+    """Poisson problem with solution u = |x|_2 prod_i sin(pi x_i) (grid.py:133-161).
+
+    u vanishes on the cube boundary (homogeneous Dirichlet data).  With
+    g = prod_i sin(pi x_i), r = |x|_2, c_i = cos(pi x_i) and G_i the product
+    of the sines without factor i:
+        -Lap u = -( g (d - 1) / r + 2 pi sum_i (x_i / r) c_i G_i - d pi^2 u ).
+    Host numpy (setup data, not the solver's hot path)."""
+    levels = as_levels(levels)
+    d = len(levels)
+
+    def exact(points: np.ndarray) -> np.ndarray:
+        x = np.atleast_2d(np.asarray(points, dtype=np.float64))
+        return np.linalg.norm(x, axis=1) * np.prod(np.sin(np.pi * x), axis=1)
+
+    def rhs(points: np.ndarray) -> np.ndarray:
+        x = np.atleast_2d(np.asarray(points, dtype=np.float64))
+        sn = np.sin(np.pi * x)
+        cs = np.cos(np.pi * x)
+        g = np.prod(sn, axis=1)
+        r = np.linalg.norm(x, axis=1)
+        u = r * g
+        mixed = np.zeros_like(r)
+        for i in range(d):
+            rest = np.prod(np.delete(sn, i, axis=1), axis=1)
+            mixed += x[:, i] / r * cs[:, i] * rest
+        return -(g * (d - 1) / r + 2.0 * np.pi * mixed - d * np.pi**2 * u)
+
+    return Problem(levels, rhs, exact)
+
+
+def sample_on_grid(func, levels) -> np.ndarray:
+    """Values of a vectorized callable at the interior points, SFC order (grid.py:164-166)."""
+    return np.asarray(func(interior_points(levels)), dtype=np.float64)

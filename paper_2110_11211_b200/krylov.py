@@ -87,6 +87,13 @@ class SolveReport:
         return out
 
 
+def initial_iterate(n: int, seed: int, A) -> np.ndarray:
+    """Seeded U[-1, 1] entries (numpy PCG64, so bit-reproducible) rescaled to
+    unit energy norm x / sqrt(x.(A x)) (krylov.py:91-99); A x on the device."""
+    x = np.random.default_rng(seed).uniform(-1.0, 1.0, size=n)
+    return x / np.sqrt(x @ np.asarray(A @ x))
+
+
 def pcg_device(op, b, x0=None, tol: float = 1e-8, max_iters: int = 20000, exact=None,
                tolerance_kind: str = "relative_residual"):
     """Device-resident PCG on CUDA tensors.

@@ -195,6 +195,22 @@ def test_pcg_split_big_supernodes_matches_reference(sfcdd, golden, name, monkeyp
     assert np.linalg.norm(rep.solution - sol) <= 1e-10 * np.linalg.norm(sol)
 
 
+@pytest.mark.parametrize("name", ["c1_g05", "small_3d", "aniso"])
+def test_pcg_sparse_coarse_factor_matches_reference(sfcdd, golden, name, monkeypatch):
+    """The coarse problem through its supernodal factor and the DAG kernel (the
+    path of coarse spaces above COARSE_DENSE_MAX dofs), forced on small cases."""
+    monkeypatch.setenv("SFCDD_COARSE_DENSE_MAX", "0")
+    g = golden.npz(f"solve_{name}.npz")
+    levels = tuple(int(v) for v in g["levels"])
+    rep, _ = _pcg(sfcdd, levels, int(g["p"]), float(g["gamma"]), int(g["q"]))
+    assert abs(rep.iterations - int(g["iterations"])) <= 1
+    h = g["residual_history"]
+    k = min(len(h), len(rep.residual_history))
+    assert (np.abs(np.asarray(rep.residual_history[:k]) - h[:k]) / h[:k]).max() <= 1e-10
+    sol = g["solution"]
+    assert np.linalg.norm(rep.solution - sol) <= 1e-10 * np.linalg.norm(sol)
+
+
 def test_pcg_c2_matches_reference(sfcdd, golden):
     g = golden.npz("solve_c2.npz")
     rep, _ = _pcg(sfcdd, (10, 10), 64, 0.5, 16)
