@@ -102,6 +102,7 @@ extern "C" int sfcdd_host_plan_solve(int64_t n, const int64_t* indptr, const int
   PlanOptions po;
   if (blob_max > 0) po.blob_max = blob_max;
   if (scratch_max > 0) po.scratch_max = scratch_max;
+  if (blob_max <= 0) choose_blob_shape(ptrs, po);
   DevicePlan plan = build_plan(ptrs, gs, gm, po);
   plan_exec_host(plan, rhs, xy);
   if (nfrag) *nfrag = plan.ngroups;

@@ -791,10 +791,9 @@ DagSolver::DagSolver(const DevicePlan& plan, int device, int64_t extra_xy) : dev
   host_tasks = plan.tasks;
   blob_max_ = round128(plan.blob_max);
   slot_bytes_ = blob_max_ + round128(8 * (int64_t)std::max(plan.max_scratch, 16));
-  // worker warps per CTA (2, 4 or 8; SFCDD_WPB overrides the default 4)
-  wpb_ = 4;
-  if (const char* e = std::getenv("SFCDD_WPB")) wpb_ = std::atoi(e);
-  SFCDD_REQUIRE(wpb_ == 2 || wpb_ == 4 || wpb_ == 8, SFCDD_EVALUE, "SFCDD_WPB must be 2, 4 or 8");
+  // worker warps per CTA: the plan's choice (plan.h choose_blob_shape, SFCDD_WPB)
+  wpb_ = plan.wpb;
+  SFCDD_REQUIRE(wpb_ == 2 || wpb_ == 4 || wpb_ == 8, SFCDD_EVALUE, "worker warps per CTA must be 2, 4 or 8");
   bool split = false;
   for (const TaskDev& T : plan.tasks) split = split || T.kind == TK_ASM_FWD || T.kind == TK_XB_BWD;
   kern_ = split ? (wpb_ == 2 ? (const void*)k_dag<2, true> : wpb_ == 4 ? (const void*)k_dag<4, true>

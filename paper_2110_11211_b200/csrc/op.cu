@@ -1438,6 +1438,7 @@ extern "C" int sfcdd_op_setup(sfcdd_op* op, void* stream) {
   op->xy_off_host = xyoff;
   PlanOptions po;
   CUDA_CHECK(cudaDeviceGetAttribute(&po.sms, cudaDevAttrMultiProcessorCount, op->device));
+  choose_blob_shape(ptrs, po);
   DevicePlan plan = build_plan(ptrs, gs, gm, po);
   op->stats.factor_nnz = plan.stored;
   op->stats.factor_nnz_l = plan.nnz_l;

@@ -76,6 +76,25 @@ PlanOptions::PlanOptions() {
   if (const char* e = std::getenv("SFCDD_ASM_RED")) asm_redundancy = std::atof(e);
   if (const char* e = std::getenv("SFCDD_XB_MIN")) xb_min_tasks = std::atoi(e);
   if (const char* e = std::getenv("SFCDD_SPLIT_MIN")) split_min_factors = std::atoi(e);
+  if (const char* e = std::getenv("SFCDD_WPB")) wpb = std::atoi(e);
+  tuned = std::getenv("SFCDD_BLOB_MAX") || std::getenv("SFCDD_WPB");
+}
+
+void choose_blob_shape(const std::vector<const HostFactor*>& factors, PlanOptions& opt) {
+  if (opt.tuned) return;
+  double big = 0.0, tot = 0.0;
+  for (const HostFactor* F : factors)
+    for (const Supernode& S : F->sn) {
+      const double v = (double)S.s * (S.s + S.m) - 0.5 * (double)S.s * (S.s - 1);
+      tot += v;
+      if (8.0 * v > opt.blob_max) big += v;  // cannot sit in a FRAG blob
+    }
+  if (std::getenv("SFCDD_PLAN_DEBUG"))
+    std::fprintf(stderr, "[plan] values in supernodes above one blob: %.1f%%\n", tot > 0.0 ? 100.0 * big / tot : 0.0);
+  if (tot > 0.0 && big > 0.42 * tot) {  // measured: C2 34 % -> 8 KB wins by 13 %; C4 47 %, C3 79 % -> 16 KB wins by 4 %, 17 %
+    opt.blob_max = 16 * 1024;
+    opt.wpb = 2;
+  }
 }
 
 DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::vector<int64_t>& gstart,
@@ -83,8 +102,10 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
   SFCDD_REQUIRE(opt.scratch_max < 65536 && opt.big_scratch_max < 65536, SFCDD_EINTERNAL,
                 "scratch positions must fit 16 bits");
   SFCDD_REQUIRE(opt.blob_max >= 2048 && opt.blob_max % 16 == 0, SFCDD_EVALUE, "blob_max must be >= 2048, 16-aligned");
+  SFCDD_REQUIRE(opt.wpb == 2 || opt.wpb == 4 || opt.wpb == 8, SFCDD_EVALUE, "SFCDD_WPB must be 2, 4 or 8");
   DevicePlan P;
   P.blob_max = opt.blob_max;
+  P.wpb = opt.wpb;
   std::vector<Group> groups;
   std::vector<std::vector<int32_t>> group_of(factors.size());
   std::vector<std::vector<int32_t>> upd_slot(factors.size());
@@ -839,13 +860,13 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
     using Ev = std::pair<double, int32_t>;
     std::vector<Ev> ev;  // min-heap of (end time, task)
     auto ev_cmp = [](const Ev& a, const Ev& b) { return a.first > b.first; };
-    // resident warps of the kernel: slots of blob_max + scratch, 4-warp CTAs,
-    // <= 21 warps/SM by registers (dag_solve.cu)
+    // resident warps of the kernel: slots of blob_max + scratch, wpb-warp
+    // CTAs, <= 20 worker warps/SM by registers (dag_solve.cu)
     int64_t workers = opt.workers;
     if (workers <= 0) {
       const int64_t slot = (opt.blob_max + 127) / 128 * 128 + (8 * std::max(P.max_scratch, 16) + 127) / 128 * 128;
-      const int64_t ctas = std::max<int64_t>(1, (227 * 1024) / (4 * slot));
-      workers = (int64_t)opt.sms * std::min<int64_t>(20, 4 * ctas);
+      const int64_t ctas = std::max<int64_t>(1, (227 * 1024) / (opt.wpb * slot));
+      workers = (int64_t)opt.sms * std::min<int64_t>(20, opt.wpb * ctas);
     }
     P.workers = (int32_t)workers;
     int64_t free_w = std::max<int64_t>(1, workers);

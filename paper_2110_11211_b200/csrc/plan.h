@@ -188,8 +188,17 @@ struct PlanOptions {
                                    // subdomains the top of the trees is latency bound and the
                                    // extra dependency hop costs more than it saves (SFCDD_SPLIT_MIN)
   double slack_us = 4.0;           // queue-order simulation: dependents become ready this late (SFCDD_SLACK_US)
-  PlanOptions();                 // environment overrides SFCDD_BLOB_MAX, SFCDD_SCRATCH_MAX
+  int32_t wpb = 4;                 // worker warps per DAG CTA: 2, 4 or 8 (SFCDD_WPB)
+  bool tuned = false;              // blob_max / wpb fixed by the environment (no automatic choice)
+  PlanOptions();                 // environment overrides SFCDD_BLOB_MAX, SFCDD_SCRATCH_MAX, ...
 };
+
+// Blob size and CTA shape for a set of factors (unless set by the
+// environment): plans whose values sit mostly in big supernodes (3-D
+// subdomains: dense separator fronts) stream 16 KB blobs with 2-worker CTAs,
+// which halves the per-column re-gathers of their COL / ROW tasks; FRAG-heavy
+// plans (2-D) keep 8 KB blobs and 4-worker CTAs (measured).
+void choose_blob_shape(const std::vector<const HostFactor*>& factors, PlanOptions& opt);
 
 struct DevicePlan {
   std::vector<uint8_t> blobs;
@@ -202,6 +211,7 @@ struct DevicePlan {
   int64_t xy_doubles = 0;
   int64_t num_supernodes = 0;
   int64_t stored = 0, nnz_l = 0;
+  int32_t wpb = 4;          // worker warps per DAG CTA the plan was simulated for
   int32_t max_scratch = 0;  // doubles, over all tasks
   int32_t max_copy = 0;     // bytes
   int32_t blob_max = 0;
