@@ -359,7 +359,6 @@ def run_gpu(args, cfg):
         ev1.record(stream)
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
-    launches = int(_lib.Stats().reserved[2]) if False else None
     s_after = _lib.Stats()
     _lib.check(_lib.lib().sfcdd_op_stats(op.handle, ctypes.byref(s_after)))
     launches_per_solve = int(s_after.reserved[2])

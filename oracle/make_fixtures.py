@@ -357,6 +357,9 @@ SOLVES = {
     # aggregates of 16320 points = 8 reduction chunks each (the R0 r partials
     # are per chunk, not per aggregate: pins the fused PCG epilogue's sums)
     "multichunk": ((9, 9), 8, 0.5, 2, False),
+    # BASELINE configs[3] at full size on one device: 4095^2, P=256, q=16,
+    # fault mode at apply 5; ~25 min and ~50 GB on the CPU
+    "c4_fault": ((12, 12), 256, 0.5, 16, False, 5),
 }
 
 

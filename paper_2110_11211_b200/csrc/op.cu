@@ -1096,6 +1096,23 @@ static void coarse_solve(sfcdd_op* op, const double* part, const int32_t* ptr, b
   k_coarse_out<<<nblocks(op->n0, VEC_THREADS), VEC_THREADS, 0, st>>>(op->coarse_dag->xy(), op->n0, y, sk, fin);
 }
 
+// kernel launches of coarse_solve / apply_device (the gpu_launches accounting
+// of sfcdd_op_pcg_ex and sfcdd_op_profile; keep in step with those functions)
+static int64_t coarse_solve_launches(const sfcdd_op* op, bool direct) {
+  return op->ainv ? 1 : (direct ? 0 : 1) + 1 + 1;  // GEMV | [segment sums] + DAG + output
+}
+static int64_t apply_launches(const sfcdd_op* op, bool pcg, bool partials_ready) {
+  const int v = op->variant;
+  const bool direct = op->nch == op->n0;
+  int64_t k = 0;
+  if (v != SFCDD_VARIANT_ONE_LEVEL) k += (partials_ready ? 0 : 1) + coarse_solve_launches(op, direct);
+  if (v == SFCDD_VARIANT_BALANCED) k += 1;  // t
+  k += 1 + 1;                               // DAG + combine
+  if (mode_of(v) == 2) k += op->tile_agg ? 2 + coarse_solve_launches(op, true) : 1 + coarse_solve_launches(op, direct);
+  if (!(pcg && mode_of(v) == 2)) k += 1;    // finalize
+  return k;
+}
+
 // the preconditioner apply on device: h = C^{-1} g.  If `pcg`, the R0 g
 // partials are already in part_c (fused into k_update) and r.h partials are
 // produced for the PCG scalars.
@@ -1714,11 +1731,8 @@ extern "C" int sfcdd_op_pcg_ex(sfcdd_op* op, const double* b_dev, double* x_dev,
   CUDA_CHECK(cudaMemcpyAsync(&hs, op->st, sizeof(DevState), cudaMemcpyDeviceToHost, st));
   CUDA_CHECK(cudaStreamSynchronize(st));
   {
-    // kernel launches of this call: init (zero, residual, apply) + 2 iterations per graph
-    const int v = op->variant;
-    // DAG + combine [+ GEMV] [+ t] [+ R0 Â w + GEMV (finalize fused away)] [+ finalize]
-    const int64_t per_apply = 1 + 1 + (v != SFCDD_VARIANT_ONE_LEVEL ? 1 : 0) + (v == SFCDD_VARIANT_BALANCED) +
-                              (mode_of(v) == 2 ? 2 : 1);
+    // kernel launches of this call: init (zero, residual [+ A x*, energy], apply) + the iterations
+    const int64_t per_apply = apply_launches(op, true, true);
     // per iteration: p-update/matvec, x/r update [+ energy error]
     const int64_t per_it = 2 + (exact_dev ? 1 : 0);
     op->stats.reserved[2] = 2 + (exact_dev ? 2 : 0) + per_apply + op->stats.reserved[3] * (per_it + per_apply);
@@ -1870,10 +1884,8 @@ extern "C" int sfcdd_op_profile(sfcdd_op* op, const double* g_dev, double* scrat
   long long zero = 0;
   CUDA_CHECK(cudaMemcpy(&op->st->apply_calls, &zero, sizeof(zero), cudaMemcpyHostToDevice));
   if (launches) {
-    const int v = op->variant;
     launches[0] = 1;
-    launches[1] = 1 + 1 + (v != SFCDD_VARIANT_ONE_LEVEL ? 2 : 0) + (v == SFCDD_VARIANT_BALANCED) +
-                  (mode_of(v) == 2 ? 2 : 0) + 1;
+    launches[1] = apply_launches(op, false, false);
     launches[2] = 1;
   }
   SFCDD_API_END
