@@ -260,6 +260,21 @@ def test_pcg_fault_mode_matches_reference(sfcdd, golden):
     assert (np.abs(np.asarray(rep.residual_history[:k]) - h[:k]) / h[:k]).max() <= 1e-10
 
 
+def test_pcg_c4_fault_mode_full_size_matches_reference(sfcdd, golden):
+    """BASELINE configs[3] at full size on one device (4095^2, P=256, q=16,
+    fault at apply 5): the bench workload of ``bench.py --config c4``."""
+    g = golden.npz("solve_c4_fault.npz")
+    dead = np.random.default_rng(42).choice(256, size=int(round(0.1 * 256)), replace=False)
+    rep, _ = _pcg(sfcdd, (12, 12), 256, 0.5, 16, fault=(5, dead))
+    assert abs(rep.iterations - int(g["iterations"])) <= 1
+    h = g["residual_history"]
+    k = min(len(h), len(rep.residual_history))
+    assert (np.abs(np.asarray(rep.residual_history[:k]) - h[:k]) / h[:k]).max() <= 1e-10
+    idx = g["solution_sample_idx"]
+    ref = g["solution_sample"]
+    assert np.linalg.norm(rep.solution[idx] - ref) <= 1e-10 * np.linalg.norm(ref)
+
+
 def test_pcg_bitwise_repeatable(sfcdd):
     r1, _ = _pcg(sfcdd, (8, 8), 32, 0.5, 4)
     r2, _ = _pcg(sfcdd, (8, 8), 32, 0.5, 4)
