@@ -65,6 +65,21 @@ int sfcdd_sfc_decode(int dim, int bits, const uint64_t* keys_hi_dev,
 int sfcdd_sfc_perm(int dim, const int32_t* levels_host, int64_t* perm_dev,
                    int64_t* rank_dev, int force_radix, void* stream);
 
+/* Curve option (north star subsystem (1): Hilbert / Lebesgue keys).  The
+ * three calls above are the Hilbert curve of the reference (curve 0); curve 1
+ * is the Lebesgue (Morton, Z-order) curve: the same MSB-first interleaving
+ * of the raw lattice coordinates, axis 0 first, without the Hilbert
+ * transform.  No reference implementation exists for curve 1 (oracle
+ * restatement only). */
+#define SFCDD_CURVE_HILBERT 0
+#define SFCDD_CURVE_LEBESGUE 1
+int sfcdd_sfc_encode_curve(int curve, int dim, int bits, const uint64_t* coords_dev, int64_t n,
+                           uint64_t* keys_hi_dev, uint64_t* keys_lo_dev, void* stream);
+int sfcdd_sfc_decode_curve(int curve, int dim, int bits, const uint64_t* keys_hi_dev,
+                           const uint64_t* keys_lo_dev, int64_t n, uint64_t* coords_dev, void* stream);
+int sfcdd_sfc_perm_curve(int curve, int dim, const int32_t* levels_host, int64_t* perm_dev,
+                         int64_t* rank_dev, int force_radix, void* stream);
+
 /* -------------------------------------------------------------- operator --
  * One handle = one grid, partition, coarse space and Schwarz configuration,
  * bound to one CUDA device.  Replaces the composition
@@ -90,7 +105,8 @@ typedef struct sfcdd_op_desc {
   int32_t host_threads;      /* setup threads (0 = hardware concurrency)    */
   int32_t shard_first;       /* shard mode: first owned subdomain           */
   int32_t shard_count;       /* shard mode: owned subdomains (0 = all)      */
-  int32_t reserved[5];
+  int32_t curve;             /* SFCDD_CURVE_HILBERT (0) | SFCDD_CURVE_LEBESGUE */
+  int32_t reserved[4];
 } sfcdd_op_desc;
 
 typedef struct sfcdd_stats {

@@ -11,7 +11,8 @@ Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s CPU arms may
 import it, and only as the checker / the timed CPU baseline.  The product
 package (``paper_2110_11211_b200``) never imports this file.
 
-Parity is PINNED: ``oracle/make_fixtures.py`` runs the reference itself in
+Parity is PINNED (Hilbert path; the Lebesgue option ``lebesgue_keys`` has no
+reference code and is unpinned): ``oracle/make_fixtures.py`` runs the reference itself in
 the build container and commits its outputs under ``tests/golden/``;
 ``tests/test_oracle_golden.py`` checks every function below against them.
 
@@ -78,17 +79,42 @@ def hilbert_keys(coords: np.ndarray, bits: int) -> tuple[np.ndarray, np.ndarray]
         q >>= 1
     for i in range(d):
         x[i] = x[i] ^ t
+    return _interleave(x, bits)
+
+
+def _interleave(x, bits: int) -> tuple[np.ndarray, np.ndarray]:
+    """sfc.py:102-107 (_pack_transpose): MSB-first, axis 0 first."""
+    d = len(x)
+    n = x[0].shape[0]
+    one = np.uint64(1)
     hi = np.zeros(n, np.uint64)
     lo = np.zeros(n, np.uint64)
-    for level in range(bits):                      # sfc.py:102-107 interleave
+    for level in range(bits):
         for i in range(d):
-            pos = level * d + (d - 1 - i)          # MSB-first, axis 0 first
+            pos = level * d + (d - 1 - i)
             bit = (x[i] >> np.uint64(level)) & one
             if pos < 64:
                 lo |= bit << np.uint64(pos)
             else:
                 hi |= bit << np.uint64(pos - 64)
     return hi, lo
+
+
+def lebesgue_keys(coords: np.ndarray, bits: int) -> tuple[np.ndarray, np.ndarray]:
+    """Lebesgue (Morton, Z-order) keys: the reference's bit interleaving
+    (sfc.py:102-107) of the RAW coordinates, without the Hilbert transform.
+
+    PARITY UNPINNED: the reference has no Lebesgue curve (north star
+    subsystem (1) names it), so this restatement is the
+    definition the device keys are checked against.
+    """
+    coords = np.asarray(coords, dtype=np.uint64)
+    n, d = coords.shape
+    if d * bits > MAX_KEY_BITS:
+        raise ValueError("key width exceeds 128 bits")
+    if d == 1:
+        return np.zeros(n, np.uint64), coords[:, 0].copy()
+    return _interleave([coords[:, i].copy() for i in range(d)], bits)
 
 
 def encode(coords, dim: int, bits: int) -> int:
@@ -115,7 +141,7 @@ def lex_coords(levels) -> np.ndarray:
     return np.stack([g.ravel() for g in grids], axis=1)
 
 
-def grid_keys(levels) -> tuple[np.ndarray, np.ndarray]:
+def grid_keys(levels, curve: str = "hilbert") -> tuple[np.ndarray, np.ndarray]:
     """grid_point_key for every interior point (sfc.py:150-169).
 
     1-based index k on axis j embeds as (k-1) << (lmax - l_j); with the
@@ -126,16 +152,16 @@ def grid_keys(levels) -> tuple[np.ndarray, np.ndarray]:
     c = lex_coords(levels).astype(np.uint64)
     for j, l in enumerate(levels):
         c[:, j] <<= np.uint64(lmax - l)
-    return hilbert_keys(c, lmax)
+    return lebesgue_keys(c, lmax) if curve == "lebesgue" else hilbert_keys(c, lmax)
 
 
-def sfc_permutation(levels) -> np.ndarray:
+def sfc_permutation(levels, curve: str = "hilbert") -> np.ndarray:
     """perm[s] = lex index of the point with the s-th smallest key (grid.py:60-77)."""
     levels = tuple(int(l) for l in levels)
     n = int(np.prod(interior_shape(levels)))
     if len(levels) == 1:
         return np.arange(n, dtype=np.int64)
-    hi, lo = grid_keys(levels)
+    hi, lo = grid_keys(levels, curve)
     return np.lexsort((lo, hi)).astype(np.int64)   # keys are unique
 
 
@@ -157,7 +183,7 @@ def stencil_constants(levels):
     return float(dhat), [float(o) for o in offs], float(t)
 
 
-def assemble_scaled_laplacian(levels) -> sp.csr_matrix:
+def assemble_scaled_laplacian(levels, curve: str = "hilbert") -> sp.csr_matrix:
     """Â = T A T in SFC order, assembled from the neighbour relation.
 
     Restates grid.py:91-130 (assemble_laplacian + symmetrize_diag) directly
@@ -167,7 +193,7 @@ def assemble_scaled_laplacian(levels) -> sp.csr_matrix:
     shape = interior_shape(levels)
     d = len(levels)
     n = int(np.prod(shape))
-    perm = sfc_permutation(levels)
+    perm = sfc_permutation(levels, curve)
     rank = np.empty(n, np.int64)
     rank[perm] = np.arange(n)
     dhat, offs, _ = stencil_constants(levels)
@@ -401,9 +427,9 @@ def fault_set(p: int, seed: int = 42, frac: float = 0.1) -> np.ndarray:
     return np.random.default_rng(seed).choice(p, size=int(round(frac * p)), replace=False)
 
 
-def solve_config(levels, p, gamma, q, seed=42, tol=1e-8, fault_iter=None, max_steps=None):
+def solve_config(levels, p, gamma, q, seed=42, tol=1e-8, fault_iter=None, max_steps=None, curve="hilbert"):
     """Full oracle pipeline of SURVEY §8(d): assemble, scale, set up, PCG from 0."""
-    A = assemble_scaled_laplacian(levels)
+    A = assemble_scaled_laplacian(levels, curve)
     n = A.shape[0]
     _, _, t = stencil_constants(levels)
     b = t * seeded_rhs(n, seed)               # b_hat = t * b (grid.py:130)

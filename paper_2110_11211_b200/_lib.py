@@ -46,6 +46,9 @@ class DeviceError(RuntimeError):
     """CUDA runtime failure (no device, launch failure, out of memory)."""
 
 
+CURVES = {"hilbert": 0, "lebesgue": 1}
+
+
 class OpDesc(ctypes.Structure):
     _fields_ = [
         ("dim", ctypes.c_int32),
@@ -63,7 +66,8 @@ class OpDesc(ctypes.Structure):
         ("host_threads", ctypes.c_int32),
         ("shard_first", ctypes.c_int32),
         ("shard_count", ctypes.c_int32),
-        ("reserved", ctypes.c_int32 * 5),
+        ("curve", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 4),
     ]
 
 
@@ -88,7 +92,7 @@ class Stats(ctypes.Structure):
 
 EXPORTS = [
     "sfcdd_last_error", "sfcdd_version", "sfcdd_sfc_encode", "sfcdd_sfc_decode",
-    "sfcdd_sfc_perm", "sfcdd_op_create", "sfcdd_op_setup", "sfcdd_op_apply",
+    "sfcdd_sfc_perm", "sfcdd_sfc_encode_curve", "sfcdd_sfc_decode_curve", "sfcdd_sfc_perm_curve", "sfcdd_op_create", "sfcdd_op_setup", "sfcdd_op_apply",
     "sfcdd_op_matvec", "sfcdd_op_pcg", "sfcdd_op_pcg_ex", "sfcdd_vec_dot", "sfcdd_vec_axpby",
     "sfcdd_op_set_fault", "sfcdd_op_reset_calls",
     "sfcdd_op_stats", "sfcdd_op_stencil", "sfcdd_op_coarse_dense", "sfcdd_op_destroy",
@@ -119,6 +123,9 @@ def lib() -> ctypes.CDLL:
         "sfcdd_sfc_encode": [ctypes.c_int, ctypes.c_int, vp, i64, vp, vp, vp],
         "sfcdd_sfc_decode": [ctypes.c_int, ctypes.c_int, vp, vp, i64, vp, vp],
         "sfcdd_sfc_perm": [ctypes.c_int, vp, vp, vp, ctypes.c_int, vp],
+        "sfcdd_sfc_encode_curve": [ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, i64, vp, vp, vp],
+        "sfcdd_sfc_decode_curve": [ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp, i64, vp, vp],
+        "sfcdd_sfc_perm_curve": [ctypes.c_int, ctypes.c_int, vp, vp, vp, ctypes.c_int, vp],
         "sfcdd_op_create": [ctypes.POINTER(OpDesc), ctypes.POINTER(vp)],
         "sfcdd_op_setup": [vp, vp],
         "sfcdd_op_apply": [vp, vp, vp, vp],

@@ -1230,6 +1230,8 @@ extern "C" int sfcdd_op_create(const sfcdd_op_desc* desc, sfcdd_op** out) {
   op->threads = desc->host_threads > 0 ? desc->host_threads : hardware_threads();
   op->shard_first = desc->shard_first;
   op->shard_count = desc->shard_count;
+  op->curve = desc->curve;
+  SFCDD_REQUIRE(op->curve == 0 || op->curve == 1, SFCDD_EVALUE, "unknown curve");
   if (op->shard_count > 0)
     SFCDD_REQUIRE(desc->shard_first >= 0 && desc->shard_first + desc->shard_count <= desc->p && desc->q >= 1,
                   SFCDD_EVALUE, "invalid shard (needs a coarse space and owned subdomains within [0, P))");
@@ -1261,7 +1263,7 @@ extern "C" int sfcdd_op_create(const sfcdd_op_desc* desc, sfcdd_op** out) {
   // SFC permutation and neighbour table
   int64_t* perm = (int64_t*)dev_alloc(op.get(), op->n * 8);
   int64_t* rank = (int64_t*)dev_alloc(op.get(), op->n * 8);
-  sfc_perm_device(op->d, op->levels, perm, rank, false, st);
+  sfc_perm_device(op->d, op->levels, perm, rank, false, st, op->curve);
   GridGeom g{};
   g.d = op->d;
   g.n = op->n;

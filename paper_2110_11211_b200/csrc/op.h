@@ -69,6 +69,7 @@ struct sfcdd_op {
   int64_t n = 0;
   int32_t p = 0, q = 0, variant = 3, weighting = 1, threads = 0;
   int32_t shard_first = 0, shard_count = 0;  // shard mode (multi-GPU): owned subdomains
+  int32_t curve = 0;                         // SFC: 0 Hilbert, 1 Lebesgue
   int64_t own_g0 = 0, own_g1 = 0;            // owned SFC segment [own_g0, own_g1)
   std::vector<int64_t> xy_off_host;          // per subdomain slot in the xy buffer (-1 none)
   int32_t n0 = 0;

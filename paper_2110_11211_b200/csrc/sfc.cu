@@ -1,4 +1,8 @@
-// Hilbert space-filling-curve keys and the SFC permutation of grid points.
+// Hilbert space-filling-curve keys and the SFC permutation of grid points
+// (plus the Lebesgue / Morton curve option: the same bit interleaving of the
+// raw lattice coordinates, no Hilbert transform; north star subsystem (1) --
+// the reference has no Lebesgue curve, so that option is checked against the
+// oracle's restatement only).
 //
 // Restates the Skilling transpose-form curve of the reference
 // (sfc.py:56-79 _axes_to_transpose, sfc.py:81-99 _transpose_to_axes,
@@ -97,7 +101,7 @@ __device__ __forceinline__ uint64_t pack_transpose64(const W* x, int d, int bits
   return k;
 }
 
-__global__ void k_encode(int d, int bits, const uint64_t* __restrict__ coords, int64_t n,
+__global__ void k_encode(int d, int bits, int curve, const uint64_t* __restrict__ coords, int64_t n,
                          uint64_t* __restrict__ hi, uint64_t* __restrict__ lo) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -108,13 +112,13 @@ __global__ void k_encode(int d, int bits, const uint64_t* __restrict__ coords, i
     lo[i] = x[0];
     return;
   }
-  axes_to_transpose(x, d, bits);
+  if (curve == CURVE_HILBERT) axes_to_transpose(x, d, bits);
   Key128 k = pack_transpose(x, d, bits);
   hi[i] = k.hi;
   lo[i] = k.lo;
 }
 
-__global__ void k_decode(int d, int bits, const uint64_t* __restrict__ hi,
+__global__ void k_decode(int d, int bits, int curve, const uint64_t* __restrict__ hi,
                          const uint64_t* __restrict__ lo, int64_t n, uint64_t* __restrict__ coords) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -133,7 +137,7 @@ __global__ void k_decode(int d, int bits, const uint64_t* __restrict__ hi,
       if (bit) x[j] |= uint64_t(1) << level;
     }
   }
-  transpose_to_axes(x, d, bits);
+  if (curve == CURVE_HILBERT) transpose_to_axes(x, d, bits);
   for (int j = 0; j < d; ++j) coords[i * d + j] = x[j];
 }
 
@@ -141,11 +145,8 @@ __device__ __forceinline__ Key128 grid_key(const GridGeom& g, int64_t lex) {
   uint32_t x[MAX_GRID_DIM];
   lex_to_lattice(g, lex, x);
   if (g.d == 1) return Key128{0, x[0]};  // grid.py:69-70: identity order
-  if (g.d * g.lmax <= 64) {
-    axes_to_transpose(x, g.d, g.lmax);
-    return Key128{0, pack_transpose64(x, g.d, g.lmax)};
-  }
-  axes_to_transpose(x, g.d, g.lmax);
+  if (g.curve == CURVE_HILBERT) axes_to_transpose(x, g.d, g.lmax);
+  if (g.d * g.lmax <= 64) return Key128{0, pack_transpose64(x, g.d, g.lmax)};
   return pack_transpose(x, g.d, g.lmax);
 }
 
@@ -284,10 +285,12 @@ static void exclusive_scan(const T* in_dev, T* out_dev, int64_t n, T* total_dev,
 static inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 void sfc_perm_device(int d, const int32_t* levels, int64_t* perm, int64_t* rank, bool force_radix,
-                     cudaStream_t st) {
+                     cudaStream_t st, int curve) {
   SFCDD_REQUIRE(d >= 1 && d <= MAX_GRID_DIM, SFCDD_EVALUE, "grid dimension must be in [1, 16]");
+  SFCDD_REQUIRE(curve == CURVE_HILBERT || curve == CURVE_LEBESGUE, SFCDD_EVALUE, "unknown curve");
   GridGeom g{};
   g.d = d;
+  g.curve = curve;
   g.lmax = 0;
   g.n = 1;
   for (int j = 0; j < d; ++j) {
@@ -369,33 +372,50 @@ void sfc_perm_device(int d, const int32_t* levels, int64_t* perm, int64_t* rank,
 
 using namespace sfcdd;
 
-extern "C" int sfcdd_sfc_encode(int dim, int bits, const uint64_t* coords_dev, int64_t n,
-                                uint64_t* keys_hi_dev, uint64_t* keys_lo_dev, void* stream) {
+extern "C" int sfcdd_sfc_encode_curve(int curve, int dim, int bits, const uint64_t* coords_dev, int64_t n,
+                                      uint64_t* keys_hi_dev, uint64_t* keys_lo_dev, void* stream) {
   SFCDD_API_BEGIN
+  SFCDD_REQUIRE(curve == CURVE_HILBERT || curve == CURVE_LEBESGUE, SFCDD_EVALUE, "unknown curve");
   SFCDD_REQUIRE(dim >= 1 && dim <= MAX_DIM, SFCDD_EVALUE, "dimension must be in [1, 64]");
   SFCDD_REQUIRE(bits >= 1 && bits <= 64 && dim * bits <= 128, SFCDD_EVALUE, "invalid curve refinement");
   if (n <= 0) return SFCDD_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  k_encode<<<blocks_for(n, 128), 128, 0, st>>>(dim, bits, coords_dev, n, keys_hi_dev, keys_lo_dev);
+  k_encode<<<blocks_for(n, 128), 128, 0, st>>>(dim, bits, curve, coords_dev, n, keys_hi_dev, keys_lo_dev);
   CUDA_CHECK(cudaGetLastError());
   SFCDD_API_END
+}
+
+extern "C" int sfcdd_sfc_decode_curve(int curve, int dim, int bits, const uint64_t* keys_hi_dev,
+                                      const uint64_t* keys_lo_dev, int64_t n, uint64_t* coords_dev, void* stream) {
+  SFCDD_API_BEGIN
+  SFCDD_REQUIRE(curve == CURVE_HILBERT || curve == CURVE_LEBESGUE, SFCDD_EVALUE, "unknown curve");
+  SFCDD_REQUIRE(dim >= 1 && dim <= MAX_DIM, SFCDD_EVALUE, "dimension must be in [1, 64]");
+  SFCDD_REQUIRE(bits >= 1 && bits <= 64 && dim * bits <= 128, SFCDD_EVALUE, "invalid curve refinement");
+  if (n <= 0) return SFCDD_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  k_decode<<<blocks_for(n, 128), 128, 0, st>>>(dim, bits, curve, keys_hi_dev, keys_lo_dev, n, coords_dev);
+  CUDA_CHECK(cudaGetLastError());
+  SFCDD_API_END
+}
+
+extern "C" int sfcdd_sfc_perm_curve(int curve, int dim, const int32_t* levels_host, int64_t* perm_dev,
+                                    int64_t* rank_dev, int force_radix, void* stream) {
+  SFCDD_API_BEGIN
+  sfc_perm_device(dim, levels_host, perm_dev, rank_dev, force_radix != 0, (cudaStream_t)stream, curve);
+  SFCDD_API_END
+}
+
+extern "C" int sfcdd_sfc_encode(int dim, int bits, const uint64_t* coords_dev, int64_t n, uint64_t* keys_hi_dev,
+                                uint64_t* keys_lo_dev, void* stream) {
+  return sfcdd_sfc_encode_curve(CURVE_HILBERT, dim, bits, coords_dev, n, keys_hi_dev, keys_lo_dev, stream);
 }
 
 extern "C" int sfcdd_sfc_decode(int dim, int bits, const uint64_t* keys_hi_dev, const uint64_t* keys_lo_dev,
                                 int64_t n, uint64_t* coords_dev, void* stream) {
-  SFCDD_API_BEGIN
-  SFCDD_REQUIRE(dim >= 1 && dim <= MAX_DIM, SFCDD_EVALUE, "dimension must be in [1, 64]");
-  SFCDD_REQUIRE(bits >= 1 && bits <= 64 && dim * bits <= 128, SFCDD_EVALUE, "invalid curve refinement");
-  if (n <= 0) return SFCDD_OK;
-  cudaStream_t st = (cudaStream_t)stream;
-  k_decode<<<blocks_for(n, 128), 128, 0, st>>>(dim, bits, keys_hi_dev, keys_lo_dev, n, coords_dev);
-  CUDA_CHECK(cudaGetLastError());
-  SFCDD_API_END
+  return sfcdd_sfc_decode_curve(CURVE_HILBERT, dim, bits, keys_hi_dev, keys_lo_dev, n, coords_dev, stream);
 }
 
 extern "C" int sfcdd_sfc_perm(int dim, const int32_t* levels_host, int64_t* perm_dev, int64_t* rank_dev,
                               int force_radix, void* stream) {
-  SFCDD_API_BEGIN
-  sfc_perm_device(dim, levels_host, perm_dev, rank_dev, force_radix != 0, (cudaStream_t)stream);
-  SFCDD_API_END
+  return sfcdd_sfc_perm_curve(CURVE_HILBERT, dim, levels_host, perm_dev, rank_dev, force_radix, stream);
 }

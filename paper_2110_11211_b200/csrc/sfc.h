@@ -11,9 +11,12 @@ constexpr int MAX_GRID_DIM = 16;
 
 // Grid geometry for the permutation kernels (C-order lex enumeration,
 // grid.py:72-75; embedding shift lmax - l_j, sfc.py:167-168).
+enum Curve : int { CURVE_HILBERT = 0, CURVE_LEBESGUE = 1 };
+
 struct GridGeom {
   int d;
   int lmax;
+  int curve;  // Curve
   int64_t n;
   int64_t shape[MAX_GRID_DIM];
   int shift[MAX_GRID_DIM];
@@ -31,6 +34,6 @@ __device__ __forceinline__ void lex_to_lattice(const GridGeom& g, int64_t lex, u
 
 // perm[s] = lex index of SFC rank s; rank = inverse (optional)
 void sfc_perm_device(int d, const int32_t* levels, int64_t* perm, int64_t* rank, bool force_radix,
-                     cudaStream_t st);
+                     cudaStream_t st, int curve = CURVE_HILBERT);
 
 }  // namespace sfcdd

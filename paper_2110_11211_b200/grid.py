@@ -53,8 +53,9 @@ def num_dofs(levels) -> int:
     return n
 
 
-def sfc_permutation_device(levels, force_radix: bool = False):
-    """perm (SFC rank -> lex index) and its inverse as int64 device tensors."""
+def sfc_permutation_device(levels, force_radix: bool = False, curve: str = "hilbert"):
+    """perm (SFC rank -> lex index) and its inverse as int64 device tensors
+    (``curve="lebesgue"``: Morton order, see sfc.py)."""
     import torch
 
     levels = as_levels(levels)
@@ -63,46 +64,50 @@ def sfc_permutation_device(levels, force_radix: bool = False):
     perm = torch.empty(n, dtype=torch.int64, device=dev)
     rank = torch.empty(n, dtype=torch.int64, device=dev)
     lv = (ctypes.c_int32 * len(levels))(*levels)
-    _lib.check(_lib.lib().sfcdd_sfc_perm(len(levels), ctypes.cast(lv, ctypes.c_void_p), perm.data_ptr(),
-                                         rank.data_ptr(), int(force_radix), _lib.stream_ptr()))
+    if curve not in _lib.CURVES:
+        raise ValueError(f"unknown curve {curve!r}")
+    _lib.check(_lib.lib().sfcdd_sfc_perm_curve(_lib.CURVES[curve], len(levels), ctypes.cast(lv, ctypes.c_void_p),
+                                               perm.data_ptr(), rank.data_ptr(), int(force_radix),
+                                               _lib.stream_ptr()))
     return perm, rank
 
 
 @lru_cache(maxsize=128)
-def sfc_permutation(levels: tuple[int, ...]) -> np.ndarray:
+def sfc_permutation(levels: tuple[int, ...], curve: str = "hilbert") -> np.ndarray:
     """``perm[s]`` = lex index of the point with the s-th smallest key (grid.py:60-77)."""
-    perm, _ = sfc_permutation_device(as_levels(levels))
+    perm, _ = sfc_permutation_device(as_levels(levels), curve=curve)
     out = perm.cpu().numpy()
     out.setflags(write=False)
     return out
 
 
-def interior_points(levels) -> np.ndarray:
+def interior_points(levels, curve: str = "hilbert") -> np.ndarray:
     """Coordinates of the interior points in SFC order, shape (N, d) (grid.py:80-88)."""
     levels = as_levels(levels)
     shape = interior_shape(levels)
     axes = [np.arange(1, s + 1, dtype=np.float64) * 2.0**-l for s, l in zip(shape, levels)]
     mesh = np.meshgrid(*axes, indexing="ij")
     pts = np.stack([m.ravel() for m in mesh], axis=1)
-    return pts[sfc_permutation(levels)]
+    return pts[sfc_permutation(levels, curve)]
 
 
-def scatter_to_lex(levels, values_sfc: np.ndarray) -> np.ndarray:
+def scatter_to_lex(levels, values_sfc: np.ndarray, curve: str = "hilbert") -> np.ndarray:
     """Reshape an SFC-ordered vector to the lexicographic d-dim array (grid.py:169-175)."""
     levels = as_levels(levels)
     shape = interior_shape(levels)
     out = np.empty(int(np.prod(shape)), dtype=np.float64)
-    out[sfc_permutation(levels)] = values_sfc
+    out[sfc_permutation(levels, curve)] = values_sfc
     return out.reshape(shape)
 
 
 class _GridHandle:
     """Device neighbour table + stencil constants for one level vector."""
 
-    def __init__(self, levels):
+    def __init__(self, levels, curve: str = "hilbert"):
         from .partition import disjoint_partition
 
         self.levels = levels
+        self.curve = curve
         self.n = num_dofs(levels)
         if len(levels) > 8:
             raise ValueError("device grids support up to 8 dimensions")
@@ -121,6 +126,7 @@ class _GridHandle:
         desc.ov_len = desc.dj_len = ln.ctypes.data
         desc.omega = om.ctypes.data
         desc.host_threads = 1
+        desc.curve = _lib.CURVES[curve]
         h = ctypes.c_void_p()
         _lib.check(_lib.lib().sfcdd_op_create(ctypes.byref(desc), ctypes.byref(h)))
         self.handle = h
@@ -149,8 +155,8 @@ class _GridHandle:
 
 
 @lru_cache(maxsize=16)
-def _grid_handle(levels) -> _GridHandle:
-    return _GridHandle(levels)
+def _grid_handle(levels, curve: str = "hilbert") -> _GridHandle:
+    return _GridHandle(levels, curve)
 
 
 class GridLaplacian:
@@ -161,8 +167,11 @@ class GridLaplacian:
     numpy arrays (returns numpy) or CUDA tensors (returns a CUDA tensor).
     """
 
-    def __init__(self, levels, scaled: bool = False):
+    def __init__(self, levels, scaled: bool = False, curve: str = "hilbert"):
+        if curve not in _lib.CURVES:
+            raise ValueError(f"unknown curve {curve!r}")
         self.levels = as_levels(levels)
+        self.curve = curve
         self.n = num_dofs(self.levels)
         self.shape = (self.n, self.n)
         self.dtype = np.float64
@@ -176,7 +185,7 @@ class GridLaplacian:
 
     @property
     def handle(self) -> _GridHandle:
-        return _grid_handle(self.levels)
+        return _grid_handle(self.levels, self.curve)
 
     @property
     def scale(self) -> float:
@@ -202,7 +211,7 @@ class GridLaplacian:
         """scipy CSR copy (diagnostics / small grids only)."""
         import scipy.sparse as sp
 
-        perm = sfc_permutation(self.levels)
+        perm = sfc_permutation(self.levels, self.curve)
         n = self.n
         rank = np.empty(n, np.int64)
         rank[perm] = np.arange(n)
@@ -228,11 +237,12 @@ class GridLaplacian:
         return self.tocsr().toarray()
 
 
-def assemble_laplacian(levels) -> GridLaplacian:
-    """(2d+1)-point FD matrix of -Laplace in SFC order (grid.py:91-114), matrix-free."""
+def assemble_laplacian(levels, curve: str = "hilbert") -> GridLaplacian:
+    """(2d+1)-point FD matrix of -Laplace in SFC order (grid.py:91-114), matrix-free.
+    ``curve="lebesgue"`` orders the unknowns along the Morton curve instead."""
     levels = as_levels(levels)
     num_dofs(levels)
-    return GridLaplacian(levels, scaled=False)
+    return GridLaplacian(levels, scaled=False, curve=curve)
 
 
 def symmetrize_diag(A, b):
@@ -241,7 +251,7 @@ def symmetrize_diag(A, b):
         if A.scaled:
             raise ValueError("matrix is already scaled")
         t = np.full(A.n, A.scale)
-        return GridLaplacian(A.levels, scaled=True), t * np.asarray(b, dtype=np.float64), t
+        return GridLaplacian(A.levels, scaled=True, curve=A.curve), t * np.asarray(b, dtype=np.float64), t
     # generic sparse input: boundary glue with the reference's formula
     import scipy.sparse as sp
 
@@ -286,6 +296,6 @@ def manufactured_poisson(levels) -> Problem:
     return Problem(levels, rhs, exact)
 
 
-def sample_on_grid(func, levels) -> np.ndarray:
+def sample_on_grid(func, levels, curve: str = "hilbert") -> np.ndarray:
     """Values of a vectorized callable at the interior points, SFC order (grid.py:164-166)."""
-    return np.asarray(func(interior_points(levels)), dtype=np.float64)
+    return np.asarray(func(interior_points(levels, curve)), dtype=np.float64)

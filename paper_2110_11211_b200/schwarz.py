@@ -76,6 +76,7 @@ class SchwarzOperator:
         desc.variant = _lib.VARIANT_CODES[config.variant]
         desc.weighting = _lib.WEIGHTING_CODES[config.weighting]
         desc.device = _lib.device().index
+        desc.curve = _lib.CURVES[getattr(A, "curve", "hilbert")]
         desc.ov_start, desc.ov_len = ov_start.ctypes.data, ov_len.ctypes.data
         desc.dj_start, desc.dj_len = dj_start.ctypes.data, dj_len.ctypes.data
         desc.omega = omega.ctypes.data

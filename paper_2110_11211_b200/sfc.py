@@ -1,5 +1,10 @@
 """d-dimensional Hilbert curve keys on the device (mirrors sfcdd.sfc).
 
+``CurveConfig(dim, bits, curve="lebesgue")`` selects the Lebesgue (Morton,
+Z-order) curve instead: the same MSB-first bit interleaving, axis 0 first, of
+the raw coordinates (north star subsystem (1); the reference has Hilbert
+only, so that option is checked against the oracle restatement).
+
 Same API and validation as the reference module (/root/reference/pkg/src/
 sfcdd/sfc.py:24-169); the key arithmetic runs in the sm_100a kernels of
 csrc/sfc.cu (Skilling transpose form, 128-bit keys as two 64-bit words).
@@ -20,12 +25,15 @@ MAX_KEY_BITS = 128
 
 @dataclass(frozen=True)
 class CurveConfig:
-    """Discrete Hilbert curve on the lattice [0, 2**bits)**dim (sfc.py:24-47)."""
+    """Discrete Hilbert (or Lebesgue) curve on the lattice [0, 2**bits)**dim (sfc.py:24-47)."""
 
     dim: int
     bits: int
+    curve: str = "hilbert"  # | "lebesgue"
 
     def __post_init__(self) -> None:
+        if self.curve not in _lib.CURVES:
+            raise ValueError(f"unknown curve {self.curve!r}")
         if self.dim < 1:
             raise ValueError(f"dimension must be positive, got {self.dim}")
         if self.bits < 1:
@@ -60,8 +68,8 @@ def encode_many(coords, cfg: CurveConfig) -> tuple[np.ndarray, np.ndarray]:
     ct = torch.from_numpy(c.view(np.int64)).to(dev)
     hi = torch.empty(n, dtype=torch.int64, device=dev)
     lo = torch.empty(n, dtype=torch.int64, device=dev)
-    _lib.check(_lib.lib().sfcdd_sfc_encode(cfg.dim, cfg.bits, ct.data_ptr(), n, hi.data_ptr(),
-                                           lo.data_ptr(), _lib.stream_ptr()))
+    _lib.check(_lib.lib().sfcdd_sfc_encode_curve(_lib.CURVES[cfg.curve], cfg.dim, cfg.bits, ct.data_ptr(), n,
+                                                 hi.data_ptr(), lo.data_ptr(), _lib.stream_ptr()))
     return hi.cpu().numpy().view(np.uint64), lo.cpu().numpy().view(np.uint64)
 
 
@@ -76,8 +84,8 @@ def decode_many(hi, lo, cfg: CurveConfig) -> np.ndarray:
     ht = torch.from_numpy(hi.view(np.int64)).to(dev)
     lt = torch.from_numpy(lo.view(np.int64)).to(dev)
     out = torch.empty(n * cfg.dim, dtype=torch.int64, device=dev)
-    _lib.check(_lib.lib().sfcdd_sfc_decode(cfg.dim, cfg.bits, ht.data_ptr(), lt.data_ptr(), n,
-                                           out.data_ptr(), _lib.stream_ptr()))
+    _lib.check(_lib.lib().sfcdd_sfc_decode_curve(_lib.CURVES[cfg.curve], cfg.dim, cfg.bits, ht.data_ptr(),
+                                                 lt.data_ptr(), n, out.data_ptr(), _lib.stream_ptr()))
     return out.cpu().numpy().view(np.uint64).reshape(n, cfg.dim)
 
 
@@ -101,7 +109,7 @@ def decode(key: int, cfg: CurveConfig) -> tuple[int, ...]:
     return tuple(int(v) for v in out[0])
 
 
-def grid_point_key(multi_index, levels) -> int:
+def grid_point_key(multi_index, levels, curve: str = "hilbert") -> int:
     """Key of a 1-based interior index of an anisotropic grid (sfc.py:150-169)."""
     ell = tuple(int(v) for v in levels)
     idx = tuple(int(v) for v in multi_index)
@@ -111,6 +119,6 @@ def grid_point_key(multi_index, levels) -> int:
         if not 1 <= k <= (1 << lj) - 1:
             raise ValueError(f"index {k} outside interior range of level {lj}")
     n = max(ell)
-    cfg = CurveConfig(len(ell), n)
+    cfg = CurveConfig(len(ell), n, curve)
     coords = tuple((k - 1) << (n - lj) for k, lj in zip(idx, ell))
     return encode(coords, cfg)

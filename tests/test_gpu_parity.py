@@ -302,8 +302,9 @@ def test_factorization_rejects_non_spd(sfcdd):
         sfcdd.Factorization(sp.csr_matrix(np.array([[1.0, 2.0], [2.0, 1.0]])))
 
 
+@pytest.mark.parametrize("curve", ["hilbert", "lebesgue"])
 @pytest.mark.parametrize("levels", [(7, 7), (6, 7), (10, 10), (4, 4, 4), (5, 6, 5), (7, 7, 7)])
-def test_tiled_stencil_bitwise_equals_neighbour_table(sfcdd, levels, monkeypatch):
+def test_tiled_stencil_bitwise_equals_neighbour_table(sfcdd, levels, monkeypatch, curve):
     """The index-free SFC-tile stencil (csrc/tiles.cpp) against the
     neighbour-table stencil on the same vector: bitwise equal."""
     n = sfcdd.num_dofs(levels)
@@ -314,7 +315,7 @@ def test_tiled_stencil_bitwise_equals_neighbour_table(sfcdd, levels, monkeypatch
             monkeypatch.setenv("SFCDD_NO_TILES", "1")
         else:
             monkeypatch.delenv("SFCDD_NO_TILES", raising=False)
-        A = sfcdd.assemble_laplacian(levels)
+        A = sfcdd.assemble_laplacian(levels, curve=curve)
         Ah, _, _ = sfcdd.symmetrize_diag(A, np.zeros(n))
         return sfcdd.schwarz.SchwarzOperator(Ah, part, sfcdd.build_coarse(part, Ah, 1),
                                              sfcdd.SchwarzConfig("balanced", "omega", 0.5, 1))
@@ -332,3 +333,47 @@ def test_tiled_stencil_bitwise_equals_neighbour_table(sfcdd, levels, monkeypatch
         outs.append(a)
     np.testing.assert_array_equal(outs[0], outs[2])
     np.testing.assert_allclose(outs[1], outs[3], rtol=1e-12, atol=1e-14 * np.abs(outs[1]).max())
+
+
+# ------------------------------------------------------ Lebesgue curve option
+@pytest.mark.parametrize("d,bits", [(2, 5), (3, 20), (5, 12), (4, 32)])
+def test_lebesgue_encode_decode_vs_oracle(sfcdd, oracle, d, bits):
+    coords = np.random.default_rng(d * bits).integers(0, 1 << bits, size=(500, d), dtype=np.uint64)
+    cfg = sfcdd.CurveConfig(d, bits, "lebesgue")
+    hi, lo = sfcdd.sfc.encode_many(coords, cfg)
+    ohi, olo = oracle.lebesgue_keys(coords, bits)
+    np.testing.assert_array_equal(hi, ohi)
+    np.testing.assert_array_equal(lo, olo)
+    np.testing.assert_array_equal(sfcdd.sfc.decode_many(hi, lo, cfg), coords)
+
+
+@pytest.mark.parametrize("levels", [(3, 3), (5, 4), (4, 4, 4), (3, 4, 5), (10, 10), (7, 7, 7)])
+@pytest.mark.parametrize("force_radix", [False, True])
+def test_lebesgue_permutation_vs_oracle(sfcdd, oracle, levels, force_radix):
+    perm, rank = sfcdd.grid.sfc_permutation_device(levels, force_radix=force_radix, curve="lebesgue")
+    want = oracle.sfc_permutation(levels, "lebesgue")
+    np.testing.assert_array_equal(perm.cpu().numpy(), want)
+    np.testing.assert_array_equal(rank.cpu().numpy()[want], np.arange(want.size))
+
+
+@pytest.mark.parametrize("levels,p,q", [((7, 7), 16, 4), ((4, 4, 4), 8, 4), ((6, 7), 12, 3)])
+def test_pcg_lebesgue_ordering_vs_oracle(sfcdd, oracle, levels, p, q):
+    """The whole pipeline on the Morton ordering (tiles, partitions, DAG,
+    coarse space) against the oracle on the same ordering."""
+    A = sfcdd.assemble_laplacian(levels, curve="lebesgue")
+    n = A.shape[0]
+    b = np.random.default_rng(42).uniform(-1.0, 1.0, size=n)
+    Ah, bh, _ = sfcdd.symmetrize_diag(A, b)
+    part = sfcdd.build_partition(n, p, 0.5)
+    op = sfcdd.setup(Ah, part, sfcdd.build_coarse(part, Ah, q), sfcdd.SchwarzConfig("balanced", "omega", 0.5, q))
+    cfg = sfcdd.SolverConfig(method="pcg", tolerance=1e-8, tolerance_kind="relative_residual")
+    rep = sfcdd.run(Ah, bh, op, cfg, np.zeros(n))
+    _, _, _, ref = oracle.solve_config(levels, p, 0.5, q, curve="lebesgue")
+    assert abs(rep.iterations - ref.iterations) <= 1
+    k = min(len(ref.residual_history), len(rep.residual_history))
+    h = np.asarray(ref.residual_history[:k])
+    assert (np.abs(np.asarray(rep.residual_history[:k]) - h) / h).max() <= 1e-10
+    assert np.linalg.norm(rep.solution - ref.solution) <= 1e-10 * np.linalg.norm(ref.solution)
+    # the scaled operator in Morton order is the oracle's matrix
+    np.testing.assert_allclose(Ah @ b, oracle.assemble_scaled_laplacian(levels, "lebesgue") @ b,
+                               rtol=1e-15, atol=1e-15)
