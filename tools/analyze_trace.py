@@ -1,7 +1,8 @@
 import numpy as np, sys
 d = np.load(sys.argv[1])
 T = d['trace'].astype(np.int64)
-sm, t0, tdep, tdat, tend = T[:,0], T[:,1], T[:,2], T[:,3], T[:,4]
+sm, t0, tdep, tdat, tend = T[:,0] & 0xffff, T[:,1], T[:,2], T[:,3], T[:,4]
+wid = T[:,0] >> 16
 kind = T[:,5]; cb = T[:,6]; vals = T[:,8]; wait = T[:,9]
 base = t0.min(); 
 print("makespan us", (tend.max()-base)/1e3)
@@ -39,3 +40,15 @@ for kind, nm in ((0, "frag_f"), (1, "frag_b")):
         print(f"   level {l}: n={sel.sum()} first phase {a:.0f} items {r:.0f}")
     last = np.array([Pp[i, min(3 + 2 * (nl[i] - 1), 9)] for i in range(len(Pp))])
     print(f"   epilogue {np.mean(Pp[:, 10] - last):.0f}")
+
+# per-worker gaps: end of a warp's task -> top of its next task (claim atomic,
+# TaskDev load, mailbox post), i.e. the per-task cost outside [t_top, t_end]
+# (needs a kernel that stores the worker id in the trace's upper sm bits)
+if wid.max() > 0:
+    o = np.lexsort((t0, wid))
+    w2, a, e = wid[o], t0[o], tend[o]
+    same = w2[1:] == w2[:-1]
+    gap = (a[1:] - e[:-1])[same]
+    print("per-worker gap between tasks: mean %.2f us, median %.2f us, p90 %.2f us" % (gap.mean()/1e3, np.median(gap)/1e3, np.percentile(gap, 90)/1e3))
+    busy = (tend - t0).sum(); span = (tend.max() - t0.min()) * (wid.max() + 1)
+    print("worker time in tasks %.1f%%, in gaps %.1f%%" % (100*busy/span, 100*gap.sum()/span))
