@@ -708,7 +708,7 @@ __global__ void __launch_bounds__((WPB + 1) * 32, 20 / WPB) k_dag(DagArgs A) {
     unsigned long long* tr = A.trace ? A.trace + 5 * (size_t)t : nullptr;
     if (lane == 0) {
       if (tr) {
-        tr[0] = smid();
+        tr[0] = smid() | ((unsigned long long)(blockIdx.x * WPB + warp) << 16);  // sm | worker id << 16
         tr[1] = gtimer();
       }
       // the blob does not depend on other tasks: copy it while waiting
