@@ -154,12 +154,16 @@ def test_gloo_world_size_2_matches_oracle():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("sparse_coarse", [False, True])
 @pytest.mark.parametrize("levels,p,gamma,q,world", [((7, 7), 16, 0.5, 4, 2), ((7, 7), 16, 0.5, 4, 4),
                                                     ((4, 4, 4), 8, 0.5, 4, 3)])
-def test_device_shards_lockstep_match_single_gpu(levels, p, gamma, q, world):
+def test_device_shards_lockstep_match_single_gpu(levels, p, gamma, q, world, sparse_coarse, monkeypatch):
+    """sparse_coarse: every rank's redundant coarse solve through the sparse
+    A0 factor and the DAG kernel (the path above 8192 coarse dofs)."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    import paper_2110_11211_b200 as sf
+    if sparse_coarse:
+        monkeypatch.setenv("SFCDD_COARSE_DENSE_MAX", "0")
 
     part = _part(levels, p, gamma)
     engines, plans = D.make_device_shards(levels, part, q, world)
