@@ -701,6 +701,8 @@ __global__ void __launch_bounds__((WPB + 1) * 32, 20 / WPB) k_dag(DagArgs A) {
       break;
     }
     const TaskDev T = A.tasks[t];
+    // issued now, consumed after the blob / dependency waits (off the claim chain)
+    const FactorDev F = A.factors[T.factor];
     // slot addresses computed from the shared base so the compiler keeps the
     // shared state space (LDS, not generic loads) for every blob/scratch access
     const int32_t* h = reinterpret_cast<const int32_t*>(smem + (size_t)warp * A.slot_bytes);
@@ -741,7 +743,6 @@ __global__ void __launch_bounds__((WPB + 1) * 32, 20 / WPB) k_dag(DagArgs A) {
     mbar_wait(bar, phase);
     phase ^= 1u;
     if (tr && lane == 0) tr[3] = gtimer();
-    const FactorDev F = A.factors[T.factor];
     switch (T.kind) {
       case TK_FRAG_FWD:
         run_frag(h, true, S, A, F, lane, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);

@@ -98,7 +98,32 @@ void choose_blob_shape(const std::vector<const HostFactor*>& factors, PlanOption
 }
 
 DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::vector<int64_t>& gstart,
-                      const std::vector<int64_t>& gmod, const PlanOptions& opt) {
+                      const std::vector<int64_t>& gmod, const PlanOptions& opt_in) {
+  PlanOptions opt = opt_in;
+  {
+    // the widest supernode sets a floor on the blob: one ROW task holds at
+    // least one row of M (s values), one COL task one column (s + m values).
+    // Large 3-D subdomains (BASELINE C5: ~65k overlapped points, separators
+    // of s ~ 2000) exceed the 16 KB shape, so the blob grows to the next power
+    // of two that fits and the CTA shape drops to 2 workers (fewer resident
+    // warps, but the plan builds instead of failing)
+    int64_t need = 0;
+    for (const HostFactor* F : factors)
+      for (const Supernode& S : F->sn)
+        need = std::max({need, blob_size(RW_WORDS, (int64_t)S.s),
+                         blob_size(CL_WORDS + 1 + (int64_t)S.m, (int64_t)S.s + S.m)});
+    if (need > opt.blob_max) {
+      int64_t b = opt.blob_max;
+      while (b < need) b *= 2;
+      SFCDD_REQUIRE(b <= 64 * 1024, SFCDD_EVALUE,
+                    "widest supernode needs a " + std::to_string(need) + "-byte task blob (> 64 KB)");
+      if (std::getenv("SFCDD_PLAN_DEBUG"))
+        std::fprintf(stderr, "[plan] blob grown %d -> %lld bytes for the widest supernode\n", opt.blob_max,
+                     (long long)b);
+      opt.blob_max = (int32_t)b;
+      opt.wpb = 2;
+    }
+  }
   SFCDD_REQUIRE(opt.scratch_max < 65536 && opt.big_scratch_max < 65536, SFCDD_EINTERNAL,
                 "scratch positions must fit 16 bits");
   SFCDD_REQUIRE(opt.blob_max >= 2048 && opt.blob_max % 16 == 0, SFCDD_EVALUE, "blob_max must be >= 2048, 16-aligned");

@@ -236,6 +236,23 @@ def test_pcg_c3_matches_reference(sfcdd, golden):
     assert np.linalg.norm(rep.solution[idx] - ref) <= 1e-10 * np.linalg.norm(ref)
 
 
+def test_pcg_c3_grown_blob_matches_reference(sfcdd, golden, monkeypatch):
+    """Separators wider than the requested blob: the plan grows the blob to
+    the next power of two that holds one ROW row / COL column (C3 with a
+    2 KB request -> 8 KB, 2-worker CTAs; the path BASELINE C5's s ~ 2000
+    separators take at 32 KB)."""
+    monkeypatch.setenv("SFCDD_BLOB_MAX", "2048")
+    g = golden.npz("solve_c3.npz")
+    rep, _ = _pcg(sfcdd, (7, 7, 7), 512, 0.5, 8)
+    assert abs(rep.iterations - int(g["iterations"])) <= 1
+    h = g["residual_history"]
+    k = min(len(h), len(rep.residual_history))
+    assert (np.abs(np.asarray(rep.residual_history[:k]) - h[:k]) / h[:k]).max() <= 1e-10
+    idx = g["solution_sample_idx"]
+    ref = g["solution_sample"]
+    assert np.linalg.norm(rep.solution[idx] - ref) <= 1e-10 * np.linalg.norm(ref)
+
+
 def test_pcg_multichunk_aggregates_match_reference(sfcdd, golden):
     """Aggregates spanning several reduction chunks: the fused PCG epilogue
     sums the per-chunk R0 r partials per aggregate (op.cu pcg_fin_epilogue)."""

@@ -122,7 +122,9 @@ def test_host_factor_rejects_non_spd():
 
 @pytest.mark.parametrize("levels,p,gamma,blob", [((7, 7), 16, 0.5, 0), ((7, 7), 16, 0.25, 4096),
                                                   ((4, 4, 4), 8, 0.5, 0), ((4, 4, 4), 8, 1.0, 2048),
-                                                  ((6, 5), 6, 0.75, 0)])
+                                                  ((6, 5), 6, 0.75, 0),
+                                                  # separators wider than a 2 KB blob row: the blob grows
+                                                  ((5, 5, 5), 4, 0.5, 2048)])
 @pytest.mark.parametrize("split", [False, True])
 def test_device_plan_host_interpreter(oracle, levels, p, gamma, blob, split, monkeypatch):
     """The fragment/blob layout the DAG kernel executes, run on the host;
