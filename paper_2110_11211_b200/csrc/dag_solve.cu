@@ -52,7 +52,8 @@ struct DagArgs {
   unsigned long long* ptrace;  // optional: per task 16 clock64 stamps (FRAG phases)
   int32_t mode;  // tuning switches (SFCDD_DAG_MODE): 1 = acquire polling, 2 = workers release directly,
                  // 4 = blob copies without the L2 evict_first hint
-  int32_t sig_ns;  // signaller idle sleep (ns, SFCDD_SIG_NS)
+  int32_t sig_ns;  // signaller idle sleep (ns, SFCDD_SIG_NS; mode bit 8)
+  uint32_t sig_wait_ns;  // signaller suspend-time hint on the post barrier (SFCDD_SIG_WAIT_NS)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -90,6 +91,27 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+
+// arrive on a count-1 barrier (release.cta): one completed phase per post
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// suspend until the phase of this parity completes or ~ns elapse (the
+// thread issues nothing meanwhile); true if the phase completed
+__device__ __forceinline__ bool mbar_wait_timed(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, %3;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(ns)
+      : "memory");
+  return ok != 0;
 }
 
 // TMA bulk copy global -> shared, completion signalled on the mbarrier
@@ -626,8 +648,9 @@ __device__ __forceinline__ void run_col(const int32_t* h, double* S, const DagAr
 // happen-before it through the CTA-scope release/acquire) and then bumps the
 // counters.  The workers never stall on the ~1 us release fence.
 template <int WPB>
-__device__ __forceinline__ void signaller(const DagArgs& A, int32_t* mbox, int32_t* nexit) {
+__device__ __forceinline__ void signaller(const DagArgs& A, int32_t* mbox, int32_t* nexit, uint64_t* sigbar) {
   int32_t v[WPB];
+  uint32_t par = 0;
   for (;;) {
     int np = 0;
 #pragma unroll
@@ -645,7 +668,14 @@ __device__ __forceinline__ void signaller(const DagArgs& A, int32_t* mbox, int32
         }
         if (np == 0) return;
       } else {
-        __nanosleep(A.sig_ns);
+        // idle: sleep on the post barrier (every mailbox post and every
+        // worker exit arrives on it) instead of spinning; the scan above
+        // decides, the barrier only wakes (a stale parity costs one extra
+        // scan and resynchronises)
+        if (A.mode & 8)
+          __nanosleep(A.sig_ns);
+        else if (mbar_wait_timed(sigbar, par, A.sig_wait_ns))
+          par ^= 1u;
         continue;
       }
     }
@@ -667,13 +697,18 @@ __global__ void __launch_bounds__((WPB + 1) * 32, 20 / WPB) k_dag(DagArgs A) {
   __shared__ __align__(8) uint64_t bars[WPB];
   __shared__ int32_t mbox[WPB];
   __shared__ int32_t nexit;
+  __shared__ __align__(8) uint64_t sigbar;
   if (A.skip && *A.skip) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x < WPB) mbox[threadIdx.x] = -1;
-  if (threadIdx.x == 0) nexit = 0;
+  if (threadIdx.x == 0) {
+    nexit = 0;
+    mbar_init(&sigbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   __syncthreads();
   if (warp == WPB) {
-    if (lane == 0) signaller<WPB>(A, mbox, &nexit);
+    if (lane == 0) signaller<WPB>(A, mbox, &nexit, &sigbar);
     return;
   }
   uint64_t* bar = &bars[warp];
@@ -696,8 +731,10 @@ __global__ void __launch_bounds__((WPB + 1) * 32, 20 / WPB) k_dag(DagArgs A) {
     if (lane == 0) t = q + A.nq * atomicAdd(qh, 1);
     t = __shfl_sync(FULL, t, 0);
     if (t >= A.ntask) {
-      if (lane == 0)  // release: ordered after this warp's last mailbox post
+      if (lane == 0) {  // release: ordered after this warp's last mailbox post
         asm volatile("red.release.cta.shared::cta.add.s32 [%0], 1;" ::"r"(smem_u32(&nexit)) : "memory");
+        mbar_arrive(&sigbar);
+      }
       break;
     }
     const TaskDev T = A.tasks[t];
@@ -775,6 +812,7 @@ __global__ void __launch_bounds__((WPB + 1) * 32, 20 / WPB) k_dag(DagArgs A) {
       } else {
         while (ld_acquire_cta(&mbox[warp]) >= 0) __nanosleep(20);  // signaller still busy with the last one
         st_release_cta(&mbox[warp], T.signal_idx);
+        mbar_arrive(&sigbar);
       }
       if (tr) tr[4] = gtimer();
     }
@@ -804,6 +842,7 @@ DagSolver::DagSolver(const DevicePlan& plan, int device, int64_t extra_xy) : dev
   split_ = split;
   if (const char* e = std::getenv("SFCDD_DAG_MODE")) mode_ = std::atoi(e);
   if (const char* e = std::getenv("SFCDD_SIG_NS")) sig_ns_ = std::atoi(e);
+  if (const char* e = std::getenv("SFCDD_SIG_WAIT_NS")) sig_wait_ns_ = std::atoi(e);
   smem_ = wpb_ * slot_bytes_;
   SFCDD_REQUIRE(smem_ <= 227 * 1024, SFCDD_EINTERNAL, "DAG shared-memory footprint exceeds 227 KB");
   auto up = [&](void** dst, const void* src, size_t bytes) {
@@ -875,6 +914,7 @@ void DagSolver::solve(const double* rhs, cudaStream_t st, const int32_t* skip) {
   a.ptrace = trace_ ? trace_ + 5 * (size_t)ntask_ : nullptr;
   a.mode = mode_;
   a.sig_ns = sig_ns_;
+  a.sig_wait_ns = (uint32_t)sig_wait_ns_;
   void* params[] = {&a};
   CUDA_CHECK(cudaLaunchKernel(kern_, dim3(grid_), dim3((wpb_ + 1) * 32), params, smem_, st));
 }

@@ -31,7 +31,8 @@ class DagSolver {
 
  private:
   int device_;
-  int32_t ngroups_ = 0, ntask_ = 0, grid_ = 1, blob_max_ = 0, slot_bytes_ = 0, smem_ = 0, wpb_ = 4, mode_ = 0, sig_ns_ = 20;
+  int32_t ngroups_ = 0, ntask_ = 0, grid_ = 1, blob_max_ = 0, slot_bytes_ = 0, smem_ = 0, wpb_ = 4, mode_ = 0, sig_ns_ = 20,
+          sig_wait_ns_ = 1000;
   bool split_ = false;  // kernel variant with ASM / XB tasks
   const void* kern_ = nullptr;
   int64_t xy_doubles_ = 0, ctr_words_ = 0, bytes_ = 0;
