@@ -9,6 +9,8 @@ print("makespan us", (tend.max()-base)/1e3)
 names = ["frag_f","frag_b","row","col","asm","xb"]
 for k in range(6):
     m = kind==k
+    if not m.any():
+        continue
     print(f"{names[k]:7s} n={m.sum():6d} claim->deps {np.mean(tdep[m]-t0[m])/1e3:6.2f}us  deps->data {np.mean(np.maximum(tdat[m]-tdep[m],0))/1e3:6.2f}  data->end {np.mean(tend[m]-tdat[m])/1e3:6.2f}  total {np.mean(tend[m]-t0[m])/1e3:6.2f}  bytes {cb[m].mean():.0f}")
 # per-warp idle: gaps between consecutive tasks of same warp unknown (no warp id); utilisation over time
 edges = np.linspace(0, (tend.max()-base), 21)
