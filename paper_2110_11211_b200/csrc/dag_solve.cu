@@ -726,10 +726,26 @@ __global__ void __launch_bounds__((WPB + 1) * 32, 20 / WPB) k_dag(DagArgs A) {
   // hook at a task's tail (claiming the next task there was measured slower:
   // holding a claimed task for even ~1 us delays the critical path)
   auto ahead = [&]() {};
+  // static mode (mode bit 16, experimental): worker w runs tasks w, w + W,
+  // w + 2W, ... of the queue order (W = resident workers).  Deadlock-free for
+  // the same reason as claiming (each worker's list follows one topological
+  // order) provided every CTA is resident -- the kernel must run alone.  No
+  // claim atomic, and the next descriptor is loaded (one word per lane)
+  // while the current task runs.
+  const bool stat = (A.mode & 16) != 0;
+  const int nw = (int)gridDim.x * WPB;
+  int ts = (int)blockIdx.x * WPB + warp;
+  constexpr int TW = (int)(sizeof(TaskDev) / 4);
+  static_assert(sizeof(TaskDev) % 4 == 0 && TW <= 32, "TaskDev words");
+  int32_t pw = (stat && lane < TW && ts < A.ntask) ? __ldg(reinterpret_cast<const int32_t*>(A.tasks + ts) + lane) : 0;
   for (;;) {
     int t = 0;
-    if (lane == 0) t = q + A.nq * atomicAdd(qh, 1);
-    t = __shfl_sync(FULL, t, 0);
+    if (stat) {
+      t = ts;
+    } else {
+      if (lane == 0) t = q + A.nq * atomicAdd(qh, 1);
+      t = __shfl_sync(FULL, t, 0);
+    }
     if (t >= A.ntask) {
       if (lane == 0) {  // release: ordered after this warp's last mailbox post
         asm volatile("red.release.cta.shared::cta.add.s32 [%0], 1;" ::"r"(smem_u32(&nexit)) : "memory");
@@ -737,7 +753,23 @@ __global__ void __launch_bounds__((WPB + 1) * 32, 20 / WPB) k_dag(DagArgs A) {
       }
       break;
     }
-    const TaskDev T = A.tasks[t];
+    TaskDev T;
+    if (stat) {
+      static_assert(offsetof(TaskDev, copy_bytes) == 8 && offsetof(TaskDev, signal_idx) == 32, "TaskDev layout");
+      T.blob_off = (int64_t)(uint32_t)__shfl_sync(FULL, pw, 0) | ((int64_t)__shfl_sync(FULL, pw, 1) << 32);
+      T.copy_bytes = __shfl_sync(FULL, pw, 2);
+      T.kind = __shfl_sync(FULL, pw, 3);
+      T.factor = __shfl_sync(FULL, pw, 4);
+      T.group = 0;
+      T.wait_idx = __shfl_sync(FULL, pw, 6);
+      T.wait_target = __shfl_sync(FULL, pw, 7);
+      T.signal_idx = __shfl_sync(FULL, pw, 8);
+      T.values = 0;
+      ts += nw;
+      pw = (lane < TW && ts < A.ntask) ? __ldg(reinterpret_cast<const int32_t*>(A.tasks + ts) + lane) : 0;
+    } else {
+      T = A.tasks[t];
+    }
     // issued now, consumed after the blob / dependency waits (off the claim chain)
     const FactorDev F = A.factors[T.factor];
     // slot addresses computed from the shared base so the compiler keeps the
