@@ -97,17 +97,36 @@ typedef struct sfcdd_op_desc {
   int32_t variant;           /* SFCDD_VARIANT_*                             */
   int32_t weighting;         /* SFCDD_WEIGHT_*                              */
   int32_t device;            /* CUDA device ordinal                         */
-  const int64_t* ov_start;   /* host, p entries: overlapped cyclic ranges   */
-  const int64_t* ov_len;
-  const int64_t* dj_start;   /* host, p entries: disjoint ranges            */
+  const int64_t* ov_start;   /* host, p entries: overlapped cyclic ranges,  */
+  const int64_t* ov_len;     /*   or NULL: computed from gamma (sfcdd_partition) */
+  const int64_t* dj_start;   /* host, p entries: disjoint ranges (NULL with ov_*) */
   const int64_t* dj_len;
-  const double* omega;       /* host, p entries (partition.py:151-157)      */
+  const double* omega;       /* host, p entries (partition.py:151-157), or NULL */
   int32_t host_threads;      /* setup threads (0 = hardware concurrency)    */
   int32_t shard_first;       /* shard mode: first owned subdomain           */
   int32_t shard_count;       /* shard mode: owned subdomains (0 = all)      */
   int32_t curve;             /* SFCDD_CURVE_HILBERT (0) | SFCDD_CURVE_LEBESGUE */
+  int32_t raw_laplacian;     /* 0: scaled Â = T A T (grid.py:117-130); 1: the
+                                unscaled A of assemble_laplacian (grid.py:91-114) */
+  int64_t gamma_num;         /* overlap gamma = gamma_num / gamma_den, used    */
+  int64_t gamma_den;         /*   when ov_start == NULL (partition.py:78-116)  */
   int32_t reserved[4];
 } sfcdd_op_desc;
+
+/* ------------------------------------------------------------ partition --
+ * Replaces partition.disjoint_partition + enlarge (partition.py:64-116):
+ * P disjoint ranges (first N mod P one longer) and the gamma-overlapped
+ * cyclic ranges, gamma = gamma_num / gamma_den exactly (the caller applies
+ * Fraction(gamma).limit_denominator(10**6), partition.py:78-81).  Errors
+ * (ValueError) as the reference: P outside [1, N], gamma < 0, overlap with
+ * P < 2, 2 gamma + 1 > P.  All outputs host arrays of P entries.          */
+int sfcdd_partition(int64_t n, int32_t p, int64_t gamma_num, int64_t gamma_den, int64_t* dj_start,
+                    int64_t* dj_len, int64_t* ov_start, int64_t* ov_len);
+/* Replaces partition.compute_weights (partition.py:151-157): counts[N]
+ * (nullable) = number of overlapped ranges covering each index, omega[P]
+ * (nullable) = max over range i of 1/counts.                              */
+int sfcdd_partition_weights(int64_t n, int32_t p, const int64_t* ov_start, const int64_t* ov_len,
+                            int32_t* counts, double* omega);
 
 typedef struct sfcdd_stats {
   int64_t n;                 /* fine dofs                                   */
@@ -224,6 +243,16 @@ int sfcdd_factor_solve(sfcdd_factor* f, const double* b_dev, double* x_dev, void
 int sfcdd_factor_info(sfcdd_factor* f, int64_t* nnz_l, int64_t* stored, int64_t* nsuper);
 void sfcdd_factor_destroy(sfcdd_factor* f);
 
+/* --------------------------------------------------- general matrix --
+ * y = A x for a CSR matrix on the device (the `A @ v` of krylov.py:257-291
+ * when A is not a grid Laplacian, e.g. test_krylov.py:154-166); summed in
+ * stored order with separate multiply/add roundings like scipy csr_matvec. */
+typedef struct sfcdd_csr sfcdd_csr;
+int sfcdd_csr_create(int64_t rows, int64_t cols, const int64_t* indptr_host, const int32_t* indices_host,
+                     const double* data_host, int32_t device, sfcdd_csr** out);
+int sfcdd_csr_matvec(sfcdd_csr* m, const double* x_dev, double* y_dev, void* stream);
+void sfcdd_csr_destroy(sfcdd_csr* m);
+
 /* --------------------------------------------------- host test hooks --
  * CPU-only checks of the host setup logic (no device needed): AMD ordering
  * and the block-inverse supernodal factor applied on the host.            */
@@ -240,6 +269,13 @@ int sfcdd_host_plan_solve(int64_t n, const int64_t* indptr, const int32_t* indic
                           const double* data, int32_t p, const int64_t* start,
                           const int64_t* len, const double* rhs, double* xy,
                           int32_t blob_max, int32_t scratch_max, int64_t* nfrag);
+
+/* Diagnostics: wall seconds of the setup phases for one SPD block
+ * (times[3]: ordering + symbolic, host numeric factorization, plan build)
+ * and sizes[6]: nnz(L), stored, supernodes, update-matrix doubles, largest
+ * front, factor flops.  numeric = 0 skips the numeric phase and the plan.  */
+int sfcdd_host_setup_timing(int64_t n, const int64_t* indptr, const int32_t* indices, const double* data,
+                            int32_t numeric, double* times, int64_t* sizes);
 
 #ifdef __cplusplus
 }

@@ -67,6 +67,9 @@ class OpDesc(ctypes.Structure):
         ("shard_first", ctypes.c_int32),
         ("shard_count", ctypes.c_int32),
         ("curve", ctypes.c_int32),
+        ("raw_laplacian", ctypes.c_int32),
+        ("gamma_num", ctypes.c_int64),
+        ("gamma_den", ctypes.c_int64),
         ("reserved", ctypes.c_int32 * 4),
     ]
 
@@ -102,6 +105,8 @@ EXPORTS = [
     "sfcdd_shard_stencil_restrict", "sfcdd_shard_finalize", "sfcdd_pack", "sfcdd_unpack",
     "sfcdd_factor_create", "sfcdd_factor_solve", "sfcdd_factor_info", "sfcdd_factor_destroy",
     "sfcdd_host_amd", "sfcdd_host_factor_solve", "sfcdd_host_plan_solve",
+    "sfcdd_partition", "sfcdd_partition_weights", "sfcdd_csr_create", "sfcdd_csr_matvec", "sfcdd_csr_destroy",
+    "sfcdd_host_setup_timing",
 ]
 
 _lib = None
@@ -161,6 +166,11 @@ def lib() -> ctypes.CDLL:
         "sfcdd_host_amd": [i64, vp, vp, vp],
         "sfcdd_host_factor_solve": [i64, vp, vp, vp, vp, vp, vp, vp],
         "sfcdd_host_plan_solve": [i64, vp, vp, vp, i32, vp, vp, vp, vp, i32, i32, vp],
+        "sfcdd_partition": [i64, i32, i64, i64, vp, vp, vp, vp],
+        "sfcdd_partition_weights": [i64, i32, vp, vp, vp, vp],
+        "sfcdd_csr_create": [i64, i64, vp, vp, vp, i32, ctypes.POINTER(vp)],
+        "sfcdd_csr_matvec": [vp, vp, vp, vp],
+        "sfcdd_host_setup_timing": [i64, vp, vp, vp, i32, vp, vp],
     }
     for name, args in sigs.items():
         fn = getattr(L, name)
@@ -170,6 +180,8 @@ def lib() -> ctypes.CDLL:
     L.sfcdd_op_destroy.restype = None
     L.sfcdd_factor_destroy.argtypes = [vp]
     L.sfcdd_factor_destroy.restype = None
+    L.sfcdd_csr_destroy.argtypes = [vp]
+    L.sfcdd_csr_destroy.restype = None
     _lib = L
     return L
 

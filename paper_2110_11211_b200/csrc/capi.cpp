@@ -1,4 +1,5 @@
 // C-ABI plumbing shared by all entry points, plus the host-only test hooks.
+#include <chrono>
 #include <cstring>
 #include <string>
 
@@ -106,5 +107,44 @@ extern "C" int sfcdd_host_plan_solve(int64_t n, const int64_t* indptr, const int
   DevicePlan plan = build_plan(ptrs, gs, gm, po);
   plan_exec_host(plan, rhs, xy);
   if (nfrag) *nfrag = plan.ngroups;
+  SFCDD_API_END
+}
+
+// Diagnostics (host only): wall seconds of the setup phases for one SPD block:
+// times[0] ordering + symbolic analysis, times[1] host numeric factorization,
+// times[2] device-plan build; sizes[0] nnz(L), sizes[1] stored, sizes[2]
+// supernodes, sizes[3] sum over supernodes of m(m+1)/2 (update-matrix doubles),
+// sizes[4] largest front, sizes[5] sum of s^3/3 + s^2 m + s m^2 (factor flops).
+extern "C" int sfcdd_host_setup_timing(int64_t n, const int64_t* indptr, const int32_t* indices,
+                                       const double* data, int32_t numeric, double* times, int64_t* sizes) {
+  SFCDD_API_BEGIN
+  CsrMatrix A = csr_from(n, indptr, indices, data);
+  FactorOptions fo;
+  auto t0 = std::chrono::steady_clock::now();
+  HostFactor F = analyze_host(A, fo);
+  auto t1 = std::chrono::steady_clock::now();
+  if (numeric) numeric_host(A, F);
+  auto t2 = std::chrono::steady_clock::now();
+  if (numeric) {
+    PlanOptions po;
+    std::vector<const HostFactor*> ptrs{&F};
+    choose_blob_shape(ptrs, po);
+    DevicePlan plan = build_plan(ptrs, {0}, {n}, po);
+  }
+  auto t3 = std::chrono::steady_clock::now();
+  times[0] = std::chrono::duration<double>(t1 - t0).count();
+  times[1] = std::chrono::duration<double>(t2 - t1).count();
+  times[2] = std::chrono::duration<double>(t3 - t2).count();
+  int64_t upd = 0, fl = 0;
+  for (const Supernode& S : F.sn) {
+    upd += (int64_t)S.m * (S.m + 1) / 2;
+    fl += (int64_t)S.s * S.s * S.s / 3 + (int64_t)S.s * S.s * S.m + (int64_t)S.s * S.m * S.m;
+  }
+  sizes[0] = F.nnz_l;
+  sizes[1] = F.stored;
+  sizes[2] = (int64_t)F.sn.size();
+  sizes[3] = upd;
+  sizes[4] = F.max_front;
+  sizes[5] = fl;
   SFCDD_API_END
 }

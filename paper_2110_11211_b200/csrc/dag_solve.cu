@@ -23,6 +23,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <map>
 #include <mutex>
 
 #include "common.h"
@@ -899,13 +900,14 @@ DagSolver::DagSolver(const DevicePlan& plan, int device, int64_t extra_xy) : dev
   {
     // the attribute is per function: only ever raise it, so every live
     // solver (several handles per process in shard emulation) can launch
+    // (the attribute is per device: the cache is keyed by device and kernel)
     static std::mutex mu;
-    static int max_smem[18] = {0};
+    static std::map<std::pair<int, const void*>, int> max_smem;
     std::lock_guard<std::mutex> g(mu);
-    const int mi = wpb_ + (split_ ? 9 : 0);
-    if (smem_ > max_smem[mi]) {
+    int& cur = max_smem[{device, kern_}];
+    if (smem_ > cur) {
       CUDA_CHECK(cudaFuncSetAttribute(kern_, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
-      max_smem[mi] = smem_;
+      cur = smem_;
     }
   }
   int per_sm = 0, sms = 0;
@@ -948,7 +950,10 @@ void DagSolver::solve(const double* rhs, cudaStream_t st, const int32_t* skip) {
   a.sig_ns = sig_ns_;
   a.sig_wait_ns = (uint32_t)sig_wait_ns_;
   void* params[] = {&a};
-  CUDA_CHECK(cudaLaunchKernel(kern_, dim3(grid_), dim3((wpb_ + 1) * 32), params, smem_, st));
+  if (mode_ & 16)  // static worker lists need every CTA resident: cooperative launch guarantees it (or fails)
+    CUDA_CHECK(cudaLaunchCooperativeKernel(kern_, dim3(grid_), dim3((wpb_ + 1) * 32), params, smem_, st));
+  else
+    CUDA_CHECK(cudaLaunchKernel(kern_, dim3(grid_), dim3((wpb_ + 1) * 32), params, smem_, st));
 }
 
 void DagSolver::set_trace(unsigned long long* dev_buf) { trace_ = dev_buf; }

@@ -90,4 +90,10 @@ void host_block_solve(const HostFactor& F, const double* b, double* x);
 
 int hardware_threads();
 
+// partition.cpp (partition.py:64-157)
+void partition_ranges(int64_t n, int32_t p, int64_t gnum, int64_t gden, std::vector<int64_t>& dj_start,
+                      std::vector<int64_t>& dj_len, std::vector<int64_t>& ov_start, std::vector<int64_t>& ov_len);
+void partition_weights(int64_t n, int32_t p, const int64_t* ov_start, const int64_t* ov_len, int32_t* counts,
+                       double* omega);
+
 }  // namespace sfcdd

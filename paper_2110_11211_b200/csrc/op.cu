@@ -903,12 +903,22 @@ __global__ void k_update(double* __restrict__ x, double* __restrict__ r, const d
       const double nrm = sqrt(tot);
       hist[k] = nrm;
       if (!st->energy_mode) {  // else k_energy decides (after the energy error is known)
+        bool stop = false;
         if (nrm <= st->tol * st->hist0) {  // krylov.py:283-286
           st->converged = 1;
-          st->done = 1;
+          stop = true;
         } else if (k >= st->max_iters) {
           st->exhausted = 1;
-          st->done = 1;
+          stop = true;
+        }
+        // with energy tracking the reference still records the energy error
+        // of this last iterate (krylov.py:186-200): k_energy turns the
+        // pending stop into done after writing ehist[k]
+        if (stop) {
+          if (st->track_energy)
+            st->stop_pending = 1;
+          else
+            st->done = 1;
         }
       }
     }
@@ -947,6 +957,10 @@ __global__ void k_energy(const double* __restrict__ x, const double* __restrict_
           st->done = 1;
         }
       }
+      if (st->stop_pending) {  // k_update's residual stop of this iteration
+        st->stop_pending = 0;
+        st->done = 1;
+      }
     }
   }
 }
@@ -959,7 +973,7 @@ __global__ void k_zero_state_pcg(DevState* st, double tol, int32_t max_iters, in
   st->tol = tol;
   st->hist0 = 0;
   st->rz = st->beta = st->pap = st->alpha = 0;
-  st->k = st->converged = st->breakdown = st->exhausted = st->have_rz = st->done = 0;
+  st->k = st->converged = st->breakdown = st->exhausted = st->have_rz = st->done = st->stop_pending = 0;
   st->max_iters = max_iters;
   st->apply_calls = 0;  // fault mode counts preconditioner calls per solve
   for (int i = 0; i < 8; ++i) st->ticket[i] = 0;
@@ -1195,6 +1209,22 @@ static void pcg_iteration(sfcdd_op* op, double* x, const double* pold, double* p
   apply_device(op, op->r, op->z, st, true, true);
 }
 
+OpScope::OpScope(sfcdd_op* op, cudaStream_t caller) : op_(op), caller_(caller), lk_(op->mu) {
+  CUDA_CHECK(cudaEventRecord(op->ev_in, caller));
+  CUDA_CHECK(cudaStreamWaitEvent(op->own_stream, op->ev_in, 0));
+}
+
+OpScope::~OpScope() noexcept(false) {
+  // the caller's stream resumes after the handle's work (also on the error
+  // path, so a failed call never leaves the caller unordered)
+  cudaError_t e1 = cudaEventRecord(op_->ev_out, op_->own_stream);
+  cudaError_t e2 = cudaStreamWaitEvent(caller_, op_->ev_out, 0);
+  if (!std::uncaught_exceptions()) {
+    CUDA_CHECK(e1);
+    CUDA_CHECK(e2);
+  }
+}
+
 }  // namespace sfcdd
 
 using namespace sfcdd;
@@ -1217,12 +1247,19 @@ extern "C" int sfcdd_op_create(const sfcdd_op_desc* desc, sfcdd_op** out) {
     op->n *= s;
     diag = diag + 2.0 * std::ldexp(1.0, 2 * desc->levels[j]);  // kron-sum diagonal (grid.py:101-110)
   }
+  SFCDD_REQUIRE(desc->raw_laplacian == 0 || desc->raw_laplacian == 1, SFCDD_EVALUE, "raw_laplacian must be 0 or 1");
   SFCDD_REQUIRE(op->n < ((int64_t)1 << 31), SFCDD_EVALUE, "grids above 2^31 points need multi-GPU sharding");
   // T A T with t = diag^-1/2 (grid.py:117-130): entries fl(fl(t a) t)
   const double t = 1.0 / std::sqrt(diag);
   op->tscale = t;
-  op->dhat = (t * diag) * t;
-  for (int j = 0; j < op->d; ++j) op->off[j] = (t * -std::ldexp(1.0, 2 * desc->levels[j])) * t;
+  op->raw = desc->raw_laplacian;
+  if (op->raw) {  // unscaled A: exact integer entries 2 sum 4^l and -4^l_j
+    op->dhat = diag;
+    for (int j = 0; j < op->d; ++j) op->off[j] = -std::ldexp(1.0, 2 * desc->levels[j]);
+  } else {
+    op->dhat = (t * diag) * t;
+    for (int j = 0; j < op->d; ++j) op->off[j] = (t * -std::ldexp(1.0, 2 * desc->levels[j])) * t;
+  }
   op->p = desc->p;
   op->q = desc->q;
   op->variant = desc->variant;
@@ -1240,11 +1277,22 @@ extern "C" int sfcdd_op_create(const sfcdd_op_desc* desc, sfcdd_op** out) {
   SFCDD_REQUIRE(op->weighting >= 0 && op->weighting <= 2, SFCDD_EVALUE, "unknown weighting");
   const bool coarse = op->variant != SFCDD_VARIANT_ONE_LEVEL;
   if (coarse) SFCDD_REQUIRE(op->q >= 1 && op->q <= op->n / op->p, SFCDD_EVALUE, "need 1 <= q <= floor(N/P)");
-  op->ov_start.assign(desc->ov_start, desc->ov_start + op->p);
-  op->ov_len.assign(desc->ov_len, desc->ov_len + op->p);
-  op->dj_start.assign(desc->dj_start, desc->dj_start + op->p);
-  op->dj_len.assign(desc->dj_len, desc->dj_len + op->p);
-  op->omega.assign(desc->omega, desc->omega + op->p);
+  if (desc->ov_start) {
+    SFCDD_REQUIRE(desc->ov_len && desc->dj_start && desc->dj_len, SFCDD_EVALUE, "incomplete ranges");
+    op->ov_start.assign(desc->ov_start, desc->ov_start + op->p);
+    op->ov_len.assign(desc->ov_len, desc->ov_len + op->p);
+    op->dj_start.assign(desc->dj_start, desc->dj_start + op->p);
+    op->dj_len.assign(desc->dj_len, desc->dj_len + op->p);
+  } else {  // the library's own partition (partition.py:130-133)
+    partition_ranges(op->n, op->p, desc->gamma_num, desc->gamma_den, op->dj_start, op->dj_len, op->ov_start,
+                     op->ov_len);
+  }
+  if (desc->omega) {
+    op->omega.assign(desc->omega, desc->omega + op->p);
+  } else {  // partition.py:151-157
+    op->omega.resize(op->p);
+    partition_weights(op->n, op->p, op->ov_start.data(), op->ov_len.data(), nullptr, op->omega.data());
+  }
   int64_t acc = 0;
   for (int i = 0; i < op->p; ++i) {
     SFCDD_REQUIRE(op->dj_start[i] == acc, SFCDD_EVALUE, "disjoint ranges must tile [0, N) in order");
@@ -1259,6 +1307,8 @@ extern "C" int sfcdd_op_create(const sfcdd_op_desc* desc, sfcdd_op** out) {
   CUDA_CHECK(cudaStreamCreateWithFlags(&op->own_stream, cudaStreamNonBlocking));
   CUDA_CHECK(cudaEventCreate(&op->ev0));
   CUDA_CHECK(cudaEventCreate(&op->ev1));
+  CUDA_CHECK(cudaEventCreateWithFlags(&op->ev_in, cudaEventDisableTiming));
+  CUDA_CHECK(cudaEventCreateWithFlags(&op->ev_out, cudaEventDisableTiming));
   cudaStream_t st = op->own_stream;
   // SFC permutation and neighbour table
   int64_t* perm = (int64_t*)dev_alloc(op.get(), op->n * 8);
@@ -1305,9 +1355,15 @@ extern "C" int sfcdd_op_create(const sfcdd_op_desc* desc, sfcdd_op** out) {
     CUDA_CHECK(cudaStreamSynchronize(st));
     CUDA_CHECK(cudaFree(das));
   } else {
-    for (int64_t s0 = 0; s0 < op->n; s0 += CHUNK) {
-      cstart.push_back(std::min<int64_t>(s0 + CHUNK, op->n));
-      cagg.push_back(-1);
+    // one-level: chunks never cross a disjoint range, so the subdomains
+    // meeting one chunk are those covering one owner's points (a fixed
+    // 2048-point grid would meet > COMBINE_MAXC ranges for tiny subdomains)
+    for (int i = 0; i < op->p; ++i) {
+      const int64_t e = op->dj_start[i] + op->dj_len[i];
+      for (int64_t s0 = op->dj_start[i]; s0 < e; s0 += CHUNK) {
+        cstart.push_back(std::min<int64_t>(s0 + CHUNK, e));
+        cagg.push_back(-1);
+      }
     }
   }
   op->nch = (int32_t)cagg.size();
@@ -1508,7 +1564,9 @@ extern "C" int sfcdd_op_setup(sfcdd_op* op, void* stream) {
         }
       std::sort(tmp.begin(), tmp.end());
       tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
-      SFCDD_REQUIRE((int)tmp.size() <= COMBINE_MAXC, SFCDD_EINTERNAL, "too many subdomains meet one chunk");
+      SFCDD_REQUIRE((int)tmp.size() <= COMBINE_MAXC, SFCDD_EVALUE,
+                    "more than " + std::to_string(COMBINE_MAXC) +
+                        " overlapped subdomains cover one disjoint range (overlap gamma too large)");
       qc.insert(qc.end(), tmp.begin(), tmp.end());
       qptr.push_back((int32_t)qc.size());
     }
@@ -1631,8 +1689,8 @@ extern "C" int sfcdd_op_apply(sfcdd_op* op, const double* g_dev, double* h_dev, 
   SFCDD_API_BEGIN
   SFCDD_REQUIRE(op && op->ready, SFCDD_EVALUE, "operator not set up");
   CUDA_CHECK(cudaSetDevice(op->device));
-  cudaStream_t st = (cudaStream_t)stream;  // NULL = legacy default stream
-  apply_device(op, g_dev, h_dev, st, false, false);
+  OpScope scope(op, (cudaStream_t)stream);  // NULL = legacy default stream
+  apply_device(op, g_dev, h_dev, scope.stream(), false, false);
   SFCDD_API_END
 }
 
@@ -1640,8 +1698,8 @@ extern "C" int sfcdd_op_matvec(sfcdd_op* op, const double* x_dev, double* y_dev,
   SFCDD_API_BEGIN
   SFCDD_REQUIRE(op, SFCDD_EVALUE, "null handle");
   CUDA_CHECK(cudaSetDevice(op->device));
-  cudaStream_t st = (cudaStream_t)stream;  // NULL = legacy default stream
-  launch_matvec(op, x_dev, y_dev, st);
+  OpScope scope(op, (cudaStream_t)stream);  // NULL = legacy default stream
+  launch_matvec(op, x_dev, y_dev, scope.stream());
   CUDA_CHECK(cudaGetLastError());
   SFCDD_API_END
 }
@@ -1662,13 +1720,17 @@ extern "C" int sfcdd_op_pcg_ex(sfcdd_op* op, const double* b_dev, double* x_dev,
   SFCDD_REQUIRE(tol_kind == 0 || tol_kind == 1, SFCDD_EVALUE, "unknown tolerance kind");
   SFCDD_REQUIRE(tol_kind == 0 || exact_dev, SFCDD_EVALUE, "energy stopping needs the exact solution");
   CUDA_CHECK(cudaSetDevice(op->device));
-  cudaStream_t st = (cudaStream_t)stream;  // NULL = legacy default stream
+  OpScope scope(op, (cudaStream_t)stream);  // NULL = legacy default stream
+  cudaStream_t st = scope.stream();
   if (op->hist_cap < max_iters + 1) {
     if (op->hist) CUDA_CHECK(cudaFree(op->hist));
     if (op->ehist) CUDA_CHECK(cudaFree(op->ehist));
     op->hist = (double*)dev_alloc(op, (size_t)(max_iters + 1) * 8);
     op->ehist = (double*)dev_alloc(op, (size_t)(max_iters + 1) * 8);
     op->hist_cap = max_iters + 1;
+    // the captured iteration graph holds the old history addresses
+    if (op->pcg_graph) CUDA_CHECK(cudaGraphExecDestroy(op->pcg_graph));
+    op->pcg_graph = nullptr;
   }
   const Stencil S = stencil_of(op);
   const Chunks C = chunks_of(op);
@@ -1989,6 +2051,8 @@ extern "C" void sfcdd_op_destroy(sfcdd_op* op) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   op->dag.reset();
+  if (op->ev_in) cudaEventDestroy(op->ev_in);
+  if (op->ev_out) cudaEventDestroy(op->ev_out);
   if (op->ev0) cudaEventDestroy(op->ev0);
   if (op->ev1) cudaEventDestroy(op->ev1);
   if (op->own_stream) cudaStreamDestroy(op->own_stream);

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <memory>
+#include <mutex>
 #include <vector>
 
 #include "common.h"
@@ -27,7 +28,7 @@ struct Stencil {
 // device-resident solver state (PCG scalars, reduction tickets, counters)
 struct DevState {
   double tol, hist0, rz, beta, pap, alpha;
-  int32_t k, converged, breakdown, exhausted, have_rz, max_iters, done, pad;
+  int32_t k, converged, breakdown, exhausted, have_rz, max_iters, done, stop_pending;
   uint32_t ticket[8];
   long long apply_calls;
   long long fault_index;
@@ -70,6 +71,7 @@ struct sfcdd_op {
   int32_t p = 0, q = 0, variant = 3, weighting = 1, threads = 0;
   int32_t shard_first = 0, shard_count = 0;  // shard mode (multi-GPU): owned subdomains
   int32_t curve = 0;                         // SFC: 0 Hilbert, 1 Lebesgue
+  int32_t raw = 0;                           // 1: unscaled A (grid.py:91-114), 0: Â = T A T
   int64_t own_g0 = 0, own_g1 = 0;            // owned SFC segment [own_g0, own_g1)
   std::vector<int64_t> xy_off_host;          // per subdomain slot in the xy buffer (-1 none)
   int32_t n0 = 0;
@@ -121,4 +123,24 @@ struct sfcdd_op {
   cudaGraphExec_t pcg_graph = nullptr;
   cudaStream_t pcg_graph_stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // re-entrancy (test_schwarz.py:208-222, linalg.py:7-8): every call that
+  // touches the handle's scratch runs on own_stream, entered and left through
+  // events on the caller's stream, with the host-side enqueue under `mu`; two
+  // threads applying one operator therefore serialize on the device
+  std::mutex mu;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
 };
+
+namespace sfcdd {
+class OpScope {
+ public:
+  OpScope(sfcdd_op* op, cudaStream_t caller);
+  ~OpScope() noexcept(false);
+  cudaStream_t stream() const { return op_->own_stream; }
+
+ private:
+  sfcdd_op* op_;
+  cudaStream_t caller_;
+  std::unique_lock<std::mutex> lk_;
+};
+}  // namespace sfcdd

@@ -3,6 +3,7 @@
 #include "plan.h"
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -136,6 +137,9 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
   std::vector<std::vector<int32_t>> upd_slot(factors.size());
   int64_t xy_off = 0;
 
+  double pt_[4] = {0, 0, 0, 0};
+  auto pt_t0 = std::chrono::steady_clock::now();
+  auto ptime = [&]() { auto t = std::chrono::steady_clock::now(); double d = std::chrono::duration<double>(t - pt_t0).count(); pt_t0 = t; return d; };
   // ---- 1. groups: greedy bottom-up clustering of small supernodes
   for (size_t fi = 0; fi < factors.size(); ++fi) {
     const HostFactor& F = *factors[fi];
@@ -247,6 +251,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
     if (groups[g].parent >= 0)
       groups[groups[g].parent].height = std::max(groups[groups[g].parent].height, groups[g].height + 1);
 
+  pt_[0] = ptime();
   // ---- 2. blobs + tasks (unordered)
   std::vector<TaskDev> tl;
   std::vector<double> tw;  // task weight (us, rough model used for the queue order)
@@ -783,6 +788,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
 
   SFCDD_REQUIRE(P.upd_doubles < (int64_t(1) << 31), SFCDD_EINTERNAL, "update buffer too large");
 
+  pt_[1] = ptime();
   // ---- 3. dependencies (counters: plan.h)
   auto FIN = [&](int32_t g) { return 1 + g; };
   auto BDONE = [&](int32_t g) { return 1 + G + g; };
@@ -831,6 +837,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
     }
   }
 
+  pt_[2] = ptime();
   // ---- 4. queue order: decreasing critical-path rank (HLFET) over the
   // combined forward/backward DAG -- a topological order (weights > 0)
   std::vector<double> wf(G, 0.0), wb(G, 0.0), wa(G, 0.0), wx(G, 0.0), rank_f(G, 0.0), rank_b(G, 0.0),
@@ -970,6 +977,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
                    wsum[5]);
     }
   }
+  pt_[3] = ptime();
   P.tasks.resize(tl.size());
   for (size_t t = 0; t < order.size(); ++t) P.tasks[t] = tl[order[t]];
 
@@ -1114,6 +1122,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
                  (double)lev_sum / std::max(1, P.nfrag), (double)small_vals / std::max(1, P.nfrag), maxh,
                  P.blobs.size() / 1e6, P.max_scratch, P.sim_us, P.workers, P.crit_us);
   }
+  if (std::getenv("SFCDD_PLAN_DEBUG")) std::fprintf(stderr, "[plan] phase seconds: groups %.2f blobs %.2f deps %.2f queue %.2f\n", pt_[0], pt_[1], pt_[2], pt_[3]);
   return P;
 }
 

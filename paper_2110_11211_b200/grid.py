@@ -103,7 +103,7 @@ def scatter_to_lex(levels, values_sfc: np.ndarray, curve: str = "hilbert") -> np
 class _GridHandle:
     """Device neighbour table + stencil constants for one level vector."""
 
-    def __init__(self, levels, curve: str = "hilbert"):
+    def __init__(self, levels, curve: str = "hilbert", raw: bool = False):
         from .partition import disjoint_partition
 
         self.levels = levels
@@ -127,6 +127,7 @@ class _GridHandle:
         desc.omega = om.ctypes.data
         desc.host_threads = 1
         desc.curve = _lib.CURVES[curve]
+        desc.raw_laplacian = 1 if raw else 0
         h = ctypes.c_void_p()
         _lib.check(_lib.lib().sfcdd_op_create(ctypes.byref(desc), ctypes.byref(h)))
         self.handle = h
@@ -155,8 +156,8 @@ class _GridHandle:
 
 
 @lru_cache(maxsize=16)
-def _grid_handle(levels, curve: str = "hilbert") -> _GridHandle:
-    return _GridHandle(levels, curve)
+def _grid_handle(levels, curve: str = "hilbert", raw: bool = False) -> _GridHandle:
+    return _GridHandle(levels, curve, raw)
 
 
 class GridLaplacian:
@@ -185,15 +186,16 @@ class GridLaplacian:
 
     @property
     def handle(self) -> _GridHandle:
-        return _grid_handle(self.levels, self.curve)
+        """Device stencil of this matrix: Â's constants, or A's exact integer
+        entries 2 sum 4^l / -4^l_j when unscaled (grid.py:101-110)."""
+        return _grid_handle(self.levels, self.curve, not self.scaled)
 
     @property
     def scale(self) -> float:
         return float(self._t)
 
     def diagonal(self) -> np.ndarray:
-        v = self.handle.dhat if self.scaled else self._diag_raw
-        return np.full(self.n, v)
+        return np.full(self.n, self.handle.dhat)
 
     def __matmul__(self, x):
         import torch
@@ -203,8 +205,6 @@ class GridLaplacian:
         if x_arr.shape[0] != self.n:
             raise ValueError(f"dimension mismatch: {self.shape} @ {tuple(x_arr.shape)}")
         y = self.handle.matvec(x_arr)
-        if not self.scaled:
-            y = y / (self._t * self._t)
         return y.cpu().numpy() if is_np else y
 
     def tocsr(self):
@@ -219,10 +219,9 @@ class GridLaplacian:
         coords = np.stack(np.unravel_index(perm, shape), axis=1)  # by SFC rank
         strides = [int(np.prod(shape[j + 1:])) for j in range(len(shape))]
         h = self.handle
-        dval = h.dhat if self.scaled else self._diag_raw
-        rows, cols, vals = [np.arange(n)], [np.arange(n)], [np.full(n, dval)]
+        rows, cols, vals = [np.arange(n)], [np.arange(n)], [np.full(n, h.dhat)]
         for j in range(len(shape)):
-            oval = h.off[j] if self.scaled else -float(4 ** self.levels[j])
+            oval = h.off[j]
             for step in (-1, 1):
                 ok = (coords[:, j] + step >= 0) & (coords[:, j] + step < shape[j])
                 s = np.nonzero(ok)[0]

@@ -122,13 +122,41 @@ def pcg_device(op, b, x0=None, tol: float = 1e-8, max_iters: int = 20000, exact=
     return x, k, bool(conv.value), hist[:k + 1].tolist(), ehist[:k + 1].tolist()
 
 
-def _check_device_operands(A, precond):
+def _matvec_fn(A):
+    """v -> A v on CUDA tensors: the device stencil for grid Laplacians, the
+    device CSR product for scipy / numpy matrices (linalg.DeviceMatrix)."""
+    from .linalg import DeviceMatrix
+
+    if isinstance(A, (GridLaplacian, DeviceMatrix)):
+        return lambda v: A @ v
+    if hasattr(A, "tocsr") or isinstance(A, np.ndarray):
+        D = DeviceMatrix(A)
+        return lambda v: D @ v
+    # any other object with @ (the reference's duck typing): host product
+    return lambda v: _to_device(np.asarray(A @ v.cpu().numpy(), dtype=np.float64))
+
+
+def _apply_fn(precond, vec):
+    """v -> C^-1 v on CUDA tensors (identity for precond=None, krylov.py:265)."""
     from .schwarz import SchwarzOperator
 
-    if not isinstance(A, GridLaplacian) or not A.scaled:
-        raise NotImplementedError("the device solvers need the scaled grid Laplacian")
-    if precond is not None and not isinstance(precond, SchwarzOperator):
-        raise NotImplementedError("the device solvers need a device SchwarzOperator (or None)")
+    if precond is None:
+        return vec.copy
+    if isinstance(precond, SchwarzOperator):
+        return precond.apply_device
+    # a caller's own preconditioner object (e.g. a dense-inverse oracle)
+    return lambda v: _to_device(np.asarray(precond.apply(v.cpu().numpy()), dtype=np.float64))
+
+
+def _graph_pcg_ok(A, precond) -> bool:
+    """The fully device-resident PCG (csrc/op.cu) runs the operator's own
+    stencil: A must be the grid Laplacian the operator was set up on."""
+    from .schwarz import SchwarzOperator
+
+    if not isinstance(precond, SchwarzOperator) or not isinstance(A, GridLaplacian):
+        return False
+    B = precond.A
+    return (A.levels, A.scaled, A.curve) == (B.levels, B.scaled, B.curve)
 
 
 def _to_device(v):
@@ -174,14 +202,14 @@ class _DeviceTracker:
     """krylov.py:171-213 on device vectors: ||r||, and with an exact solution
     the energy error sqrt(max(e.(b - r - A x*), 0)), e = x - x*."""
 
-    def __init__(self, A, b, cfg: SolverConfig, exact, vec: _Vec):
+    def __init__(self, matvec, b, cfg: SolverConfig, exact, vec: _Vec):
         if cfg.tolerance_kind == "energy_error_reduction" and exact is None:
             raise ValueError("energy stopping needs the exact solution")
         self.vec = vec
         self.b = b
         self.cfg = cfg
         self.exact = exact
-        self.a_exact = A @ exact if exact is not None else None
+        self.a_exact = matvec(exact) if exact is not None else None
         self.energy_history: list[float] = []
         self.residual_history: list[float] = []
         self._baseline = None
@@ -221,16 +249,14 @@ def pcg(A, b, precond, cfg: SolverConfig, x0, exact=None) -> SolveReport:
     Runs entirely on the device (csrc/op.cu, CUDA-graph iteration) with the
     reference tracker: residual history always, energy-error history when
     ``exact`` is given, stopping on ``cfg.tolerance_kind``."""
-    from .schwarz import SchwarzOperator
-
     t0 = time.perf_counter()
     if (precond is not None and not getattr(precond, "symmetric", True)
             and not cfg.force_unsymmetric):
         raise ValueError("preconditioner is not symmetric; use fcg or force_unsymmetric")
     if cfg.tolerance_kind == "energy_error_reduction" and exact is None:
         raise ValueError("energy stopping needs the exact solution")
-    if not isinstance(precond, SchwarzOperator) or not isinstance(A, GridLaplacian) or not A.scaled:
-        raise NotImplementedError("device PCG needs the scaled grid Laplacian and a device SchwarzOperator")
+    if not _graph_pcg_ok(A, precond):
+        return _pcg_composed(A, b, precond, cfg, x0, exact, t0)
     to_numpy = isinstance(b, np.ndarray)
     out = pcg_device(precond, _to_device(b), _to_device(x0), cfg.tolerance, cfg.max_iters,
                      exact=None if exact is None else _to_device(exact), tolerance_kind=cfg.tolerance_kind)
@@ -239,6 +265,46 @@ def pcg(A, b, precond, cfg: SolverConfig, x0, exact=None) -> SolveReport:
     rep.solution = x.cpu().numpy() if to_numpy else x
     rep.wall_time = time.perf_counter() - t0
     return rep
+
+
+def _pcg_composed(A, b, precond, cfg: SolverConfig, x0, exact, t0) -> SolveReport:
+    """PCG for any matrix / preconditioner pair (krylov.py:257-291): the
+    products run on the device (stencil, CSR product, Schwarz apply or the
+    identity for precond=None) and the vector algebra through the
+    deterministic BLAS-1 kernels; the control flow is the reference's."""
+    n = b.shape[0]
+    vec = _Vec(n)
+    mv = _matvec_fn(A)
+    apply_c = _apply_fn(precond, vec)
+    to_numpy = isinstance(b, np.ndarray)
+    bd = _to_device(b)
+    tracker = _DeviceTracker(mv, bd, cfg, None if exact is None else _to_device(exact), vec)
+    x = vec.copy(_to_device(x0))
+    r = vec.axpby(1.0, bd, -1.0, mv(x))
+    report = SolveReport("pcg", 0, False, [], [])
+    if tracker.record(x, r):
+        report.converged = True
+        return _finish(report, t0, x, tracker, to_numpy)
+    z = apply_c(r)
+    p = vec.copy(z)
+    rz = vec.dot(r, z)
+    for k in range(1, cfg.max_iters + 1):
+        Ap = mv(p)
+        pAp = vec.dot(p, Ap)
+        if pAp <= 0.0:
+            raise BreakdownError(f"nonpositive curvature at iteration {k}")
+        alpha = rz / pAp
+        vec.axpby(alpha, p, 1.0, x)
+        vec.axpby(-alpha, Ap, 1.0, r)
+        report.iterations = k
+        if tracker.record(x, r):
+            report.converged = True
+            break
+        z = apply_c(r)
+        rz_new = vec.dot(r, z)
+        p = vec.axpby(1.0, z, rz_new / rz, p)
+        rz = rz_new
+    return _finish(report, t0, x, tracker, to_numpy)
 
 
 def estimate_extremal_eigs(apply_ca, n: int, *, iters: int | None = None, seed: int = 0, a_matvec=None,
@@ -310,26 +376,26 @@ def richardson(A, b, precond, cfg: SolverConfig, x0, exact=None) -> SolveReport:
     ``damping="optimal"``: xi = 2/(lambda_min + lambda_max) of C^-1 A from
     estimate_extremal_eigs.  Every product runs on the device."""
     t0 = time.perf_counter()
-    _check_device_operands(A, precond)
     n = b.shape[0]
     vec = _Vec(n)
-    apply_c = precond.apply_device if precond is not None else vec.copy
+    mv = _matvec_fn(A)
+    apply_c = _apply_fn(precond, vec)
     lam = (None, None)
     if cfg.damping == "optimal":
         if precond is not None and not getattr(precond, "symmetric", True):
             raise ValueError("optimal damping requires a symmetric preconditioner")
-        lam = estimate_extremal_eigs(lambda v: apply_c(A @ v), n, iters=cfg.eig_iters, seed=cfg.seed,
-                                     a_matvec=lambda v: A @ v)
+        lam = estimate_extremal_eigs(lambda v: apply_c(mv(v)), n, iters=cfg.eig_iters, seed=cfg.seed,
+                                     a_matvec=mv)
         xi = 2.0 / (lam[0] + lam[1])
     else:
         xi = float(cfg.damping)
     to_numpy = isinstance(b, np.ndarray)
     bd = _to_device(b)
-    tracker = _DeviceTracker(A, bd, cfg, None if exact is None else _to_device(exact), vec)
+    tracker = _DeviceTracker(mv, bd, cfg, None if exact is None else _to_device(exact), vec)
     x = vec.copy(_to_device(x0))
     report = SolveReport("richardson", 0, False, [], [], lambda_min=lam[0], lambda_max=lam[1], damping=xi)
     for k in range(cfg.max_iters + 1):
-        r = vec.axpby(1.0, bd, -1.0, A @ x)  # b - A x
+        r = vec.axpby(1.0, bd, -1.0, mv(x))  # b - A x
         if tracker.record(x, r):
             report.iterations, report.converged = k, True
             break
@@ -347,15 +413,15 @@ def fcg(A, b, precond, cfg: SolverConfig, x0, exact=None) -> SolveReport:
     against the stored ones (the last ``cfg.fcg_window``, or all), so
     non-symmetric preconditioners (e.g. the deflated variant) are admissible."""
     t0 = time.perf_counter()
-    _check_device_operands(A, precond)
     n = b.shape[0]
     vec = _Vec(n)
-    apply_c = precond.apply_device if precond is not None else vec.copy
+    mv = _matvec_fn(A)
+    apply_c = _apply_fn(precond, vec)
     to_numpy = isinstance(b, np.ndarray)
     bd = _to_device(b)
-    tracker = _DeviceTracker(A, bd, cfg, None if exact is None else _to_device(exact), vec)
+    tracker = _DeviceTracker(mv, bd, cfg, None if exact is None else _to_device(exact), vec)
     x = vec.copy(_to_device(x0))
-    r = vec.axpby(1.0, bd, -1.0, A @ x)
+    r = vec.axpby(1.0, bd, -1.0, mv(x))
     report = SolveReport("fcg", 0, False, [], [])
     if tracker.record(x, r):
         report.converged = True
@@ -365,7 +431,7 @@ def fcg(A, b, precond, cfg: SolverConfig, x0, exact=None) -> SolveReport:
         p = vec.copy(apply_c(r))
         for pj, Apj, pApj in directions:
             vec.axpby(-(vec.dot(p, Apj) / pApj), pj, 1.0, p)
-        Ap = A @ p
+        Ap = mv(p)
         pAp = vec.dot(p, Ap)
         if pAp <= 0.0:
             raise BreakdownError(f"nonpositive curvature at iteration {k}")

@@ -82,6 +82,44 @@ class Factorization:
         return x.cpu().numpy() if is_np else x
 
 
+class DeviceMatrix:
+    """A general sparse matrix held on the device (C ABI ``sfcdd_csr_*``):
+    the ``A @ v`` of the solvers when A is not a grid Laplacian
+    (krylov.py:257-291 is duck-typed over it; test_krylov.py:154-166).
+    ``@`` maps CUDA tensors to CUDA tensors and numpy to numpy; the product
+    is summed in scipy's csr_matvec order, so it matches scipy bit for bit."""
+
+    def __init__(self, A):
+        B = as_csr(A.tocsr() if hasattr(A, "tocsr") else A)
+        self.shape = B.shape
+        self.n = B.shape[0]
+        self.dtype = np.float64
+        self._keep = (np.ascontiguousarray(B.indptr, np.int64), np.ascontiguousarray(B.indices, np.int32),
+                      np.ascontiguousarray(B.data, np.float64))
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib().sfcdd_csr_create(B.shape[0], B.shape[1], *(a.ctypes.data for a in self._keep),
+                                               _lib.device().index, ctypes.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        try:
+            _lib.lib().sfcdd_csr_destroy(self._h)
+        except Exception:
+            pass
+
+    def __matmul__(self, x):
+        import torch
+
+        is_np = isinstance(x, np.ndarray) or not hasattr(x, "data_ptr")
+        xt = (torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)) if is_np else x).to(
+            _lib.device(), torch.float64).contiguous()
+        if xt.shape[0] != self.shape[1]:
+            raise ValueError(f"dimension mismatch: {self.shape} @ {tuple(xt.shape)}")
+        y = torch.empty(self.shape[0], dtype=torch.float64, device=xt.device)
+        _lib.check(_lib.lib().sfcdd_csr_matvec(self._h, xt.data_ptr(), y.data_ptr(), _lib.stream_ptr()))
+        return y.cpu().numpy() if is_np else y
+
+
 def factorize(A) -> Factorization:
     return Factorization(A)
 

@@ -19,7 +19,7 @@ import numpy as np
 from . import _lib
 from .coarse import CoarseSpace
 from .grid import GridLaplacian
-from .partition import Partition, compute_weights, is_half_integer
+from .partition import Partition, build_partition, compute_weights, gamma_fraction, is_half_integer
 
 VARIANTS = ("one_level", "additive_two_level", "deflated", "balanced")
 WEIGHTINGS = ("none", "omega", "d_matrix")
@@ -44,9 +44,9 @@ class SchwarzOperator:
 
     def __init__(self, A, part: Partition, coarse: CoarseSpace | None, config: SchwarzConfig,
                  workers: int = 1):
-        if not isinstance(A, GridLaplacian) or not A.scaled:
-            raise ValueError("the device Schwarz operator needs the scaled grid Laplacian "
-                             "(grid.symmetrize_diag(grid.assemble_laplacian(levels), b)[0])")
+        if not isinstance(A, GridLaplacian):
+            raise ValueError("the device Schwarz operator needs a grid Laplacian "
+                             "(grid.assemble_laplacian(levels), optionally through grid.symmetrize_diag)")
         self.A = A
         self.partition = part
         self.coarse = coarse
@@ -62,12 +62,21 @@ class SchwarzOperator:
         if config.variant != "one_level" and coarse is None:
             raise ValueError(f"variant {config.variant!r} needs a coarse space")
         q = coarse.q if (coarse is not None and config.variant != "one_level") else 0
-        ov_start = np.array([r.start for r in part.overlapped], np.int64)
-        ov_len = np.array([r.length for r in part.overlapped], np.int64)
-        dj_start = np.array([r.start for r in part.disjoint], np.int64)
-        dj_len = np.array([r.length for r in part.disjoint], np.int64)
-        omega = np.ascontiguousarray(self.weights.omega, dtype=np.float64)
         desc = _lib.OpDesc()
+        # the library partitions N by gamma itself (csrc/partition.cpp); explicit
+        # ranges are passed only for a partition that build_partition would not give
+        num, den = gamma_fraction(part.gamma)
+        desc.gamma_num, desc.gamma_den = num, den
+        keep = []
+        if part != build_partition(part.n, part.p, part.gamma):
+            arrs = [np.array([r.start for r in part.overlapped], np.int64),
+                    np.array([r.length for r in part.overlapped], np.int64),
+                    np.array([r.start for r in part.disjoint], np.int64),
+                    np.array([r.length for r in part.disjoint], np.int64),
+                    np.ascontiguousarray(self.weights.omega, dtype=np.float64)]
+            keep.extend(arrs)
+            desc.ov_start, desc.ov_len, desc.dj_start, desc.dj_len, desc.omega = (a.ctypes.data for a in arrs)
+        desc.raw_laplacian = 0 if A.scaled else 1
         desc.dim = len(A.levels)
         for j, l in enumerate(A.levels):
             desc.levels[j] = l
@@ -77,9 +86,6 @@ class SchwarzOperator:
         desc.weighting = _lib.WEIGHTING_CODES[config.weighting]
         desc.device = _lib.device().index
         desc.curve = _lib.CURVES[getattr(A, "curve", "hilbert")]
-        desc.ov_start, desc.ov_len = ov_start.ctypes.data, ov_len.ctypes.data
-        desc.dj_start, desc.dj_len = dj_start.ctypes.data, dj_len.ctypes.data
-        desc.omega = omega.ctypes.data
         desc.host_threads = _lib.host_threads()
         h = ctypes.c_void_p()
         _lib.check(_lib.lib().sfcdd_op_create(ctypes.byref(desc), ctypes.byref(h)))

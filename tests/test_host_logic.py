@@ -210,3 +210,31 @@ def test_aggregate_sizes():
     assert aggregate_sizes(12, 3) == [4, 4, 4]
     assert aggregate_sizes(11, 3) == [4, 4, 3]
     assert aggregate_sizes(5, 5) == [1, 1, 1, 1, 1]
+
+
+def test_library_partition_matches_oracle_property(oracle):
+    """csrc/partition.cpp (ranges from N, P, gamma num/den; prefix-sum window
+    sums) against the oracle's restatement of partition.py:64-157 over a
+    sweep of sizes, counts and fractional overlaps, including 2 gamma + 1 = P
+    and gammas with large denominators."""
+    rng = np.random.default_rng(7)
+    gammas = [0.0, 0.1, 0.2, 0.25, 0.3, 1 / 3, 0.5, 0.75, 1.0, 1.25, 1.5, 2.0, 2.5, 0.123457, 3.75]
+    for _ in range(300):
+        p = int(rng.integers(2, 40))
+        n = int(rng.integers(p, 5000))
+        g = gammas[int(rng.integers(len(gammas)))]
+        if 2 * g + 1 > p:
+            with pytest.raises(ValueError):
+                pt.build_partition(n, p, g)
+            continue
+        part = pt.build_partition(n, p, g)
+        dj = oracle.disjoint_partition(n, p)
+        ov = oracle.enlarge(dj, g)
+        assert [(r.start, r.length) for r in part.disjoint] == [(r.start, r.length) for r in dj]
+        assert [(r.start, r.length) for r in part.overlapped] == [(r.start, r.length) for r in ov]
+        counts, diags, omega = oracle.weights(ov, n)
+        w = pt.compute_weights(part)
+        np.testing.assert_array_equal(w.counts, counts)
+        np.testing.assert_array_equal(w.omega, omega)
+        for a, b in zip(w.diagonals, diags):
+            np.testing.assert_array_equal(a, b)
