@@ -270,6 +270,12 @@ int sfcdd_host_plan_solve(int64_t n, const int64_t* indptr, const int32_t* indic
                           const int64_t* len, const double* rhs, double* xy,
                           int32_t blob_max, int32_t scratch_max, int64_t* nfrag);
 
+/* The deferred-value plan (metadata segments + value descriptors, used when
+ * the factor values are produced on the device) rebuilds byte for byte the
+ * blob image of the plan built from host values; *mismatch = differing bytes. */
+int sfcdd_host_plan_deferred_check(int64_t n, const int64_t* indptr, const int32_t* indices,
+                                   const double* data, int32_t p, const int64_t* start, const int64_t* len,
+                                   int64_t* mismatch, int64_t* nseg, int64_t* nvd);
 /* Diagnostics: wall seconds of the setup phases for one SPD block
  * (times[3]: ordering + symbolic, host numeric factorization, plan build)
  * and sizes[6]: nnz(L), stored, supernodes, update-matrix doubles, largest

@@ -106,7 +106,7 @@ EXPORTS = [
     "sfcdd_factor_create", "sfcdd_factor_solve", "sfcdd_factor_info", "sfcdd_factor_destroy",
     "sfcdd_host_amd", "sfcdd_host_factor_solve", "sfcdd_host_plan_solve",
     "sfcdd_partition", "sfcdd_partition_weights", "sfcdd_csr_create", "sfcdd_csr_matvec", "sfcdd_csr_destroy",
-    "sfcdd_host_setup_timing",
+    "sfcdd_host_setup_timing", "sfcdd_host_plan_deferred_check",
 ]
 
 _lib = None
@@ -171,6 +171,7 @@ def lib() -> ctypes.CDLL:
         "sfcdd_csr_create": [i64, i64, vp, vp, vp, i32, ctypes.POINTER(vp)],
         "sfcdd_csr_matvec": [vp, vp, vp, vp],
         "sfcdd_host_setup_timing": [i64, vp, vp, vp, i32, vp, vp],
+        "sfcdd_host_plan_deferred_check": [i64, vp, vp, vp, i32, vp, vp, vp, vp, vp],
     }
     for name, args in sigs.items():
         fn = getattr(L, name)

@@ -64,6 +64,59 @@ class CoarseSpace:
         return self._matrix
 
 
+    @property
+    def factorization(self):
+        """Device direct solver of A0 (linalg.Factorization, coarse.py:59-60)."""
+        if getattr(self, "_fact", None) is None:
+            from .linalg import Factorization
+
+            self._fact = Factorization(self.matrix)
+        return self._fact
+
+
+class DeflationOperators:
+    """F = R0^T A0^-1 R0, G = I - A F, G^T = I - F A (coarse.py:63-84) on the
+    device: R0 / R0^T as device CSR products, A0^-1 by the device direct
+    solver, A by its device matvec; numpy or CUDA tensors in and out."""
+
+    def __init__(self, cs: CoarseSpace, A):
+        if A.shape[1] != cs.restriction.shape[1]:
+            raise ValueError("coarse space size does not match matrix")
+        from .krylov import _matvec_fn
+        from .linalg import DeviceMatrix
+
+        self._cs = cs
+        R = cs.restriction
+        self._R = DeviceMatrix(R)
+        self._Rt = DeviceMatrix(R.T.tocsr())
+        self._A = _matvec_fn(A)
+
+    @staticmethod
+    def _io(fn, v):
+        from .krylov import _to_device
+
+        is_np = isinstance(v, np.ndarray) or not hasattr(v, "data_ptr")
+        out = fn(_to_device(v))
+        return out.cpu().numpy() if is_np else out
+
+    def _F(self, v):
+        return self._Rt @ self._cs.factorization.solve(self._R @ v)
+
+    def coarse_correction(self, v):
+        return self._io(self._F, v)
+
+    def project(self, v):
+        return self._io(lambda x: x - self._A(self._F(x)), v)
+
+    def project_transpose(self, v):
+        return self._io(lambda x: x - self._F(self._A(x)), v)
+
+
+def deflation_ops(cs: CoarseSpace, A) -> DeflationOperators:
+    """coarse.py:87-88."""
+    return DeflationOperators(cs, A)
+
+
 def build_coarse(part: Partition, A, q: int) -> CoarseSpace:
     """Validate and describe the coarse space (coarse.py:38-60)."""
     if not 1 <= q <= part.n // part.p:

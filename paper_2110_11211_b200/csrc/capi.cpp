@@ -148,3 +148,49 @@ extern "C" int sfcdd_host_setup_timing(int64_t n, const int64_t* indptr, const i
   sizes[5] = fl;
   SFCDD_API_END
 }
+
+// Test hook (host only): the deferred-value plan (metadata segments + value
+// descriptors, the path of device-side factor values) rebuilds exactly the
+// blob image of the plan built with host values.  *mismatch = number of
+// differing bytes (0 expected); *nseg / *nvd = segment / descriptor counts.
+extern "C" int sfcdd_host_plan_deferred_check(int64_t n, const int64_t* indptr, const int32_t* indices,
+                                              const double* data, int32_t p, const int64_t* start,
+                                              const int64_t* len, int64_t* mismatch, int64_t* nseg,
+                                              int64_t* nvd) {
+  SFCDD_API_BEGIN
+  CsrMatrix A = csr_from(n, indptr, indices, data);
+  std::vector<HostFactor> fs(p), sym(p);
+  FactorOptions fo;
+  for (int32_t i = 0; i < p; ++i) {
+    CsrMatrix B = extract_block(A, start[i], len[i]);
+    fs[i] = factorize_host(B, fo);
+    sym[i] = analyze_host(B, fo);
+  }
+  std::vector<const HostFactor*> pv, ps;
+  std::vector<int64_t> gs, gm;
+  for (int32_t i = 0; i < p; ++i) {
+    pv.push_back(&fs[i]);
+    ps.push_back(&sym[i]);
+    gs.push_back(start[i]);
+    gm.push_back(n);
+  }
+  PlanOptions po;
+  choose_blob_shape(pv, po);
+  DevicePlan full = build_plan(pv, gs, gm, po);
+  po.defer_values = true;
+  DevicePlan def = build_plan(ps, gs, gm, po);
+  SFCDD_REQUIRE(def.blob_bytes == full.blob_bytes, SFCDD_EINTERNAL, "deferred plan size differs");
+  std::vector<uint8_t> img((size_t)def.blob_bytes, 0);
+  for (const MetaSeg& s : def.segs) std::memcpy(img.data() + s.dev_off, def.blobs.data() + s.host_off, s.bytes);
+  for (const ValDesc& d : def.vdesc) place_values(d, fs[d.factor].val.data() + d.src, img.data());
+  int64_t bad = 0;
+  for (int64_t i = 0; i < def.blob_bytes; ++i) bad += img[i] != full.blobs[i];
+  *mismatch = bad;
+  *nseg = (int64_t)def.segs.size();
+  *nvd = (int64_t)def.vdesc.size();
+  SFCDD_REQUIRE(def.tasks.size() == full.tasks.size(), SFCDD_EINTERNAL, "task count differs");
+  for (size_t t = 0; t < def.tasks.size(); ++t)
+    SFCDD_REQUIRE(std::memcmp(&def.tasks[t], &full.tasks[t], sizeof(TaskDev)) == 0, SFCDD_EINTERNAL,
+                  "task lists differ");
+  SFCDD_API_END
+}

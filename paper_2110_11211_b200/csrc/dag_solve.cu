@@ -854,7 +854,63 @@ __global__ void __launch_bounds__((WPB + 1) * 32, 20 / WPB) k_dag(DagArgs A) {
 
 inline int32_t round128(int64_t x) { return (int32_t)((x + 127) / 128 * 128); }
 
+// deferred-value plans: metadata segments (16-byte multiples) -> blob buffer
+__global__ void k_meta_scatter(const MetaSeg* __restrict__ segs, int64_t nseg, const uint8_t* __restrict__ img,
+                               uint8_t* __restrict__ blobs) {
+  for (int64_t sg = blockIdx.x; sg < nseg; sg += gridDim.x) {
+    const MetaSeg S = segs[sg];
+    const int4* src = reinterpret_cast<const int4*>(img + S.host_off);
+    int4* dst = reinterpret_cast<int4*>(blobs + S.dev_off);
+    for (int64_t i = threadIdx.x; i < S.bytes / 16; i += blockDim.x) dst[i] = src[i];
+  }
+}
+
+// value placement (plan.h ValDesc, host twin place_values in plan.cpp): one
+// warp per descriptor; src = the factor's packed values (HostFactor::val layout)
+__global__ void k_place_values(const ValDesc* __restrict__ vd, int64_t nvd, const double* __restrict__ vals,
+                               const int64_t* __restrict__ fbase, int32_t f0, uint8_t* __restrict__ blobs) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t q = w0; q < nvd; q += nw) {
+    const ValDesc d = vd[q];
+    const double* M = vals + fbase[d.factor - f0] + d.src;
+    double* out = reinterpret_cast<double*>(blobs + d.dst);
+    if (d.kind == VD_COPY) {
+      for (int32_t i = lane; i < d.len; i += 32) out[i] = M[i];
+    } else if (d.kind == VD_ROW) {
+      for (int32_t k = 0; k < d.len; ++k) {
+        const double* col = M + packed_col_off(d.s, d.m, k);
+        for (int32_t i = max(0, k - d.p0) + lane; i < d.w; i += 32) out[(int64_t)k * d.w + i] = col[d.p0 + i - k];
+      }
+    } else {
+      for (int32_t j = 0; j < d.w; ++j) {
+        const double* col = M + packed_col_off(d.s, d.m, d.p0 + j);
+        for (int32_t r = j + lane; r < d.len; r += 32) out[(int64_t)r * d.w + j] = col[r - j];
+      }
+    }
+  }
+}
+
 }  // namespace
+
+void DagSolver::place_values(int32_t f0, int32_t f1, const double* vals_dev, const int64_t* fbase_host,
+                             cudaStream_t st) {
+  SFCDD_REQUIRE(f0 >= 0 && f1 <= (int32_t)vd_ptr_.size() - 1 && f0 <= f1, SFCDD_EINTERNAL, "factor range");
+  const int64_t q0 = vd_ptr_[f0], q1 = vd_ptr_[f1];
+  if (q1 == q0) return;
+  ValDesc* dvd = nullptr;
+  int64_t* dfb = nullptr;
+  CUDA_CHECK(cudaMallocAsync(&dvd, (q1 - q0) * sizeof(ValDesc), st));
+  CUDA_CHECK(cudaMallocAsync(&dfb, (f1 - f0) * sizeof(int64_t), st));
+  CUDA_CHECK(cudaMemcpyAsync(dvd, vdesc_.data() + q0, (q1 - q0) * sizeof(ValDesc), cudaMemcpyHostToDevice, st));
+  CUDA_CHECK(cudaMemcpyAsync(dfb, fbase_host, (f1 - f0) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  const int64_t blocks = std::min<int64_t>((q1 - q0 + 7) / 8, 148 * 16);
+  k_place_values<<<(unsigned)blocks, 256, 0, st>>>(dvd, q1 - q0, vals_dev, dfb, f0, blobs_);
+  CUDA_CHECK(cudaGetLastError());
+  CUDA_CHECK(cudaFreeAsync(dvd, st));
+  CUDA_CHECK(cudaFreeAsync(dfb, st));
+}
 
 DagSolver::DagSolver(const DevicePlan& plan, int device, int64_t extra_xy) : device_(device) {
   CUDA_CHECK(cudaSetDevice(device));
@@ -883,7 +939,37 @@ DagSolver::DagSolver(const DevicePlan& plan, int device, int64_t extra_xy) : dev
     if (bytes) CUDA_CHECK(cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice));
     bytes_ += std::max<size_t>(bytes, 16);
   };
-  up((void**)&blobs_, plan.blobs.data(), plan.blobs.size());
+  if (!plan.deferred) {
+    SFCDD_REQUIRE((int64_t)plan.blobs.size() == plan.blob_bytes, SFCDD_EINTERNAL, "blob image size");
+    up((void**)&blobs_, plan.blobs.data(), plan.blobs.size());
+  } else {
+    // metadata now (staged image + segment scatter), values later (place_values)
+    CUDA_CHECK(cudaMalloc(&blobs_, std::max<int64_t>(plan.blob_bytes, 16)));
+    bytes_ += std::max<int64_t>(plan.blob_bytes, 16);
+    CUDA_CHECK(cudaMemset(blobs_, 0, std::max<int64_t>(plan.blob_bytes, 16)));
+    uint8_t* img = nullptr;
+    MetaSeg* sg = nullptr;
+    CUDA_CHECK(cudaMalloc(&img, std::max<size_t>(plan.blobs.size(), 16)));
+    CUDA_CHECK(cudaMalloc(&sg, std::max<size_t>(plan.segs.size() * sizeof(MetaSeg), 16)));
+    CUDA_CHECK(cudaMemcpy(img, plan.blobs.data(), plan.blobs.size(), cudaMemcpyHostToDevice));
+    CUDA_CHECK(cudaMemcpy(sg, plan.segs.data(), plan.segs.size() * sizeof(MetaSeg), cudaMemcpyHostToDevice));
+    if (!plan.segs.empty()) {
+      k_meta_scatter<<<(unsigned)std::min<size_t>(plan.segs.size(), 148 * 64), 128>>>(
+          sg, (int64_t)plan.segs.size(), img, blobs_);
+      CUDA_CHECK(cudaGetLastError());
+    }
+    CUDA_CHECK(cudaDeviceSynchronize());
+    CUDA_CHECK(cudaFree(img));
+    CUDA_CHECK(cudaFree(sg));
+  }
+  // value descriptors grouped by factor (deferred plans: filled by place_values)
+  if (plan.deferred) vdesc_ = plan.vdesc;
+  vd_ptr_.assign(plan.factors.size() + 1, 0);
+  {
+    std::vector<int64_t> cnt(plan.factors.size() + 1, 0);
+    for (const ValDesc& d : plan.vdesc) cnt[d.factor + 1]++;
+    for (size_t f = 0; f < plan.factors.size(); ++f) vd_ptr_[f + 1] = vd_ptr_[f] + cnt[f + 1];
+  }
   up((void**)&tasks_, plan.tasks.data(), plan.tasks.size() * sizeof(TaskDev));
   up((void**)&factors_, plan.factors.data(), plan.factors.size() * sizeof(FactorDev));
   CUDA_CHECK(cudaMalloc(&upd_, std::max<int64_t>(plan.upd_doubles, 2) * 8));

@@ -28,6 +28,9 @@ class DagSolver {
   // diagnostics: per-task timestamps {sm, top, deps ok, data ok, end} (5 x u64 per task)
   void set_trace(unsigned long long* dev_buf);
   int32_t ntask() const { return ntask_; }
+  // deferred-value plans: place the packed values of factors [f0, f1) into
+  // the blobs; vals_dev + fbase_host[f - f0] = factor f's HostFactor::val
+  void place_values(int32_t f0, int32_t f1, const double* vals_dev, const int64_t* fbase_host, cudaStream_t st);
 
  private:
   int device_;
@@ -45,6 +48,8 @@ class DagSolver {
   int32_t* qhead_ = nullptr;
   int32_t nq_ = 16;
   unsigned long long* trace_ = nullptr;
+  std::vector<ValDesc> vdesc_;   // deferred plans only
+  std::vector<int64_t> vd_ptr_;  // descriptor range per factor
 
  public:
   std::vector<TaskDev> host_tasks;

@@ -1209,6 +1209,61 @@ static void pcg_iteration(sfcdd_op* op, double* x, const double* pold, double* p
   apply_device(op, op->r, op->z, st, true, true);
 }
 
+// Numeric factorization of the local blocks with their values placed into
+// the deferred-value DAG plan.  Host path: multifrontal Cholesky per block on
+// host threads, each block's packed values streamed to the device and placed
+// by the plan's value descriptors as soon as it is done (host memory holds a
+// few blocks' values at a time).
+template <class BlockFn>
+void numeric_factor_blocks_host(sfcdd_op* op, std::vector<HostFactor>& fs, int32_t sf, BlockFn&& local_block) {
+  const int64_t nf = (int64_t)fs.size();
+  int64_t max_stored = 1;
+  for (const HostFactor& F : fs) max_stored = std::max(max_stored, F.stored);
+  const int threads = (int)std::max<int64_t>(1, std::min<int64_t>(op->threads, nf));
+  std::vector<double*> stage(threads, nullptr);
+  std::vector<cudaStream_t> streams(threads, nullptr);
+  for (int t = 0; t < threads; ++t) {
+    CUDA_CHECK(cudaMalloc(&stage[t], max_stored * 8));
+    CUDA_CHECK(cudaStreamCreateWithFlags(&streams[t], cudaStreamNonBlocking));
+  }
+  std::atomic<int64_t> next{0};
+  std::exception_ptr err;
+  std::mutex mu;
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t)
+    pool.emplace_back([&, t]() {
+      try {
+        CUDA_CHECK(cudaSetDevice(op->device));
+        for (;;) {
+          const int64_t li = next.fetch_add(1);
+          if (li >= nf) return;
+          HostFactor& F = fs[li];
+          numeric_host(local_block(sf + li), F);
+          CUDA_CHECK(cudaMemcpyAsync(stage[t], F.val.data(), F.stored * 8, cudaMemcpyHostToDevice, streams[t]));
+          const int64_t base = 0;
+          op->dag->place_values((int32_t)li, (int32_t)li + 1, stage[t], &base, streams[t]);
+          CUDA_CHECK(cudaStreamSynchronize(streams[t]));
+          std::vector<double>().swap(F.val);
+        }
+      } catch (...) {
+        std::lock_guard<std::mutex> g(mu);
+        if (!err) err = std::current_exception();
+        next = nf;
+      }
+    });
+  for (auto& th : pool) th.join();
+  for (int t = 0; t < threads; ++t) {
+    cudaFree(stage[t]);
+    cudaStreamDestroy(streams[t]);
+  }
+  if (err) std::rethrow_exception(err);
+}
+
+template <class BlockFn>
+void numeric_factor_blocks(sfcdd_op* op, std::vector<HostFactor>& fs, int32_t sf, BlockFn&& local_block) {
+  numeric_factor_blocks_host(op, fs, sf, local_block);
+}
+
 OpScope::OpScope(sfcdd_op* op, cudaStream_t caller) : op_(op), caller_(caller), lk_(op->mu) {
   CUDA_CHECK(cudaEventRecord(op->ev_in, caller));
   CUDA_CHECK(cudaStreamWaitEvent(op->own_stream, op->ev_in, 0));
@@ -1455,10 +1510,7 @@ extern "C" int sfcdd_op_setup(sfcdd_op* op, void* stream) {
   // shard mode: only the owned subdomains [sf, sf + sc) are factorized
   const int32_t sf = op->shard_count > 0 ? op->shard_first : 0;
   const int32_t sc = op->shard_count > 0 ? op->shard_count : op->p;
-  std::vector<HostFactor> fs(sc);
-  FactorOptions fo;
-  parallel_for(sc, op->threads, [&](int64_t li) {
-    const int64_t i = sf + li;
+  auto local_block = [&](int64_t i) {
     const int64_t start = op->ov_start[i], len = op->ov_len[i];
     CsrMatrix B;
     B.n = len;
@@ -1482,8 +1534,12 @@ extern "C" int sfcdd_op_setup(sfcdd_op* op, void* stream) {
       }
       B.indptr[ro + 1] = B.indices.size();
     }
-    fs[li] = factorize_host(B, fo);
-  });
+    return B;
+  };
+  // 1. ordering + symbolic analysis of every block (host threads)
+  std::vector<HostFactor> fs(sc);
+  FactorOptions fo;
+  parallel_for(sc, op->threads, [&](int64_t li) { fs[li] = analyze_host(local_block(sf + li), fo); });
   auto t1 = std::chrono::steady_clock::now();
   std::vector<const HostFactor*> ptrs;
   std::vector<int64_t> gs, gm, xyoff(op->p, -1);
@@ -1511,17 +1567,27 @@ extern "C" int sfcdd_op_setup(sfcdd_op* op, void* stream) {
     }
   }
   op->xy_off_host = xyoff;
+  // 2. execution plan from the symbolic factors (metadata now, values later)
   PlanOptions po;
   CUDA_CHECK(cudaDeviceGetAttribute(&po.sms, cudaDevAttrMultiProcessorCount, op->device));
+  po.defer_values = true;
+  po.threads = op->threads;
   choose_blob_shape(ptrs, po);
   DevicePlan plan = build_plan(ptrs, gs, gm, po);
+  auto t2p = std::chrono::steady_clock::now();
   op->stats.factor_nnz = plan.stored;
   op->stats.factor_nnz_l = plan.nnz_l;
   op->stats.num_tasks = (int64_t)plan.tasks.size();
   op->stats.num_supernodes = plan.num_supernodes;
   op->dag.reset(new DagSolver(plan, op->device, extra));
   op->dev_bytes += op->dag->device_bytes();
+  plan = DevicePlan();
+  // 3. numeric factorization of every block, values placed into the blobs
+  numeric_factor_blocks(op, fs, sf, local_block);
   fs.clear();
+  auto t2n = std::chrono::steady_clock::now();
+  op->stats.reserved[4] = (int64_t)(1e6 * std::chrono::duration<double>(t2p - t1).count());   // plan us
+  op->stats.reserved[5] = (int64_t)(1e6 * std::chrono::duration<double>(t2n - t2p).count());  // numeric us
   // combination tables: candidates per disjoint range (ascending subdomain)
   std::vector<int32_t> cptr{0}, cand;
   for (int k = 0; k < op->p; ++k) {
@@ -1680,7 +1746,8 @@ extern "C" int sfcdd_op_setup(sfcdd_op* op, void* stream) {
   auto t2 = std::chrono::steady_clock::now();
   op->stats.n = n;
   op->stats.n0 = op->n0;
-  op->stats.factor_seconds = std::chrono::duration<double>(t1 - t0).count();
+  op->stats.order_seconds = std::chrono::duration<double>(t1 - t0).count();
+  op->stats.factor_seconds = std::chrono::duration<double>(t2n - t2p).count();
   op->stats.setup_seconds = std::chrono::duration<double>(t2 - t0).count();
   SFCDD_API_END
 }

@@ -3,6 +3,7 @@
 #include "plan.h"
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -10,6 +11,8 @@
 #include <map>
 #include <numeric>
 #include <string>
+#include <thread>
+#include <mutex>
 
 #include "common.h"
 
@@ -47,19 +50,105 @@ void put_pair(std::vector<int32_t>& v, int32_t lo, int32_t hi) {
   v.push_back((int32_t)((uint32_t)lo | ((uint32_t)hi << 16)));
 }
 
-// append one blob (meta ints + values) to the plan, returns its offset
-int64_t emit_blob(DevicePlan& P, std::vector<int32_t>& ints, int32_t val_off_word, const std::vector<double>& vals,
-                  int32_t& copy_bytes) {
-  const int64_t meta_bytes = align16(4 * (int64_t)ints.size());
-  if (val_off_word >= 0) ints[val_off_word] = (int32_t)meta_bytes;
-  const int64_t val_bytes = align16(8 * (int64_t)vals.size());
-  const int64_t off = (int64_t)P.blobs.size();
-  copy_bytes = (int32_t)(meta_bytes + val_bytes);
-  P.blobs.resize(P.blobs.size() + meta_bytes + val_bytes, 0);
-  std::memcpy(P.blobs.data() + off, ints.data(), 4 * ints.size());
-  if (!vals.empty()) std::memcpy(P.blobs.data() + off + meta_bytes, vals.data(), 8 * vals.size());
-  P.max_copy = std::max(P.max_copy, copy_bytes);
-  return off;
+// Blob output of one factor (factor-local offsets; merged in factor order).
+struct FactorEmit {
+  bool defer = false;
+  int32_t factor = 0;
+  int64_t size = 0;                  // device bytes emitted (local offsets)
+  std::vector<uint8_t> image;        // all bytes, or metadata only (defer)
+  std::vector<MetaSeg> segs;         // defer: local dev_off / image host_off
+  std::vector<ValDesc> vdesc;        // dst = local device byte offset
+  std::vector<int64_t> asm_patches;  // image byte offsets of asm16 words to rebase
+  std::vector<TaskDev> tasks;
+  std::vector<double> tw;
+  int32_t max_scratch = 0, max_copy = 0;
+
+  int64_t put_meta(const std::vector<int32_t>& ints, int64_t meta_bytes) {
+    const int64_t off = size;
+    const int64_t h = (int64_t)image.size();
+    if (defer) segs.push_back(MetaSeg{off, h, meta_bytes});
+    image.resize(h + meta_bytes, 0);
+    std::memcpy(image.data() + h, ints.data(), 4 * ints.size());
+    size += meta_bytes;
+    return h;
+  }
+  // metadata-only record (global assembly record of a huge supernode)
+  int64_t raw(const std::vector<int32_t>& ints) {
+    const int64_t off = size;
+    put_meta(ints, align16(4 * (int64_t)ints.size()));
+    return off;
+  }
+  // one blob: metadata + nvals values placed by descriptors (their dst is
+  // relative to the value area); asm_word >= 0: that int holds asm16
+  int64_t emit_descs(std::vector<int32_t>& ints, int32_t val_off_word, int64_t nvals, const ValDesc* vd, size_t nvd,
+                     int32_t& copy_bytes, const HostFactor* F, int32_t asm_word = -1) {
+    const int64_t meta_bytes = align16(4 * (int64_t)ints.size());
+    if (val_off_word >= 0) ints[val_off_word] = (int32_t)meta_bytes;
+    const int64_t val_bytes = align16(8 * nvals);
+    const int64_t off = size;
+    const int64_t h = put_meta(ints, meta_bytes);
+    if (asm_word >= 0) asm_patches.push_back(h + 4 * (int64_t)asm_word);
+    if (!defer) image.resize(image.size() + val_bytes, 0);
+    size += val_bytes;
+    for (size_t i = 0; i < nvd; ++i) {
+      ValDesc d = vd[i];
+      d.dst += off + meta_bytes;
+      d.factor = factor;
+      vdesc.push_back(d);
+      if (!defer) {
+        SFCDD_REQUIRE(F && !F->val.empty(), SFCDD_EINTERNAL, "plan without values needs defer_values");
+        ValDesc hd = d;
+        hd.dst -= off;  // into this blob's bytes of the image (image offset == off here)
+        place_values(hd, F->val.data() + d.src, image.data() + h);
+      }
+    }
+    copy_bytes = (int32_t)(meta_bytes + val_bytes);
+    max_copy = std::max(max_copy, copy_bytes);
+    return off;
+  }
+  int64_t emit(std::vector<int32_t>& ints, int32_t val_off_word, int64_t nvals, const ValDesc* vd,
+               int32_t& copy_bytes, const HostFactor& F, int32_t asm_word = -1) {
+    return emit_descs(ints, val_off_word, nvals, vd, vd ? 1 : 0, copy_bytes, &F, asm_word);
+  }
+  int64_t emit(std::vector<int32_t>& ints, int32_t val_off_word, int64_t nvals, const ValDesc* vd,
+               int32_t& copy_bytes) {
+    return emit_descs(ints, val_off_word, nvals, vd, vd ? 1 : 0, copy_bytes, nullptr);
+  }
+  int64_t emit_frag(std::vector<int32_t>& ints, int32_t val_off_word, int64_t nvals, const std::vector<ValDesc>& vd,
+                    int32_t& copy_bytes, const HostFactor& F) {
+    return emit_descs(ints, val_off_word, nvals, vd.data(), vd.size(), copy_bytes, &F);
+  }
+};
+
+template <class Fn>
+void parallel_range(int64_t n, int threads, Fn fn) {
+  if (threads <= 0) threads = hardware_threads();
+  threads = (int)std::max<int64_t>(1, std::min<int64_t>(threads, n));
+  if (threads == 1) {
+    for (int64_t i = 0; i < n; ++i) fn(i);
+    return;
+  }
+  std::atomic<int64_t> next{0};
+  std::vector<std::thread> pool;
+  std::exception_ptr err;
+  std::mutex mu;
+  for (int t = 0; t < threads; ++t)
+    pool.emplace_back([&]() {
+      for (;;) {
+        const int64_t i = next.fetch_add(1);
+        if (i >= n) return;
+        try {
+          fn(i);
+        } catch (...) {
+          std::lock_guard<std::mutex> g(mu);
+          if (!err) err = std::current_exception();
+          next = n;
+          return;
+        }
+      }
+    });
+  for (auto& th : pool) th.join();
+  if (err) std::rethrow_exception(err);
 }
 
 inline int64_t blob_size(int64_t ints, int64_t vals) { return align16(4 * ints) + align16(8 * vals); }
@@ -95,6 +184,29 @@ void choose_blob_shape(const std::vector<const HostFactor*>& factors, PlanOption
   if (tot > 0.0 && big > 0.42 * tot) {  // measured: C2 34 % -> 8 KB wins by 13 %; C4 47 %, C3 79 % -> 16 KB wins by 4 %, 17 %
     opt.blob_max = 16 * 1024;
     opt.wpb = 2;
+  }
+}
+
+void place_values(const ValDesc& d, const double* M, uint8_t* buf) {
+  double* out = reinterpret_cast<double*>(buf + d.dst);
+  switch (d.kind) {
+    case VD_COPY:
+      std::memcpy(out, M, 8 * (size_t)d.len);
+      break;
+    case VD_ROW:  // out[k R + i] = M[r0 + i, k]
+      for (int32_t k = 0; k < d.len; ++k) {
+        const double* col = M + packed_col_off(d.s, d.m, k);
+        for (int32_t i = std::max(0, k - d.p0); i < d.w; ++i) out[(int64_t)k * d.w + i] = col[d.p0 + i - k];
+      }
+      break;
+    case VD_COL:  // out[r c + j] = M[k0 + r, k0 + j]
+      for (int32_t j = 0; j < d.w; ++j) {
+        const double* col = M + packed_col_off(d.s, d.m, d.p0 + j);
+        for (int32_t r = j; r < d.len; ++r) out[(int64_t)r * d.w + j] = col[r - j];
+      }
+      break;
+    default:
+      throw Error(SFCDD_EINTERNAL, "unknown value descriptor");
   }
 }
 
@@ -239,9 +351,17 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
     gr.parent = p < 0 ? -1 : group_of[gr.factor][p];
     if (gr.parent >= 0) groups[gr.parent].kids.push_back(g);
     if (gr.big) {
+      // update-buffer slots of a BIG group, allocated up front so that the
+      // blob emission below can run per factor in parallel: y_J (s), the
+      // assembled front [f_J ; f_B] (s + m, used in ASM mode) and -x_B (m,
+      // used in XB mode)
       const Supernode& J = F.sn[gr.top];
       gr.y_off = P.upd_doubles;
       P.upd_doubles += J.s;
+      gr.f_off = P.upd_doubles;
+      P.upd_doubles += J.s + J.m;
+      gr.xb_off = P.upd_doubles;
+      P.upd_doubles += J.m;
       ++P.nbig;
     } else {
       ++P.nfrag;
@@ -252,18 +372,33 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
       groups[groups[g].parent].height = std::max(groups[groups[g].parent].height, groups[g].height + 1);
 
   pt_[0] = ptime();
-  // ---- 2. blobs + tasks (unordered)
+  // ---- 2. blobs + tasks (unordered), emitted per factor in parallel into
+  // factor-local buffers (offsets relative to the factor), then merged in
+  // factor order (deterministic for any thread count)
   std::vector<TaskDev> tl;
   std::vector<double> tw;  // task weight (us, rough model used for the queue order)
+  std::vector<int32_t> gbegin(factors.size() + 1, G);
+  for (int32_t g = G - 1; g >= 0; --g) gbegin[groups[g].factor] = g;
+  for (int64_t fi = (int64_t)factors.size() - 1; fi >= 0; --fi)
+    if (gbegin[fi] == G) gbegin[fi] = gbegin[fi + 1];
+  const bool defer = opt.defer_values;
+  std::vector<FactorEmit> emits(factors.size());
+  if (!defer)
+    for (const HostFactor* F : factors)
+      SFCDD_REQUIRE(F->val.size() == (size_t)F->stored, SFCDD_EINTERNAL, "plan without values needs defer_values");
+  auto emit_factor = [&](int64_t fi_) {
+  const size_t fi = (size_t)fi_;
+  FactorEmit& E = emits[fi];
+  E.defer = defer;
+  E.factor = (int32_t)fi;
   std::vector<int32_t> ints;
-  std::vector<double> vals;
   std::vector<int32_t> loc;
-  std::vector<std::vector<int32_t>> col2sn(factors.size());
-  for (size_t fi = 0; fi < factors.size(); ++fi) {
+  std::vector<int32_t> col2sn_f;
+  {
     const HostFactor& F = *factors[fi];
-    col2sn[fi].assign(F.n, -1);
+    col2sn_f.assign(F.n, -1);
     for (size_t k = 0; k < F.sn.size(); ++k)
-      for (int32_t t = 0; t < F.sn[k].s; ++t) col2sn[fi][F.sn[k].col0 + t] = (int32_t)k;
+      for (int32_t t = 0; t < F.sn[k].s; ++t) col2sn_f[F.sn[k].col0 + t] = (int32_t)k;
   }
   auto add_task = [&](int32_t g, int32_t kind, int64_t off, int32_t bytes, int64_t nvals, double w) {
     TaskDev T{};
@@ -273,24 +408,17 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
     T.factor = groups[g].factor;
     T.group = g;
     T.values = (int32_t)nvals;
-    tl.push_back(T);
-    tw.push_back(w);
-    Group& G_ = groups[g];
-    std::vector<int32_t>& lst = kind == TK_ASM_FWD ? G_.atask
-                                : kind == TK_XB_BWD ? G_.xtask
-                                : (kind == TK_FRAG_FWD || kind == TK_ROW_FWD) ? G_.ftask
-                                                                                : G_.btask;
-    lst.push_back((int32_t)tl.size() - 1);
+    E.tasks.push_back(T);
+    E.tw.push_back(w);
   };
-  for (int32_t g = 0; g < G; ++g) {
-    Group& gr = groups[g];
+  for (int32_t g = gbegin[fi]; g < gbegin[fi + 1]; ++g) {
+    const Group& gr = groups[g];
     const HostFactor& F = *factors[gr.factor];
     const Supernode& Top = F.sn[gr.top];
     if (gr.big) {
       // ---------------------------------------------------------- BIG
       const Supernode& S = Top;
       const int32_t s = S.s, m = S.m;
-      const double* Mv = F.val.data() + S.val_off;
       // child update indices summed into each front position (fixed order:
       // children, then rows)
       std::vector<std::vector<int32_t>> contrib(s + m);
@@ -355,18 +483,10 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
           if (p < s + m) nnz += (int32_t)contrib[p].size();
         }
         for (int32_t p = 0; p < s + m; ++p) ints.insert(ints.end(), contrib[p].begin(), contrib[p].end());
-        const int64_t asm_off = (int64_t)P.blobs.size();
-        SFCDD_REQUIRE(asm_off % 16 == 0 && asm_off / 16 < (int64_t(1) << 31), SFCDD_EINTERNAL,
-                      "blob buffer too large");
-        P.blobs.resize(P.blobs.size() + align16(4 * (int64_t)ints.size()), 0);
-        std::memcpy(P.blobs.data() + asm_off, ints.data(), 4 * ints.size());
+        const int64_t asm_off = E.raw(ints);  // factor-local; rebased (asm16 patches) at the merge
         asm16 = (int32_t)(asm_off / 16);
       }
-      if (use_asm) {  // the assembled front [f_J ; f_B]
-        gr.f_off = P.upd_doubles;
-        P.upd_doubles += s + m;
-      }
-      if (use_asm) {
+      if (use_asm) {  // the assembled front [f_J ; f_B] at gr.f_off
         // forward assembly: f = [f_J ; f_B] in chunks of front positions
         for (int32_t q0 = 0; q0 < s + m;) {
           int32_t nq = 0;
@@ -396,9 +516,8 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
           ints[AS_SRC] = (int32_t)ints.size();
           for (int32_t q = q0; q < q0 + nq; ++q) ints.insert(ints.end(), contrib[q].begin(), contrib[q].end());
           while (ints.size() % 4) ints.push_back(0);
-          vals.clear();
           int32_t bytes = 0;
-          const int64_t off = emit_blob(P, ints, -1, vals, bytes);  // metadata only
+          const int64_t off = E.emit(ints, -1, 0, nullptr, bytes);  // metadata only
           ints.clear();
           add_task(g, TK_ASM_FWD, off, bytes, 0, 1.2 + 0.004 * (nq + (double)e));
           q0 += nq;
@@ -434,15 +553,19 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
           }
         }
         ints[RW_SCRATCH] = C + NB;
-        vals.assign((size_t)R * C, 0.0);
-        for (int32_t k = 0; k < C; ++k)
-          for (int32_t i = 0; i < R; ++i) {
-            const int32_t row = r0 + i;
-            if (k <= row) vals[(size_t)k * R + i] = Mv[packed_col_off(s, m, k) + (row - k)];
-          }
+        // values: R x C column-major, (i, k) = M[r0 + i, k] for k <= r0 + i
+        ValDesc vd{};
+        vd.src = S.val_off;
+        vd.kind = VD_ROW;
+        vd.s = s;
+        vd.m = m;
+        vd.p0 = r0;
+        vd.w = R;
+        vd.len = C;
+        const int32_t asm_word = asm16 >= 0 ? RW_ASM16 : -1;
         int32_t bytes = 0;
-        const int64_t off = emit_blob(P, ints, RW_VAL_OFF, vals, bytes);
-        P.max_scratch = std::max<int32_t>(P.max_scratch, C + NB);
+        const int64_t off = E.emit(ints, RW_VAL_OFF, (int64_t)R * C, &vd, bytes, F, asm_word);
+        E.max_scratch = std::max<int32_t>(E.max_scratch, C + NB);
         add_task(g, TK_ROW_FWD, off, bytes, (int64_t)R * C, (use_asm ? 1.8 : 2.36) + 0.0013 * R * C);
       }
       // backward column blocks, dense row-major L x c (L = s+m-k0); -x_B is
@@ -458,11 +581,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
       // XB also when a column block with its inline row list cannot fit a blob
       const bool inline_fits = blob_size(CL_WORDS + 1 + m, (int64_t)(s + m)) <= opt.blob_max;
       const bool use_xb = m > 0 && ((split_ok && ncol_tasks >= opt.xb_min_tasks) || !inline_fits);
-      if (use_xb) {  // -x_B
-        gr.xb_off = P.upd_doubles;
-        P.upd_doubles += m;
-      }
-      if (use_xb) {
+      if (use_xb) {  // -x_B at gr.xb_off
         for (int32_t a0 = 0; a0 < m;) {
           int32_t na = std::min<int32_t>(m - a0, opt.asm_max);
           while (na > 1 && blob_size(XB_WORDS + na, 0) > opt.blob_max) --na;
@@ -473,9 +592,8 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
           ints[XB_ROWS] = (int32_t)ints.size();
           for (int32_t a = a0; a < a0 + na; ++a) ints.push_back(F.perm[F.rows[S.rows_off + a]]);
           while (ints.size() % 4) ints.push_back(0);
-          vals.clear();
           int32_t bytes = 0;
-          const int64_t off = emit_blob(P, ints, -1, vals, bytes);  // metadata only
+          const int64_t off = E.emit(ints, -1, 0, nullptr, bytes);  // metadata only
           ints.clear();
           add_task(g, TK_XB_BWD, off, bytes, 0, 1.2 + 0.003 * na);
           a0 += na;
@@ -502,16 +620,19 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
           for (int32_t a = 0; a < m; ++a) ints.push_back(F.perm[F.rows[S.rows_off + a]]);
         }
         ints[CL_SCRATCH] = L;
-        vals.assign((size_t)L * c, 0.0);
-        int64_t nv = 0;
-        for (int32_t r = 0; r < L; ++r)
-          for (int32_t j = 0; j < c && j <= r; ++j) {
-            vals[(size_t)r * c + j] = Mv[packed_col_off(s, m, k0 + j) + (r - j)];
-            ++nv;
-          }
+        // values: L x c row-major, (r, j) = M[k0 + r, k0 + j] for j <= r
+        const int64_t nv = (int64_t)L * c - (int64_t)c * (c - 1) / 2;
+        ValDesc vd{};
+        vd.src = S.val_off;
+        vd.kind = VD_COL;
+        vd.s = s;
+        vd.m = m;
+        vd.p0 = k0;
+        vd.w = c;
+        vd.len = L;
         int32_t bytes = 0;
-        const int64_t off = emit_blob(P, ints, CL_VAL_OFF, vals, bytes);
-        P.max_scratch = std::max<int32_t>(P.max_scratch, L);
+        const int64_t off = E.emit(ints, CL_VAL_OFF, (int64_t)L * c, &vd, bytes, F);
+        E.max_scratch = std::max<int32_t>(E.max_scratch, L);
         add_task(g, TK_COL_BWD, off, bytes, nv, (use_xb ? 1.8 : 2.24) + 0.0013 * nv);
         k0 += c;
       }
@@ -520,7 +641,8 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
     // ------------------------------------------------------------ FRAG
     const int32_t nsn = (int32_t)gr.sns.size();
     ints.assign(H_WORDS, 0);
-    vals.clear();
+    std::vector<ValDesc> fvd;
+    int64_t fvals = 0;
     ints[H_NSN] = nsn;
     ints[H_TOP_UPD] = upd_slot[gr.factor][gr.top];
     loc.assign(F.sn.size(), -1);
@@ -602,11 +724,18 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
       int32_t* R = &ints[ints[H_REC] + R_WORDS * i];
       SFCDD_REQUIRE(S.s < 4096 && S.m < 32768, SFCDD_EINTERNAL, "supernode too large for a FRAG record");
       R[R_SM] = S.s | (S.m << 16);
-      R[R_VAL] = (int32_t)vals.size();
+      R[R_VAL] = (int32_t)fvals;
       R[R_SCR] = scr[i];
       R[R_CPOS] = cpos[i];
-      const double* v = F.val.data() + S.val_off;
-      vals.insert(vals.end(), v, v + packed_size(S.s, S.m));
+      ValDesc vd{};
+      vd.dst = 8 * fvals;  // within the value area (emit() rebases)
+      vd.src = S.val_off;
+      vd.kind = VD_COPY;
+      vd.s = S.s;
+      vd.m = S.m;
+      vd.len = (int32_t)packed_size(S.s, S.m);
+      fvd.push_back(vd);
+      fvals += packed_size(S.s, S.m);
       nvals += packed_size(S.s, S.m);
     }
     // Backward items of one level.  Supernodes with s <= 32 are packed into
@@ -712,7 +841,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         const Supernode& S = sn_of(j);
         for (int32_t a = 0; a < S.m; ++a) {
           const int32_t r = F.rows[S.rows_off + a];
-          const int32_t owner = col2sn[gr.factor][r];
+          const int32_t owner = col2sn_f[r];
           int32_t src;
           if (owner >= 0 && loc[owner] >= 0) {
             src = cpos[lid[loc[owner]]] + (r - (int32_t)F.sn[owner].col0);
@@ -778,14 +907,71 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
     ints[H_ZERO] = nsn > 0 ? cpos[0] : 0;  // frontal slots [0, cpos[0])
     SFCDD_REQUIRE(scratch_used <= opt.scratch_max, SFCDD_EINTERNAL, "fragment scratch exceeds budget");
     int32_t bytes = 0;
-    const int64_t off = emit_blob(P, ints, H_VAL_OFF, vals, bytes);
+    const int64_t off = E.emit_frag(ints, H_VAL_OFF, fvals, fvd, bytes, F);
     SFCDD_REQUIRE(bytes <= opt.blob_max, SFCDD_EINTERNAL, "fragment blob exceeds the slot budget");
-    P.max_scratch = std::max(P.max_scratch, scratch_used);
+    E.max_scratch = std::max(E.max_scratch, scratch_used);
     // task time model (us), fitted to traced C2 launches (tools/trace_dag.py)
     add_task(g, TK_FRAG_FWD, off, bytes, nvals, 2.13 + 0.0041 * nvals + 0.57 * nlev);
     add_task(g, TK_FRAG_BWD, off, bytes, nvals, 1.11 + 0.0021 * nvals + 0.68 * nlev);
   }
 
+  };  // emit_factor
+  parallel_range((int64_t)factors.size(), opt.threads, emit_factor);
+  // merge in factor order: rebase blob offsets, value descriptors and the
+  // global assembly-record references (asm16)
+  P.deferred = defer;
+  {
+    int64_t tot = 0, meta_tot = 0;
+    for (const FactorEmit& E : emits) {
+      tot += E.size;
+      meta_tot += (int64_t)E.image.size();
+    }
+    SFCDD_REQUIRE(tot / 16 < (int64_t(1) << 31), SFCDD_EINTERNAL, "blob buffer too large");
+    P.blob_bytes = tot;
+    P.blobs.reserve(defer ? meta_tot : tot);
+  }
+  int64_t cursor = 0;
+  for (FactorEmit& E : emits) {
+    const int64_t dbase = cursor;
+    for (const auto& pa : E.asm_patches) {  // int32 word at image byte offset pa
+      int32_t v;
+      std::memcpy(&v, E.image.data() + pa, 4);
+      v += (int32_t)(dbase / 16);
+      std::memcpy(E.image.data() + pa, &v, 4);
+    }
+    if (defer) {
+      const int64_t hbase = (int64_t)P.blobs.size();
+      for (MetaSeg sg : E.segs) {
+        sg.dev_off += dbase;
+        sg.host_off += hbase;
+        P.segs.push_back(sg);
+      }
+    }
+    P.blobs.insert(P.blobs.end(), E.image.begin(), E.image.end());
+    E.image.clear();
+    E.image.shrink_to_fit();
+    for (ValDesc vd : E.vdesc) {
+      vd.dst += dbase;
+      P.vdesc.push_back(vd);
+    }
+    E.vdesc.clear();
+    E.vdesc.shrink_to_fit();
+    for (size_t t = 0; t < E.tasks.size(); ++t) {
+      TaskDev T = E.tasks[t];
+      T.blob_off += dbase;
+      tl.push_back(T);
+      tw.push_back(E.tw[t]);
+      Group& G_ = groups[T.group];
+      std::vector<int32_t>& lst = T.kind == TK_ASM_FWD ? G_.atask
+                                  : T.kind == TK_XB_BWD ? G_.xtask
+                                  : (T.kind == TK_FRAG_FWD || T.kind == TK_ROW_FWD) ? G_.ftask
+                                                                                      : G_.btask;
+      lst.push_back((int32_t)tl.size() - 1);
+    }
+    cursor += E.size;
+    P.max_scratch = std::max(P.max_scratch, E.max_scratch);
+    P.max_copy = std::max(P.max_copy, E.max_copy);
+  }
   SFCDD_REQUIRE(P.upd_doubles < (int64_t(1) << 31), SFCDD_EINTERNAL, "update buffer too large");
 
   pt_[1] = ptime();
@@ -981,7 +1167,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
   P.tasks.resize(tl.size());
   for (size_t t = 0; t < order.size(); ++t) P.tasks[t] = tl[order[t]];
 
-  if (std::getenv("SFCDD_PLAN_DEBUG")) {
+  if (std::getenv("SFCDD_PLAN_DEBUG") && !P.deferred) {  // (parses the host blob image)
     int64_t big_vals = 0, small_vals = 0, lev_sum = 0, sn_sum = 0, nrow = 0, ncol = 0;
     int32_t maxh = 0;
     for (const TaskDev& T : P.tasks) {

@@ -173,6 +173,40 @@ enum ColHdr {
 
 constexpr int SMALL_MAX_S = 64;  // wider supernodes are always BIG
 
+// ------------------------------------------------ factor value placement
+// Where a factor's packed block-inverse values (HostFactor::val layout:
+// supernode J's M at val_off, column-major packed trapezoid) land in the
+// blob buffer.  One descriptor per FRAG supernode and per ROW / COL task;
+// the same descriptors fill the blobs on the host (from HostFactor::val) or
+// on the device (from values a device factorization produced), so plans can
+// be built before any numeric factorization (PlanOptions::defer_values).
+enum ValDescKind : int32_t {
+  VD_COPY = 0,  // len consecutive values (a whole packed M block)
+  VD_ROW = 1,   // ROW blob: R x C column-major, (i, k) = M[r0 + i, k], k <= r0 + i
+  VD_COL = 2,   // COL blob: L x c row-major, (r, j) = M[k0 + r, k0 + j], j <= r
+};
+struct ValDesc {
+  int64_t dst;     // byte offset in the blob buffer
+  int64_t src;     // offset of J's packed M in its factor's values (Supernode::val_off)
+  int32_t factor;  // factor id within the plan
+  int32_t kind;    // ValDescKind
+  int32_t s, m;    // supernode shape
+  int32_t p0;      // ROW: r0; COL: k0
+  int32_t w;       // ROW: R; COL: c
+  int32_t len;     // COPY: count; ROW: C; COL: L
+  int32_t pad;
+};
+static_assert(sizeof(ValDesc) == 48, "ValDesc layout");
+// metadata segment of a deferred-value plan: host bytes [host_off, +bytes)
+// go to blob byte offset dev_off
+struct MetaSeg {
+  int64_t dev_off;
+  int64_t host_off;
+  int64_t bytes;
+};
+// host version of the placement (the device kernel follows it exactly)
+void place_values(const ValDesc& d, const double* M /* J's packed block */, uint8_t* blob_buffer);
+
 struct PlanOptions {
   int32_t blob_max = 8 * 1024;   // bytes of a task blob (slot blob area)
   int32_t scratch_max = 512;     // doubles of FRAG scratch (< 65536)
@@ -190,6 +224,9 @@ struct PlanOptions {
   double slack_us = 4.0;           // queue-order simulation: dependents become ready this late (SFCDD_SLACK_US)
   int32_t wpb = 4;                 // worker warps per DAG CTA: 2, 4 or 8 (SFCDD_WPB)
   bool tuned = false;              // blob_max / wpb fixed by the environment (no automatic choice)
+  bool defer_values = false;       // build the plan from symbolic factors: blobs hold metadata only
+                                   // (DevicePlan::segs), values are placed later by the descriptors
+  int32_t threads = 0;             // host threads for the per-factor blob emission (0: hardware)
   PlanOptions();                 // environment overrides SFCDD_BLOB_MAX, SFCDD_SCRATCH_MAX, ...
 };
 
@@ -201,7 +238,13 @@ struct PlanOptions {
 void choose_blob_shape(const std::vector<const HostFactor*>& factors, PlanOptions& opt);
 
 struct DevicePlan {
+  // the blob buffer's host image: every byte (values included), or with
+  // `deferred` only the metadata, laid out by `segs`
   std::vector<uint8_t> blobs;
+  bool deferred = false;
+  int64_t blob_bytes = 0;        // device size of the blob buffer
+  std::vector<MetaSeg> segs;     // deferred: metadata placement
+  std::vector<ValDesc> vdesc;    // value placement, grouped by factor (ascending)
   std::vector<TaskDev> tasks;
   std::vector<FactorDev> factors;
   int32_t ngroups = 0;

@@ -235,6 +235,37 @@ class GridLaplacian:
     def toarray(self) -> np.ndarray:
         return self.tocsr().toarray()
 
+    # scipy-matrix behaviour for diagnostics (A.T, A[idx][:, idx], A - B,
+    # A != A.T ...): delegated to the materialised CSR copy, as the reference
+    # returns a CSR matrix from assemble_laplacian (grid.py:91-114)
+    def _csr(self):
+        c = getattr(self, "_csr_cache", None)
+        if c is None:
+            c = self.tocsr()
+            self._csr_cache = c
+        return c
+
+    def __getattr__(self, name):
+        # never materialise implicitly for attribute probes on large grids
+        if name.startswith("_") or self.__dict__.get("n", 0) > (1 << 22):
+            raise AttributeError(name)
+        return getattr(self._csr(), name)
+
+    def __getitem__(self, key):
+        return self._csr()[key]
+
+    def __sub__(self, other):
+        return self._csr() - (other._csr() if isinstance(other, GridLaplacian) else other)
+
+    def __add__(self, other):
+        return self._csr() + (other._csr() if isinstance(other, GridLaplacian) else other)
+
+    def __ne__(self, other):
+        return self._csr() != (other._csr() if isinstance(other, GridLaplacian) else other)
+
+    def __rmatmul__(self, other):
+        return other @ self._csr()
+
 
 def assemble_laplacian(levels, curve: str = "hilbert") -> GridLaplacian:
     """(2d+1)-point FD matrix of -Laplace in SFC order (grid.py:91-114), matrix-free.

@@ -309,6 +309,23 @@ def _pcg_composed(A, b, precond, cfg: SolverConfig, x0, exact, t0) -> SolveRepor
 
 def estimate_extremal_eigs(apply_ca, n: int, *, iters: int | None = None, seed: int = 0, a_matvec=None,
                            force_iterative: bool = False, stagnation_tol: float = 2e-5, min_iters: int = 40):
+    """Extremal eigenvalues of C^-1 A (krylov.py:102-168) for numpy callables
+    (the reference's interface): the callables are wrapped to device vectors
+    and the estimate runs in estimate_extremal_eigs_device."""
+
+    def dev(fn):
+        if fn is None:
+            return None
+        return lambda v: _to_device(np.asarray(fn(v.cpu().numpy()), dtype=np.float64))
+
+    return estimate_extremal_eigs_device(dev(apply_ca), n, iters=iters, seed=seed, a_matvec=dev(a_matvec),
+                                         force_iterative=force_iterative, stagnation_tol=stagnation_tol,
+                                         min_iters=min_iters)
+
+
+def estimate_extremal_eigs_device(apply_ca, n: int, *, iters: int | None = None, seed: int = 0, a_matvec=None,
+                                  force_iterative: bool = False, stagnation_tol: float = 2e-5,
+                                  min_iters: int = 40):
     """Extremal eigenvalues of a preconditioned SPD operator (krylov.py:102-168).
 
     ``apply_ca`` and ``a_matvec`` map CUDA tensors to CUDA tensors (device
@@ -384,8 +401,8 @@ def richardson(A, b, precond, cfg: SolverConfig, x0, exact=None) -> SolveReport:
     if cfg.damping == "optimal":
         if precond is not None and not getattr(precond, "symmetric", True):
             raise ValueError("optimal damping requires a symmetric preconditioner")
-        lam = estimate_extremal_eigs(lambda v: apply_c(mv(v)), n, iters=cfg.eig_iters, seed=cfg.seed,
-                                     a_matvec=mv)
+        lam = estimate_extremal_eigs_device(lambda v: apply_c(mv(v)), n, iters=cfg.eig_iters, seed=cfg.seed,
+                                            a_matvec=mv)
         xi = 2.0 / (lam[0] + lam[1])
     else:
         xi = float(cfg.damping)

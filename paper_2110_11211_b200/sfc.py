@@ -122,3 +122,54 @@ def grid_point_key(multi_index, levels, curve: str = "hilbert") -> int:
     cfg = CurveConfig(len(ell), n, curve)
     coords = tuple((k - 1) << (n - lj) for k, lj in zip(idx, ell))
     return encode(coords, cfg)
+
+
+def holder_bound(dim: int) -> float:
+    """2 sqrt(dim + 3), the bound on the curve's Holder quotient (sfc.py:172-174)."""
+    return 2.0 * float(np.sqrt(dim + 3))
+
+
+def _split(keys: list[int]) -> tuple[np.ndarray, np.ndarray]:
+    hi = np.array([k >> 64 for k in keys], dtype=np.uint64)
+    lo = np.array([k & ((1 << 64) - 1) for k in keys], dtype=np.uint64)
+    return hi, lo
+
+
+def holder_estimate(cfg: CurveConfig, samples: int, seed: int = 0) -> float:
+    """Largest |s(x) - s(y)|_2 / |x - y|^(1/dim) over sampled curve parameter
+    pairs (sfc.py:177-207).  The key pairs are the reference's seeded draws
+    (little-endian default_rng bytes masked to key_bits); all points are
+    decoded in one batch on the device."""
+    if samples < 2:
+        raise ValueError("need at least 2 samples")
+    rng = np.random.default_rng(seed)
+    kb = cfg.key_bits
+    mask = (1 << kb) - 1
+    nbytes = (kb + 7) // 8
+    a, b = [], []
+    for _ in range(samples):
+        k1 = int.from_bytes(rng.bytes(nbytes), "little") & mask
+        k2 = int.from_bytes(rng.bytes(nbytes), "little") & mask
+        if k1 != k2:
+            a.append(k1)
+            b.append(k2)
+    if not a:
+        return 0.0
+    pa = decode_many(*_split(a), cfg).astype(np.float64)
+    pb = decode_many(*_split(b), cfg).astype(np.float64)
+    dist = np.sqrt(((pa - pb) ** 2).sum(axis=1)) * (1.0 / cfg.side)
+    param = np.array([abs(x - y) for x, y in zip(a, b)], dtype=np.float64) * np.ldexp(1.0, -kb)
+    return float(np.max(dist / param ** (1.0 / cfg.dim)))
+
+
+def curve_diagnostics(cfg: CurveConfig) -> dict:
+    """Exhaustive bijectivity / unit-step check over all 2**key_bits keys
+    (sfc.py:210-229): decode every key on the device, re-encode, compare."""
+    total = 1 << cfg.key_bits
+    keys = np.arange(total, dtype=np.uint64)
+    zeros = np.zeros(total, dtype=np.uint64)
+    pts = decode_many(zeros, keys, cfg)
+    hi, lo = encode_many(pts, cfg)
+    bijective = bool(np.all(hi == 0) and np.array_equal(lo, keys))
+    steps = np.abs(np.diff(pts.astype(np.int64), axis=0)).sum(axis=1)
+    return {"bijective": bijective, "adjacent": bool(np.all(steps == 1))}

@@ -81,7 +81,7 @@ def test_richardson_matches_reference(sfcdd, golden, tag):
     _same(rep, g, f"{tag}_rich_fixed", 1e-9, its_slack=1)
     # the forced Lanczos path (n <= 300 would otherwise be dense)
     At = lambda v: A @ v  # noqa: E731
-    lam = sfcdd.krylov.estimate_extremal_eigs(lambda v: op.apply_device(At(v)), n, seed=42, a_matvec=At,
+    lam = sfcdd.krylov.estimate_extremal_eigs_device(lambda v: op.apply_device(At(v)), n, seed=42, a_matvec=At,
                                               force_iterative=True)
     np.testing.assert_allclose(lam, g[f"{tag}_lanczos_forced"], rtol=1e-9)
 

@@ -238,3 +238,21 @@ def test_library_partition_matches_oracle_property(oracle):
         np.testing.assert_array_equal(w.omega, omega)
         for a, b in zip(w.diagonals, diags):
             np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("levels,p", [((6, 6), 8), ((4, 4, 4), 8), ((7, 7), 16)])
+def test_deferred_value_plan_rebuilds_blob_image(oracle, levels, p):
+    """Plans built from symbolic factors (values placed later by descriptors,
+    the device-factorization path) give the identical blob image and task
+    list as plans built from host values."""
+    A = oracle.assemble_scaled_laplacian(levels)
+    ov = oracle.enlarge(oracle.disjoint_partition(A.shape[0], p), 0.5)
+    n, ip, ix, dv = _csr_args(A)
+    st = np.array([r.start for r in ov], np.int64)
+    ln = np.array([r.length for r in ov], np.int64)
+    bad, nseg, nvd = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    _lib.check(_lib.lib().sfcdd_host_plan_deferred_check(n, ip.ctypes.data, ix.ctypes.data, dv.ctypes.data, p,
+                                                         st.ctypes.data, ln.ctypes.data, ctypes.byref(bad),
+                                                         ctypes.byref(nseg), ctypes.byref(nvd)))
+    assert nseg.value > 0 and nvd.value > 0
+    assert bad.value == 0
