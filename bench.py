@@ -49,6 +49,8 @@ CONFIGS = {
     "c4": ((12, 12), 256, 0.5, 16, "C4: 2D 4095^2 interior (l=(12,12)), P=256, gamma=0.5, q=16 (64x64 coarse); "
                                    "fault mode: apply 5 of every solve zeroes the local pieces of "
                                    "default_rng(42).choice(256, 26) (SURVEY §8(d))"),
+    "c5": ((8, 8, 8), 512, 0.5, 64, "C5: 3D 255^3 interior (l=(8,8,8)), P=512, gamma=0.5, q=64 (coarse 1/8 per "
+                                    "dimension: N0 = 32768), the 1-GPU point of the weak-scaling sweep"),
 }
 METRIC = "PCG DOF-iterations/s (SFC two-level Schwarz, Poisson)"
 UNIT = "DOF-it/s"

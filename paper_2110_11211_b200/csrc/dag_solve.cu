@@ -534,9 +534,10 @@ __device__ __forceinline__ void run_row(const int32_t* h, double* S, const DagAr
     warp_gather(
         C + NB, lane, [&](int q) { return __ldcg(f + (q < C ? q : r0 + (q - C))); },
         [&](int q, double v) { S[q] = v; });
-  } else if (h[RW_ASM16] >= 0) {
+  } else if (h[RW_ASM_HI] >= 0) {
     // huge s: J's assembly record in global memory [s, m] cols ptr src
-    const int32_t* am = reinterpret_cast<const int32_t*>(A.blobs + 16 * (int64_t)h[RW_ASM16]);
+    const int64_t o16 = (int64_t)(uint32_t)h[RW_ASM16] | ((int64_t)h[RW_ASM_HI] << 32);
+    const int32_t* am = reinterpret_cast<const int32_t*>(A.blobs + 16 * o16);
     const int32_t* cols = am + 2;
     const int32_t* ptr = cols + s;
     const int32_t* src = ptr + s + __ldg(am + 1) + 1;

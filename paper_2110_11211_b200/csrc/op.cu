@@ -19,6 +19,7 @@
 #include <mutex>
 #include <thread>
 
+#include "gpu_factor.h"
 #include "op.h"
 #include "plan.h"
 #include "tiles.h"
@@ -1259,9 +1260,67 @@ void numeric_factor_blocks_host(sfcdd_op* op, std::vector<HostFactor>& fs, int32
   if (err) std::rethrow_exception(err);
 }
 
+// Device path (default): batches of blocks, sized to the free device memory,
+// factorized by gpu_factor_batch straight into a device value buffer that
+// place_values moves into the blobs.  SFCDD_HOST_NUMERIC=1 selects the host
+// path (A/B comparisons).
+template <class BlockFn>
+void numeric_factor_blocks_device(sfcdd_op* op, std::vector<HostFactor>& fs, int32_t sf, BlockFn&& local_block) {
+  const int64_t nf = (int64_t)fs.size();
+  size_t free_b = 0, total_b = 0;
+  CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+  int64_t budget = std::min<int64_t>((int64_t)(0.6 * (double)free_b), int64_t(48) << 30);
+  if (const char* e = std::getenv("SFCDD_FACTOR_BUDGET_GB")) budget = (int64_t)(std::atof(e) * (1 << 30));
+  cudaStream_t st = op->own_stream;
+  double dev_s = 0.0;
+  int64_t f0 = 0;
+  while (f0 < nf) {
+    // batch [f0, f1): values + update matrices + tier-3 workspace within budget
+    int64_t f1 = f0, need = 0;
+    while (f1 < nf) {
+      const HostFactor& F = fs[f1];
+      const int64_t b = 8 * (F.stored + gpu_factor_update_doubles(F) + gpu_factor_work_bound(F)) + 64 * (int64_t)F.sn.size();
+      if (f1 > f0 && need + b > budget) break;
+      need += b;
+      ++f1;
+    }
+    std::vector<GpuFactorInput> in(f1 - f0);
+    parallel_for(f1 - f0, op->threads,
+                 [&](int64_t i) { gpu_factor_prepare(fs[f0 + i], local_block(sf + f0 + i), in[i]); });
+    std::vector<const HostFactor*> fp;
+    std::vector<const GpuFactorInput*> ip;
+    std::vector<int64_t> base;
+    int64_t tot = 0;
+    for (int64_t i = f0; i < f1; ++i) {
+      fp.push_back(&fs[i]);
+      ip.push_back(&in[i - f0]);
+      base.push_back(tot);
+      tot += fs[i].stored;
+    }
+    double* vals = nullptr;
+    CUDA_CHECK(cudaMallocAsync(&vals, std::max<int64_t>(tot, 2) * 8, st));
+    try {
+      gpu_factor_batch(fp, ip, vals, base, st, &dev_s);
+      op->dag->place_values((int32_t)f0, (int32_t)f1, vals, base.data(), st);
+      CUDA_CHECK(cudaFreeAsync(vals, st));
+      CUDA_CHECK(cudaStreamSynchronize(st));
+    } catch (...) {
+      cudaFreeAsync(vals, st);
+      cudaStreamSynchronize(st);
+      throw;
+    }
+    f0 = f1;
+  }
+  op->stats.reserved[6] = (int64_t)(1e6 * dev_s);  // device factorization time (us)
+}
+
 template <class BlockFn>
 void numeric_factor_blocks(sfcdd_op* op, std::vector<HostFactor>& fs, int32_t sf, BlockFn&& local_block) {
-  numeric_factor_blocks_host(op, fs, sf, local_block);
+  const char* e = std::getenv("SFCDD_HOST_NUMERIC");
+  if (e && std::atoi(e) != 0)
+    numeric_factor_blocks_host(op, fs, sf, local_block);
+  else
+    numeric_factor_blocks_device(op, fs, sf, local_block);
 }
 
 OpScope::OpScope(sfcdd_op* op, cudaStream_t caller) : op_(op), caller_(caller), lk_(op->mu) {

@@ -473,7 +473,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
       const bool use_asm = split_ok && gathered >= opt.asm_redundancy * (s + m);
       const bool global_asm = !use_asm && (huge || !row_split(true, split_i));
       const auto& split = (use_asm || global_asm) ? split_a : split_i;
-      int32_t asm16 = -1;
+      int64_t asm16 = -1;
       if (global_asm) {
         ints.assign({s, m});
         for (int32_t c = 0; c < s; ++c) ints.push_back(F.perm[S.col0 + c]);
@@ -484,7 +484,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         }
         for (int32_t p = 0; p < s + m; ++p) ints.insert(ints.end(), contrib[p].begin(), contrib[p].end());
         const int64_t asm_off = E.raw(ints);  // factor-local; rebased (asm16 patches) at the merge
-        asm16 = (int32_t)(asm_off / 16);
+        asm16 = asm_off / 16;
       }
       if (use_asm) {  // the assembled front [f_J ; f_B] at gr.f_off
         // forward assembly: f = [f_J ; f_B] in chunks of front positions
@@ -536,7 +536,8 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         ints[RW_YOFF] = (int32_t)gr.y_off;
         ints[RW_UOFF] = upd_slot[gr.factor][gr.top];
         ints[RW_FOFF] = use_asm ? (int32_t)gr.f_off : -1;
-        ints[RW_ASM16] = asm16;
+        ints[RW_ASM16] = (int32_t)(uint32_t)(asm16 & 0xffffffffLL);
+        ints[RW_ASM_HI] = asm16 >= 0 ? (int32_t)(asm16 >> 32) : -1;
         if (!use_asm && !global_asm) {
           ints[RW_COLS] = (int32_t)ints.size();
           for (int32_t c = 0; c < C; ++c) ints.push_back(F.perm[S.col0 + c]);
@@ -926,18 +927,22 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
       tot += E.size;
       meta_tot += (int64_t)E.image.size();
     }
-    SFCDD_REQUIRE(tot / 16 < (int64_t(1) << 31), SFCDD_EINTERNAL, "blob buffer too large");
     P.blob_bytes = tot;
     P.blobs.reserve(defer ? meta_tot : tot);
   }
   int64_t cursor = 0;
   for (FactorEmit& E : emits) {
     const int64_t dbase = cursor;
-    for (const auto& pa : E.asm_patches) {  // int32 word at image byte offset pa
-      int32_t v;
-      std::memcpy(&v, E.image.data() + pa, 4);
-      v += (int32_t)(dbase / 16);
-      std::memcpy(E.image.data() + pa, &v, 4);
+    for (const auto& pa : E.asm_patches) {  // (lo, hi) int32 words at image byte offset pa
+      uint32_t lo;
+      int32_t hi;
+      std::memcpy(&lo, E.image.data() + pa, 4);
+      std::memcpy(&hi, E.image.data() + pa + 4, 4);
+      const int64_t v = ((int64_t)hi << 32 | lo) + dbase / 16;
+      lo = (uint32_t)(v & 0xffffffffLL);
+      hi = (int32_t)(v >> 32);
+      std::memcpy(E.image.data() + pa, &lo, 4);
+      std::memcpy(E.image.data() + pa + 4, &hi, 4);
     }
     if (defer) {
       const int64_t hbase = (int64_t)P.blobs.size();

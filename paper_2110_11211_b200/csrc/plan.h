@@ -148,8 +148,9 @@ enum RowHdr {
   RW_COLS,     //   int offset: ro[C] (rhs gather)
   RW_PTR,      //   int offset: ptr[C+NB+1] / src[nnz]: CSR over the task's front
   RW_SRC,      //   positions (f_J[0:C), then its NB update rows) of child update indices
-  RW_ASM16,    // or (huge s, >= 0): byte offset / 16 of J's global assembly record
-               // [s, m] [cols (s)] [ptr (s+m+1)] [src] over FRONT positions
+  RW_ASM16,    // or (huge s): byte offset / 16 of J's global assembly record, low 32 bits
+  RW_ASM_HI,   //   ... high bits (-1: no record); record = [s, m] [cols (s)] [ptr (s+m+1)] [src]
+               //   over FRONT positions
   RW_VAL_OFF,  // byte offset of the values
   RW_SCRATCH,  // doubles of scratch used
   RW_WORDS

@@ -60,8 +60,9 @@ void plan_exec_host(const DevicePlan& P, const double* rhs, double* xy) {
         for (int32_t q = 0; q < C; ++q) S[q] = f[q];
         for (int32_t i = 0; i < NB; ++i) S[C + i] = f[r0 + i];
       } else {
-        const bool ga = h[RW_ASM16] >= 0;  // global assembly record (huge s)
-        const int32_t* am = reinterpret_cast<const int32_t*>(P.blobs.data() + 16 * (int64_t)std::max(0, h[RW_ASM16]));
+        const bool ga = h[RW_ASM_HI] >= 0;  // global assembly record (huge s)
+        const int64_t o16 = ga ? ((int64_t)(uint32_t)h[RW_ASM16] | ((int64_t)h[RW_ASM_HI] << 32)) : 0;
+        const int32_t* am = reinterpret_cast<const int32_t*>(P.blobs.data() + 16 * o16);
         const int32_t* cols = ga ? am + 2 : h + h[RW_COLS];
         const int32_t* ptr = ga ? am + 2 + am[0] : h + h[RW_PTR];
         const int32_t* src = ga ? ptr + am[0] + am[1] + 1 : h + h[RW_SRC];
