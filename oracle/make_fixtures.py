@@ -360,7 +360,33 @@ SOLVES = {
     # BASELINE configs[3] at full size on one device: 4095^2, P=256, q=16,
     # fault mode at apply 5; ~25 min and ~50 GB on the CPU
     "c4_fault": ((12, 12), 256, 0.5, 16, False, 5),
+    # C5-shaped reduced grid (BASELINE configs[4]): 3-D, gamma = 1/2, q = 64 and
+    # C5's subdomain size (31k disjoint / 62.5k overlapped points), P = 8
+    # instead of 512 so the reference's SuperLU setup fits this container
+    "c5shape": ((6, 6, 6), 8, 0.5, 64, True),
 }
+
+# perm hashes of the C5 weak-scaling levels (BASELINE configs[4] at G = 1, 2,
+# 4, 8), from the reference's own sfc_permutation (minutes to ~1 h each)
+C5_LEVELS = [(8, 8, 8), (8, 8, 9), (8, 9, 9), (9, 9, 9)]
+
+
+def make_c5_perm_hashes(ref):
+    path = OUT / "perm_hashes.json"
+    for lv in C5_LEVELS:
+        hashes = json.loads(path.read_text()) if path.exists() else {}
+        key = "_".join(map(str, lv))
+        if key in hashes:
+            continue
+        t0 = time.time()
+        p = ref.grid.sfc_permutation(lv)
+        h = perm_hash(p)
+        del p
+        ref.grid.sfc_permutation.cache_clear()
+        hashes = json.loads(path.read_text()) if path.exists() else {}
+        hashes[key] = h
+        path.write_text(json.dumps(hashes, indent=1))
+        print(f"perm {lv}: {time.time() - t0:.1f}s", flush=True)
 
 
 def main():
@@ -372,6 +398,9 @@ def main():
     ref = load_reference()
     if args.only == "harness":
         make_harness(ref)
+        return
+    if args.only == "c5_perms":
+        make_c5_perm_hashes(ref)
         return
     if args.only:
         make_solve(ref, args.only, *SOLVES[args.only])
