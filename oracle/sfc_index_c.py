@@ -81,3 +81,33 @@ def aggregates(dj_start, dj_len, q: int) -> np.ndarray:
     rc = lib().oracle_aggregates(p, ds.ctypes.data, dl.ctypes.data, q, out.ctypes.data)
     assert rc == 0
     return out
+
+
+def scaled_block(levels, perm, rank, start, length):
+    """Â restricted to the cyclic SFC range [start, start + length): the
+    reference's Â[idx][:, idx] (schwarz.py:58-61), assembled from the C
+    oracle's permutation and the stencil constants (grid.py:91-130)."""
+    import scipy.sparse as sp
+    import sfcdd_oracle as O
+
+    n = perm.shape[0]
+    shape = O.interior_shape(levels)
+    dhat, offs, _ = O.stencil_constants(levels)
+    idx = (start + np.arange(length)) % n
+    lex = perm[idx]
+    coords = np.stack(np.unravel_index(lex, shape), axis=1)
+    strides = [int(np.prod(shape[j + 1:])) for j in range(len(shape))]
+    rows, cols, vals = [np.arange(length)], [np.arange(length)], [np.full(length, dhat)]
+    for j in range(len(shape)):
+        for step in (-1, 1):
+            ok = (coords[:, j] + step >= 0) & (coords[:, j] + step < shape[j])
+            r = np.nonzero(ok)[0]
+            nb = rank[lex[r] + step * strides[j]]
+            loc = (nb - start) % n
+            inside = loc < length
+            rows.append(r[inside])
+            cols.append(loc[inside])
+            vals.append(np.full(int(inside.sum()), offs[j]))
+    B = sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))), shape=(length, length))
+    B.sort_indices()
+    return B

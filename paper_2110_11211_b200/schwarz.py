@@ -110,7 +110,12 @@ class SchwarzOperator:
     def stats(self) -> dict:
         s = _lib.Stats()
         _lib.check(_lib.lib().sfcdd_op_stats(self._h, ctypes.byref(s)))
-        return {f: getattr(s, f) for f, _ in _lib.Stats._fields_ if f != "reserved"}
+        out = {f: getattr(s, f) for f, _ in _lib.Stats._fields_ if f != "reserved"}
+        # setup phases (csrc/op.cu sfcdd_op_setup): ordering + symbolic
+        # analysis, execution plan, numeric factorization (wall / device)
+        out["plan_seconds"] = s.reserved[4] * 1e-6
+        out["numeric_device_seconds"] = s.reserved[6] * 1e-6
+        return out
 
     def coarse_matrix_dense(self) -> np.ndarray:
         n0 = self.stats()["n0"]
