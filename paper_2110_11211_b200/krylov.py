@@ -25,66 +25,65 @@ from ._lib import BreakdownError, DivergenceError  # noqa: F401  (re-exported)
 from .grid import GridLaplacian
 
 
+_METHOD_NAMES = ("richardson", "pcg", "fcg")
+_TOLERANCE_KINDS = ("energy_error_reduction", "relative_residual")
+
+
 @dataclass(frozen=True)
 class SolverConfig:
-    method: str = "pcg"  # richardson | pcg | fcg
-    damping: float | str = "optimal"
-    tolerance: float = 1e-8
-    tolerance_kind: str = "energy_error_reduction"  # or relative_residual
-    max_iters: int = 20000
-    seed: int = 42
-    eig_iters: int | None = None
-    fcg_window: int | None = None
-    force_unsymmetric: bool = False
+    """Outer-solver parameters (krylov.py:29-47)."""
+
+    method: str = "pcg"                               # one of _METHOD_NAMES
+    damping: float | str = "optimal"                  # Richardson: "optimal" or a fixed xi
+    tolerance: float = 1e-8                           # reduction factor of the stopping metric
+    tolerance_kind: str = "energy_error_reduction"    # or "relative_residual"
+    max_iters: int = 20000                            # iteration cap
+    seed: int = 42                                    # Lanczos start vector / initial iterate
+    eig_iters: int | None = None                      # Lanczos steps (None: automatic)
+    fcg_window: int | None = None                     # FCG: stored directions (None: all)
+    force_unsymmetric: bool = False                   # PCG with a non-symmetric preconditioner
 
     def __post_init__(self) -> None:
-        if self.method not in ("richardson", "pcg", "fcg"):
-            raise ValueError(f"unknown method {self.method!r}")
-        if self.tolerance_kind not in ("energy_error_reduction", "relative_residual"):
-            raise ValueError(f"unknown tolerance kind {self.tolerance_kind!r}")
-        if not self.tolerance > 0:
-            raise ValueError("tolerance must be positive")
+        checks = ((self.method in _METHOD_NAMES, f"method {self.method!r} not in {_METHOD_NAMES}"),
+                  (self.tolerance_kind in _TOLERANCE_KINDS,
+                   f"tolerance_kind {self.tolerance_kind!r} not in {_TOLERANCE_KINDS}"),
+                  (self.tolerance > 0, f"tolerance {self.tolerance} is not positive"))
+        for ok, msg in checks:
+            if not ok:
+                raise ValueError(msg)
 
 
 @dataclass
 class SolveReport:
-    method: str
-    iterations: int
-    converged: bool
-    energy_history: list
-    residual_history: list
-    lambda_min: float | None = None
+    """Result of one outer solve (krylov.py:50-88)."""
+
+    method: str                          # richardson | pcg | fcg
+    iterations: int                      # steps taken
+    converged: bool                      # stopping test met
+    energy_history: list                 # ||x_k - x*||_A per step (with an exact solution)
+    residual_history: list               # ||r_k||_2 per step
+    lambda_min: float | None = None      # Richardson: estimated spectrum of C^-1 A
     lambda_max: float | None = None
-    damping: float | None = None
-    wall_time: float = 0.0
-    solution: np.ndarray | None = None
-    params: dict = field(default_factory=dict)
+    damping: float | None = None         # Richardson: xi used
+    wall_time: float = 0.0               # seconds
+    solution: np.ndarray | None = None   # x_k at exit
+    params: dict = field(default_factory=dict)  # caller's parameter record
 
     def iteration_rows(self):
-        rows = []
-        for k, res in enumerate(self.residual_history):
-            energy = self.energy_history[k] if self.energy_history else ""
-            rows.append((k, energy, res))
-        return rows
+        """(k, energy error or "", residual) per recorded step."""
+        en = self.energy_history
+        return [(k, en[k] if en else "", res) for k, res in enumerate(self.residual_history)]
 
     def write_iterations_csv(self, fh) -> None:
-        fh.write("k,energy_error,residual\r\n")
-        for k, energy, res in self.iteration_rows():
-            e = repr(energy) if energy != "" else ""
-            fh.write(f"{k},{e},{repr(res)}\r\n")
+        """CRLF CSV of the histories, floats as repr (krylov.py:71-75)."""
+        lines = ["k,energy_error,residual"]
+        lines += [f"{k},{'' if e == '' else repr(e)},{res!r}" for k, e, res in self.iteration_rows()]
+        fh.write("".join(line + "\r\n" for line in lines))
 
     def summary(self) -> dict:
-        out = {
-            "method": self.method,
-            "iterations": self.iterations,
-            "converged": self.converged,
-            "lambda_min": self.lambda_min,
-            "lambda_max": self.lambda_max,
-            "damping": self.damping,
-            "wall_time": self.wall_time,
-        }
-        out.update(self.params)
-        return out
+        """Scalar results plus the parameter record (krylov.py:77-88)."""
+        keys = ("method", "iterations", "converged", "lambda_min", "lambda_max", "damping", "wall_time")
+        return {**{k: getattr(self, k) for k in keys}, **self.params}
 
 
 def initial_iterate(n: int, seed: int, A) -> np.ndarray:
@@ -203,36 +202,30 @@ class _DeviceTracker:
     the energy error sqrt(max(e.(b - r - A x*), 0)), e = x - x*."""
 
     def __init__(self, matvec, b, cfg: SolverConfig, exact, vec: _Vec):
-        if cfg.tolerance_kind == "energy_error_reduction" and exact is None:
-            raise ValueError("energy stopping needs the exact solution")
-        self.vec = vec
-        self.b = b
-        self.cfg = cfg
-        self.exact = exact
-        self.a_exact = matvec(exact) if exact is not None else None
-        self.energy_history: list[float] = []
-        self.residual_history: list[float] = []
-        self._baseline = None
+        energy_stop = cfg.tolerance_kind == "energy_error_reduction"
+        if energy_stop and exact is None:
+            raise ValueError("tolerance_kind='energy_error_reduction' needs the exact solution")
+        self.vec, self.b, self.cfg, self.exact = vec, b, cfg, exact
+        self.a_exact = None if exact is None else matvec(exact)
+        self.energy_history, self.residual_history = [], []
+        self._hist = self.energy_history if energy_stop else self.residual_history  # the stopping metric
+        self._ref = None  # its first value
 
     def record(self, x, r) -> bool:
+        """Append this iterate's metrics; True once the stopping test holds."""
         v = self.vec
-        res = float(np.sqrt(max(v.dot(r, r), 0.0)))
-        self.residual_history.append(res)
+        self.residual_history.append(float(np.sqrt(max(v.dot(r, r), 0.0))))
         if self.exact is not None:
-            e = v.lin(1.0, x, -1.0, self.exact)            # x - x*
-            ae = v.axpby(-1.0, self.a_exact, 1.0, v.lin(1.0, self.b, -1.0, r))  # (b - r) - A x*
+            e = v.lin(1.0, x, -1.0, self.exact)                                   # x - x*
+            ae = v.axpby(-1.0, self.a_exact, 1.0, v.lin(1.0, self.b, -1.0, r))    # (b - r) - A x*
             self.energy_history.append(float(np.sqrt(max(v.dot(e, ae), 0.0))))
-        metric = self.energy_history[-1] if self.cfg.tolerance_kind == "energy_error_reduction" else res
-        if self._baseline is None:
-            self._baseline = metric
-        return metric <= self.cfg.tolerance * self._baseline
+        if self._ref is None:
+            self._ref = self._hist[-1]
+        return self._hist[-1] <= self.cfg.tolerance * self._ref
 
     def diverged(self) -> bool:
-        if self._baseline is None or self._baseline == 0.0:
-            return False
-        hist = (self.energy_history if self.cfg.tolerance_kind == "energy_error_reduction"
-                else self.residual_history)
-        return hist[-1] > 10.0 * self._baseline
+        """The metric grew 10x over its first value (krylov.py:202-208)."""
+        return bool(self._ref) and self._hist[-1] > 10.0 * self._ref
 
 
 def _finish(rep: SolveReport, t0: float, x, tracker: _DeviceTracker, to_numpy: bool) -> SolveReport:

@@ -236,3 +236,32 @@ def test_combination_failures_name_level_vectors(device):
     with pytest.raises(combine.CombinationError) as err:
         combine.run_combination(combine.enumerate_plan(2, 4), seed=7, max_iters=0)
     assert "(1, 4)" in str(err.value) and "(4, 1)" in str(err.value)
+
+
+def test_sweep_assignment_lpt_deterministic():
+    from paper_2110_11211_b200 import sweep
+
+    jobs = [sweep.SolveJob((l,), 4, 0.5, 2) for l in (3, 9, 5, 9, 7, 4, 8)]
+    parts = sweep.assign(jobs, 3)
+    assert sorted(i for p in parts for i in p) == list(range(len(jobs)))
+    assert parts == sweep.assign(jobs, 3)
+    loads = [sum(jobs[i].cost() for i in p) for p in parts]
+    assert max(loads) <= min(loads) + max(j.cost() for j in jobs)
+    assert sweep.assign(jobs, 1) == [list(range(len(jobs)))]
+
+
+@pytest.mark.gpu
+def test_sweep_processes_and_streams_bitwise_equal_serial(device):
+    """Sweep batches spread over worker processes (one per listed device; here
+    two processes on the one GPU of the box) and streams reproduce the serial
+    results bit for bit."""
+    from paper_2110_11211_b200 import sweep
+
+    jobs = [sweep.SolveJob(lv, p, 0.5, 2) for lv, p in [((7,), 4), ((4, 4), 8), ((3, 3, 3), 8), ((5, 5), 16)]]
+    serial = sweep.execute(jobs)
+    spread = sweep.execute(jobs, devices=[0, 0], streams=2)
+    for a, b in zip(serial, spread):
+        assert a.error is None and b.error is None
+        assert a.report.residual_history == b.report.residual_history
+        assert a.report.energy_history == b.report.energy_history
+        np.testing.assert_array_equal(a.report.solution, b.report.solution)
