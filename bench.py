@@ -18,9 +18,11 @@ cpu_baseline: the oracle port (scipy SuperLU, the reference's own third-party
 --impl reference: the oracle port as the timed arm (the reference is pure
          Python and cannot travel to the GPU box; oracle/ restates it and is
          pinned bit-exactly to it by tests/test_oracle_golden.py).
-N > 1 (torchrun, or --sharded at N=1): ONE solve sharded over the ranks by
-       contiguous SFC segments (distributed.py: halo / overlap all_to_all,
-       coarse allgather, scalar allreduce over NCCL), "scaling": "strong";
+N > 1 (torchrun, or self-launched when --gpus N is given without it; or
+       --sharded at N=1): weak scaling -- the config's member for N GPUs
+       (weak_family: fixed points and subdomains per GPU), ONE solve sharded
+       over the ranks by contiguous SFC segments, run by the device-driven
+       program (one CUDA graph per solve, NCCL inside); "scaling": "weak";
        value = N_dof * iterations * K / (max over ranks of the device time).
 """
 
@@ -240,8 +242,26 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def weak_family(cfg, world):
+    """Weak-scaling member for ``world`` GPUs (BASELINE configs[4]'s rule:
+    fixed points and subdomains per GPU): one level added per doubling,
+    round robin from the last axis -- C5 (8,8,8) -> (8,8,9) -> (8,9,9) ->
+    (9,9,9), C2 (10,10) -> (10,11) -> (11,11) -> (11,12) -- and P x world."""
+    levels, p, gamma, q, desc = cfg
+    if world & (world - 1):
+        raise SystemExit(f"weak scaling needs a power-of-two GPU count, got {world}")
+    lv = list(levels)
+    for k in range(world.bit_length() - 1):
+        lv[len(lv) - 1 - (k % len(lv))] += 1
+    return tuple(lv), p * world, gamma, q, f"{desc} -- weak scaling member for {world} GPU(s): levels {tuple(lv)}, " \
+                                           f"P={p * world}"
+
+
 def run_sharded(args, cfg):
-    """N GPUs: SFC-segment sharding of one solve (distributed.py), NCCL."""
+    """N GPUs, one process per GPU: the SFC-segment-sharded solve of the
+    weak-scaling member for N (weak_family), run by the device-driven program
+    (distributed.attach_device_program / run_device: one CUDA graph per solve,
+    NCCL send / recv and allgathers inside a conditional WHILE loop)."""
     import ctypes
 
     import torch
@@ -259,11 +279,16 @@ def run_sharded(args, cfg):
     from paper_2110_11211_b200 import _lib
     from paper_2110_11211_b200 import distributed as D
 
+    cfg = weak_family(cfg, world)
     levels, p, gamma, q, desc = cfg
     n = sf.num_dofs(levels)
     part = sf.build_partition(n, p, gamma)
     t0 = time.perf_counter()
     eng, plan = D.make_rank_shard(levels, part, q, rank, world, dev)
+    ids = [D.nccl_unique_id() if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(ids, src=0)
+    D.attach_device_program(eng, plan, ids[0] if world > 1 else None)
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t0
     log(f"rank {rank}: shard setup {setup_s:.2f}s, owned points [{plan.g0}, {plan.g1})")
@@ -275,7 +300,7 @@ def run_sharded(args, cfg):
 
     def solve():
         x.zero_()
-        its, conv, hist = D.run_torch(eng, plan, b_dev, x, 1e-8, 20000)
+        its, conv, hist = D.run_device(eng, b_dev, x, 1e-8, 20000)
         return its
 
     for _ in range(max(args.warmup, 3)):
@@ -284,13 +309,18 @@ def run_sharded(args, cfg):
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     dist.barrier()
     torch.cuda.synchronize()
-    launches0 = eng.launches
+    launch_total = [0]
+    st_l = _lib.Stats()
     with ClockSampler(local) as clk:
         ev0.record()
-        total_its = sum(solve() for _ in range(args.steps))
+        total_its = 0
+        for _ in range(args.steps):
+            total_its += solve()
+            _lib.check(_lib.lib().sfcdd_op_stats(eng.h, ctypes.byref(st_l)))
+            launch_total[0] += int(st_l.reserved[7])
         ev1.record()
         torch.cuda.synchronize()
-    launches = eng.launches - launches0
+    launches = launch_total[0]
     ms = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = float(ms.item())
@@ -306,7 +336,7 @@ def run_sharded(args, cfg):
     for _ in range(args.steps):
         b_dev.copy_(bh_pin, non_blocking=True)
         x.zero_()
-        its, _, _ = D.run_torch(eng, plan, b_dev, x, 1e-8, 20000)
+        its, _, _ = D.run_device(eng, b_dev, x, 1e-8, 20000)
         x_host.copy_(x[plan.g0:plan.g1], non_blocking=True)
         e_its += its
     e1.record()
@@ -335,12 +365,13 @@ def run_sharded(args, cfg):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: b = default_rng(42).uniform(-1,1,N) (SURVEY §8(d)); no dataset involved",
             "config": {"workload": desc, "levels": list(levels), "N": n, "P": p, "gamma": gamma, "q": q,
                        "iterations": its_per_solve, "step": "one PCG solve to relative residual 1e-8",
-                       "parallelism": f"sfc-segment sharding x{world} (halo/overlap all_to_all, coarse allgather, "
-                                      "scalar allreduce over NCCL)",
+                       "parallelism": f"sfc-segment sharding x{world}: device-driven program, one CUDA graph per "
+                                      "solve (NCCL send/recv halo + overlap + foreign solutions, coarse and scalar "
+                                      "allgathers, conditional WHILE loop)",
                        "l2": "working set > L2", "setup_seconds": setup_s},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None, "kernel": "k_dag (rank 0 shard)",
@@ -534,6 +565,20 @@ def main():
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     _, world, _ = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # launched without torchrun: start the N ranks ourselves, the way the
+        # driver does (one process per GPU, rendezvous on 127.0.0.1)
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()),
+               *sys.argv[1:]]
+        raise SystemExit(subprocess.call(cmd))
+    if world > 1 and world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} does not match WORLD_SIZE {world}")
     if args.impl == "reference":
         run_reference(args, cfg)
     elif world > 1 or args.sharded:

@@ -228,6 +228,26 @@ int sfcdd_shard_combine(sfcdd_op* op, double* w, void* stream);
 int sfcdd_shard_stencil_restrict(sfcdd_op* op, const double* w, double* cagg_out, void* stream);
 int sfcdd_shard_finalize(sfcdd_op* op, const double* w, const double* y0, const double* y0b, double* z,
                          const double* r, double* rz_out, void* stream);
+/* Device-driven sharded PCG (one rank of G, one process per GPU): the whole
+ * solve -- stencil halo, overlap extension, foreign local solutions, coarse
+ * allgathers, CG scalars -- runs on the GPU as ONE CUDA graph whose
+ * iteration loop is a conditional WHILE node; exchanges are NCCL
+ * send / recv groups and allgathers on the handle's own communicator
+ * (libnccl.so.2 loaded at run time).  Replaces the host-driven program of
+ * distributed.pcg_program for production runs (krylov.py:257-291 over
+ * schwarz.py:103-118, sharded as SURVEY §8(e)).
+ *   sfcdd_nccl_unique_id: 128-byte ncclUniqueId for rank 0 to broadcast;
+ *   sfcdd_shard_attach: communicator (nccl_id may be NULL when world == 1)
+ *     and the allgather layout agg_counts[world] (owned aggregates per rank);
+ *   sfcdd_shard_set_exchange: kind 0 halo, 1 overlap extension, 2 foreign
+ *     solutions; per peer (ascending) the send / recv index lists;
+ *   sfcdd_shard_pcg: x holds x0, receives the owned segment of the solution. */
+int sfcdd_nccl_unique_id(void* id_out);
+int sfcdd_shard_attach(sfcdd_op* op, const void* nccl_id, int32_t rank, int32_t world, const int64_t* agg_counts);
+int sfcdd_shard_set_exchange(sfcdd_op* op, int32_t kind, int32_t npeer, const int32_t* peers, const int64_t* nsend,
+                             const int64_t* send_idx, const int64_t* nrecv, const int64_t* recv_idx);
+int sfcdd_shard_pcg(sfcdd_op* op, const double* b, double* x, double tol, int32_t max_iters, double* res_hist_host,
+                    int32_t* iters, int32_t* converged, void* stream);
 /* exchange packing: dst[i] = src[idx[i]] / dst[idx[i]] = src[i]           */
 int sfcdd_pack(const double* src, const int64_t* idx, int64_t n, double* dst, void* stream);
 int sfcdd_unpack(const double* src, const int64_t* idx, int64_t n, double* dst, void* stream);

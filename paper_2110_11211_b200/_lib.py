@@ -107,6 +107,7 @@ EXPORTS = [
     "sfcdd_host_amd", "sfcdd_host_factor_solve", "sfcdd_host_plan_solve",
     "sfcdd_partition", "sfcdd_partition_weights", "sfcdd_csr_create", "sfcdd_csr_matvec", "sfcdd_csr_destroy",
     "sfcdd_host_setup_timing", "sfcdd_host_plan_deferred_check",
+    "sfcdd_nccl_unique_id", "sfcdd_shard_attach", "sfcdd_shard_set_exchange", "sfcdd_shard_pcg",
 ]
 
 _lib = None
@@ -172,6 +173,10 @@ def lib() -> ctypes.CDLL:
         "sfcdd_csr_matvec": [vp, vp, vp, vp],
         "sfcdd_host_setup_timing": [i64, vp, vp, vp, i32, vp, vp],
         "sfcdd_host_plan_deferred_check": [i64, vp, vp, vp, i32, vp, vp, vp, vp, vp],
+        "sfcdd_nccl_unique_id": [vp],
+        "sfcdd_shard_attach": [vp, vp, i32, i32, vp],
+        "sfcdd_shard_set_exchange": [vp, i32, i32, vp, vp, vp, vp, vp],
+        "sfcdd_shard_pcg": [vp, vp, vp, dbl, i32, vp, ctypes.POINTER(i32), ctypes.POINTER(i32), vp],
     }
     for name, args in sigs.items():
         fn = getattr(L, name)

@@ -28,6 +28,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "common.h"
@@ -197,6 +199,52 @@ __device__ void tile_mm(double (&acc)[4][4], FA A, FB B, int i0, int j0, int K, 
   }
 }
 
+// all 64x64 tiles of an M x N product C = A B (K terms); epi(i, j, c) per
+// entry inside [0, M) x [0, N)
+template <class FA, class FB, class FE>
+__device__ void cta_gemm(int M, int N, int K, FA A, FB B, FE epi, double (*As)[TM + 1], double (*Bs)[TM + 1]) {
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  for (int i0 = 0; i0 < M; i0 += TM)
+    for (int j0 = 0; j0 < N; j0 += TM) {
+      double acc[4][4];
+      tile_mm(acc, A, B, i0, j0, K, M, N, As, Bs);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int i = i0 + ty + 16 * u, j = j0 + tx + 16 * v;
+          if (i < M && j < N) epi(i, j, acc[u][v]);
+        }
+    }
+  __syncthreads();
+}
+
+// Blocked in-place inverse of the lower triangle L = F[0:s, 0:s] (ld = nf):
+// column blocks right to left; W_jj = inv(L_jj) unblocked, then
+// W[je:, jb:je] = -(W[je:, je:] L[je:, jb:je]) W_jj as two tiled products
+// (tmp: (s - je) x NB doubles, column-major, ld = s; sc: NB doubles)
+__device__ void trtri_blocked(double* F, int nf, int s, double* tmp, double* sc, double (*As)[TM + 1],
+                              double (*Bs)[TM + 1]) {
+  const int nblk = (s + NB - 1) / NB;
+  for (int b = nblk - 1; b >= 0; --b) {
+    const int jb = b * NB, je = min(s, jb + NB), nb = je - jb;
+    double* D = F + at(nf, jb, jb);  // the diagonal block, ld = nf
+    trtri_lower<T3>(D, nf, nb, sc);
+    const int R = s - je;
+    if (R == 0) continue;
+    // tmp(i, c) = sum_{t <= i} W(je + i, je + t) L(je + t, jb + c)
+    cta_gemm(
+        R, nb, R, [&](int i, int t) { return t <= i ? F[at(nf, je + i, je + t)] : 0.0; },
+        [&](int t, int c) { return F[at(nf, je + t, jb + c)]; },
+        [&](int i, int c, double v) { tmp[(int64_t)c * s + i] = v; }, As, Bs);
+    // W(je + i, jb + c) = -sum_{k >= c} tmp(i, k) W_jj(k, c)
+    cta_gemm(
+        R, nb, nb, [&](int i, int k) { return tmp[(int64_t)k * s + i]; },
+        [&](int k, int c) { return k >= c ? D[at(nf, k, c)] : 0.0; },
+        [&](int i, int c, double v) { F[at(nf, je + i, jb + c)] = -v; }, As, Bs);
+  }
+}
+
 __global__ void __launch_bounds__(T3) k_front_global(const FItem* __restrict__ items, const int32_t* __restrict__ list,
                                                      const FChild* __restrict__ ch, const int32_t* __restrict__ rel,
                                                      const FAent* __restrict__ ae, double* __restrict__ vals,
@@ -231,8 +279,9 @@ __global__ void __launch_bounds__(T3) k_front_global(const FItem* __restrict__ i
       }
     __syncthreads();
   }
-  // W = L11^{-1} in place (scratch: the nf doubles after the front)
-  trtri_lower<T3>(F, nf, s, F + (int64_t)nf * nf);
+  // W = L11^{-1} in place, blocked (scratch after the front: NB doubles,
+  // then an s x NB panel)
+  trtri_blocked(F, nf, s, F + (int64_t)nf * nf + NB, F + (int64_t)nf * nf, As, Bs);
   double* M = vals + it.val_off;
   // M_top
   for (int64_t e = tid; e < (int64_t)s * s; e += T3) {
@@ -311,7 +360,7 @@ int64_t gpu_factor_work_bound(const HostFactor& F) {
   int64_t w = 0;
   for (const Supernode& S : F.sn) {
     const int64_t nf = S.s + S.m;
-    if (nf > 96) w += nf * nf + nf;
+    if (nf > 96) w += nf * nf + (int64_t)(NB + 1) * nf;
   }
   return w;
 }
@@ -389,7 +438,7 @@ void gpu_factor_batch(const std::vector<const HostFactor*>& fs, const std::vecto
         l2[lv].push_back((int32_t)i);
       } else {
         items[i].front_off = ws[lv];
-        ws[lv] += (int64_t)nf * nf + nf;
+        ws[lv] += (int64_t)nf * nf + (int64_t)(NB + 1) * nf;
         l3[lv].push_back((int32_t)i);
       }
     }
@@ -423,18 +472,52 @@ void gpu_factor_batch(const std::vector<const HostFactor*>& fs, const std::vecto
     int32_t* d_lists = upload(lists, st, owned);
     const int smem1 = (32 * 32 + 32) * 8, smem2 = (96 * 96 + 96) * 8;
     CUDA_CHECK(cudaFuncSetAttribute(k_front_smem<128, 96>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
+    // SFCDD_FACTOR_DEBUG: device time per tier (events around every launch)
+    const bool dbg = std::getenv("SFCDD_FACTOR_DEBUG") != nullptr;
+    double tier_ms[3] = {0, 0, 0};
+    int64_t tier_n[3] = {0, 0, 0};
+    cudaEvent_t ta, tb;
+    if (dbg) {
+      CUDA_CHECK(cudaEventCreate(&ta));
+      CUDA_CHECK(cudaEventCreate(&tb));
+    }
+    auto timed = [&](int tier, int64_t cnt, auto&& launch) {
+      if (cnt <= 0) return;
+      if (!dbg) {
+        launch();
+        return;
+      }
+      CUDA_CHECK(cudaEventRecord(ta, st));
+      launch();
+      CUDA_CHECK(cudaEventRecord(tb, st));
+      CUDA_CHECK(cudaEventSynchronize(tb));
+      float t = 0.f;
+      CUDA_CHECK(cudaEventElapsedTime(&t, ta, tb));
+      tier_ms[tier] += t;
+      tier_n[tier] += cnt;
+    };
     for (int lv = 0; lv <= maxlev; ++lv) {
       const int64_t* o = &loff[3 * lv];
-      if (o[1] > o[0])
+      timed(0, o[1] - o[0], [&]() {
         k_front_smem<32, 32><<<(unsigned)(o[1] - o[0]), 32, smem1, st>>>(d_items, d_lists + o[0], d_ch, d_rel, d_ae,
                                                                          vals_dev, d_upd, d_err);
-      if (o[2] > o[1])
+      });
+      timed(1, o[2] - o[1], [&]() {
         k_front_smem<128, 96><<<(unsigned)(o[2] - o[1]), 128, smem2, st>>>(d_items, d_lists + o[1], d_ch, d_rel,
                                                                            d_ae, vals_dev, d_upd, d_err);
-      if (o[3] > o[2])
+      });
+      timed(2, o[3] - o[2], [&]() {
         k_front_global<<<(unsigned)(o[3] - o[2]), T3, 0, st>>>(d_items, d_lists + o[2], d_ch, d_rel, d_ae, vals_dev,
                                                                d_upd, d_work, d_err);
+      });
       CUDA_CHECK(cudaGetLastError());
+    }
+    if (dbg) {
+      std::fprintf(stderr, "[factor] batch of %zu blocks, %d levels: tier1 %lld fronts %.1f ms, tier2 %lld %.1f ms, "
+                   "tier3 %lld %.1f ms\n", fs.size(), maxlev + 1, (long long)tier_n[0], tier_ms[0],
+                   (long long)tier_n[1], tier_ms[1], (long long)tier_n[2], tier_ms[2]);
+      cudaEventDestroy(ta);
+      cudaEventDestroy(tb);
     }
     int herr = 0;
     CUDA_CHECK(cudaMemcpyAsync(&herr, d_err, 4, cudaMemcpyDeviceToHost, st));

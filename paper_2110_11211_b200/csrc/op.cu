@@ -2177,6 +2177,7 @@ extern "C" void sfcdd_op_destroy(sfcdd_op* op) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   op->dag.reset();
+  if (op->srt) destroy_shard_runtime(op->srt);
   if (op->ev_in) cudaEventDestroy(op->ev_in);
   if (op->ev_out) cudaEventDestroy(op->ev_out);
   if (op->ev0) cudaEventDestroy(op->ev0);
@@ -2213,9 +2214,10 @@ __global__ void k_sh_residual(const double* __restrict__ b, const double* __rest
   }
 }
 
-__global__ void k_sh_pm(const double* __restrict__ z, const double* __restrict__ pold, double beta, Stencil S,
+__global__ void k_sh_pm(const double* __restrict__ z, const double* __restrict__ pold, double beta_h, Stencil S,
                         Chunks C, int ch0, double* __restrict__ pnew, double* __restrict__ ap,
-                        double* __restrict__ part) {
+                        double* __restrict__ part, const double* __restrict__ beta_d = nullptr) {
+  const double beta = beta_d ? *beta_d : beta_h;  // device-driven PCG: beta on the device
   const int ch = ch0 + blockIdx.x;
   double s = 0.0;
   const int64_t c_end = C.start[ch + 1];
@@ -2235,8 +2237,11 @@ __global__ void k_sh_pm(const double* __restrict__ z, const double* __restrict__
 }
 
 __global__ void k_sh_update(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
-                            const double* __restrict__ ap, double alpha, Chunks C, int ch0,
-                            double* __restrict__ prr, double* __restrict__ pc) {
+                            const double* __restrict__ ap, double alpha_h, Chunks C, int ch0,
+                            double* __restrict__ prr, double* __restrict__ pc,
+                            const double* __restrict__ alpha_d = nullptr, const int32_t* __restrict__ skip = nullptr) {
+  if (skip && *skip) return;  // breakdown: x and r stay those of the last iterate
+  const double alpha = alpha_d ? *alpha_d : alpha_h;
   const int ch = ch0 + blockIdx.x;
   double rr = 0.0, cs = 0.0;
   const int64_t c_end = C.start[ch + 1];
@@ -2671,5 +2676,475 @@ extern "C" int sfcdd_vec_axpby(double a, const double* x_dev, double b, double* 
   const unsigned blocks = (unsigned)std::min<int64_t>(4 * 148, (n + VEC_THREADS - 1) / VEC_THREADS);
   k_axpby<<<blocks, VEC_THREADS, 0, (cudaStream_t)stream>>>(a, x_dev, b, y_dev, n);
   CUDA_CHECK(cudaGetLastError());
+  SFCDD_API_END
+}
+
+// ================================================ device-driven shard PCG
+// Multi-GPU (VERDICT r1 "next" 4): one rank's balanced-Schwarz
+// PCG (krylov.py:257-291 over schwarz.py:103-118) with every exchange and
+// every scalar on the device -- NCCL point-to-point for the halo / overlap
+// / foreign-solution exchanges, NCCL allgathers for the Bank-Holst coarse
+// restrictions (every rank then solves the full coarse problem) and for the
+// CG scalar partials (summed in rank order on the device, so all ranks take
+// bitwise identical decisions) -- captured ONCE as a CUDA graph whose
+// iteration loop is a conditional WHILE node: a solve is one graph launch,
+// with no host round trip per iteration.  Same step order and exchange
+// plans as distributed.pcg_program (the host-driven reference
+// implementation of this program, kept for lockstep and gloo tests).
+// NCCL is loaded with dlopen (libnccl.so.2, the one torch already loaded
+// when present), so the library itself has no link dependency on it.
+#include <dlfcn.h>
+#include <nccl.h>
+
+namespace sfcdd {
+namespace {
+
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    auto sym = [&](const char* n) { return dlsym(h, n); };
+    api.GetUniqueId = (decltype(api.GetUniqueId))sym("ncclGetUniqueId");
+    api.CommInitRank = (decltype(api.CommInitRank))sym("ncclCommInitRank");
+    api.CommDestroy = (decltype(api.CommDestroy))sym("ncclCommDestroy");
+    api.Send = (decltype(api.Send))sym("ncclSend");
+    api.Recv = (decltype(api.Recv))sym("ncclRecv");
+    api.AllGather = (decltype(api.AllGather))sym("ncclAllGather");
+    api.GroupStart = (decltype(api.GroupStart))sym("ncclGroupStart");
+    api.GroupEnd = (decltype(api.GroupEnd))sym("ncclGroupEnd");
+    api.GetErrorString = (decltype(api.GetErrorString))sym("ncclGetErrorString");
+    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Send && api.Recv && api.AllGather &&
+             api.GroupStart && api.GroupEnd && api.GetErrorString;
+  });
+  return api;
+}
+
+#define NCCL_CHECK(expr)                                                                       \
+  do {                                                                                         \
+    ncclResult_t _r = (expr);                                                                  \
+    if (_r != ncclSuccess)                                                                     \
+      throw ::sfcdd::Error(SFCDD_ECUDA, std::string("NCCL: ") + nccl().GetErrorString(_r));  \
+  } while (0)
+
+// device scalars of the sharded PCG
+struct ShState {
+  double rz, pap, alpha, beta, h0, tol;
+  int32_t k, done, conv, brk, max_iters, pad;
+};
+
+__device__ __forceinline__ double rank_sum(const double* v, int world) {
+  double s = 0.0;
+  for (int i = 0; i < world; ++i) s += v[i];  // rank order: identical on every rank
+  return s;
+}
+
+struct ShParams {
+  double tol;
+  int32_t max_iters, pad;
+};
+__global__ void k_sc_start(ShState* st, const ShParams* prm) {
+  st->tol = prm->tol;
+  st->max_iters = prm->max_iters;
+  st->k = st->done = st->conv = st->brk = 0;
+  st->rz = st->pap = st->alpha = st->beta = st->h0 = 0.0;
+}
+// ||r0|| (krylov.py:267-271)
+__global__ void k_sc_r0(ShState* st, const double* all, int world, double* hist) {
+  const double h0 = sqrt(rank_sum(all, world));
+  st->h0 = h0;
+  hist[0] = h0;
+  if (h0 <= st->tol * h0) st->done = st->conv = 1;
+}
+__global__ void k_sc_rz0(ShState* st, const double* all, int world) { st->rz = rank_sum(all, world); }
+// alpha = rz / p.Ap; nonpositive curvature stops the loop (krylov.py:276-281)
+__global__ void k_sc_alpha(ShState* st, const double* all, int world) {
+  const double pap = rank_sum(all, world);
+  st->pap = pap;
+  if (!(pap > 0.0)) {
+    st->brk = 1;
+    st->done = 1;
+  } else {
+    st->alpha = st->rz / pap;
+  }
+}
+// history and stopping (krylov.py:283-286); sets the WHILE condition
+__global__ void k_sc_rr(ShState* st, const double* all, int world, double* hist, cudaGraphConditionalHandle h) {
+  if (!st->brk) {
+    const int k = st->k + 1;
+    st->k = k;
+    const double nrm = sqrt(rank_sum(all, world));
+    hist[k] = nrm;
+    if (nrm <= st->tol * st->h0) {
+      st->conv = 1;
+      st->done = 1;
+    } else if (k >= st->max_iters) {
+      st->done = 1;
+    }
+  }
+  cudaGraphSetConditional(h, st->done ? 0u : 1u);
+}
+// beta = rz' / rz (krylov.py:287-290)
+__global__ void k_sc_beta(ShState* st, const double* all, int world) {
+  const double rzn = rank_sum(all, world);
+  st->beta = rzn / st->rz;
+  st->rz = rzn;
+}
+__global__ void k_copy(const double* __restrict__ a, double* __restrict__ b, int64_t g0, int64_t g1) {
+  const int64_t g = g0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g < g1) b[g] = a[g];
+}
+// allgathered, padded coarse restrictions -> the full N0 vector
+__global__ void k_unpad(const double* __restrict__ all, const int64_t* __restrict__ off, int world, int64_t mx,
+                        double* __restrict__ out) {
+  const int h = blockIdx.y;
+  const int64_t cnt = off[h + 1] - off[h];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
+    out[off[h] + i] = all[h * mx + i];
+}
+
+}  // namespace
+
+struct ShardExchange {
+  std::vector<int32_t> peers;
+  std::vector<int64_t> ns, nr, soff, roff;
+  int64_t stot = 0, rtot = 0;
+  int64_t *sidx = nullptr, *ridx = nullptr;
+  double *sbuf = nullptr, *rbuf = nullptr;
+};
+
+struct ShardRuntime {
+  int rank = 0, world = 1;
+  ncclComm_t comm = nullptr;
+  bool coll = false;  // collectives through NCCL (world > 1, or forced at world 1 with an id: tests)
+  ShardExchange ex[3];  // 0 halo, 1 ext (overlap extension of t), 2 xy (foreign solutions)
+  std::vector<int64_t> agg_off;  // allgather layout (world + 1)
+  int64_t agg_max = 0;
+  int64_t* d_agg_off = nullptr;
+  double *gsend = nullptr, *gall = nullptr, *c1 = nullptr, *c2 = nullptr;
+  double *spart = nullptr, *sall = nullptr;
+  double *r = nullptr, *z = nullptr, *w = nullptr, *t = nullptr, *pold = nullptr, *pnew = nullptr, *ap = nullptr;
+  double *y0 = nullptr, *y0b = nullptr;
+  ShState* st = nullptr;
+  ShParams* prm = nullptr;  // tol / max_iters of the next solve (read by the graph's first kernel)
+  ShParams prm_host{};
+  double* hist = nullptr;
+  int32_t hist_cap = 0;
+  cudaGraphExec_t graph = nullptr;
+  const double* gb = nullptr;
+  double* gx = nullptr;
+  int64_t k_pro = 0, k_body = 0;  // kernel nodes: prologue, one loop iteration
+  std::vector<void*> owned;
+  ~ShardRuntime() {
+    if (graph) cudaGraphExecDestroy(graph);
+    for (void* p : owned) cudaFree(p);
+    if (comm && nccl().ok) nccl().CommDestroy(comm);
+  }
+  template <class T>
+  T* alloc(int64_t n) {
+    T* p = nullptr;
+    CUDA_CHECK(cudaMalloc(&p, std::max<int64_t>(n, 1) * sizeof(T)));
+    owned.push_back(p);
+    return p;
+  }
+};
+
+void destroy_shard_runtime(ShardRuntime* r) { delete r; }
+
+namespace {
+
+ShardRuntime& runtime(sfcdd_op* op) {
+  SFCDD_REQUIRE(op && op->ready && op->shard_count > 0, SFCDD_EVALUE, "needs a set-up shard-mode operator");
+  if (!op->srt) {
+    op->srt = new ShardRuntime();
+    op->srt->agg_off.assign(2, 0);
+  }
+  return *op->srt;
+}
+
+// one exchange: pack -> grouped send / recv -> unpack (no-op without peers)
+void sh_exchange(sfcdd_op* op, ShardRuntime& R, int kind, double* buf, cudaStream_t st) {
+  ShardExchange& E = R.ex[kind];
+  if (E.peers.empty()) return;
+  if (E.stot) k_pack<<<nblocks(E.stot, 256), 256, 0, st>>>(buf, E.sidx, E.stot, E.sbuf);
+  NCCL_CHECK(nccl().GroupStart());
+  for (size_t i = 0; i < E.peers.size(); ++i) {
+    if (E.ns[i]) NCCL_CHECK(nccl().Send(E.sbuf + E.soff[i], E.ns[i], ncclDouble, E.peers[i], R.comm, st));
+    if (E.nr[i]) NCCL_CHECK(nccl().Recv(E.rbuf + E.roff[i], E.nr[i], ncclDouble, E.peers[i], R.comm, st));
+  }
+  NCCL_CHECK(nccl().GroupEnd());
+  if (E.rtot) k_unpack<<<nblocks(E.rtot, 256), 256, 0, st>>>(E.rbuf, E.ridx, E.rtot, buf);
+  (void)op;
+}
+
+// rank partial (one double at spart) -> sall[world]
+const double* sh_scalars(ShardRuntime& R, cudaStream_t st) {
+  if (!R.coll) return R.spart;
+  NCCL_CHECK(nccl().AllGather(R.spart, R.sall, 1, ncclDouble, R.comm, st));
+  return R.sall;  // rank order (identical sum on every rank)
+}
+
+// owned coarse restrictions (at gsend) -> full N0 vector out
+void sh_coarse_gather(sfcdd_op* op, ShardRuntime& R, double* out, cudaStream_t st) {
+  if (!R.coll) {
+    CUDA_CHECK(cudaMemcpyAsync(out, R.gsend, (size_t)op->n0 * 8, cudaMemcpyDeviceToDevice, st));
+    return;
+  }
+  NCCL_CHECK(nccl().AllGather(R.gsend, R.gall, R.agg_max, ncclDouble, R.comm, st));
+  k_unpad<<<dim3(nblocks(R.agg_max, 256), R.world), 256, 0, st>>>(R.gall, R.d_agg_off, R.world, R.agg_max, out);
+}
+
+void sh_coarse_solve(sfcdd_op* op, const double* c, double* y, cudaStream_t st) {
+  if (!op->ainv) {
+    op->coarse_dag->solve(c, st);
+    CUDA_CHECK(cudaMemcpyAsync(y, op->coarse_dag->xy(), (size_t)op->n0 * 8, cudaMemcpyDeviceToDevice, st));
+  } else {
+    k_gemv_c<<<nblocks(op->n0, VEC_THREADS / 32), VEC_THREADS, (size_t)op->n0 * 8, st>>>(op->ainv, c, op->n0, y);
+  }
+}
+
+// z = C^{-1} g with rz partial = g.z (schwarz.py:103-118 balanced branch);
+// cagg at gsend holds the owned R0 g
+void sh_apply(sfcdd_op* op, ShardRuntime& R, const double* g, cudaStream_t st) {
+  const ShardRange SR = shard_range(op);
+  sh_coarse_gather(op, R, R.c1, st);
+  sh_coarse_solve(op, R.c1, R.y0, st);
+  k_sh_tvec<<<nblocks(SR.g1 - SR.g0, VEC_THREADS), VEC_THREADS, 0, st>>>(g, R.y0, op->agg, stencil_of(op), SR.g0,
+                                                                         SR.g1, R.t);
+  sh_exchange(op, R, 1, R.t, st);
+  op->dag->solve(R.t, st);
+  sh_exchange(op, R, 2, op->dag->xy(), st);
+  CUDA_CHECK(sfcdd_shard_combine(op, R.w, st) == SFCDD_OK ? cudaSuccess : cudaErrorUnknown);
+  sh_exchange(op, R, 0, R.w, st);
+  k_sh_stencil_chunks<<<SR.ch1 - SR.ch0, VEC_THREADS, 0, st>>>(R.w, stencil_of(op), chunks_of(op), SR.ch0,
+                                                               op->part_b);
+  k_agg_sums<<<nblocks(SR.a1 - SR.a0, 128), 128, 0, st>>>(op->part_b, op->agg_ptr, SR.a0, SR.a1, R.gsend);
+  sh_coarse_gather(op, R, R.c2, st);
+  sh_coarse_solve(op, R.c2, R.y0b, st);
+  k_sh_finalize<<<SR.ch1 - SR.ch0, VEC_THREADS, 0, st>>>(R.w, R.y0, R.y0b, chunks_of(op), SR.ch0,
+                                                         mode_of(op->variant), R.z, g, op->part_a);
+  k_sum_range<<<1, VEC_THREADS, 0, st>>>(op->part_a, SR.ch0, SR.ch1, R.spart);
+}
+
+// first half of an iteration: p = z + beta p_old, Ap, alpha, x/r update,
+// ||r||, R0 r; k_sc_rr sets the loop condition
+void sh_half(sfcdd_op* op, ShardRuntime& R, double* x, cudaGraphConditionalHandle h, cudaStream_t st) {
+  const ShardRange SR = shard_range(op);
+  sh_exchange(op, R, 0, R.z, st);
+  sh_exchange(op, R, 0, R.pold, st);
+  k_sh_pm<<<SR.ch1 - SR.ch0, VEC_THREADS, 0, st>>>(R.z, R.pold, 0.0, stencil_of(op), chunks_of(op), SR.ch0,
+                                                   R.pnew, R.ap, op->part_a, &R.st->beta);
+  k_sum_range<<<1, VEC_THREADS, 0, st>>>(op->part_a, SR.ch0, SR.ch1, R.spart);
+  k_sc_alpha<<<1, 1, 0, st>>>(R.st, sh_scalars(R, st), R.world);
+  k_sh_update<<<SR.ch1 - SR.ch0, VEC_THREADS, 0, st>>>(x, R.r, R.pnew, R.ap, 0.0, chunks_of(op), SR.ch0, op->part_b,
+                                                       op->part_c, &R.st->alpha, &R.st->brk);
+  k_sum_range<<<1, VEC_THREADS, 0, st>>>(op->part_b, SR.ch0, SR.ch1, R.spart);
+  k_agg_sums<<<nblocks(SR.a1 - SR.a0, 128), 128, 0, st>>>(op->part_c, op->agg_ptr, SR.a0, SR.a1, R.gsend);
+  k_sc_rr<<<1, 1, 0, st>>>(R.st, sh_scalars(R, st), R.world, R.hist, h);
+}
+
+// the whole solve as one graph: start, r0, z0 = C^{-1} r0, first half
+// iteration, then WHILE (not done) { z = C^{-1} r, beta, p_old <- p, half }
+void sh_build_graph(sfcdd_op* op, ShardRuntime& R, const double* b, double* x) {
+  const ShardRange SR = shard_range(op);
+  cudaStream_t cs = op->own_stream;
+  cudaGraph_t graph;
+  CUDA_CHECK(cudaGraphCreate(&graph, 0));
+  cudaGraphConditionalHandle h;
+  CUDA_CHECK(cudaGraphConditionalHandleCreate(&h, graph, 0, cudaGraphCondAssignDefault));
+  // prologue
+  CUDA_CHECK(cudaStreamBeginCaptureToGraph(cs, graph, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  k_sc_start<<<1, 1, 0, cs>>>(R.st, R.prm);
+  sh_exchange(op, R, 0, x, cs);
+  k_sh_residual<<<SR.ch1 - SR.ch0, VEC_THREADS, 0, cs>>>(b, x, stencil_of(op), chunks_of(op), SR.ch0, R.r,
+                                                         op->part_b, op->part_c);
+  k_sum_range<<<1, VEC_THREADS, 0, cs>>>(op->part_b, SR.ch0, SR.ch1, R.spart);
+  k_agg_sums<<<nblocks(SR.a1 - SR.a0, 128), 128, 0, cs>>>(op->part_c, op->agg_ptr, SR.a0, SR.a1, R.gsend);
+  k_sc_r0<<<1, 1, 0, cs>>>(R.st, sh_scalars(R, cs), R.world, R.hist);
+  sh_apply(op, R, R.r, cs);
+  k_sc_rz0<<<1, 1, 0, cs>>>(R.st, sh_scalars(R, cs), R.world);
+  CUDA_CHECK(cudaMemsetAsync(R.pold, 0, (size_t)op->n * 8, cs));
+  sh_half(op, R, x, h, cs);
+  // the loop node after the prologue
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  cudaStreamCaptureStatus cst;
+  CUDA_CHECK(cudaStreamGetCaptureInfo(cs, &cst, nullptr, nullptr, &deps, &ndeps));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t loop;
+  CUDA_CHECK(cudaGraphAddNode(&loop, graph, deps, ndeps, &cp));
+  CUDA_CHECK(cudaStreamUpdateCaptureDependencies(cs, &loop, 1, cudaStreamSetCaptureDependencies));
+  cudaGraph_t tmp;
+  CUDA_CHECK(cudaStreamEndCapture(cs, &tmp));
+  // loop body
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  CUDA_CHECK(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  sh_apply(op, R, R.r, cs);
+  k_sc_beta<<<1, 1, 0, cs>>>(R.st, sh_scalars(R, cs), R.world);
+  k_copy<<<nblocks(op->n, 256), 256, 0, cs>>>(R.pnew, R.pold, 0, op->n);
+  sh_half(op, R, x, h, cs);
+  CUDA_CHECK(cudaStreamEndCapture(cs, &tmp));
+  // kernel nodes of the prologue and of one loop iteration (launch accounting)
+  auto kernels = [](cudaGraph_t g) {
+    size_t nn = 0;
+    CUDA_CHECK(cudaGraphGetNodes(g, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    CUDA_CHECK(cudaGraphGetNodes(g, nodes.data(), &nn));
+    int64_t k = 0;
+    for (cudaGraphNode_t nd : nodes) {
+      cudaGraphNodeType ty;
+      CUDA_CHECK(cudaGraphNodeGetType(nd, &ty));
+      k += ty == cudaGraphNodeTypeKernel;
+    }
+    return k;
+  };
+  R.k_body = kernels(body);
+  R.k_pro = kernels(graph);
+  if (R.graph) CUDA_CHECK(cudaGraphExecDestroy(R.graph));
+  CUDA_CHECK(cudaGraphInstantiate(&R.graph, graph, 0));
+  CUDA_CHECK(cudaGraphDestroy(graph));
+  R.gb = b;
+  R.gx = x;
+}
+
+}  // namespace
+}  // namespace sfcdd
+
+extern "C" int sfcdd_nccl_unique_id(void* id_out) {
+  SFCDD_API_BEGIN
+  SFCDD_REQUIRE(id_out, SFCDD_EVALUE, "null argument");
+  SFCDD_REQUIRE(nccl().ok, SFCDD_ECUDA, "libnccl.so.2 could not be loaded");
+  ncclUniqueId id;
+  NCCL_CHECK(nccl().GetUniqueId(&id));
+  std::memcpy(id_out, &id, sizeof(id));
+  SFCDD_API_END
+}
+
+extern "C" int sfcdd_shard_attach(sfcdd_op* op, const void* nccl_id, int32_t rank, int32_t world,
+                                  const int64_t* agg_counts) {
+  SFCDD_API_BEGIN
+  ShardRuntime& R = runtime(op);
+  SFCDD_REQUIRE(world >= 1 && rank >= 0 && rank < world, SFCDD_EVALUE, "invalid rank / world");
+  CUDA_CHECK(cudaSetDevice(op->device));
+  R.rank = rank;
+  R.world = world;
+  if (world > 1 || nccl_id) {  // a world-1 communicator runs the same collectives (tests)
+    SFCDD_REQUIRE(nccl_id, SFCDD_EVALUE, "world > 1 needs an NCCL unique id");
+    R.coll = true;
+    SFCDD_REQUIRE(nccl().ok, SFCDD_ECUDA, "libnccl.so.2 could not be loaded");
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    NCCL_CHECK(nccl().CommInitRank(&R.comm, world, id, rank));
+  }
+  R.agg_off.assign(world + 1, 0);
+  for (int h = 0; h < world; ++h) {
+    R.agg_off[h + 1] = R.agg_off[h] + agg_counts[h];
+    R.agg_max = std::max<int64_t>(R.agg_max, agg_counts[h]);
+  }
+  SFCDD_REQUIRE(R.agg_off[world] == op->n0, SFCDD_EVALUE, "aggregate counts must sum to N0");
+  const ShardRange SR = shard_range(op);
+  SFCDD_REQUIRE(agg_counts[rank] == SR.a1 - SR.a0, SFCDD_EVALUE, "own aggregate count mismatch");
+  R.d_agg_off = R.alloc<int64_t>(world + 1);
+  CUDA_CHECK(cudaMemcpy(R.d_agg_off, R.agg_off.data(), (world + 1) * 8, cudaMemcpyHostToDevice));
+  R.gsend = R.alloc<double>(std::max<int64_t>(R.agg_max, op->n0));
+  R.gall = R.alloc<double>(R.agg_max * world);
+  R.c1 = R.alloc<double>(op->n0);
+  R.c2 = R.alloc<double>(op->n0);
+  R.spart = R.alloc<double>(1);
+  R.sall = R.alloc<double>(world);
+  for (double** v : {&R.r, &R.z, &R.w, &R.t, &R.pold, &R.pnew, &R.ap}) {
+    *v = R.alloc<double>(op->n);
+    CUDA_CHECK(cudaMemset(*v, 0, (size_t)op->n * 8));
+  }
+  R.y0 = R.alloc<double>(op->n0);
+  R.y0b = R.alloc<double>(op->n0);
+  R.st = R.alloc<ShState>(1);
+  R.prm = R.alloc<ShParams>(1);
+  if (op->ainv && (size_t)op->n0 * 8 > 48 * 1024)
+    CUDA_CHECK(cudaFuncSetAttribute(k_gemv_c, cudaFuncAttributeMaxDynamicSharedMemorySize, COARSE_DENSE_MAX * 8));
+  SFCDD_API_END
+}
+
+// kind 0 halo, 1 ext, 2 xy: the (peer, send indices, recv indices) lists of
+// distributed.build_plans, concatenated per kind (peers ascending)
+extern "C" int sfcdd_shard_set_exchange(sfcdd_op* op, int32_t kind, int32_t npeer, const int32_t* peers,
+                                        const int64_t* nsend, const int64_t* send_idx, const int64_t* nrecv,
+                                        const int64_t* recv_idx) {
+  SFCDD_API_BEGIN
+  ShardRuntime& R = runtime(op);
+  SFCDD_REQUIRE(kind >= 0 && kind < 3, SFCDD_EVALUE, "exchange kind must be 0, 1 or 2");
+  SFCDD_REQUIRE(npeer == 0 || R.world > 1, SFCDD_EVALUE, "exchanges need world > 1");
+  ShardExchange& E = R.ex[kind];
+  E = ShardExchange();
+  for (int i = 0; i < npeer; ++i) {
+    SFCDD_REQUIRE(peers[i] >= 0 && peers[i] < R.world && peers[i] != R.rank, SFCDD_EVALUE, "invalid peer");
+    E.peers.push_back(peers[i]);
+    E.ns.push_back(nsend[i]);
+    E.nr.push_back(nrecv[i]);
+    E.soff.push_back(E.stot);
+    E.roff.push_back(E.rtot);
+    E.stot += nsend[i];
+    E.rtot += nrecv[i];
+  }
+  E.sidx = R.alloc<int64_t>(E.stot);
+  E.ridx = R.alloc<int64_t>(E.rtot);
+  E.sbuf = R.alloc<double>(E.stot);
+  E.rbuf = R.alloc<double>(E.rtot);
+  if (E.stot) CUDA_CHECK(cudaMemcpy(E.sidx, send_idx, E.stot * 8, cudaMemcpyHostToDevice));
+  if (E.rtot) CUDA_CHECK(cudaMemcpy(E.ridx, recv_idx, E.rtot * 8, cudaMemcpyHostToDevice));
+  if (R.graph) CUDA_CHECK(cudaGraphExecDestroy(R.graph));
+  R.graph = nullptr;
+  SFCDD_API_END
+}
+
+// one sharded PCG solve (x holds x0 on entry; the owned segment of the
+// solution on exit); res_hist_host: max_iters + 1 doubles
+extern "C" int sfcdd_shard_pcg(sfcdd_op* op, const double* b, double* x, double tol, int32_t max_iters,
+                               double* res_hist_host, int32_t* iters, int32_t* converged, void* stream) {
+  SFCDD_API_BEGIN
+  ShardRuntime& R = runtime(op);
+  SFCDD_REQUIRE(R.st, SFCDD_EVALUE, "call sfcdd_shard_attach first");
+  SFCDD_REQUIRE(tol > 0 && max_iters >= 1, SFCDD_EVALUE, "need tol > 0 and max_iters >= 1");
+  CUDA_CHECK(cudaSetDevice(op->device));
+  OpScope scope(op, (cudaStream_t)stream);
+  cudaStream_t st = scope.stream();
+  if (R.hist_cap < max_iters + 1) {
+    R.hist = R.alloc<double>(max_iters + 1);
+    R.hist_cap = max_iters + 1;
+    if (R.graph) CUDA_CHECK(cudaGraphExecDestroy(R.graph));
+    R.graph = nullptr;
+  }
+  if (!R.graph || R.gb != b || R.gx != x) sh_build_graph(op, R, b, x);
+  R.prm_host = ShParams{tol, max_iters, 0};
+  CUDA_CHECK(cudaMemcpyAsync(R.prm, &R.prm_host, sizeof(ShParams), cudaMemcpyHostToDevice, st));
+  CUDA_CHECK(cudaGraphLaunch(R.graph, st));
+  ShState hs;
+  CUDA_CHECK(cudaMemcpyAsync(&hs, R.st, sizeof(ShState), cudaMemcpyDeviceToHost, st));
+  CUDA_CHECK(cudaStreamSynchronize(st));
+  if (res_hist_host) CUDA_CHECK(cudaMemcpy(res_hist_host, R.hist, (size_t)(hs.k + 1) * 8, cudaMemcpyDeviceToHost));
+  *iters = hs.k;
+  *converged = hs.conv;
+  // kernels launched by this solve (graph kernel nodes: the prologue holds the
+  // first half iteration, every further iteration is one body execution)
+  op->stats.reserved[7] = R.k_pro + (int64_t)std::max(0, hs.k - 1) * R.k_body;
+  if (hs.brk) throw Error(SFCDD_EBREAKDOWN, "nonpositive curvature at iteration " + std::to_string(hs.k + 1));
   SFCDD_API_END
 }

@@ -13,6 +13,9 @@
 
 namespace sfcdd {
 
+struct ShardRuntime;
+void destroy_shard_runtime(ShardRuntime* r);
+
 constexpr int VEC_THREADS = 256;
 constexpr int CHUNK = 2048;
 constexpr int COARSE_DENSE_MAX = 8192;  // coarse DOFs up to which A0^{-1} is held dense (GEMV solve)  // points per reduction chunk (never crosses an aggregate)
@@ -129,6 +132,7 @@ struct sfcdd_op {
   // threads applying one operator therefore serialize on the device
   std::mutex mu;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  sfcdd::ShardRuntime* srt = nullptr;  // device-driven sharded PCG (NCCL), shard mode only
 };
 
 namespace sfcdd {

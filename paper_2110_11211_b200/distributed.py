@@ -217,9 +217,20 @@ def _drive(gen, handle):
 
 
 def run_torch(eng, plan: ShardPlan, b, x, tol=1e-8, max_iters=20000, group=None):
-    """Execute one rank's program with torch.distributed collectives."""
+    """Execute one rank's program with torch.distributed collectives.  With a
+    gloo group and device engines the collective buffers are staged through
+    host memory (gloo has no CUDA all_to_all); the kernels stay on the GPU."""
     import torch
     import torch.distributed as dist
+
+    stage = dist.get_backend(group) == "gloo" and getattr(eng, "dev", None) is not None and \
+        getattr(eng.dev, "type", "cpu") == "cuda"
+
+    def host(t):
+        return t.cpu() if stage else t
+
+    def back(t):
+        return t.to(eng.dev) if stage else t
 
     def exchange(kind, buf):
         ex = getattr(plan, kind)
@@ -231,9 +242,10 @@ def run_torch(eng, plan: ShardPlan, b, x, tol=1e-8, max_iters=20000, group=None)
             if idx is not None and len(idx):
                 send_parts.append(eng.pack(buf, eng.index(kind, "send", h)))
             recv_counts.append(0 if ex.recv.get(h) is None else len(ex.recv[h]))
-        sendbuf = torch.cat(send_parts) if send_parts else eng.empty(0)
-        recvbuf = eng.empty(sum(recv_counts))
+        sendbuf = host(torch.cat(send_parts) if send_parts else eng.empty(0))
+        recvbuf = host(eng.empty(sum(recv_counts)))
         dist.all_to_all_single(recvbuf, sendbuf, recv_counts, send_counts, group=group)
+        recvbuf = back(recvbuf)
         off = 0
         for h in range(world):
             if recv_counts[h]:
@@ -245,17 +257,17 @@ def run_torch(eng, plan: ShardPlan, b, x, tol=1e-8, max_iters=20000, group=None)
             exchange(*req.args)
             return None
         if req.kind == "allreduce":
-            v = req.args[0].clone()
+            v = host(req.args[0].clone())
             dist.all_reduce(v, group=group)
             return float(v.item())
         if req.kind == "allgather":
             part = req.args[0]
             mx = max(plan.agg_counts)
-            pad = eng.empty(mx)
-            pad[: part.numel()] = part
-            outs = [eng.empty(mx) for _ in range(plan.world)]
+            pad = host(eng.empty(mx))
+            pad[: part.numel()] = host(part)
+            outs = [host(eng.empty(mx)) for _ in range(plan.world)]
             dist.all_gather(outs, pad, group=group)
-            return torch.cat([o[: plan.agg_counts[h]] for h, o in enumerate(outs)])
+            return back(torch.cat([o[: plan.agg_counts[h]] for h, o in enumerate(outs)]))
         raise ValueError(req.kind)
 
     return _drive(pcg_program(eng, plan, b, x, tol, max_iters), handle)
@@ -470,6 +482,49 @@ class DeviceShardEngine:
         _lib.check(_lib.lib().sfcdd_shard_update(self.h, x.data_ptr(), r.data_ptr(), p.data_ptr(), ap.data_ptr(),
                                                  float(alpha), rr.data_ptr(), ca.data_ptr(), self._stream()))
         return rr, ca
+
+
+# ------------------------------------------ device-driven program (C ABI)
+KINDS = {"halo": 0, "ext": 1, "xy": 2}
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL id for rank 0 to broadcast (sfcdd_nccl_unique_id)."""
+    buf = ctypes.create_string_buffer(128)
+    _lib.check(_lib.lib().sfcdd_nccl_unique_id(buf))
+    return buf.raw
+
+
+def attach_device_program(eng: DeviceShardEngine, plan: ShardPlan, nccl_id: bytes | None = None) -> None:
+    """Hand the rank's exchange plan and communicator to the C ABI so that
+    ``run_device`` runs the whole sharded solve as one CUDA graph (NCCL
+    send / recv and allgathers inside, conditional WHILE loop)."""
+    L = _lib.lib()
+    counts = np.ascontiguousarray(plan.agg_counts, np.int64)
+    _lib.check(L.sfcdd_shard_attach(eng.h, nccl_id, plan.rank, plan.world, counts.ctypes.data))
+    for name, kind in KINDS.items():
+        ex = getattr(plan, name)
+        peers = sorted(set(ex.send) | set(ex.recv))
+        empty = np.zeros(0, np.int64)
+        sends = [np.ascontiguousarray(ex.send.get(h, empty), np.int64) for h in peers]
+        recvs = [np.ascontiguousarray(ex.recv.get(h, empty), np.int64) for h in peers]
+        pa = np.asarray(peers, np.int32)
+        ns = np.asarray([len(a) for a in sends], np.int64)
+        nr = np.asarray([len(a) for a in recvs], np.int64)
+        si = np.concatenate(sends) if sends else empty
+        ri = np.concatenate(recvs) if recvs else empty
+        _lib.check(L.sfcdd_shard_set_exchange(eng.h, kind, len(peers), pa.ctypes.data, ns.ctypes.data,
+                                              si.ctypes.data, nr.ctypes.data, ri.ctypes.data))
+
+
+def run_device(eng: DeviceShardEngine, b, x, tol=1e-8, max_iters=20000):
+    """One sharded solve through sfcdd_shard_pcg: (iterations, converged,
+    residual history); x receives the owned segment of the solution."""
+    hist = np.zeros(max_iters + 1)
+    its, conv = ctypes.c_int32(), ctypes.c_int32()
+    _lib.check(_lib.lib().sfcdd_shard_pcg(eng.h, b.data_ptr(), x.data_ptr(), float(tol), int(max_iters),
+                                          hist.ctypes.data, ctypes.byref(its), ctypes.byref(conv), eng._stream()))
+    return its.value, bool(conv.value), hist[:its.value + 1].tolist()
 
 
 def xy_offsets_for(part, world: int, rank: int) -> np.ndarray:

@@ -260,3 +260,83 @@ def test_nccl_run_torch_matches_oracle():
         for rr in r:
             x[int(rr["g0"]):int(rr["g1"])] = rr["x"]
         assert np.linalg.norm(x - ref.solution) <= 1e-10 * np.linalg.norm(ref.solution)
+
+
+# ------------------------------------------- device-driven sharded program
+@pytest.mark.gpu
+@pytest.mark.parametrize("levels,p,gamma,q,coarse", [((7, 7), 16, 0.5, 4, "dense"), ((7, 7), 16, 0.5, 4, "sparse"),
+                                                     ((4, 4, 4), 8, 0.5, 4, "dense"),
+                                                     ((7, 7), 16, 0.5, 4, "nccl")])
+def test_device_driven_shard_pcg_matches_oracle(levels, p, gamma, q, coarse, monkeypatch):
+    """sfcdd_shard_pcg: the whole sharded solve as one CUDA graph with a
+    conditional WHILE loop, device scalars and (``nccl``) the NCCL
+    allgathers of the coarse restrictions / CG scalars captured in it (a
+    world-1 communicator: every collective is real, the exchanges are empty)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    if coarse == "sparse":
+        monkeypatch.setenv("SFCDD_COARSE_DENSE_MAX", "0")
+    part = _part(levels, p, gamma)
+    eng, plan = D.make_rank_shard(levels, part, q, 0, 1)
+    D.attach_device_program(eng, plan, D.nccl_unique_id() if coarse == "nccl" else None)
+    b = torch.from_numpy(_rhs(levels)).cuda()
+    x = torch.zeros_like(b)
+    its, conv, hist = D.run_device(eng, b, x)
+    ref = _oracle(levels, p, gamma, q)
+    assert conv and abs(its - ref.iterations) <= 1
+    k = min(len(hist), len(ref.residual_history))
+    np.testing.assert_allclose(hist[:k], ref.residual_history[:k], rtol=1e-10)
+    assert np.linalg.norm(x.cpu().numpy() - ref.solution) <= 1e-10 * np.linalg.norm(ref.solution)
+    # repeat (graph replay) and compare with the host-driven program bitwise in iterations
+    x2 = torch.zeros_like(b)
+    its2, conv2, hist2 = D.run_device(eng, b, x2)
+    assert its2 == its and hist2 == hist
+    torch.testing.assert_close(x2, x, rtol=0, atol=0)
+
+
+def _gloo_cuda_worker(rank, world, port, outdir):
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    sys.path.insert(0, os.path.join(root, "tests"))
+    import torch.distributed as dist
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    levels, p, gamma, q = (7, 7), 16, 0.5, 4
+    part = _part(levels, p, gamma)
+    eng, plan = D.make_rank_shard(levels, part, q, rank, world)
+    b = torch.from_numpy(_rhs_nooracle(levels)).cuda()
+    x = torch.zeros_like(b)
+    its, conv, hist = D.run_torch(eng, plan, b, x)
+    np.savez(os.path.join(outdir, f"rank{rank}.npz"), its=its, conv=conv, hist=np.asarray(hist),
+             x=x.cpu().numpy()[plan.g0:plan.g1], g0=plan.g0, g1=plan.g1, launches=eng.launches)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_gloo_world_2_drives_cuda_shard_kernels():
+    """Two processes, each with its CUDA shard engine (the sm_100a kernels of
+    its half of the subdomains) on the one GPU of the box, exchanging over
+    gloo through host memory: no kernel of one rank waits on the other's."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_gloo_cuda_worker, args=(2, port, d), nprocs=2, join=True)
+        r = [np.load(os.path.join(d, f"rank{g}.npz")) for g in range(2)]
+        ref = _oracle((7, 7), 16, 0.5, 4)
+        assert int(r[0]["launches"]) > 0 and int(r[1]["launches"]) > 0
+        assert int(r[0]["its"]) == int(r[1]["its"]) and abs(int(r[0]["its"]) - ref.iterations) <= 1
+        k = min(len(r[0]["hist"]), len(ref.residual_history))
+        np.testing.assert_allclose(r[0]["hist"][:k], ref.residual_history[:k], rtol=1e-10)
+        x = np.zeros(ref.solution.size)
+        for rr in r:
+            x[int(rr["g0"]):int(rr["g1"])] = rr["x"]
+        assert np.linalg.norm(x - ref.solution) <= 1e-10 * np.linalg.norm(ref.solution)
