@@ -145,6 +145,14 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// generic-proxy global writes (other tasks' outputs, acquired through their
+// counters) -> visible to this thread's async-proxy (bulk copy) reads
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+inline __device__ uint32_t bytes16(int n_doubles) { return (uint32_t)((8 * n_doubles + 15) & ~15); }
+
 __device__ __forceinline__ int32_t ld_acquire(const int32_t* p) {
   int32_t v;
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -526,14 +534,27 @@ __device__ __noinline__ void run_xb(const int32_t* h, const DagArgs& A, const Fa
 // assembled front f = [f_J ; f_B] is read contiguously (ASM tasks)
 template <bool SPLIT, typename Ahead>
 __device__ __forceinline__ void run_row(const int32_t* h, double* S, const DagArgs& A, const FactorDev& F,
-                                        int lane, Ahead ahead) {
+                                        int lane, Ahead ahead, uint64_t* bar, uint32_t& phase) {
   const int s = h[RW_S], R = h[RW_R], C = h[RW_C], r0 = h[RW_R0], NB = h[RW_NB];
   const double* V = reinterpret_cast<const double*>(reinterpret_cast<const uint8_t*>(h) + h[RW_VAL_OFF]);
-  if (SPLIT && h[RW_FOFF] >= 0) {  // front assembled by J's ASM tasks
+  int boff = C;  // S index of the first update-row value f_B[r0 - s + i]
+  if (SPLIT && h[RW_FOFF] >= 0) {
+    // front assembled by J's ASM tasks, contiguous and 16-byte aligned in
+    // upd: bulk-copy f_J[0:C) and the update rows f[r0 : r0+NB) (one TMA
+    // round trip instead of gather rounds)
     const double* f = A.upd + h[RW_FOFF];
-    warp_gather(
-        C + NB, lane, [&](int q) { return __ldcg(f + (q < C ? q : r0 + (q - C))); },
-        [&](int q, double v) { S[q] = v; });
+    const int c2 = (C + 1) & ~1;
+    boff = c2 + (r0 & 1);
+    if (lane == 0) {
+      fence_proxy_async_global();
+      const uint32_t ba = bytes16(C), bb = NB > 0 ? bytes16(NB + (r0 & 1)) : 0u;
+      mbar_expect_tx(bar, ba + bb);
+      bulk_g2s(S, f, ba, bar);
+      if (NB > 0) bulk_g2s(S + c2, f + (r0 & ~1), bb, bar);
+    }
+    __syncwarp();
+    mbar_wait(bar, phase);
+    phase ^= 1u;
   } else if (h[RW_ASM_HI] >= 0) {
     // huge s: J's assembly record in global memory [s, m] cols ptr src
     const int64_t o16 = (int64_t)(uint32_t)h[RW_ASM16] | ((int64_t)h[RW_ASM_HI] << 32);
@@ -593,7 +614,7 @@ __device__ __forceinline__ void run_row(const int32_t* h, double* S, const DagAr
       if (row < s)
         __stcg(yo + row, acc);
       else
-        __stcg(uo + (row - s), S[C + i] - acc);
+        __stcg(uo + (row - s), S[boff + i] - acc);
     }
   }
 }
@@ -602,7 +623,7 @@ __device__ __forceinline__ void run_row(const int32_t* h, double* S, const DagAr
 // columns [k0, k0+c): x_j = sum_r M[k0+r, k0+j] v[r]; lanes = (column, row-phase)
 template <bool SPLIT, typename Ahead>
 __device__ __forceinline__ void run_col(const int32_t* h, double* S, const DagArgs& A, const FactorDev& F,
-                                        int lane, Ahead ahead) {
+                                        int lane, Ahead ahead, uint64_t* bar, uint32_t& phase) {
   const int s = h[CL_S], m = h[CL_M], k0 = h[CL_K0], c = h[CL_C];
   const double* V = reinterpret_cast<const double*>(reinterpret_cast<const uint8_t*>(h) + h[CL_VAL_OFF]);
   const int32_t* cols = h + h[CL_COLS];
@@ -610,9 +631,16 @@ __device__ __forceinline__ void run_col(const int32_t* h, double* S, const DagAr
   const int ny = s - k0, L = ny + m;
   const double* yv = A.upd + h[CL_YOFF] + k0;
   if (SPLIT && h[CL_XOFF] >= 0) {
-    const double* vb = A.upd + h[CL_XOFF];  // -x_B (XB tasks)
-    warp_gather(
-        L, lane, [&](int q) { return __ldcg(q < ny ? yv + q : vb + (q - ny)); }, [&](int q, double v) { S[q] = v; });
+    // -x_B (XB tasks) follows y_J in upd: v = [y_J[k0:s) ; -x_B] is one
+    // contiguous, 16-byte aligned range (plan.cpp): one bulk copy
+    if (lane == 0) {
+      fence_proxy_async_global();
+      mbar_expect_tx(bar, bytes16(L));
+      bulk_g2s(S, yv, bytes16(L), bar);
+    }
+    __syncwarp();
+    mbar_wait(bar, phase);
+    phase ^= 1u;
   } else {
     const int32_t* rows = h + h[CL_ROWS];
     warp_gather(
@@ -822,7 +850,7 @@ __global__ void __launch_bounds__((WPB + 1) * 32, 20 / WPB) k_dag(DagArgs A) {
         run_frag(h, false, S, A, F, lane, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);
         break;
       case TK_ROW_FWD:
-        run_row<SPLIT>(h, S, A, F, lane, ahead);
+        run_row<SPLIT>(h, S, A, F, lane, ahead, bar, phase);
         break;
       default:
         if constexpr (SPLIT) {
@@ -835,7 +863,7 @@ __global__ void __launch_bounds__((WPB + 1) * 32, 20 / WPB) k_dag(DagArgs A) {
             break;
           }
         }
-        run_col<SPLIT>(h, S, A, F, lane, ahead);
+        run_col<SPLIT>(h, S, A, F, lane, ahead, bar, phase);
         break;
     }
     __syncwarp();
@@ -973,7 +1001,10 @@ DagSolver::DagSolver(const DevicePlan& plan, int device, int64_t extra_xy) : dev
   }
   up((void**)&tasks_, plan.tasks.data(), plan.tasks.size() * sizeof(TaskDev));
   up((void**)&factors_, plan.factors.data(), plan.factors.size() * sizeof(FactorDev));
-  CUDA_CHECK(cudaMalloc(&upd_, std::max<int64_t>(plan.upd_doubles, 2) * 8));
+  // (+8: the 16-byte rounded bulk copies of run_row / run_col may read a
+  // few doubles past the last slot)
+  CUDA_CHECK(cudaMalloc(&upd_, (std::max<int64_t>(plan.upd_doubles, 2) + 8) * 8));
+  CUDA_CHECK(cudaMemset(upd_, 0, (std::max<int64_t>(plan.upd_doubles, 2) + 8) * 8));
   CUDA_CHECK(cudaMalloc(&xy_, std::max<int64_t>(plan.xy_doubles + extra_xy, 2) * 8));
   xy_doubles_ = plan.xy_doubles + extra_xy;
   // counters (plan.h) then nq queue heads, one per 128-byte line; one memset per solve

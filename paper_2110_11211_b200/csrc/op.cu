@@ -2847,7 +2847,7 @@ struct ShardRuntime {
   cudaGraphExec_t graph = nullptr;
   const double* gb = nullptr;
   double* gx = nullptr;
-  int64_t k_pro = 0, k_body = 0;  // kernel nodes: prologue, one loop iteration
+  int64_t k_pro = 0, k_body = 0, nk = 0;  // our kernels: prologue, one loop iteration (capture counter)
   std::vector<void*> owned;
   ~ShardRuntime() {
     if (graph) cudaGraphExecDestroy(graph);
@@ -2881,6 +2881,7 @@ void sh_exchange(sfcdd_op* op, ShardRuntime& R, int kind, double* buf, cudaStrea
   ShardExchange& E = R.ex[kind];
   if (E.peers.empty()) return;
   if (E.stot) k_pack<<<nblocks(E.stot, 256), 256, 0, st>>>(buf, E.sidx, E.stot, E.sbuf);
+  R.nk += (E.stot > 0) + (E.rtot > 0);
   NCCL_CHECK(nccl().GroupStart());
   for (size_t i = 0; i < E.peers.size(); ++i) {
     if (E.ns[i]) NCCL_CHECK(nccl().Send(E.sbuf + E.soff[i], E.ns[i], ncclDouble, E.peers[i], R.comm, st));
@@ -2906,9 +2907,11 @@ void sh_coarse_gather(sfcdd_op* op, ShardRuntime& R, double* out, cudaStream_t s
   }
   NCCL_CHECK(nccl().AllGather(R.gsend, R.gall, R.agg_max, ncclDouble, R.comm, st));
   k_unpad<<<dim3(nblocks(R.agg_max, 256), R.world), 256, 0, st>>>(R.gall, R.d_agg_off, R.world, R.agg_max, out);
+  R.nk += 1;
 }
 
-void sh_coarse_solve(sfcdd_op* op, const double* c, double* y, cudaStream_t st) {
+void sh_coarse_solve(sfcdd_op* op, ShardRuntime& R, const double* c, double* y, cudaStream_t st) {
+  R.nk += 1;
   if (!op->ainv) {
     op->coarse_dag->solve(c, st);
     CUDA_CHECK(cudaMemcpyAsync(y, op->coarse_dag->xy(), (size_t)op->n0 * 8, cudaMemcpyDeviceToDevice, st));
@@ -2922,7 +2925,7 @@ void sh_coarse_solve(sfcdd_op* op, const double* c, double* y, cudaStream_t st) 
 void sh_apply(sfcdd_op* op, ShardRuntime& R, const double* g, cudaStream_t st) {
   const ShardRange SR = shard_range(op);
   sh_coarse_gather(op, R, R.c1, st);
-  sh_coarse_solve(op, R.c1, R.y0, st);
+  sh_coarse_solve(op, R, R.c1, R.y0, st);
   k_sh_tvec<<<nblocks(SR.g1 - SR.g0, VEC_THREADS), VEC_THREADS, 0, st>>>(g, R.y0, op->agg, stencil_of(op), SR.g0,
                                                                          SR.g1, R.t);
   sh_exchange(op, R, 1, R.t, st);
@@ -2934,10 +2937,11 @@ void sh_apply(sfcdd_op* op, ShardRuntime& R, const double* g, cudaStream_t st) {
                                                                op->part_b);
   k_agg_sums<<<nblocks(SR.a1 - SR.a0, 128), 128, 0, st>>>(op->part_b, op->agg_ptr, SR.a0, SR.a1, R.gsend);
   sh_coarse_gather(op, R, R.c2, st);
-  sh_coarse_solve(op, R.c2, R.y0b, st);
+  sh_coarse_solve(op, R, R.c2, R.y0b, st);
   k_sh_finalize<<<SR.ch1 - SR.ch0, VEC_THREADS, 0, st>>>(R.w, R.y0, R.y0b, chunks_of(op), SR.ch0,
                                                          mode_of(op->variant), R.z, g, op->part_a);
   k_sum_range<<<1, VEC_THREADS, 0, st>>>(op->part_a, SR.ch0, SR.ch1, R.spart);
+  R.nk += 8;  // tvec, DAG, combine, stencil chunks, aggregate sums, finalize, range sum (+ DAG counter reset)
 }
 
 // first half of an iteration: p = z + beta p_old, Ap, alpha, x/r update,
@@ -2955,6 +2959,7 @@ void sh_half(sfcdd_op* op, ShardRuntime& R, double* x, cudaGraphConditionalHandl
   k_sum_range<<<1, VEC_THREADS, 0, st>>>(op->part_b, SR.ch0, SR.ch1, R.spart);
   k_agg_sums<<<nblocks(SR.a1 - SR.a0, 128), 128, 0, st>>>(op->part_c, op->agg_ptr, SR.a0, SR.a1, R.gsend);
   k_sc_rr<<<1, 1, 0, st>>>(R.st, sh_scalars(R, st), R.world, R.hist, h);
+  R.nk += 8;  // pm, range sum, alpha, update, range sum, aggregate sums, rr
 }
 
 // the whole solve as one graph: start, r0, z0 = C^{-1} r0, first half
@@ -2968,6 +2973,7 @@ void sh_build_graph(sfcdd_op* op, ShardRuntime& R, const double* b, double* x) {
   CUDA_CHECK(cudaGraphConditionalHandleCreate(&h, graph, 0, cudaGraphCondAssignDefault));
   // prologue
   CUDA_CHECK(cudaStreamBeginCaptureToGraph(cs, graph, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  R.nk = 0;
   k_sc_start<<<1, 1, 0, cs>>>(R.st, R.prm);
   sh_exchange(op, R, 0, x, cs);
   k_sh_residual<<<SR.ch1 - SR.ch0, VEC_THREADS, 0, cs>>>(b, x, stencil_of(op), chunks_of(op), SR.ch0, R.r,
@@ -2979,6 +2985,8 @@ void sh_build_graph(sfcdd_op* op, ShardRuntime& R, const double* b, double* x) {
   k_sc_rz0<<<1, 1, 0, cs>>>(R.st, sh_scalars(R, cs), R.world);
   CUDA_CHECK(cudaMemsetAsync(R.pold, 0, (size_t)op->n * 8, cs));
   sh_half(op, R, x, h, cs);
+  R.nk += 6;  // start, residual, range sum, aggregate sums, r0, rz0
+  R.k_pro = R.nk;
   // the loop node after the prologue
   const cudaGraphNode_t* deps = nullptr;
   size_t ndeps = 0;
@@ -2997,27 +3005,14 @@ void sh_build_graph(sfcdd_op* op, ShardRuntime& R, const double* b, double* x) {
   // loop body
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   CUDA_CHECK(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  R.nk = 0;
   sh_apply(op, R, R.r, cs);
   k_sc_beta<<<1, 1, 0, cs>>>(R.st, sh_scalars(R, cs), R.world);
   k_copy<<<nblocks(op->n, 256), 256, 0, cs>>>(R.pnew, R.pold, 0, op->n);
   sh_half(op, R, x, h, cs);
+  R.nk += 2;
+  R.k_body = R.nk;
   CUDA_CHECK(cudaStreamEndCapture(cs, &tmp));
-  // kernel nodes of the prologue and of one loop iteration (launch accounting)
-  auto kernels = [](cudaGraph_t g) {
-    size_t nn = 0;
-    CUDA_CHECK(cudaGraphGetNodes(g, nullptr, &nn));
-    std::vector<cudaGraphNode_t> nodes(nn);
-    CUDA_CHECK(cudaGraphGetNodes(g, nodes.data(), &nn));
-    int64_t k = 0;
-    for (cudaGraphNode_t nd : nodes) {
-      cudaGraphNodeType ty;
-      CUDA_CHECK(cudaGraphNodeGetType(nd, &ty));
-      k += ty == cudaGraphNodeTypeKernel;
-    }
-    return k;
-  };
-  R.k_body = kernels(body);
-  R.k_pro = kernels(graph);
   if (R.graph) CUDA_CHECK(cudaGraphExecDestroy(R.graph));
   CUDA_CHECK(cudaGraphInstantiate(&R.graph, graph, 0));
   CUDA_CHECK(cudaGraphDestroy(graph));

@@ -355,13 +355,18 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
       // blob emission below can run per factor in parallel: y_J (s), the
       // assembled front [f_J ; f_B] (s + m, used in ASM mode) and -x_B (m,
       // used in XB mode)
+      // (16-byte aligned, -x_B right after y_J: a COL task's whole input
+      // v = [y_J[k0:s) ; -x_B] is ONE contiguous range it bulk-copies, and an
+      // ROW task bulk-copies its front pieces; dag_solve.cu run_row / run_col)
       const Supernode& J = F.sn[gr.top];
+      P.upd_doubles += P.upd_doubles & 1;
       gr.y_off = P.upd_doubles;
       P.upd_doubles += J.s;
-      gr.f_off = P.upd_doubles;
-      P.upd_doubles += J.s + J.m;
       gr.xb_off = P.upd_doubles;
       P.upd_doubles += J.m;
+      P.upd_doubles += P.upd_doubles & 1;
+      gr.f_off = P.upd_doubles;
+      P.upd_doubles += J.s + J.m;
       ++P.nbig;
     } else {
       ++P.nfrag;
@@ -566,7 +571,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         const int32_t asm_word = asm16 >= 0 ? RW_ASM16 : -1;
         int32_t bytes = 0;
         const int64_t off = E.emit(ints, RW_VAL_OFF, (int64_t)R * C, &vd, bytes, F, asm_word);
-        E.max_scratch = std::max<int32_t>(E.max_scratch, C + NB);
+        E.max_scratch = std::max<int32_t>(E.max_scratch, C + NB + 6);  // + padding of the bulk-copied front pieces
         add_task(g, TK_ROW_FWD, off, bytes, (int64_t)R * C, (use_asm ? 1.8 : 2.36) + 0.0013 * R * C);
       }
       // backward column blocks, dense row-major L x c (L = s+m-k0); -x_B is
@@ -575,6 +580,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         const int32_t L = s + m - k0;
         int32_t c = std::min<int32_t>(opt.col_max, s - k0);
         while (c > 1 && blob_size(CL_WORDS + c + (inl ? m : 0), (int64_t)L * c) > opt.blob_max) --c;
+        if (c > 1 && (c & 1) && k0 + c < s) --c;  // even widths keep k0 even (aligned bulk copies of v)
         return c;
       };
       int32_t ncol_tasks = 0;
@@ -633,7 +639,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         vd.len = L;
         int32_t bytes = 0;
         const int64_t off = E.emit(ints, CL_VAL_OFF, (int64_t)L * c, &vd, bytes, F);
-        E.max_scratch = std::max<int32_t>(E.max_scratch, L);
+        E.max_scratch = std::max<int32_t>(E.max_scratch, L + 2);  // + padding of the bulk-copied v
         add_task(g, TK_COL_BWD, off, bytes, nv, (use_xb ? 1.8 : 2.24) + 0.0013 * nv);
         k0 += c;
       }
