@@ -115,6 +115,18 @@ __device__ __forceinline__ bool mbar_wait_timed(uint64_t* bar, uint32_t parity, 
   return ok != 0;
 }
 
+// Watchdog (never fires in a correct run): a wait that exceeds this many
+// ns traps the kernel -- a launch error for the caller instead of a hung GPU
+constexpr unsigned long long DAG_WATCHDOG_NS = 20ull * 1000 * 1000 * 1000;
+
+// mbarrier wait with the watchdog (1 us suspend hints per try)
+__device__ __forceinline__ void mbar_wait_guard(uint64_t* bar, uint32_t parity) {
+  if (mbar_wait_timed(bar, parity, 1000)) return;
+  const unsigned long long t0 = gtimer();
+  while (!mbar_wait_timed(bar, parity, 1000))
+    if (gtimer() - t0 > DAG_WATCHDOG_NS) __trap();
+}
+
 // TMA bulk copy global -> shared, completion signalled on the mbarrier
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -553,7 +565,7 @@ __device__ __forceinline__ void run_row(const int32_t* h, double* S, const DagAr
       if (NB > 0) bulk_g2s(S + c2, f + (r0 & ~1), bb, bar);
     }
     __syncwarp();
-    mbar_wait(bar, phase);
+    mbar_wait_guard(bar, phase);
     phase ^= 1u;
   } else if (h[RW_ASM_HI] >= 0) {
     // huge s: J's assembly record in global memory [s, m] cols ptr src
@@ -630,16 +642,19 @@ __device__ __forceinline__ void run_col(const int32_t* h, double* S, const DagAr
   double* xy = A.xy + F.xy_off;
   const int ny = s - k0, L = ny + m;
   const double* yv = A.upd + h[CL_YOFF] + k0;
+  double* Sv = S;  // v[r] = Sv[r]
   if (SPLIT && h[CL_XOFF] >= 0) {
     // -x_B (XB tasks) follows y_J in upd: v = [y_J[k0:s) ; -x_B] is one
-    // contiguous, 16-byte aligned range (plan.cpp): one bulk copy
+    // contiguous range (plan.cpp), bulk-copied from its 16-byte aligned start
+    const int sh = (int)((h[CL_YOFF] + k0) & 1);
+    Sv = S + sh;
     if (lane == 0) {
       fence_proxy_async_global();
-      mbar_expect_tx(bar, bytes16(L));
-      bulk_g2s(S, yv, bytes16(L), bar);
+      mbar_expect_tx(bar, bytes16(L + sh));
+      bulk_g2s(S, yv - sh, bytes16(L + sh), bar);
     }
     __syncwarp();
-    mbar_wait(bar, phase);
+    mbar_wait_guard(bar, phase);
     phase ^= 1u;
   } else {
     const int32_t* rows = h + h[CL_ROWS];
@@ -659,15 +674,138 @@ __device__ __forceinline__ void run_col(const int32_t* h, double* S, const DagAr
       const double* v = V + jj;
       int r = ph;
       for (; r + P < L; r += 2 * P) {
-        a0 = fma(v[r * c], S[r], a0);
-        a1 = fma(v[(r + P) * c], S[r + P], a1);
+        a0 = fma(v[r * c], Sv[r], a0);
+        a1 = fma(v[(r + P) * c], Sv[r + P], a1);
       }
-      if (r < L) a0 = fma(v[r * c], S[r], a0);
+      if (r < L) a0 = fma(v[r * c], Sv[r], a0);
     }
     double acc = a0 + a1;
     for (int o = CP; o < 32; o <<= 1) acc += __shfl_xor_sync(FULL, acc, o);
     if (ph == 0 && jj < c) __stcg(xy + cols[jj], acc);
   }
+}
+
+// ============================================ streamed BIG tasks (plan.h)
+// Double-buffered chunk pipeline inside one warp: lane 0 keeps two chunks
+// (values + the matching front / v piece, one bulk copy each) in flight on
+// the warp's two mbarriers while the lanes consume the previous one.
+struct Pipe {
+  uint64_t* bar[2];
+  uint32_t* phase[2];
+};
+
+// ROW: rows [r0, r0+R) of out = M f_J, values R x C column-major in HBM
+__device__ __noinline__ void run_row_stream(const int32_t* h, uint8_t* slot, double* S, const DagArgs& A,
+                                            const uint8_t* gblob, int lane, Pipe pp) {
+  const int s = h[RW_S], R = h[RW_R], C = h[RW_C], r0 = h[RW_R0], NB = h[RW_NB], Kc = h[RW_STREAM];
+  const double* gV = reinterpret_cast<const double*>(gblob + h[RW_VAL_OFF]);
+  const double* f = A.upd + h[RW_FOFF];
+  const uint32_t vb_bytes = bytes16(R * Kc);
+  double* vbuf[2] = {reinterpret_cast<double*>(slot + STREAM_META),
+                     reinterpret_cast<double*>(slot + STREAM_META + vb_bytes)};
+  double* fbuf[2] = {S, S + Kc};
+  double* fB = S + 2 * Kc;  // f[r0 - (r0 & 1) ...] for the update rows
+  const int nch = (C + Kc - 1) / Kc;
+  auto issue = [&](int ch, uint32_t extra) {  // lane 0: chunk ch into buffer ch & 1
+    const int k0 = ch * Kc, kc = min(Kc, C - k0);
+    uint64_t* b = pp.bar[ch & 1];
+    const uint32_t bv = bytes16(R * kc), bf = bytes16(kc);
+    mbar_expect_tx(b, bv + bf + extra);
+    bulk_g2s(vbuf[ch & 1], gV + (int64_t)k0 * R, bv, b);
+    bulk_g2s(fbuf[ch & 1], f + k0, bf, b);
+  };
+  if (lane == 0) {
+    fence_proxy_async_global();
+    const uint32_t bb = NB > 0 ? bytes16(NB + (r0 & 1)) : 0u;
+    issue(0, bb);
+    if (NB > 0) bulk_g2s(fB, f + (r0 & ~1), bb, pp.bar[0]);
+    if (nch > 1) issue(1, 0);
+  }
+  const int RP = R >= 32 ? 32 : (R <= 1 ? 1 : 1 << (32 - __clz(R - 1)));  // lanes per phase
+  const int P = 32 / RP;
+  const int il = lane & (RP - 1), ph = lane / RP;
+  double a0 = 0.0, a1 = 0.0;
+  for (int ch = 0; ch < nch; ++ch) {
+    const int q = ch & 1;
+    mbar_wait_guard(pp.bar[q], *pp.phase[q]);
+    *pp.phase[q] ^= 1u;
+    const int kc = min(Kc, C - ch * Kc);
+    if (il < R) {
+      const double* v = vbuf[q] + il;
+      const double* fc = fbuf[q];
+      int k = ph;
+      for (; k + P < kc; k += 2 * P) {
+        a0 = fma(v[k * R], fc[k], a0);
+        a1 = fma(v[(k + P) * R], fc[k + P], a1);
+      }
+      if (k < kc) a0 = fma(v[k * R], fc[k], a0);
+    }
+    __syncwarp();  // buffer q consumed
+    if (lane == 0 && ch + 2 < nch) issue(ch + 2, 0);
+  }
+  double acc = a0 + a1;
+  for (int o = RP; o < 32; o <<= 1) acc += __shfl_xor_sync(FULL, acc, o);
+  if (ph == 0 && il < R) {
+    const int row = r0 + il;
+    if (row < s)
+      __stcg(A.upd + h[RW_YOFF] + row, acc);
+    else
+      __stcg(A.upd + h[RW_UOFF] + (row - s), fB[(r0 & 1) + il] - acc);
+  }
+}
+
+// COL: columns [k0, k0+c) of x_J = M^T v, values L x c row-major in HBM,
+// v = [y_J[k0:s) ; -x_B] contiguous in upd (XB mode or m = 0)
+__device__ __noinline__ void run_col_stream(const int32_t* h, uint8_t* slot, double* S, const DagArgs& A,
+                                            const FactorDev& F, const uint8_t* gblob, int lane, Pipe pp) {
+  const int s = h[CL_S], m = h[CL_M], k0 = h[CL_K0], c = h[CL_C], Lq = h[CL_STREAM];
+  const int L = s - k0 + m;
+  const double* gV = reinterpret_cast<const double*>(gblob + h[CL_VAL_OFF]);
+  const double* yv = A.upd + h[CL_YOFF] + k0;
+  const int32_t* cols = h + h[CL_COLS];
+  const uint32_t vb_bytes = bytes16(Lq * c);
+  double* vbuf[2] = {reinterpret_cast<double*>(slot + STREAM_META),
+                     reinterpret_cast<double*>(slot + STREAM_META + vb_bytes)};
+  double* xbuf[2] = {S, S + Lq + 2};
+  const int nch = (L + Lq - 1) / Lq;
+  auto issue = [&](int ch) {
+    const int q0 = ch * Lq, lq = min(Lq, L - q0);
+    uint64_t* b = pp.bar[ch & 1];
+    const uint32_t bv = bytes16(lq * c), bx = bytes16(lq);
+    mbar_expect_tx(b, bv + bx);
+    bulk_g2s(vbuf[ch & 1], gV + (int64_t)q0 * c, bv, b);
+    bulk_g2s(xbuf[ch & 1], yv + q0, bx, b);
+  };
+  if (lane == 0) {
+    fence_proxy_async_global();
+    issue(0);
+    if (nch > 1) issue(1);
+  }
+  const int CP = c >= 32 ? 32 : (c <= 1 ? 1 : 1 << (32 - __clz(c - 1)));
+  const int P = 32 / CP;
+  const int j = lane & (CP - 1), ph = lane / CP;
+  double a0 = 0.0, a1 = 0.0;
+  for (int ch = 0; ch < nch; ++ch) {
+    const int q = ch & 1;
+    mbar_wait_guard(pp.bar[q], *pp.phase[q]);
+    *pp.phase[q] ^= 1u;
+    const int lq = min(Lq, L - ch * Lq);
+    if (j < c) {
+      const double* v = vbuf[q] + j;
+      const double* xv = xbuf[q];
+      int r = ph;
+      for (; r + P < lq; r += 2 * P) {
+        a0 = fma(v[r * c], xv[r], a0);
+        a1 = fma(v[(r + P) * c], xv[r + P], a1);
+      }
+      if (r < lq) a0 = fma(v[r * c], xv[r], a0);
+    }
+    __syncwarp();
+    if (lane == 0 && ch + 2 < nch) issue(ch + 2);
+  }
+  double acc = a0 + a1;
+  for (int o = CP; o < 32; o <<= 1) acc += __shfl_xor_sync(FULL, acc, o);
+  if (ph == 0 && j < c) __stcg(A.xy + F.xy_off + cols[j], acc);
 }
 
 // ================================================================ kernel
@@ -725,6 +863,7 @@ template <int WPB, bool SPLIT>
 __global__ void __launch_bounds__((WPB + 1) * 32, 20 / WPB) k_dag(DagArgs A) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bars[WPB];
+  __shared__ __align__(8) uint64_t bars2[WPB];  // second chunk buffer of streamed tasks
   __shared__ int32_t mbox[WPB];
   __shared__ int32_t nexit;
   __shared__ __align__(8) uint64_t sigbar;
@@ -742,12 +881,14 @@ __global__ void __launch_bounds__((WPB + 1) * 32, 20 / WPB) k_dag(DagArgs A) {
     return;
   }
   uint64_t* bar = &bars[warp];
+  uint64_t* bar2 = &bars2[warp];
   if (lane == 0) {
     mbar_init(bar, 1);
+    mbar_init(bar2, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
-  uint32_t phase = 0;
+  uint32_t phase = 0, phase2 = 0;
   // queue of this warp (interleaved split of the global order: spreads the
   // claim atomics over nq lines; deadlock-free, the smallest unfinished task
   // is always claimable)
@@ -823,15 +964,25 @@ __global__ void __launch_bounds__((WPB + 1) * 32, 20 / WPB) k_dag(DagArgs A) {
       if (T.wait_idx >= 0) {
         // relaxed polling (no L1 invalidation per poll), one acquire at the end
         unsigned ns = 32;
+        unsigned polls = 0;
+        unsigned long long t0 = 0;
+        auto watchdog = [&]() {  // a dependency that never completes traps instead of hanging the GPU
+          if ((++polls & 4095u) == 0) {
+            if (t0 == 0) t0 = gtimer();
+            else if (gtimer() - t0 > DAG_WATCHDOG_NS) __trap();
+          }
+        };
         if (A.mode & 1) {
           while (ld_acquire(A.ctr + T.wait_idx) < T.wait_target) {
             __nanosleep(ns);
             ns = ns < 256 ? 2 * ns : 256;
+            watchdog();
           }
         } else {
           while (ld_relaxed(A.ctr + T.wait_idx) < T.wait_target) {
             __nanosleep(ns);
             ns = ns < 256 ? 2 * ns : 256;
+            watchdog();
           }
           (void)ld_acquire(A.ctr + T.wait_idx);
         }
@@ -839,7 +990,7 @@ __global__ void __launch_bounds__((WPB + 1) * 32, 20 / WPB) k_dag(DagArgs A) {
       if (tr) tr[2] = gtimer();
     }
     __syncwarp();
-    mbar_wait(bar, phase);
+    mbar_wait_guard(bar, phase);
     phase ^= 1u;
     if (tr && lane == 0) tr[3] = gtimer();
     switch (T.kind) {
@@ -850,7 +1001,11 @@ __global__ void __launch_bounds__((WPB + 1) * 32, 20 / WPB) k_dag(DagArgs A) {
         run_frag(h, false, S, A, F, lane, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);
         break;
       case TK_ROW_FWD:
-        run_row<SPLIT>(h, S, A, F, lane, ahead, bar, phase);
+        if (SPLIT && h[RW_STREAM] > 0)
+          run_row_stream(h, smem + (size_t)warp * A.slot_bytes, S, A, A.blobs + T.blob_off, lane,
+                         Pipe{{bar, bar2}, {&phase, &phase2}});
+        else
+          run_row<SPLIT>(h, S, A, F, lane, ahead, bar, phase);
         break;
       default:
         if constexpr (SPLIT) {
@@ -863,7 +1018,11 @@ __global__ void __launch_bounds__((WPB + 1) * 32, 20 / WPB) k_dag(DagArgs A) {
             break;
           }
         }
-        run_col<SPLIT>(h, S, A, F, lane, ahead, bar, phase);
+        if (SPLIT && h[CL_STREAM] > 0)
+          run_col_stream(h, smem + (size_t)warp * A.slot_bytes, S, A, F, A.blobs + T.blob_off, lane,
+                         Pipe{{bar, bar2}, {&phase, &phase2}});
+        else
+          run_col<SPLIT>(h, S, A, F, lane, ahead, bar, phase);
         break;
     }
     __syncwarp();

@@ -81,7 +81,7 @@ struct FactorEmit {
   // one blob: metadata + nvals values placed by descriptors (their dst is
   // relative to the value area); asm_word >= 0: that int holds asm16
   int64_t emit_descs(std::vector<int32_t>& ints, int32_t val_off_word, int64_t nvals, const ValDesc* vd, size_t nvd,
-                     int32_t& copy_bytes, const HostFactor* F, int32_t asm_word = -1) {
+                     int32_t& copy_bytes, const HostFactor* F, int32_t asm_word = -1, bool streamed = false) {
     const int64_t meta_bytes = align16(4 * (int64_t)ints.size());
     if (val_off_word >= 0) ints[val_off_word] = (int32_t)meta_bytes;
     const int64_t val_bytes = align16(8 * nvals);
@@ -102,13 +102,14 @@ struct FactorEmit {
         place_values(hd, F->val.data() + d.src, image.data() + h);
       }
     }
-    copy_bytes = (int32_t)(meta_bytes + val_bytes);
+    // streamed tasks copy their metadata only; the values stay in HBM
+    copy_bytes = (int32_t)(streamed ? meta_bytes : meta_bytes + val_bytes);
     max_copy = std::max(max_copy, copy_bytes);
     return off;
   }
   int64_t emit(std::vector<int32_t>& ints, int32_t val_off_word, int64_t nvals, const ValDesc* vd,
-               int32_t& copy_bytes, const HostFactor& F, int32_t asm_word = -1) {
-    return emit_descs(ints, val_off_word, nvals, vd, vd ? 1 : 0, copy_bytes, &F, asm_word);
+               int32_t& copy_bytes, const HostFactor& F, int32_t asm_word = -1, bool streamed = false) {
+    return emit_descs(ints, val_off_word, nvals, vd, vd ? 1 : 0, copy_bytes, &F, asm_word, streamed);
   }
   int64_t emit(std::vector<int32_t>& ints, int32_t val_off_word, int64_t nvals, const ValDesc* vd,
                int32_t& copy_bytes) {
@@ -167,6 +168,8 @@ PlanOptions::PlanOptions() {
   if (const char* e = std::getenv("SFCDD_XB_MIN")) xb_min_tasks = std::atoi(e);
   if (const char* e = std::getenv("SFCDD_SPLIT_MIN")) split_min_factors = std::atoi(e);
   if (const char* e = std::getenv("SFCDD_WPB")) wpb = std::atoi(e);
+  if (const char* e = std::getenv("SFCDD_STREAM_ROWS")) stream_rows = std::max(0, std::atoi(e));
+  if (const char* e = std::getenv("SFCDD_STREAM_COLS")) stream_cols = std::max(2, std::atoi(e) & ~1);
   tuned = std::getenv("SFCDD_BLOB_MAX") || std::getenv("SFCDD_WPB");
 }
 
@@ -221,10 +224,12 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
     // of two that fits and the CTA shape drops to 2 workers (fewer resident
     // warps, but the plan builds instead of failing)
     int64_t need = 0;
+    const bool streams = opt.stream_rows > 0 && (int64_t)factors.size() >= opt.split_min_factors;
     for (const HostFactor* F : factors)
       for (const Supernode& S : F->sn)
-        need = std::max({need, blob_size(RW_WORDS, (int64_t)S.s),
-                         blob_size(CL_WORDS + 1 + (int64_t)S.m, (int64_t)S.s + S.m)});
+        if (!streams)  // streamed plans never need more than the chosen blob
+          need = std::max({need, blob_size(RW_WORDS, (int64_t)S.s),
+                           blob_size(CL_WORDS + 1 + (int64_t)S.m, (int64_t)S.s + S.m)});
     if (need > opt.blob_max) {
       int64_t b = opt.blob_max;
       while (b < need) b *= 2;
@@ -463,8 +468,21 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         return true;
       };
       std::vector<std::pair<int32_t, int32_t>> split_a, split_i;
-      SFCDD_REQUIRE(row_split(false, split_a), SFCDD_EINTERNAL,
-                    "big supernode row does not fit a task blob (s = " + std::to_string(s) + ")");
+      // streamed mode (many-factor plans): row blocks of stream_rows rows;
+      // blocks whose values exceed the blob stream them in chunks (plan.h)
+      const bool streaming = opt.stream_rows > 0 && (int64_t)factors.size() >= opt.split_min_factors;
+      const int32_t CB = ((opt.blob_max - STREAM_META) / 2) & ~15;  // bytes of one chunk buffer
+      if (streaming) {
+        for (int32_t r0 = 0; r0 < s + m;) {
+          const int32_t lim = r0 < s ? s : s + m;
+          const int32_t Re = std::min(opt.stream_rows, lim - r0);
+          split_a.emplace_back(r0, Re);
+          r0 += Re;
+        }
+      } else {
+        SFCDD_REQUIRE(row_split(false, split_a), SFCDD_EINTERNAL,
+                      "big supernode row does not fit a task blob (s = " + std::to_string(s) + ")");
+      }
       double gathered = 0.0;
       for (const auto& rb : split_a) gathered += rb.first < s ? rb.first + rb.second : s + rb.second;
       // three ways to assemble f_J for the ROW tasks: ASM tasks (once, one
@@ -475,7 +493,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
       for (int32_t q = 0; q < s; ++q) fj_nnz += (int64_t)contrib[q].size();
       const bool huge = 4 * (RW_WORDS + 2 * s + 1 + fj_nnz) > opt.blob_max / 2;
       const bool split_ok = (int64_t)factors.size() >= opt.split_min_factors;
-      const bool use_asm = split_ok && gathered >= opt.asm_redundancy * (s + m);
+      const bool use_asm = streaming || (split_ok && gathered >= opt.asm_redundancy * (s + m));
       const bool global_asm = !use_asm && (huge || !row_split(true, split_i));
       const auto& split = (use_asm || global_asm) ? split_a : split_i;
       int64_t asm16 = -1;
@@ -559,6 +577,13 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
           }
         }
         ints[RW_SCRATCH] = C + NB;
+        // streamed when the block does not fit the blob: Kc columns per chunk
+        int32_t Kc = 0;
+        if (streaming && blob_size(RW_WORDS, (int64_t)R * C) > opt.blob_max) {
+          Kc = std::max(2, ((CB / 8) / R) & ~1);
+          ints[RW_STREAM] = Kc;
+          ints[RW_SCRATCH] = 2 * Kc + NB + 4;
+        }
         // values: R x C column-major, (i, k) = M[r0 + i, k] for k <= r0 + i
         ValDesc vd{};
         vd.src = S.val_off;
@@ -570,14 +595,15 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         vd.len = C;
         const int32_t asm_word = asm16 >= 0 ? RW_ASM16 : -1;
         int32_t bytes = 0;
-        const int64_t off = E.emit(ints, RW_VAL_OFF, (int64_t)R * C, &vd, bytes, F, asm_word);
-        E.max_scratch = std::max<int32_t>(E.max_scratch, C + NB + 6);  // + padding of the bulk-copied front pieces
+        const int64_t off = E.emit(ints, RW_VAL_OFF, (int64_t)R * C, &vd, bytes, F, asm_word, Kc > 0);
+        E.max_scratch = std::max<int32_t>(E.max_scratch, Kc > 0 ? 2 * Kc + NB + 4 : C + NB + 6);  // + padding
         add_task(g, TK_ROW_FWD, off, bytes, (int64_t)R * C, (use_asm ? 1.8 : 2.36) + 0.0013 * R * C);
       }
       // backward column blocks, dense row-major L x c (L = s+m-k0); -x_B is
       // gathered once by XB tasks when J has many column blocks
       auto col_width = [&](int32_t k0, bool inl) {
         const int32_t L = s + m - k0;
+        if (streaming) return std::min<int32_t>(opt.stream_cols, s - k0);  // even, oversized blocks stream
         int32_t c = std::min<int32_t>(opt.col_max, s - k0);
         while (c > 1 && blob_size(CL_WORDS + c + (inl ? m : 0), (int64_t)L * c) > opt.blob_max) --c;
         if (c > 1 && (c & 1) && k0 + c < s) --c;  // even widths keep k0 even (aligned bulk copies of v)
@@ -587,7 +613,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
       for (int32_t k0 = 0; k0 < s; k0 += col_width(k0, false)) ++ncol_tasks;
       // XB also when a column block with its inline row list cannot fit a blob
       const bool inline_fits = blob_size(CL_WORDS + 1 + m, (int64_t)(s + m)) <= opt.blob_max;
-      const bool use_xb = m > 0 && ((split_ok && ncol_tasks >= opt.xb_min_tasks) || !inline_fits);
+      const bool use_xb = m > 0 && (streaming || (split_ok && ncol_tasks >= opt.xb_min_tasks) || !inline_fits);
       if (use_xb) {  // -x_B at gr.xb_off
         for (int32_t a0 = 0; a0 < m;) {
           int32_t na = std::min<int32_t>(m - a0, opt.asm_max);
@@ -609,8 +635,11 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
       for (int32_t k0 = 0; k0 < s;) {
         const int32_t L = s + m - k0;
         const int32_t c = col_width(k0, !use_xb);
-        SFCDD_REQUIRE(blob_size(CL_WORDS + c + (use_xb ? 0 : m), (int64_t)L * c) <= opt.blob_max &&
-                          L <= opt.big_scratch_max,
+        int32_t Lq = 0;
+        if (streaming && (blob_size(CL_WORDS + c, (int64_t)L * c) > opt.blob_max || L + 2 > opt.big_scratch_max))
+          Lq = std::max(2, ((CB / 8) / c) & ~1);
+        SFCDD_REQUIRE(Lq > 0 || (blob_size(CL_WORDS + c + (use_xb ? 0 : m), (int64_t)L * c) <= opt.blob_max &&
+                                 L <= opt.big_scratch_max),
                       SFCDD_EINTERNAL,
                       "big supernode column does not fit a task blob (s+m = " + std::to_string(s + m) + ")");
         ints.assign(CL_WORDS, 0);
@@ -626,7 +655,8 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
           ints[CL_ROWS] = (int32_t)ints.size();
           for (int32_t a = 0; a < m; ++a) ints.push_back(F.perm[F.rows[S.rows_off + a]]);
         }
-        ints[CL_SCRATCH] = L;
+        ints[CL_SCRATCH] = Lq > 0 ? 2 * (Lq + 2) : L;
+        ints[CL_STREAM] = Lq;
         // values: L x c row-major, (r, j) = M[k0 + r, k0 + j] for j <= r
         const int64_t nv = (int64_t)L * c - (int64_t)c * (c - 1) / 2;
         ValDesc vd{};
@@ -638,8 +668,8 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         vd.w = c;
         vd.len = L;
         int32_t bytes = 0;
-        const int64_t off = E.emit(ints, CL_VAL_OFF, (int64_t)L * c, &vd, bytes, F);
-        E.max_scratch = std::max<int32_t>(E.max_scratch, L + 2);  // + padding of the bulk-copied v
+        const int64_t off = E.emit(ints, CL_VAL_OFF, (int64_t)L * c, &vd, bytes, F, -1, Lq > 0);
+        E.max_scratch = std::max<int32_t>(E.max_scratch, Lq > 0 ? 2 * (Lq + 2) : L + 2);  // + padding
         add_task(g, TK_COL_BWD, off, bytes, nv, (use_xb ? 1.8 : 2.24) + 0.0013 * nv);
         k0 += c;
       }

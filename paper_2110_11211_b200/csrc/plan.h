@@ -153,6 +153,7 @@ enum RowHdr {
                //   over FRONT positions
   RW_VAL_OFF,  // byte offset of the values
   RW_SCRATCH,  // doubles of scratch used
+  RW_STREAM,   // streamed task (> 0): columns per chunk (values stay in HBM, see below)
   RW_WORDS
 };
 // COL blob: backward columns [k0, k0+c) of J.  Values: L x c dense row-major
@@ -169,8 +170,19 @@ enum ColHdr {
   CL_ROWS,     // (CL_XOFF < 0) int offset: ro of the m below rows
   CL_VAL_OFF,  // byte offset of the values
   CL_SCRATCH,
+  CL_STREAM,   // streamed task (> 0): rows per chunk
   CL_WORDS
 };
+
+// Streamed BIG tasks (many-factor plans, ASM / XB mode): a ROW / COL block
+// whose values exceed the blob is not copied whole; the task copies only its
+// metadata, then streams the values in chunks (ROW: Kc columns of the R x C
+// column-major block; COL: Lq rows of the L x c row-major block) together
+// with the matching front / v pieces, double-buffered through the slot:
+// [meta (<= STREAM_META bytes) | value buffer 0 | value buffer 1] in the blob
+// area, [piece 0 | piece 1 | f_B rows] in the scratch area.  No blob growth,
+// whatever the separator size (BASELINE C5: s ~ 2300).
+constexpr int STREAM_META = 256;
 
 constexpr int SMALL_MAX_S = 64;  // wider supernodes are always BIG
 
@@ -228,6 +240,8 @@ struct PlanOptions {
   bool defer_values = false;       // build the plan from symbolic factors: blobs hold metadata only
                                    // (DevicePlan::segs), values are placed later by the descriptors
   int32_t threads = 0;             // host threads for the per-factor blob emission (0: hardware)
+  int32_t stream_rows = 16;        // streamed ROW tasks: rows per task (SFCDD_STREAM_ROWS; 0 disables streaming)
+  int32_t stream_cols = 16;        // streamed COL tasks: columns per task (SFCDD_STREAM_COLS)
   PlanOptions();                 // environment overrides SFCDD_BLOB_MAX, SFCDD_SCRATCH_MAX, ...
 };
 

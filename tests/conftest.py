@@ -35,3 +35,11 @@ def oracle():
     import sfcdd_oracle
 
     return sfcdd_oracle
+
+
+def pytest_collection_modifyitems(config, items):
+    """GPU tests get a hard per-test timeout (thread method: a stuck CUDA call
+    cannot hang the whole job; the DAG kernel's own watchdog traps first)."""
+    for item in items:
+        if item.get_closest_marker("gpu") and not item.get_closest_marker("timeout"):
+            item.add_marker(pytest.mark.timeout(900, method="thread"))

@@ -236,12 +236,16 @@ def test_pcg_c3_matches_reference(sfcdd, golden):
     assert np.linalg.norm(rep.solution[idx] - ref) <= 1e-10 * np.linalg.norm(ref)
 
 
-def test_pcg_c3_grown_blob_matches_reference(sfcdd, golden, monkeypatch):
-    """Separators wider than the requested blob: the plan grows the blob to
-    the next power of two that holds one ROW row / COL column (C3 with a
-    2 KB request -> 8 KB, 2-worker CTAs; the path BASELINE C5's s ~ 2000
-    separators take at 32 KB)."""
+@pytest.mark.parametrize("mode", ["grown", "streamed"])
+def test_pcg_c3_grown_blob_matches_reference(sfcdd, golden, mode, monkeypatch):
+    """Separators wider than the requested blob.  ``grown``: the plan grows
+    the blob to the next power of two that holds one ROW row / COL column
+    (C3 with a 2 KB request -> 8 KB, 2-worker CTAs).  ``streamed``: the
+    default of many-subdomain plans -- the oversized ROW / COL blocks stream
+    their values in double-buffered chunks through the 2 KB slot (the path
+    of BASELINE C5's s ~ 2300 separators)."""
     monkeypatch.setenv("SFCDD_BLOB_MAX", "2048")
+    monkeypatch.setenv("SFCDD_STREAM_ROWS", "0" if mode == "grown" else "16")
     g = golden.npz("solve_c3.npz")
     rep, _ = _pcg(sfcdd, (7, 7, 7), 512, 0.5, 8)
     assert abs(rep.iterations - int(g["iterations"])) <= 1

@@ -125,14 +125,17 @@ def test_host_factor_rejects_non_spd():
                                                   ((6, 5), 6, 0.75, 0),
                                                   # separators wider than a 2 KB blob row: the blob grows
                                                   ((5, 5, 5), 4, 0.5, 2048)])
-@pytest.mark.parametrize("split", [False, True])
+@pytest.mark.parametrize("split", [False, "stream", "nostream"])
 def test_device_plan_host_interpreter(oracle, levels, p, gamma, blob, split, monkeypatch):
     """The fragment/blob layout the DAG kernel executes, run on the host;
-    ``split`` forces the ASM / XB task path of big supernodes (plan.h)."""
+    ``split`` forces the ASM / XB task path of big supernodes (plan.h), with
+    the streamed ROW / COL blocks (``stream``: values beyond the blob stay in
+    HBM and are consumed in chunks) or without (blob growth)."""
     if split:
         monkeypatch.setenv("SFCDD_SPLIT_MIN", "1")
         monkeypatch.setenv("SFCDD_ASM_RED", "1")
         monkeypatch.setenv("SFCDD_XB_MIN", "1")
+        monkeypatch.setenv("SFCDD_STREAM_ROWS", "0" if split == "nostream" else "8")
     A = oracle.assemble_scaled_laplacian(levels)
     n = A.shape[0]
     ov = oracle.enlarge(oracle.disjoint_partition(n, p), gamma)
