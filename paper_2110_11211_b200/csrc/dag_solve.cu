@@ -22,9 +22,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <map>
 #include <mutex>
+#include <type_traits>
 
 #include "common.h"
 #include "dag_solve.h"
@@ -55,6 +57,10 @@ struct DagArgs {
                  // 4 = blob copies without the L2 evict_first hint
   int32_t sig_ns;  // signaller idle sleep (ns, SFCDD_SIG_NS; mode bit 8)
   uint32_t sig_wait_ns;  // signaller suspend-time hint on the post barrier (SFCDD_SIG_WAIT_NS)
+  int32_t* diag;  // mode bit 32 (SFCDD_DAG_MODE, debugging): a dependency wait that times out records
+                  // {1, task, wait_idx, value, target, kind} here and every warp leaves at its next wait
+                  // instead of trapping; the host reads it back after the launch
+  unsigned long long watchdog_ns;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -117,7 +123,7 @@ __device__ __forceinline__ bool mbar_wait_timed(uint64_t* bar, uint32_t parity, 
 
 // Watchdog (never fires in a correct run): a wait that exceeds this many
 // ns traps the kernel -- a launch error for the caller instead of a hung GPU
-constexpr unsigned long long DAG_WATCHDOG_NS = 20ull * 1000 * 1000 * 1000;
+constexpr unsigned long long DAG_WATCHDOG_NS = 20ull * 1000 * 1000 * 1000;  // bulk-copy waits
 
 // mbarrier wait with the watchdog (1 us suspend hints per try)
 __device__ __forceinline__ void mbar_wait_guard(uint64_t* bar, uint32_t parity) {
@@ -541,12 +547,12 @@ __device__ __noinline__ void run_xb(const int32_t* h, const DagArgs& A, const Fa
   warp_gather(na, lane, [&](int q) { return -__ldcg(xy + rows[q]); }, [&](int q, double v) { __stcg(vb + q, v); });
 }
 
-// ====================================================== ROW (big forward)
-// rows [r0, r0+R) of out = M f_J; lanes = (row, k-phase) when R < 32; the
-// assembled front f = [f_J ; f_B] is read contiguously (ASM tasks)
-template <bool SPLIT, typename Ahead>
-__device__ __forceinline__ void run_row(const int32_t* h, double* S, const DagArgs& A, const FactorDev& F,
-                                        int lane, Ahead ahead, uint64_t* bar, uint32_t& phase) {
+// ================================================= BLOB ROW (big forward)
+// values in the slot: rows [r0, r0+R) of out = M f_J; lanes = (row, k-phase)
+// when R < 32; the assembled front f = [f_J ; f_B] is read contiguously (ASM tasks)
+template <bool SPLIT>
+__device__ __forceinline__ void run_row_blob(const int32_t* h, double* S, const DagArgs& A, const FactorDev& F,
+                                             int lane, uint64_t* bar, uint32_t& phase) {
   const int s = h[RW_S], R = h[RW_R], C = h[RW_C], r0 = h[RW_R0], NB = h[RW_NB];
   const double* V = reinterpret_cast<const double*>(reinterpret_cast<const uint8_t*>(h) + h[RW_VAL_OFF]);
   int boff = C;  // S index of the first update-row value f_B[r0 - s + i]
@@ -557,6 +563,7 @@ __device__ __forceinline__ void run_row(const int32_t* h, double* S, const DagAr
     const double* f = A.upd + h[RW_FOFF];
     const int c2 = (C + 1) & ~1;
     boff = c2 + (r0 & 1);
+    __syncwarp();  // every lane has observed the blob copy's phase before the barrier is armed again
     if (lane == 0) {
       fence_proxy_async_global();
       const uint32_t ba = bytes16(C), bb = NB > 0 ? bytes16(NB + (r0 & 1)) : 0u;
@@ -565,7 +572,7 @@ __device__ __forceinline__ void run_row(const int32_t* h, double* S, const DagAr
       if (NB > 0) bulk_g2s(S + c2, f + (r0 & ~1), bb, bar);
     }
     __syncwarp();
-    mbar_wait_guard(bar, phase);
+    mbar_wait(bar, phase);
     phase ^= 1u;
   } else if (h[RW_ASM_HI] >= 0) {
     // huge s: J's assembly record in global memory [s, m] cols ptr src
@@ -600,7 +607,6 @@ __device__ __forceinline__ void run_row(const int32_t* h, double* S, const DagAr
       S[q] = acc;
     }
   }
-  ahead();
   __syncwarp();
   const int RP = R >= 32 ? 32 : (R <= 1 ? 1 : 1 << (32 - __clz(R - 1)));  // lanes per phase
   const int P = 32 / RP;
@@ -631,30 +637,31 @@ __device__ __forceinline__ void run_row(const int32_t* h, double* S, const DagAr
   }
 }
 
-// ===================================================== COL (big backward)
+// ================================================ BLOB COL (big backward)
 // columns [k0, k0+c): x_j = sum_r M[k0+r, k0+j] v[r]; lanes = (column, row-phase)
-template <bool SPLIT, typename Ahead>
-__device__ __forceinline__ void run_col(const int32_t* h, double* S, const DagArgs& A, const FactorDev& F,
-                                        int lane, Ahead ahead, uint64_t* bar, uint32_t& phase) {
+template <bool SPLIT>
+__device__ __forceinline__ void run_col_blob(const int32_t* h, double* S, const DagArgs& A, const FactorDev& F,
+                                             int lane, uint64_t* bar, uint32_t& phase) {
   const int s = h[CL_S], m = h[CL_M], k0 = h[CL_K0], c = h[CL_C];
   const double* V = reinterpret_cast<const double*>(reinterpret_cast<const uint8_t*>(h) + h[CL_VAL_OFF]);
   const int32_t* cols = h + h[CL_COLS];
   double* xy = A.xy + F.xy_off;
   const int ny = s - k0, L = ny + m;
   const double* yv = A.upd + h[CL_YOFF] + k0;
-  double* Sv = S;  // v[r] = Sv[r]
+  const double* Sv = S;  // v[r] = Sv[r]
   if (SPLIT && h[CL_XOFF] >= 0) {
     // -x_B (XB tasks) follows y_J in upd: v = [y_J[k0:s) ; -x_B] is one
     // contiguous range (plan.cpp), bulk-copied from its 16-byte aligned start
     const int sh = (int)((h[CL_YOFF] + k0) & 1);
     Sv = S + sh;
+    __syncwarp();  // every lane has observed the blob copy's phase before the barrier is armed again
     if (lane == 0) {
       fence_proxy_async_global();
       mbar_expect_tx(bar, bytes16(L + sh));
       bulk_g2s(S, yv - sh, bytes16(L + sh), bar);
     }
     __syncwarp();
-    mbar_wait_guard(bar, phase);
+    mbar_wait(bar, phase);
     phase ^= 1u;
   } else {
     const int32_t* rows = h + h[CL_ROWS];
@@ -662,7 +669,6 @@ __device__ __forceinline__ void run_col(const int32_t* h, double* S, const DagAr
         L, lane, [&](int q) { return q < ny ? __ldcg(yv + q) : -__ldcg(xy + rows[q - ny]); },
         [&](int q, double v) { S[q] = v; });
   }
-  ahead();
   __syncwarp();
   const int CP = c >= 32 ? 32 : (c <= 1 ? 1 : 1 << (32 - __clz(c - 1)));  // lanes per phase
   const int P = 32 / CP;
@@ -685,127 +691,173 @@ __device__ __forceinline__ void run_col(const int32_t* h, double* S, const DagAr
   }
 }
 
-// ============================================ streamed BIG tasks (plan.h)
-// Double-buffered chunk pipeline inside one warp: lane 0 keeps two chunks
-// (values + the matching front / v piece, one bulk copy each) in flight on
-// the warp's two mbarriers while the lanes consume the previous one.
-struct Pipe {
-  uint64_t* bar[2];
-  uint32_t* phase[2];
-};
+// ================================================ dense blocks (ROW / COL)
+// DIRECT blocks: the dense ROW / COL blocks of wide separators stay in HBM
+// and are streamed into registers -- any size, every factor value is used
+// exactly once -- where a BLOB block (above) arrives in the slot with its
+// metadata in one bulk copy, the lowest-latency form for small blocks.
+//
+// dense_dot: lane (il, ph) accumulates sum_k V[k W + il] vec[k] over
+// k = ph, ph + P, ... (W <= 32 lanes per vector entry, P = 32 / pow2(W) entry
+// phases), DU loads per lane in flight ahead of the FMAs (two register
+// groups), then a butterfly over the phases.  ROW: W = R rows, k = columns of
+// the R x C column-major block, vec = f_J.  COL: W = c columns, k = rows of
+// the L x c row-major block, vec = [y_J[k0:s) ; -x_B].
+//  * RING = false: vec sits in the slot scratch (gathered by the task);
+//  * RING = true: vec is contiguous in the update buffer (ASM / XB tasks
+//    wrote it) and travels through a two-slot ring of RING_CHUNK doubles by
+//    bulk copies on the warp's mbarrier, the next chunk in flight while the
+//    current one is consumed: vec[k] = gvec[k + sh], gvec 16-byte aligned.
+constexpr int DU = 16;
 
-// ROW: rows [r0, r0+R) of out = M f_J, values R x C column-major in HBM
-__device__ __noinline__ void run_row_stream(const int32_t* h, uint8_t* slot, double* S, const DagArgs& A,
-                                            const uint8_t* gblob, int lane, Pipe pp) {
-  const int s = h[RW_S], R = h[RW_R], C = h[RW_C], r0 = h[RW_R0], NB = h[RW_NB], Kc = h[RW_STREAM];
-  const double* gV = reinterpret_cast<const double*>(gblob + h[RW_VAL_OFF]);
-  const double* f = A.upd + h[RW_FOFF];
-  const uint32_t vb_bytes = bytes16(R * Kc);
-  double* vbuf[2] = {reinterpret_cast<double*>(slot + STREAM_META),
-                     reinterpret_cast<double*>(slot + STREAM_META + vb_bytes)};
-  double* fbuf[2] = {S, S + Kc};
-  double* fB = S + 2 * Kc;  // f[r0 - (r0 & 1) ...] for the update rows
-  const int nch = (C + Kc - 1) / Kc;
-  auto issue = [&](int ch, uint32_t extra) {  // lane 0: chunk ch into buffer ch & 1
-    const int k0 = ch * Kc, kc = min(Kc, C - k0);
-    uint64_t* b = pp.bar[ch & 1];
-    const uint32_t bv = bytes16(R * kc), bf = bytes16(kc);
-    mbar_expect_tx(b, bv + bf + extra);
-    bulk_g2s(vbuf[ch & 1], gV + (int64_t)k0 * R, bv, b);
-    bulk_g2s(fbuf[ch & 1], f + k0, bf, b);
-  };
-  if (lane == 0) {
-    fence_proxy_async_global();
-    const uint32_t bb = NB > 0 ? bytes16(NB + (r0 & 1)) : 0u;
-    issue(0, bb);
-    if (NB > 0) bulk_g2s(fB, f + (r0 & ~1), bb, pp.bar[0]);
-    if (nch > 1) issue(1, 0);
-  }
-  const int RP = R >= 32 ? 32 : (R <= 1 ? 1 : 1 << (32 - __clz(R - 1)));  // lanes per phase
-  const int P = 32 / RP;
-  const int il = lane & (RP - 1), ph = lane / RP;
-  double a0 = 0.0, a1 = 0.0;
-  for (int ch = 0; ch < nch; ++ch) {
-    const int q = ch & 1;
-    mbar_wait_guard(pp.bar[q], *pp.phase[q]);
-    *pp.phase[q] ^= 1u;
-    const int kc = min(Kc, C - ch * Kc);
-    if (il < R) {
-      const double* v = vbuf[q] + il;
-      const double* fc = fbuf[q];
-      int k = ph;
-      for (; k + P < kc; k += 2 * P) {
-        a0 = fma(v[k * R], fc[k], a0);
-        a1 = fma(v[(k + P) * R], fc[k + P], a1);
-      }
-      if (k < kc) a0 = fma(v[k * R], fc[k], a0);
-    }
-    __syncwarp();  // buffer q consumed
-    if (lane == 0 && ch + 2 < nch) issue(ch + 2, 0);
-  }
-  double acc = a0 + a1;
-  for (int o = RP; o < 32; o <<= 1) acc += __shfl_xor_sync(FULL, acc, o);
-  if (ph == 0 && il < R) {
-    const int row = r0 + il;
-    if (row < s)
-      __stcg(A.upd + h[RW_YOFF] + row, acc);
-    else
-      __stcg(A.upd + h[RW_UOFF] + (row - s), fB[(r0 & 1) + il] - acc);
-  }
-}
-
-// COL: columns [k0, k0+c) of x_J = M^T v, values L x c row-major in HBM,
-// v = [y_J[k0:s) ; -x_B] contiguous in upd (XB mode or m = 0)
-__device__ __noinline__ void run_col_stream(const int32_t* h, uint8_t* slot, double* S, const DagArgs& A,
-                                            const FactorDev& F, const uint8_t* gblob, int lane, Pipe pp) {
-  const int s = h[CL_S], m = h[CL_M], k0 = h[CL_K0], c = h[CL_C], Lq = h[CL_STREAM];
-  const int L = s - k0 + m;
-  const double* gV = reinterpret_cast<const double*>(gblob + h[CL_VAL_OFF]);
-  const double* yv = A.upd + h[CL_YOFF] + k0;
-  const int32_t* cols = h + h[CL_COLS];
-  const uint32_t vb_bytes = bytes16(Lq * c);
-  double* vbuf[2] = {reinterpret_cast<double*>(slot + STREAM_META),
-                     reinterpret_cast<double*>(slot + STREAM_META + vb_bytes)};
-  double* xbuf[2] = {S, S + Lq + 2};
-  const int nch = (L + Lq - 1) / Lq;
-  auto issue = [&](int ch) {
-    const int q0 = ch * Lq, lq = min(Lq, L - q0);
-    uint64_t* b = pp.bar[ch & 1];
-    const uint32_t bv = bytes16(lq * c), bx = bytes16(lq);
-    mbar_expect_tx(b, bv + bx);
-    bulk_g2s(vbuf[ch & 1], gV + (int64_t)q0 * c, bv, b);
-    bulk_g2s(xbuf[ch & 1], yv + q0, bx, b);
-  };
-  if (lane == 0) {
-    fence_proxy_async_global();
-    issue(0);
-    if (nch > 1) issue(1);
-  }
-  const int CP = c >= 32 ? 32 : (c <= 1 ? 1 : 1 << (32 - __clz(c - 1)));
-  const int P = 32 / CP;
-  const int j = lane & (CP - 1), ph = lane / CP;
-  double a0 = 0.0, a1 = 0.0;
-  for (int ch = 0; ch < nch; ++ch) {
-    const int q = ch & 1;
-    mbar_wait_guard(pp.bar[q], *pp.phase[q]);
-    *pp.phase[q] ^= 1u;
-    const int lq = min(Lq, L - ch * Lq);
-    if (j < c) {
-      const double* v = vbuf[q] + j;
-      const double* xv = xbuf[q];
-      int r = ph;
-      for (; r + P < lq; r += 2 * P) {
-        a0 = fma(v[r * c], xv[r], a0);
-        a1 = fma(v[(r + P) * c], xv[r + P], a1);
-      }
-      if (r < lq) a0 = fma(v[r * c], xv[r], a0);
-    }
+// (ONE inlined copy in the kernel: run_dense below is the only caller; the
+// kernel's code size matters -- every resident warp runs a different path)
+__device__ __forceinline__ double dense_dot(const double* __restrict__ V, bool ring, int W, int Len, double* S,
+                                            const double* gvec, int sh, uint64_t* bar, uint32_t& phase, int lane) {
+  const int WP = W >= 32 ? 32 : (W <= 2 ? 2 : 1 << (32 - __clz(W - 1)));  // lanes per phase (P <= 16)
+  const int P = 32 / WP;
+  const int ph = lane / WP;
+  const int il = min(lane & (WP - 1), W - 1);  // lanes >= W repeat the last one (result unused)
+  const int nj = (Len - ph + P - 1) / P;       // vector entries of this lane's phase (>= 0)
+  const int ng = ((Len + P - 1) / P + DU - 1) / DU;
+  const double* q = V + (size_t)ph * W + il;   // this lane's next value
+  const int vs = P * W;                        // value stride per vector entry of the phase
+  if (ring) {
+    // every lane has observed the barrier phase of the task's blob copy before
+    // the barrier is armed again (a lane still polling the old parity would
+    // see two completed phases as none)
     __syncwarp();
-    if (lane == 0 && ch + 2 < nch) issue(ch + 2);
+    if (lane == 0) {
+      fence_proxy_async_global();  // the producers' generic-proxy writes -> this bulk read
+      fence_proxy_async();         // earlier generic reads of the ring slot -> async write
+      const uint32_t nb = bytes16(min(RING_CHUNK, Len) + sh);
+      mbar_expect_tx(bar, nb);
+      bulk_g2s(S, gvec, nb, bar);
+    }
   }
-  double acc = a0 + a1;
-  for (int o = CP; o < 32; o <<= 1) acc += __shfl_xor_sync(FULL, acc, o);
-  if (ph == 0 && j < c) __stcg(A.xy + F.xy_off + cols[j], acc);
+  double d[DU];
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  const int GPC = ring ? RING_CHUNK / (P * DU) : ng;  // groups per ring chunk (>= 1)
+  const double* fq = S + ph;  // vec entry of this lane's next value (no ring)
+  for (int g = 0; g < ng; ++g) {
+    // DU independent loads per lane in flight (the only latency the loop pays)
+    const int left = nj - g * DU;  // entries of this lane still to do
+#pragma unroll
+    for (int u = 0; u < DU; ++u) d[u] = u < left ? __ldcs(q + u * vs) : 0.0;  // streamed from HBM, evict-first
+    q += (size_t)DU * vs;
+    if (ring && g % GPC == 0) {
+      const int c = g / GPC;
+      mbar_wait_guard(bar, phase);
+      phase ^= 1u;
+      // every lane has consumed chunk c - 1 (its slot may be refilled) and has
+      // observed chunk c's phase (the barrier may be armed again)
+      __syncwarp();
+      if (lane == 0 && RING_CHUNK * (c + 1) < Len) {
+        fence_proxy_async();
+        const uint32_t nb = bytes16(min(RING_CHUNK, Len - RING_CHUNK * (c + 1)) + sh);
+        mbar_expect_tx(bar, nb);
+        bulk_g2s(S + ((c + 1) & 1) * RING_STRIDE, gvec + RING_CHUNK * (c + 1), nb, bar);
+      }
+      fq = S + (c & 1) * RING_STRIDE + sh + ph;
+    }
+#pragma unroll
+    for (int u = 0; u < DU; u += 4) {
+      a0 = fma(d[u], u < left ? fq[P * u] : 0.0, a0);
+      a1 = fma(d[u + 1], u + 1 < left ? fq[P * (u + 1)] : 0.0, a1);
+      a2 = fma(d[u + 2], u + 2 < left ? fq[P * (u + 2)] : 0.0, a2);
+      a3 = fma(d[u + 3], u + 3 < left ? fq[P * (u + 3)] : 0.0, a3);
+    }
+    fq += P * DU;
+  }
+  double acc = (a0 + a1) + (a2 + a3);
+  for (int o = WP; o < 32; o <<= 1) acc += __shfl_xor_sync(FULL, acc, o);
+  return acc;
+}
+static_assert(RING_CHUNK % (16 * DU) == 0, "a ring chunk holds whole groups for every phase count");
+
+// DIRECT ROW (big forward): rows [r0, r0+R) of out = M f_J: y rows (< s) or update
+// rows u = f_B - out.  DIRECT COL (big backward): columns [k0, k0+c):
+// x_j = sum_r M[k0+r, k0+j] v[r], v = [y_J[k0:s) ; -x_B].
+template <bool SPLIT>
+__device__ __forceinline__ uint32_t run_dense(bool is_row, const int32_t* h, double* S, const DagArgs& A,
+                                              const FactorDev& F, const uint8_t* gblob, int lane, uint64_t* bar,
+                                              uint32_t phase) {
+  double* xy = A.xy + F.xy_off;
+  const double* V;
+  const double* gvec = nullptr;
+  bool ring = false;
+  int W, Len, sh = 0;
+  double fb = 0.0;
+  if (is_row) {
+    const int s = h[RW_S], R = h[RW_R], C = h[RW_C], r0 = h[RW_R0], NB = h[RW_NB];
+    V = reinterpret_cast<const double*>(gblob + h[RW_VAL_OFF]);
+    W = R;
+    Len = C;
+    if (SPLIT && h[RW_FOFF] >= 0) {
+      // front assembled by J's ASM tasks, contiguous and 16-byte aligned in upd
+      gvec = A.upd + h[RW_FOFF];
+      ring = true;
+      if (NB > 0 && lane < R) fb = __ldcg(gvec + r0 + lane);
+    } else {
+      // f = base + child updates in fixed order (base 0 for update rows), from
+      // the metadata in the slot or from J's global assembly record
+      // [s, m] cols ptr src over front positions (every load one global round trip)
+      const bool ga = h[RW_ASM_HI] >= 0;
+      const int64_t o16 = (int64_t)(uint32_t)h[RW_ASM16] | ((int64_t)h[RW_ASM_HI] << 32);
+      const int32_t* am = reinterpret_cast<const int32_t*>(A.blobs + 16 * o16);
+      const int32_t* cols = ga ? am + 2 : h + h[RW_COLS];
+      const int32_t* ptr = ga ? cols + s : h + h[RW_PTR];
+      const int32_t* src = ga ? ptr + s + __ldg(am + 1) + 1 : h + h[RW_SRC];
+      for (int q = lane; q < C + NB; q += 32) {
+        const int p = ga && q >= C ? r0 + (q - C) : q;
+        const int e0 = ptr[p], e1 = ptr[p + 1];
+        double a = q < C ? __ldg(A.rhs + gidx(F, cols[q])) : 0.0;
+        int e = e0;
+        for (; e + 2 <= e1; e += 2) {
+          const double u0 = __ldcg(A.upd + src[e]), u1 = __ldcg(A.upd + src[e + 1]);
+          a += u0;
+          a += u1;
+        }
+        if (e < e1) a += __ldcg(A.upd + src[e]);
+        S[q] = a;
+      }
+      __syncwarp();
+      if (NB > 0 && lane < R) fb = S[C + lane];
+    }
+  } else {
+    const int s = h[CL_S], m = h[CL_M], k0 = h[CL_K0];
+    V = reinterpret_cast<const double*>(gblob + h[CL_VAL_OFF]);
+    W = h[CL_C];
+    const int ny = s - k0;
+    Len = ny + m;
+    const double* yv = A.upd + h[CL_YOFF] + k0;
+    if (SPLIT && h[CL_XOFF] >= 0) {
+      // -x_B (XB tasks) follows y_J in upd: v is one contiguous range (plan.cpp)
+      sh = (int)((h[CL_YOFF] + k0) & 1);
+      gvec = yv - sh;
+      ring = true;
+    } else {
+      const int32_t* rows = h + h[CL_ROWS];
+      warp_gather(
+          Len, lane, [&](int q) { return q < ny ? __ldcg(yv + q) : -__ldcg(xy + rows[q - ny]); },
+          [&](int q, double v) { S[q] = v; });
+      __syncwarp();
+    }
+  }
+  const double acc = dense_dot(V, SPLIT && ring, W, Len, S, gvec, sh, bar, phase, lane);
+  // after the butterfly every phase holds the sum: lane i (< W <= lanes per phase) owns row / column i
+  if (lane < W) {
+    if (is_row) {
+      const int row = h[RW_R0] + lane, s = h[RW_S];
+      if (row < s)
+        __stcg(A.upd + h[RW_YOFF] + row, acc);
+      else
+        __stcg(A.upd + h[RW_UOFF] + (row - s), fb - acc);
+    } else {
+      __stcg(xy + (h + h[CL_COLS])[lane], acc);
+    }
+  }
+  return phase;
 }
 
 // ================================================================ kernel
@@ -859,11 +911,11 @@ __device__ __forceinline__ void signaller(const DagArgs& A, int32_t* mbox, int32
 
 // SPLIT: the plan has ASM / XB tasks (many-subdomain configurations); the
 // kernel without them keeps the smaller code of the common case
-template <int WPB, bool SPLIT>
-__global__ void __launch_bounds__((WPB + 1) * 32, 20 / WPB) k_dag(DagArgs A) {
+// DIRECT: the plan has ROW / COL blocks streamed from HBM (wide separators)
+template <int WPB, bool SPLIT, bool DIRECT>
+__global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? 72 : 96) k_dag(DagArgs A) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bars[WPB];
-  __shared__ __align__(8) uint64_t bars2[WPB];  // second chunk buffer of streamed tasks
   __shared__ int32_t mbox[WPB];
   __shared__ int32_t nexit;
   __shared__ __align__(8) uint64_t sigbar;
@@ -881,14 +933,12 @@ __global__ void __launch_bounds__((WPB + 1) * 32, 20 / WPB) k_dag(DagArgs A) {
     return;
   }
   uint64_t* bar = &bars[warp];
-  uint64_t* bar2 = &bars2[warp];
   if (lane == 0) {
     mbar_init(bar, 1);
-    mbar_init(bar2, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
-  uint32_t phase = 0, phase2 = 0;
+  uint32_t phase = 0;
   // queue of this warp (interleaved split of the global order: spreads the
   // claim atomics over nq lines; deadlock-free, the smallest unfinished task
   // is always claimable)
@@ -909,6 +959,7 @@ __global__ void __launch_bounds__((WPB + 1) * 32, 20 / WPB) k_dag(DagArgs A) {
   constexpr int TW = (int)(sizeof(TaskDev) / 4);
   static_assert(sizeof(TaskDev) % 4 == 0 && TW <= 32, "TaskDev words");
   int32_t pw = (stat && lane < TW && ts < A.ntask) ? __ldg(reinterpret_cast<const int32_t*>(A.tasks + ts) + lane) : 0;
+  int dead = 0;
   for (;;) {
     int t = 0;
     if (stat) {
@@ -969,17 +1020,30 @@ __global__ void __launch_bounds__((WPB + 1) * 32, 20 / WPB) k_dag(DagArgs A) {
         auto watchdog = [&]() {  // a dependency that never completes traps instead of hanging the GPU
           if ((++polls & 4095u) == 0) {
             if (t0 == 0) t0 = gtimer();
-            else if (gtimer() - t0 > DAG_WATCHDOG_NS) __trap();
+            if (A.mode & 32) {  // diagnostic mode: record the stuck wait, let every warp leave
+              if (ld_relaxed(A.diag) != 0) dead = 1;
+              else if (gtimer() - t0 > A.watchdog_ns && atomicCAS(A.diag, 0, 1) == 0) {
+                A.diag[1] = t;
+                A.diag[2] = T.wait_idx;
+                A.diag[3] = ld_relaxed(A.ctr + T.wait_idx);
+                A.diag[4] = T.wait_target;
+                A.diag[5] = T.kind;
+                A.diag[6] = T.group;
+                dead = 1;
+              }
+            } else if (gtimer() - t0 > A.watchdog_ns) {
+              __trap();
+            }
           }
         };
         if (A.mode & 1) {
-          while (ld_acquire(A.ctr + T.wait_idx) < T.wait_target) {
+          while (!dead && ld_acquire(A.ctr + T.wait_idx) < T.wait_target) {
             __nanosleep(ns);
             ns = ns < 256 ? 2 * ns : 256;
             watchdog();
           }
         } else {
-          while (ld_relaxed(A.ctr + T.wait_idx) < T.wait_target) {
+          while (!dead && ld_relaxed(A.ctr + T.wait_idx) < T.wait_target) {
             __nanosleep(ns);
             ns = ns < 256 ? 2 * ns : 256;
             watchdog();
@@ -992,38 +1056,31 @@ __global__ void __launch_bounds__((WPB + 1) * 32, 20 / WPB) k_dag(DagArgs A) {
     __syncwarp();
     mbar_wait_guard(bar, phase);
     phase ^= 1u;
-    if (tr && lane == 0) tr[3] = gtimer();
-    switch (T.kind) {
-      case TK_FRAG_FWD:
-        run_frag(h, true, S, A, F, lane, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);
-        break;
-      case TK_FRAG_BWD:
-        run_frag(h, false, S, A, F, lane, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);
-        break;
-      case TK_ROW_FWD:
-        if (SPLIT && h[RW_STREAM] > 0)
-          run_row_stream(h, smem + (size_t)warp * A.slot_bytes, S, A, A.blobs + T.blob_off, lane,
-                         Pipe{{bar, bar2}, {&phase, &phase2}});
-        else
-          run_row<SPLIT>(h, S, A, F, lane, ahead, bar, phase);
-        break;
-      default:
-        if constexpr (SPLIT) {
-          if (T.kind == TK_ASM_FWD) {
-            run_asm(h, A, F, lane);
-            break;
-          }
-          if (T.kind == TK_XB_BWD) {
-            run_xb(h, A, F, lane);
-            break;
-          }
+    if (A.mode & 32) {  // diagnostic mode: leave once a stuck wait was recorded
+      dead = __shfl_sync(FULL, dead, 0);
+      if (dead) {
+        if (lane == 0) {
+          asm volatile("red.release.cta.shared::cta.add.s32 [%0], 1;" ::"r"(smem_u32(&nexit)) : "memory");
+          mbar_arrive(&sigbar);
         }
-        if (SPLIT && h[CL_STREAM] > 0)
-          run_col_stream(h, smem + (size_t)warp * A.slot_bytes, S, A, F, A.blobs + T.blob_off, lane,
-                         Pipe{{bar, bar2}, {&phase, &phase2}});
-        else
-          run_col<SPLIT>(h, S, A, F, lane, ahead, bar, phase);
         break;
+      }
+    }
+    if (tr && lane == 0) tr[3] = gtimer();
+    if (T.kind == TK_FRAG_FWD || T.kind == TK_FRAG_BWD) {
+      run_frag(h, T.kind == TK_FRAG_FWD, S, A, F, lane, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);
+    } else if (SPLIT && T.kind == TK_ASM_FWD) {
+      run_asm(h, A, F, lane);
+    } else if (SPLIT && T.kind == TK_XB_BWD) {
+      run_xb(h, A, F, lane);
+    } else if (T.kind == TK_ROW_FWD && h[RW_INBLOB]) {
+      run_row_blob<SPLIT>(h, S, A, F, lane, bar, phase);
+    } else if (T.kind == TK_COL_BWD && h[CL_INBLOB]) {
+      run_col_blob<SPLIT>(h, S, A, F, lane, bar, phase);
+    } else if constexpr (DIRECT) {
+      phase = run_dense<SPLIT>(T.kind == TK_ROW_FWD, h, S, A, F, A.blobs + T.blob_off, lane, bar, phase);
+    } else {
+      __trap();  // a DIRECT block in a plan built without them
     }
     __syncwarp();
     if (lane == 0) {
@@ -1112,10 +1169,14 @@ DagSolver::DagSolver(const DevicePlan& plan, int device, int64_t extra_xy) : dev
   SFCDD_REQUIRE(wpb_ == 2 || wpb_ == 4 || wpb_ == 8, SFCDD_EVALUE, "worker warps per CTA must be 2, 4 or 8");
   bool split = false;
   for (const TaskDev& T : plan.tasks) split = split || T.kind == TK_ASM_FWD || T.kind == TK_XB_BWD;
-  kern_ = split ? (wpb_ == 2 ? (const void*)k_dag<2, true> : wpb_ == 4 ? (const void*)k_dag<4, true>
-                                                                      : (const void*)k_dag<8, true>)
-                : (wpb_ == 2 ? (const void*)k_dag<2, false> : wpb_ == 4 ? (const void*)k_dag<4, false>
-                                                                       : (const void*)k_dag<8, false>);
+  auto pick = [&](auto sp, auto dr) -> const void* {
+    constexpr bool SP = decltype(sp)::value, DR = decltype(dr)::value;
+    return wpb_ == 2 ? (const void*)k_dag<2, SP, DR> : wpb_ == 4 ? (const void*)k_dag<4, SP, DR> : (const void*)k_dag<8, SP, DR>;
+  };
+  using T_ = std::true_type;
+  using F_ = std::false_type;
+  kern_ = split ? (plan.has_direct ? pick(T_{}, T_{}) : pick(T_{}, F_{}))
+                : (plan.has_direct ? pick(F_{}, T_{}) : pick(F_{}, F_{}));
   split_ = split;
   if (const char* e = std::getenv("SFCDD_DAG_MODE")) mode_ = std::atoi(e);
   if (const char* e = std::getenv("SFCDD_SIG_NS")) sig_ns_ = std::atoi(e);
@@ -1170,9 +1231,10 @@ DagSolver::DagSolver(const DevicePlan& plan, int device, int64_t extra_xy) : dev
   nq_ = 16;
   if (const char* e = std::getenv("SFCDD_QUEUES")) nq_ = std::max(1, std::atoi(e));
   const int64_t cw = (1 + CTR_PER_GROUP * (int64_t)ngroups_ + 31) / 32 * 32;
-  ctr_words_ = cw + 32 * (int64_t)nq_;
+  ctr_words_ = cw + 32 * (int64_t)nq_ + 32;  // + one line of diagnostics (mode bit 32)
   CUDA_CHECK(cudaMalloc(&ctr_, ctr_words_ * 4));
   qhead_ = ctr_ + cw;
+  if (const char* e = std::getenv("SFCDD_WATCHDOG_MS")) watchdog_ms_ = std::max(1, std::atoi(e));
   bytes_ += std::max<int64_t>(plan.upd_doubles, 2) * 8 + std::max<int64_t>(xy_doubles_, 2) * 8 + ctr_words_ * 4;
   {
     // the attribute is per function: only ever raise it, so every live
@@ -1193,6 +1255,9 @@ DagSolver::DagSolver(const DevicePlan& plan, int device, int64_t extra_xy) : dev
   SFCDD_REQUIRE(per_sm >= 1, SFCDD_EINTERNAL, "DAG kernel cannot be resident");
   if (const char* e = std::getenv("SFCDD_CTAS_PER_SM")) per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
   grid_ = std::max(1, std::min(per_sm * sms, (ntask_ + wpb_ - 1) / wpb_));
+  if (std::getenv("SFCDD_PLAN_DEBUG"))
+    std::fprintf(stderr, "[dag] %d tasks, %d-worker CTAs, slot %d B (blob %d), %d B smem per CTA, %d CTAs per SM, grid %d\n",
+                 ntask_, wpb_, slot_bytes_, blob_max_, smem_, per_sm, grid_);
 }
 
 DagSolver::~DagSolver() {
@@ -1226,11 +1291,24 @@ void DagSolver::solve(const double* rhs, cudaStream_t st, const int32_t* skip) {
   a.mode = mode_;
   a.sig_ns = sig_ns_;
   a.sig_wait_ns = (uint32_t)sig_wait_ns_;
+  a.diag = qhead_ + 32 * (int64_t)nq_;
+  a.watchdog_ns = 1000000ull * (unsigned long long)watchdog_ms_;
   void* params[] = {&a};
   if (mode_ & 16)  // static worker lists need every CTA resident: cooperative launch guarantees it (or fails)
     CUDA_CHECK(cudaLaunchCooperativeKernel(kern_, dim3(grid_), dim3((wpb_ + 1) * 32), params, smem_, st));
   else
     CUDA_CHECK(cudaLaunchKernel(kern_, dim3(grid_), dim3((wpb_ + 1) * 32), params, smem_, st));
+  if (mode_ & 32) {  // diagnostic mode (not capturable): report a stuck dependency wait
+    int32_t d[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    CUDA_CHECK(cudaMemcpyAsync(d, a.diag, sizeof(d), cudaMemcpyDeviceToHost, st));
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    if (d[0] != 0)
+      throw Error(SFCDD_EINTERNAL, "DAG dependency wait timed out: task " + std::to_string(d[1]) + " (kind " +
+                                       std::to_string(d[5]) + ", group " + std::to_string(d[6]) + ") waits on counter " +
+                                       std::to_string(d[2]) + " = " + std::to_string(d[3]) + " < " +
+                                       std::to_string(d[4]) + " of " + std::to_string(ngroups_) + " groups, " +
+                                       std::to_string(ntask_) + " tasks");
+  }
 }
 
 void DagSolver::set_trace(unsigned long long* dev_buf) { trace_ = dev_buf; }

@@ -39,6 +39,7 @@ class DagSolver {
   bool split_ = false;  // kernel variant with ASM / XB tasks
   const void* kern_ = nullptr;
   int64_t xy_doubles_ = 0, ctr_words_ = 0, bytes_ = 0;
+  int32_t watchdog_ms_ = 20000;  // dependency-wait watchdog (SFCDD_WATCHDOG_MS)
   uint8_t* blobs_ = nullptr;
   TaskDev* tasks_ = nullptr;
   FactorDev* factors_ = nullptr;

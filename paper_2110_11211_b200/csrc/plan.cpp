@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -62,6 +63,7 @@ struct FactorEmit {
   std::vector<TaskDev> tasks;
   std::vector<double> tw;
   int32_t max_scratch = 0, max_copy = 0;
+  bool has_direct = false;
 
   int64_t put_meta(const std::vector<int32_t>& ints, int64_t meta_bytes) {
     const int64_t off = size;
@@ -81,7 +83,7 @@ struct FactorEmit {
   // one blob: metadata + nvals values placed by descriptors (their dst is
   // relative to the value area); asm_word >= 0: that int holds asm16
   int64_t emit_descs(std::vector<int32_t>& ints, int32_t val_off_word, int64_t nvals, const ValDesc* vd, size_t nvd,
-                     int32_t& copy_bytes, const HostFactor* F, int32_t asm_word = -1, bool streamed = false) {
+                     int32_t& copy_bytes, const HostFactor* F, int32_t asm_word = -1, bool meta_only = false) {
     const int64_t meta_bytes = align16(4 * (int64_t)ints.size());
     if (val_off_word >= 0) ints[val_off_word] = (int32_t)meta_bytes;
     const int64_t val_bytes = align16(8 * nvals);
@@ -102,14 +104,14 @@ struct FactorEmit {
         place_values(hd, F->val.data() + d.src, image.data() + h);
       }
     }
-    // streamed tasks copy their metadata only; the values stay in HBM
-    copy_bytes = (int32_t)(streamed ? meta_bytes : meta_bytes + val_bytes);
+    // ROW / COL tasks copy their metadata only; the values stay in HBM
+    copy_bytes = (int32_t)(meta_only ? meta_bytes : meta_bytes + val_bytes);
     max_copy = std::max(max_copy, copy_bytes);
     return off;
   }
   int64_t emit(std::vector<int32_t>& ints, int32_t val_off_word, int64_t nvals, const ValDesc* vd,
-               int32_t& copy_bytes, const HostFactor& F, int32_t asm_word = -1, bool streamed = false) {
-    return emit_descs(ints, val_off_word, nvals, vd, vd ? 1 : 0, copy_bytes, &F, asm_word, streamed);
+               int32_t& copy_bytes, const HostFactor& F, int32_t asm_word = -1, bool meta_only = false) {
+    return emit_descs(ints, val_off_word, nvals, vd, vd ? 1 : 0, copy_bytes, &F, asm_word, meta_only);
   }
   int64_t emit(std::vector<int32_t>& ints, int32_t val_off_word, int64_t nvals, const ValDesc* vd,
                int32_t& copy_bytes) {
@@ -160,16 +162,16 @@ PlanOptions::PlanOptions() {
   if (const char* e = std::getenv("SFCDD_BLOB_MAX")) blob_max = std::atoi(e);
   if (const char* e = std::getenv("SFCDD_SCRATCH_MAX")) scratch_max = std::atoi(e);
   if (const char* e = std::getenv("SFCDD_WORKERS")) workers = std::atoi(e);
-  if (const char* e = std::getenv("SFCDD_ROW_MAX")) row_max = std::max(1, std::atoi(e));
-  if (const char* e = std::getenv("SFCDD_COL_MAX")) col_max = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("SFCDD_ROW_MAX")) row_max = std::min(32, std::max(1, std::atoi(e)));
+  if (const char* e = std::getenv("SFCDD_COL_MAX")) col_max = std::min(32, std::max(1, std::atoi(e)));
   if (const char* e = std::getenv("SFCDD_SLACK_US")) slack_us = std::atof(e);
   if (const char* e = std::getenv("SFCDD_ASM_MAX")) asm_max = std::max(32, std::atoi(e));
   if (const char* e = std::getenv("SFCDD_ASM_RED")) asm_redundancy = std::atof(e);
   if (const char* e = std::getenv("SFCDD_XB_MIN")) xb_min_tasks = std::atoi(e);
+  if (const char* e = std::getenv("SFCDD_DIRECT_ROWS")) direct_min_rows = std::atoi(e);
+  if (const char* e = std::getenv("SFCDD_DIRECT_COLS")) direct_min_cols = std::atoi(e);
   if (const char* e = std::getenv("SFCDD_SPLIT_MIN")) split_min_factors = std::atoi(e);
   if (const char* e = std::getenv("SFCDD_WPB")) wpb = std::atoi(e);
-  if (const char* e = std::getenv("SFCDD_STREAM_ROWS")) stream_rows = std::max(0, std::atoi(e));
-  if (const char* e = std::getenv("SFCDD_STREAM_COLS")) stream_cols = std::max(2, std::atoi(e) & ~1);
   tuned = std::getenv("SFCDD_BLOB_MAX") || std::getenv("SFCDD_WPB");
 }
 
@@ -217,30 +219,17 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
                       const std::vector<int64_t>& gmod, const PlanOptions& opt_in) {
   PlanOptions opt = opt_in;
   {
-    // the widest supernode sets a floor on the blob: one ROW task holds at
-    // least one row of M (s values), one COL task one column (s + m values).
-    // Large 3-D subdomains (BASELINE C5: ~65k overlapped points, separators
-    // of s ~ 2000) exceed the 16 KB shape, so the blob grows to the next power
-    // of two that fits and the CTA shape drops to 2 workers (fewer resident
-    // warps, but the plan builds instead of failing)
-    int64_t need = 0;
-    const bool streams = opt.stream_rows > 0 && (int64_t)factors.size() >= opt.split_min_factors;
+    // DIRECT blocks only where the plan needs them: a supernode so wide that
+    // not even one row / one column of its dense block fits a blob (BASELINE
+    // C5: s ~ 2300).  Such plans stream every wide supernode; the others keep
+    // the smaller kernel without the streaming path.
+    bool need = false;
     for (const HostFactor* F : factors)
       for (const Supernode& S : F->sn)
-        if (!streams)  // streamed plans never need more than the chosen blob
-          need = std::max({need, blob_size(RW_WORDS, (int64_t)S.s),
-                           blob_size(CL_WORDS + 1 + (int64_t)S.m, (int64_t)S.s + S.m)});
-    if (need > opt.blob_max) {
-      int64_t b = opt.blob_max;
-      while (b < need) b *= 2;
-      SFCDD_REQUIRE(b <= 64 * 1024, SFCDD_EVALUE,
-                    "widest supernode needs a " + std::to_string(need) + "-byte task blob (> 64 KB)");
-      if (std::getenv("SFCDD_PLAN_DEBUG"))
-        std::fprintf(stderr, "[plan] blob grown %d -> %lld bytes for the widest supernode\n", opt.blob_max,
-                     (long long)b);
-      opt.blob_max = (int32_t)b;
-      opt.wpb = 2;
-    }
+        need = need || blob_size(RW_WORDS, (int64_t)S.s) > opt.blob_max ||
+               blob_size(CL_WORDS + 1, (int64_t)S.s + S.m) > opt.blob_max;
+    if (opt.direct_min_rows < 0) opt.direct_min_rows = need ? 8 : 0;
+    if (opt.direct_min_cols < 0) opt.direct_min_cols = need ? 4 : 0;
   }
   SFCDD_REQUIRE(opt.scratch_max < 65536 && opt.big_scratch_max < 65536, SFCDD_EINTERNAL,
                 "scratch positions must fit 16 bits");
@@ -438,16 +427,43 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         SFCDD_REQUIRE(upd_slot[gr.factor][c] >= 0, SFCDD_EINTERNAL, "big child without update slot");
         for (int32_t a = 0; a < K.m; ++a) contrib[F.rel[K.rel_off + a]].push_back(upd_slot[gr.factor][c] + a);
       }
-      // forward row blocks that never straddle s.  ASM mode: values only;
-      // inline mode: + the assembly CSR of the task's front positions
+      // forward row blocks that never straddle s (rows [0, s): y rows; rows
+      // [s, s+m): update rows).  BLOB blocks: as many rows as fit the blob
+      // next to the metadata -- values and metadata arrive in ONE bulk copy,
+      // the lowest-latency form for the many small dense blocks.  A supernode
+      // too wide for that (fewer than direct_min_rows rows per blob at full
+      // width) is cut into balanced blocks of <= row_max rows whose values
+      // stay in HBM and are streamed into registers (DIRECT; dag_solve.cu).
       auto row_nnz = [&](int32_t r0, int32_t C, int32_t NB) {
         int64_t nnz = 0;
         for (int32_t q = 0; q < C + NB; ++q) nnz += (int64_t)contrib[q < C ? q : r0 + (q - C)].size();
         return nnz;
       };
+      auto balanced = [&](int32_t lo, int32_t hi, int32_t wmax, std::vector<std::pair<int32_t, int32_t>>& out) {
+        const int32_t n = hi - lo;
+        if (n <= 0) return;
+        const int32_t nt = (n + wmax - 1) / wmax, w = (n + nt - 1) / nt;
+        for (int32_t r0 = lo; r0 < hi; r0 += w) out.emplace_back(r0, std::min(w, hi - r0));
+      };
+      const bool split_ok = (int64_t)factors.size() >= opt.split_min_factors;
+      const bool direct_rows =
+          (opt.blob_max - align16(4 * (int64_t)RW_WORDS)) / (8 * (int64_t)s) < opt.direct_min_rows;
       auto row_split = [&](bool inl, std::vector<std::pair<int32_t, int32_t>>& out) {
-        static const int32_t cand[] = {256, 192, 128, 96, 64, 32, 16, 8, 4, 2, 1};
         out.clear();
+        if (direct_rows) {
+          balanced(0, s, opt.row_max, out);
+          balanced(s, s + m, opt.row_max, out);
+          if (inl)  // the task's own assembly CSR must fit the blob, its front piece the scratch
+            for (const auto& rb : out) {
+              const int32_t r0 = rb.first, R = rb.second;
+              const int32_t C = r0 < s ? r0 + R : s, NB = r0 < s ? 0 : R;
+              if (blob_size(RW_WORDS + C + (C + NB + 1) + row_nnz(r0, C, NB), 0) > opt.blob_max ||
+                  C + NB + 2 > opt.big_scratch_max)
+                return false;
+            }
+          return true;
+        }
+        static const int32_t cand[] = {32, 16, 8, 4, 2, 1};
         for (int32_t r0 = 0; r0 < s + m;) {
           const int32_t lim = r0 < s ? s : s + m;
           int32_t R = 0;
@@ -456,7 +472,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
             const int32_t Re = std::min(cnd, lim - r0);
             const int32_t C = r0 < s ? r0 + Re : s, NB = r0 < s ? 0 : Re;
             const int64_t meta = inl ? RW_WORDS + C + (C + NB + 1) + row_nnz(r0, C, NB) : RW_WORDS;
-            if (blob_size(meta, (int64_t)Re * C) <= opt.blob_max && C + NB <= opt.big_scratch_max) {
+            if (blob_size(meta, (int64_t)Re * C) <= opt.blob_max && C + NB + 2 <= opt.big_scratch_max) {
               R = Re;
               break;
             }
@@ -468,32 +484,21 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         return true;
       };
       std::vector<std::pair<int32_t, int32_t>> split_a, split_i;
-      // streamed mode (many-factor plans): row blocks of stream_rows rows;
-      // blocks whose values exceed the blob stream them in chunks (plan.h)
-      const bool streaming = opt.stream_rows > 0 && (int64_t)factors.size() >= opt.split_min_factors;
-      const int32_t CB = ((opt.blob_max - STREAM_META) / 2) & ~15;  // bytes of one chunk buffer
-      if (streaming) {
-        for (int32_t r0 = 0; r0 < s + m;) {
-          const int32_t lim = r0 < s ? s : s + m;
-          const int32_t Re = std::min(opt.stream_rows, lim - r0);
-          split_a.emplace_back(r0, Re);
-          r0 += Re;
-        }
-      } else {
-        SFCDD_REQUIRE(row_split(false, split_a), SFCDD_EINTERNAL,
-                      "big supernode row does not fit a task blob (s = " + std::to_string(s) + ")");
-      }
+      SFCDD_REQUIRE(row_split(false, split_a), SFCDD_EINTERNAL,
+                    "big supernode row does not fit a task blob (s = " + std::to_string(s) + ")");
       double gathered = 0.0;
       for (const auto& rb : split_a) gathered += rb.first < s ? rb.first + rb.second : s + rb.second;
-      // three ways to assemble f_J for the ROW tasks: ASM tasks (once, one
-      // extra dependency hop), a global assembly record shared by the ROW
-      // tasks (huge s: the metadata would crowd the values out of the blobs),
-      // or inline metadata in every ROW blob
+      // three ways to assemble the front for the ROW tasks: ASM tasks (once per
+      // supernode, one extra dependency hop; the ROW tasks then read f through
+      // the vector ring), a global assembly record shared by the ROW tasks
+      // (the metadata would crowd the values out of the blobs, or not fit), or
+      // inline metadata in every ROW blob
       int64_t fj_nnz = 0;
       for (int32_t q = 0; q < s; ++q) fj_nnz += (int64_t)contrib[q].size();
-      const bool huge = 4 * (RW_WORDS + 2 * s + 1 + fj_nnz) > opt.blob_max / 2;
-      const bool split_ok = (int64_t)factors.size() >= opt.split_min_factors;
-      const bool use_asm = streaming || (split_ok && gathered >= opt.asm_redundancy * (s + m));
+      const bool huge = !direct_rows && 4 * (RW_WORDS + 2 * s + 1 + fj_nnz) > opt.blob_max / 2;
+      const bool scratch_ok = s + opt.row_max + 2 <= opt.big_scratch_max;  // inline / record modes hold f_J in the slot
+      const bool use_asm =
+          !scratch_ok || (split_ok && (direct_rows || gathered >= opt.asm_redundancy * (s + m)));
       const bool global_asm = !use_asm && (huge || !row_split(true, split_i));
       const auto& split = (use_asm || global_asm) ? split_a : split_i;
       int64_t asm16 = -1;
@@ -576,15 +581,12 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
             ints.insert(ints.end(), cl.begin(), cl.end());
           }
         }
-        ints[RW_SCRATCH] = C + NB;
-        // streamed when the block does not fit the blob: Kc columns per chunk
-        int32_t Kc = 0;
-        if (streaming && blob_size(RW_WORDS, (int64_t)R * C) > opt.blob_max) {
-          Kc = std::max(2, ((CB / 8) / R) & ~1);
-          ints[RW_STREAM] = Kc;
-          ints[RW_SCRATCH] = 2 * Kc + NB + 4;
-        }
-        // values: R x C column-major, (i, k) = M[r0 + i, k] for k <= r0 + i
+        // scratch: the vector ring (ASM mode) or the task's own front piece
+        const int32_t scr = direct_rows && use_asm ? 2 * RING_STRIDE : C + NB + 6;  // (+ padding of bulk-copied pieces)
+        ints[RW_SCRATCH] = scr;
+        ints[RW_INBLOB] = direct_rows ? 0 : 1;
+        // values: R x C column-major, (i, k) = M[r0 + i, k] for k <= r0 + i;
+        // DIRECT blocks leave them in HBM (the task copies its metadata only)
         ValDesc vd{};
         vd.src = S.val_off;
         vd.kind = VD_ROW;
@@ -595,25 +597,49 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         vd.len = C;
         const int32_t asm_word = asm16 >= 0 ? RW_ASM16 : -1;
         int32_t bytes = 0;
-        const int64_t off = E.emit(ints, RW_VAL_OFF, (int64_t)R * C, &vd, bytes, F, asm_word, Kc > 0);
-        E.max_scratch = std::max<int32_t>(E.max_scratch, Kc > 0 ? 2 * Kc + NB + 4 : C + NB + 6);  // + padding
+        const int64_t off = E.emit(ints, RW_VAL_OFF, (int64_t)R * C, &vd, bytes, F, asm_word, direct_rows);
+        SFCDD_REQUIRE(bytes <= opt.blob_max, SFCDD_EINTERNAL, "ROW blob exceeds the slot");
+        E.has_direct = E.has_direct || direct_rows;
+        E.max_scratch = std::max<int32_t>(E.max_scratch, scr);
         add_task(g, TK_ROW_FWD, off, bytes, (int64_t)R * C, (use_asm ? 1.8 : 2.36) + 0.0013 * R * C);
       }
-      // backward column blocks, dense row-major L x c (L = s+m-k0); -x_B is
-      // gathered once by XB tasks when J has many column blocks
+      // backward column blocks, dense row-major L x c (L = s+m-k0): BLOB blocks
+      // (as many columns as fit the blob) or, when fewer than direct_min_cols
+      // columns of the full height would fit, DIRECT blocks of <= col_max
+      // columns streamed from HBM.  -x_B is gathered once per supernode by XB
+      // tasks where many COL tasks would repeat the gather (the COL tasks then
+      // read v = [y_J[k0:s) ; -x_B] through the vector ring) or where the
+      // inline row list / gathered v would not fit the slot
+      const bool direct_cols =
+          (opt.blob_max - align16(4 * (int64_t)(CL_WORDS + opt.col_max))) / (8 * (int64_t)(s + m)) < opt.direct_min_cols;
       auto col_width = [&](int32_t k0, bool inl) {
         const int32_t L = s + m - k0;
-        if (streaming) return std::min<int32_t>(opt.stream_cols, s - k0);  // even, oversized blocks stream
         int32_t c = std::min<int32_t>(opt.col_max, s - k0);
         while (c > 1 && blob_size(CL_WORDS + c + (inl ? m : 0), (int64_t)L * c) > opt.blob_max) --c;
-        if (c > 1 && (c & 1) && k0 + c < s) --c;  // even widths keep k0 even (aligned bulk copies of v)
         return c;
       };
-      int32_t ncol_tasks = 0;
-      for (int32_t k0 = 0; k0 < s; k0 += col_width(k0, false)) ++ncol_tasks;
-      // XB also when a column block with its inline row list cannot fit a blob
-      const bool inline_fits = blob_size(CL_WORDS + 1 + m, (int64_t)(s + m)) <= opt.blob_max;
-      const bool use_xb = m > 0 && (streaming || (split_ok && ncol_tasks >= opt.xb_min_tasks) || !inline_fits);
+      std::vector<std::pair<int32_t, int32_t>> csplit;
+      bool ring_col, use_xb;
+      if (direct_cols) {
+        balanced(0, s, opt.col_max, csplit);
+        const bool inline_fits =
+            blob_size(CL_WORDS + opt.col_max + m, 0) <= opt.blob_max && s + m + 2 <= opt.big_scratch_max;
+        ring_col = split_ok || !inline_fits;  // v is contiguous in upd: y_J then -x_B
+        use_xb = m > 0 && ring_col;
+      } else {
+        int32_t ncol_tasks = 0;
+        for (int32_t k0 = 0; k0 < s; k0 += col_width(k0, false)) ++ncol_tasks;
+        // XB also when a column block with its inline row list cannot fit a blob
+        const bool inline_fits =
+            blob_size(CL_WORDS + 1 + m, (int64_t)(s + m)) <= opt.blob_max && s + m + 2 <= opt.big_scratch_max;
+        use_xb = m > 0 && ((split_ok && ncol_tasks >= opt.xb_min_tasks) || !inline_fits);
+        ring_col = use_xb || (m == 0 && !inline_fits);
+        for (int32_t k0 = 0; k0 < s;) {
+          const int32_t c = col_width(k0, !ring_col);
+          csplit.emplace_back(k0, c);
+          k0 += c;
+        }
+      }
       if (use_xb) {  // -x_B at gr.xb_off
         for (int32_t a0 = 0; a0 < m;) {
           int32_t na = std::min<int32_t>(m - a0, opt.asm_max);
@@ -632,32 +658,26 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
           a0 += na;
         }
       }
-      for (int32_t k0 = 0; k0 < s;) {
+      for (const auto& cb : csplit) {
+        const int32_t k0 = cb.first, c = cb.second;
         const int32_t L = s + m - k0;
-        const int32_t c = col_width(k0, !use_xb);
-        int32_t Lq = 0;
-        if (streaming && (blob_size(CL_WORDS + c, (int64_t)L * c) > opt.blob_max || L + 2 > opt.big_scratch_max))
-          Lq = std::max(2, ((CB / 8) / c) & ~1);
-        SFCDD_REQUIRE(Lq > 0 || (blob_size(CL_WORDS + c + (use_xb ? 0 : m), (int64_t)L * c) <= opt.blob_max &&
-                                 L <= opt.big_scratch_max),
-                      SFCDD_EINTERNAL,
-                      "big supernode column does not fit a task blob (s+m = " + std::to_string(s + m) + ")");
         ints.assign(CL_WORDS, 0);
         ints[CL_S] = s;
         ints[CL_M] = m;
         ints[CL_K0] = k0;
         ints[CL_C] = c;
         ints[CL_YOFF] = (int32_t)gr.y_off;
-        ints[CL_XOFF] = use_xb ? (int32_t)gr.xb_off : -1;
+        ints[CL_XOFF] = ring_col ? (int32_t)gr.xb_off : -1;
         ints[CL_COLS] = (int32_t)ints.size();
         for (int32_t j = 0; j < c; ++j) ints.push_back(F.perm[S.col0 + k0 + j]);
-        if (!use_xb) {
+        if (!ring_col) {
           ints[CL_ROWS] = (int32_t)ints.size();
           for (int32_t a = 0; a < m; ++a) ints.push_back(F.perm[F.rows[S.rows_off + a]]);
         }
-        ints[CL_SCRATCH] = Lq > 0 ? 2 * (Lq + 2) : L;
-        ints[CL_STREAM] = Lq;
-        // values: L x c row-major, (r, j) = M[k0 + r, k0 + j] for j <= r
+        const int32_t scr = direct_cols && ring_col ? 2 * RING_STRIDE : L + 2;
+        ints[CL_SCRATCH] = scr;
+        ints[CL_INBLOB] = direct_cols ? 0 : 1;
+        // values: L x c row-major, (r, j) = M[k0 + r, k0 + j] for j <= r (DIRECT: left in HBM)
         const int64_t nv = (int64_t)L * c - (int64_t)c * (c - 1) / 2;
         ValDesc vd{};
         vd.src = S.val_off;
@@ -668,10 +688,12 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         vd.w = c;
         vd.len = L;
         int32_t bytes = 0;
-        const int64_t off = E.emit(ints, CL_VAL_OFF, (int64_t)L * c, &vd, bytes, F, -1, Lq > 0);
-        E.max_scratch = std::max<int32_t>(E.max_scratch, Lq > 0 ? 2 * (Lq + 2) : L + 2);  // + padding
+        const int64_t off = E.emit(ints, CL_VAL_OFF, (int64_t)L * c, &vd, bytes, F, -1, direct_cols);
+        SFCDD_REQUIRE(bytes <= opt.blob_max, SFCDD_EINTERNAL,
+                      "big supernode column does not fit a task blob (s+m = " + std::to_string(s + m) + ")");
+        E.has_direct = E.has_direct || direct_cols;
+        E.max_scratch = std::max<int32_t>(E.max_scratch, scr);
         add_task(g, TK_COL_BWD, off, bytes, nv, (use_xb ? 1.8 : 2.24) + 0.0013 * nv);
-        k0 += c;
       }
       continue;
     }
@@ -1012,6 +1034,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
     cursor += E.size;
     P.max_scratch = std::max(P.max_scratch, E.max_scratch);
     P.max_copy = std::max(P.max_copy, E.max_copy);
+    P.has_direct = P.has_direct || E.has_direct;
   }
   SFCDD_REQUIRE(P.upd_doubles < (int64_t(1) << 31), SFCDD_EINTERNAL, "update buffer too large");
 
@@ -1313,6 +1336,30 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
       for (int k = 0; k < TK_KINDS; ++k)
         std::fprintf(stderr, "[plan] %s: %.0f tasks, copied %.1f MB, values %.1f MB (%.2fx), %.0f B/task\n", nm[k],
                      nt[k], cb[k] / 1e6, vb[k] / 1e6, cb[k] / std::max(1.0, vb[k]), cb[k] / std::max(1.0, nt[k]));
+    }
+    {  // FRAG blob-size histogram, and the fragments hanging off BIG parents (sibling packing potential)
+      double hb[6] = {0, 0, 0, 0, 0, 0}, nbp = 0, bbp = 0, nroot = 0;
+      std::map<int32_t, std::pair<double, double>> per_parent;  // BIG parent group -> (fragments, bytes)
+      for (const TaskDev& T : P.tasks) {
+        if (T.kind != TK_FRAG_FWD) continue;
+        const int b = T.copy_bytes < 512 ? 0 : T.copy_bytes < 1024 ? 1 : T.copy_bytes < 2048 ? 2 : T.copy_bytes < 4096 ? 3
+                      : T.copy_bytes < 8192 ? 4 : 5;
+        hb[b] += 1;
+        const int32_t pg = groups[T.group].parent;
+        if (pg < 0) nroot += 1;
+        else if (groups[pg].big) {
+          nbp += 1;
+          bbp += T.copy_bytes;
+          per_parent[pg].first += 1;
+          per_parent[pg].second += T.copy_bytes;
+        }
+      }
+      double bins = 0;
+      for (const auto& kv : per_parent) bins += std::ceil(kv.second.second / (0.85 * opt.blob_max));
+      std::fprintf(stderr,
+                   "[plan] FRAG blob bytes: <512 %.0f <1K %.0f <2K %.0f <4K %.0f <8K %.0f >=8K %.0f; children of BIG "
+                   "parents %.0f (%.0f B avg, %zu parents -> ~%.0f packed bins), roots %.0f\n",
+                   hb[0], hb[1], hb[2], hb[3], hb[4], hb[5], nbp, bbp / std::max(1.0, nbp), per_parent.size(), bins, nroot);
     }
     {  // per-level FRAG work profile
       double nl = 0, runs = 0, pairs = 0, fi = 0, bi = 0, bpr = 0, ncol = 0, nxu = 0, nxx = 0, nf = 0, maxr = 0;

@@ -122,9 +122,9 @@ enum SnRecField { R_SM = 0, R_SCR, R_VAL, R_CPOS, R_WORDS };
 //   f  [s+m] at AS_FOFF: f_J = rhs + child updates, f_B = child updates
 //   vb [m]   at XB_XOFF: -x_B
 // so ROW / COL blobs carry values only (plus the column ids COL stores to).
-// The split costs one dependency hop, so it is used only where the inline
-// gathers would be repeated by many tasks (PlanOptions::asm_redundancy,
-// xb_min_tasks); otherwise ROW / COL tasks gather for themselves.
+// The split costs one dependency hop, so it is used in many-factor plans
+// (PlanOptions::split_min_factors) and wherever a task could not hold its
+// input vector in the slot; otherwise ROW / COL tasks gather for themselves.
 //
 // ASM blob: front positions [q0, q0+nq) of J: cols (ro of the positions < s),
 // ptr[nq+1] / src[nnz] = CSR of the child update indices summed into each
@@ -134,8 +134,10 @@ enum AsmHdr { AS_S = 0, AS_Q0, AS_NQ, AS_FOFF, AS_COLS, AS_PTR, AS_SRC, AS_WORDS
 enum XbHdr { XB_A0 = 0, XB_NA, XB_XOFF, XB_ROWS, XB_WORDS };
 // ROW blob: forward rows [r0, r0+R) of J (all < s: y rows, or all >= s:
 // update rows).  Values: R x C dense column-major (leading dim R), entry
-// (i, k) = M[r0+i, k] (zero where k > r0+i), C = min(r0+R, s).  Scratch:
-// [f_J[0:C) ; f_B[r0 : r0+NB)] loaded from f.
+// (i, k) = M[r0+i, k] (zero where k > r0+i), C = min(r0+R, s); they follow
+// the metadata in the blob buffer (copied with it: BLOB, or not: DIRECT).  Scratch:
+// ASM mode: a two-chunk ring of f_J pieces; inline mode: [f_J[0:C) ;
+// f_B[r0 : r0+NB)] assembled by the task.
 enum RowHdr {
   RW_S = 0,
   RW_R,        // rows in the block
@@ -153,12 +155,14 @@ enum RowHdr {
                //   over FRONT positions
   RW_VAL_OFF,  // byte offset of the values
   RW_SCRATCH,  // doubles of scratch used
-  RW_STREAM,   // streamed task (> 0): columns per chunk (values stay in HBM, see below)
+  RW_INBLOB,   // 1: the values follow the metadata in the slot (BLOB block); 0: they stay in HBM (DIRECT)
   RW_WORDS
 };
 // COL blob: backward columns [k0, k0+c) of J.  Values: L x c dense row-major
 // block of M (L = s+m-k0 rows starting at row k0), entry (r, j) =
-// M[k0+r, k0+j] (zero where r < j).  Scratch: v = [y_J[k0:s) ; -x_B] (L).
+// M[k0+r, k0+j] (zero where r < j), streamed from HBM like the ROW values.
+// Scratch: XB mode: a two-chunk ring of v pieces; inline mode:
+// v = [y_J[k0:s) ; -x_B] (L) gathered by the task.
 enum ColHdr {
   CL_S = 0,
   CL_M,
@@ -170,19 +174,17 @@ enum ColHdr {
   CL_ROWS,     // (CL_XOFF < 0) int offset: ro of the m below rows
   CL_VAL_OFF,  // byte offset of the values
   CL_SCRATCH,
-  CL_STREAM,   // streamed task (> 0): rows per chunk
+  CL_INBLOB,   // 1: values in the slot (BLOB block); 0: in HBM (DIRECT)
   CL_WORDS
 };
 
-// Streamed BIG tasks (many-factor plans, ASM / XB mode): a ROW / COL block
-// whose values exceed the blob is not copied whole; the task copies only its
-// metadata, then streams the values in chunks (ROW: Kc columns of the R x C
-// column-major block; COL: Lq rows of the L x c row-major block) together
-// with the matching front / v pieces, double-buffered through the slot:
-// [meta (<= STREAM_META bytes) | value buffer 0 | value buffer 1] in the blob
-// area, [piece 0 | piece 1 | f_B rows] in the scratch area.  No blob growth,
-// whatever the separator size (BASELINE C5: s ~ 2300).
-constexpr int STREAM_META = 256;
+// Vector ring of the ROW / COL tasks whose input vector is contiguous in the
+// update buffer (ASM / XB mode): chunks of RING_CHUNK doubles are bulk-copied
+// into two alternating scratch slots of RING_STRIDE doubles (one leading
+// double for a misaligned start + padding to 16 bytes), so the scratch need
+// does not grow with the separator size (BASELINE C5: s ~ 2300).
+constexpr int RING_CHUNK = 256;
+constexpr int RING_STRIDE = RING_CHUNK + 2;
 
 constexpr int SMALL_MAX_S = 64;  // wider supernodes are always BIG
 
@@ -221,16 +223,20 @@ struct MetaSeg {
 void place_values(const ValDesc& d, const double* M /* J's packed block */, uint8_t* blob_buffer);
 
 struct PlanOptions {
-  int32_t blob_max = 8 * 1024;   // bytes of a task blob (slot blob area)
+  int32_t blob_max = 8 * 1024;   // bytes of a task blob (slot blob area): FRAG blobs, BIG metadata
   int32_t scratch_max = 512;     // doubles of FRAG scratch (< 65536)
   int32_t big_scratch_max = 8192;  // doubles of scratch a BIG task may use
   int32_t workers = 0;             // warps assumed by the queue-order simulation (0: from the slot size; SFCDD_WORKERS)
   int32_t sms = 148;               // SMs of the target device (set by the caller)
-  int32_t row_max = 32;            // rows per ROW task (SFCDD_ROW_MAX; latency vs task count)
-  int32_t col_max = 16;            // columns per COL task (SFCDD_COL_MAX)
+  int32_t row_max = 32;            // rows per ROW task (SFCDD_ROW_MAX; latency vs task count), <= 32
+  int32_t col_max = 16;            // columns per COL task (SFCDD_COL_MAX), <= 32
   int32_t asm_max = 256;           // front positions per ASM task (SFCDD_ASM_MAX)
-  double asm_redundancy = 4.0;     // ASM when ROW tasks would gather the front >= this often (SFCDD_ASM_RED)
-  int32_t xb_min_tasks = 4;        // XB when J has >= this many COL tasks (SFCDD_XB_MIN)
+  double asm_redundancy = 4.0;     // BLOB supernodes: ASM when the ROW tasks would gather the front >= this often (SFCDD_ASM_RED)
+  int32_t xb_min_tasks = 4;        // BLOB supernodes: XB when J has >= this many COL tasks (SFCDD_XB_MIN)
+  int32_t direct_min_rows = -1;    // a supernode whose blob would hold fewer full-width rows streams DIRECT ROW blocks
+                                   // (SFCDD_DIRECT_ROWS; 0: never, 1 << 20: always; -1: 8 in plans that hold a
+                                   // supernode too wide for any BLOB block, else 0 -- measured)
+  int32_t direct_min_cols = -1;    // ... fewer full-height columns: DIRECT COL blocks (SFCDD_DIRECT_COLS; -1: 4 / 0)
   int32_t split_min_factors = 256; // ASM / XB only in plans of >= this many factors: with few
                                    // subdomains the top of the trees is latency bound and the
                                    // extra dependency hop costs more than it saves (SFCDD_SPLIT_MIN)
@@ -240,16 +246,13 @@ struct PlanOptions {
   bool defer_values = false;       // build the plan from symbolic factors: blobs hold metadata only
                                    // (DevicePlan::segs), values are placed later by the descriptors
   int32_t threads = 0;             // host threads for the per-factor blob emission (0: hardware)
-  int32_t stream_rows = 16;        // streamed ROW tasks: rows per task (SFCDD_STREAM_ROWS; 0 disables streaming)
-  int32_t stream_cols = 16;        // streamed COL tasks: columns per task (SFCDD_STREAM_COLS)
   PlanOptions();                 // environment overrides SFCDD_BLOB_MAX, SFCDD_SCRATCH_MAX, ...
 };
 
 // Blob size and CTA shape for a set of factors (unless set by the
 // environment): plans whose values sit mostly in big supernodes (3-D
-// subdomains: dense separator fronts) stream 16 KB blobs with 2-worker CTAs,
-// which halves the per-column re-gathers of their COL / ROW tasks; FRAG-heavy
-// plans (2-D) keep 8 KB blobs and 4-worker CTAs (measured).
+// subdomains) use 16 KB blobs with 2-worker CTAs, FRAG-heavy plans (2-D) keep
+// 8 KB blobs and 4-worker CTAs (measured).
 void choose_blob_shape(const std::vector<const HostFactor*>& factors, PlanOptions& opt);
 
 struct DevicePlan {
@@ -269,6 +272,7 @@ struct DevicePlan {
   int64_t xy_doubles = 0;
   int64_t num_supernodes = 0;
   int64_t stored = 0, nnz_l = 0;
+  bool has_direct = false;  // some ROW / COL task streams its values from HBM (selects the kernel variant)
   int32_t wpb = 4;          // worker warps per DAG CTA the plan was simulated for
   int32_t max_scratch = 0;  // doubles, over all tasks
   int32_t max_copy = 0;     // bytes

@@ -236,16 +236,26 @@ def test_pcg_c3_matches_reference(sfcdd, golden):
     assert np.linalg.norm(rep.solution[idx] - ref) <= 1e-10 * np.linalg.norm(ref)
 
 
-@pytest.mark.parametrize("mode", ["grown", "streamed"])
-def test_pcg_c3_grown_blob_matches_reference(sfcdd, golden, mode, monkeypatch):
-    """Separators wider than the requested blob.  ``grown``: the plan grows
-    the blob to the next power of two that holds one ROW row / COL column
-    (C3 with a 2 KB request -> 8 KB, 2-worker CTAs).  ``streamed``: the
-    default of many-subdomain plans -- the oversized ROW / COL blocks stream
-    their values in double-buffered chunks through the 2 KB slot (the path
-    of BASELINE C5's s ~ 2300 separators)."""
-    monkeypatch.setenv("SFCDD_BLOB_MAX", "2048")
-    monkeypatch.setenv("SFCDD_STREAM_ROWS", "0" if mode == "grown" else "16")
+@pytest.mark.parametrize("mode", ["blob2k", "direct", "narrow", "inline", "direct-inline"])
+def test_pcg_c3_dense_block_shapes_match_reference(sfcdd, golden, mode, monkeypatch):
+    """Dense ROW / COL blocks of big supernodes: BLOB blocks travel with
+    their metadata, DIRECT blocks (wide separators: the path of BASELINE
+    C5's s ~ 2300) stream their values from HBM.  ``blob2k``: separators far
+    wider than a 2 KB blob (mostly DIRECT); ``direct``: every block DIRECT;
+    ``narrow``: DIRECT 6-row / 3-column blocks (several vector phases per
+    warp, non power of two widths); ``inline`` / ``direct-inline``: the
+    few-factor path (ROW / COL tasks gather their own vectors into the slot)
+    forced on a 512-factor plan."""
+    if mode == "blob2k":
+        monkeypatch.setenv("SFCDD_BLOB_MAX", "2048")
+    if mode in ("direct", "narrow", "direct-inline"):
+        monkeypatch.setenv("SFCDD_DIRECT_ROWS", str(1 << 20))
+        monkeypatch.setenv("SFCDD_DIRECT_COLS", str(1 << 20))
+    if mode == "narrow":
+        monkeypatch.setenv("SFCDD_ROW_MAX", "6")
+        monkeypatch.setenv("SFCDD_COL_MAX", "3")
+    if mode in ("inline", "direct-inline"):
+        monkeypatch.setenv("SFCDD_SPLIT_MIN", "100000")
     g = golden.npz("solve_c3.npz")
     rep, _ = _pcg(sfcdd, (7, 7, 7), 512, 0.5, 8)
     assert abs(rep.iterations - int(g["iterations"])) <= 1

@@ -123,19 +123,28 @@ def test_host_factor_rejects_non_spd():
 @pytest.mark.parametrize("levels,p,gamma,blob", [((7, 7), 16, 0.5, 0), ((7, 7), 16, 0.25, 4096),
                                                   ((4, 4, 4), 8, 0.5, 0), ((4, 4, 4), 8, 1.0, 2048),
                                                   ((6, 5), 6, 0.75, 0),
-                                                  # separators wider than a 2 KB blob row: the blob grows
+                                                  # separators far wider than a 2 KB blob: ROW / COL values
+                                                  # never pass through the blob
                                                   ((5, 5, 5), 4, 0.5, 2048)])
-@pytest.mark.parametrize("split", [False, "stream", "nostream"])
+@pytest.mark.parametrize("split", [False, "wide", "narrow", "direct", "direct-inline"])
 def test_device_plan_host_interpreter(oracle, levels, p, gamma, blob, split, monkeypatch):
     """The fragment/blob layout the DAG kernel executes, run on the host;
     ``split`` forces the ASM / XB task path of big supernodes (plan.h), with
-    the streamed ROW / COL blocks (``stream``: values beyond the blob stay in
-    HBM and are consumed in chunks) or without (blob growth)."""
+    the default 32-row / 16-column blocks (``wide``) or narrow, non power of
+    two blocks (``narrow``: several vector phases per lane group);
+    ``direct``: every dense block streams its values from HBM (the form of
+    the wide separators), with ASM / XB tasks or with inline gathers."""
     if split:
-        monkeypatch.setenv("SFCDD_SPLIT_MIN", "1")
-        monkeypatch.setenv("SFCDD_ASM_RED", "1")
-        monkeypatch.setenv("SFCDD_XB_MIN", "1")
-        monkeypatch.setenv("SFCDD_STREAM_ROWS", "0" if split == "nostream" else "8")
+        if split != "direct-inline":
+            monkeypatch.setenv("SFCDD_SPLIT_MIN", "1")
+            monkeypatch.setenv("SFCDD_ASM_RED", "1")
+            monkeypatch.setenv("SFCDD_XB_MIN", "1")
+        if split == "narrow":
+            monkeypatch.setenv("SFCDD_ROW_MAX", "6")
+            monkeypatch.setenv("SFCDD_COL_MAX", "3")
+        if split.startswith("direct"):
+            monkeypatch.setenv("SFCDD_DIRECT_ROWS", str(1 << 20))
+            monkeypatch.setenv("SFCDD_DIRECT_COLS", str(1 << 20))
     A = oracle.assemble_scaled_laplacian(levels)
     n = A.shape[0]
     ov = oracle.enlarge(oracle.disjoint_partition(n, p), gamma)

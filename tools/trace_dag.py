@@ -11,7 +11,8 @@ sys.path.insert(0, str(ROOT))
 import paper_2110_11211_b200 as sf  # noqa: E402
 from paper_2110_11211_b200 import _lib  # noqa: E402
 
-CFG = {"c1": ((7, 7), 16, 0.5, 4), "c2": ((10, 10), 64, 0.5, 16), "c3": ((7, 7, 7), 512, 0.5, 8)}
+CFG = {"c1": ((7, 7), 16, 0.5, 4), "c2": ((10, 10), 64, 0.5, 16), "c3": ((7, 7, 7), 512, 0.5, 8),
+       "c4": ((12, 12), 256, 0.5, 16), "c5": ((8, 8, 8), 512, 0.5, 64)}
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
 levels, p, gamma, q = CFG[name]
 A = sf.assemble_laplacian(levels)
