@@ -31,6 +31,10 @@
 #include "common.h"
 #include "dag_solve.h"
 
+#ifndef SFCDD_LEAN
+#define SFCDD_LEAN 0  // experiment switches (tools/build_variants.sh): 1 no watchdog / diagnostics, 2 launch-bounds
+#endif                // register cap, 4 specialised FRAG calls, 8 no syncwarp before the ROW front copy
+
 namespace sfcdd {
 
 namespace {
@@ -563,7 +567,7 @@ __device__ __forceinline__ void run_row_blob(const int32_t* h, double* S, const 
     const double* f = A.upd + h[RW_FOFF];
     const int c2 = (C + 1) & ~1;
     boff = c2 + (r0 & 1);
-    __syncwarp();  // every lane has observed the blob copy's phase before the barrier is armed again
+    if (!(SFCDD_LEAN & 8)) __syncwarp();  // every lane has observed the blob copy's phase before the barrier is armed again
     if (lane == 0) {
       fence_proxy_async_global();
       const uint32_t ba = bytes16(C), bb = NB > 0 ? bytes16(NB + (r0 & 1)) : 0u;
@@ -913,7 +917,11 @@ __device__ __forceinline__ void signaller(const DagArgs& A, int32_t* mbox, int32
 // kernel without them keeps the smaller code of the common case
 // DIRECT: the plan has ROW / COL blocks streamed from HBM (wide separators)
 template <int WPB, bool SPLIT, bool DIRECT>
+#if SFCDD_LEAN & 2
+__global__ void __launch_bounds__((WPB + 1) * 32, 20 / WPB) k_dag(DagArgs A) {
+#else
 __global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? 72 : 96) k_dag(DagArgs A) {
+#endif
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bars[WPB];
   __shared__ int32_t mbox[WPB];
@@ -1018,6 +1026,7 @@ __global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? 72 : 96
         unsigned polls = 0;
         unsigned long long t0 = 0;
         auto watchdog = [&]() {  // a dependency that never completes traps instead of hanging the GPU
+          if (SFCDD_LEAN & 1) return;
           if ((++polls & 4095u) == 0) {
             if (t0 == 0) t0 = gtimer();
             if (A.mode & 32) {  // diagnostic mode: record the stuck wait, let every warp leave
@@ -1037,13 +1046,13 @@ __global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? 72 : 96
           }
         };
         if (A.mode & 1) {
-          while (!dead && ld_acquire(A.ctr + T.wait_idx) < T.wait_target) {
+          while (!((SFCDD_LEAN & 16) ? 0 : dead) && ld_acquire(A.ctr + T.wait_idx) < T.wait_target) {
             __nanosleep(ns);
             ns = ns < 256 ? 2 * ns : 256;
             watchdog();
           }
         } else {
-          while (!dead && ld_relaxed(A.ctr + T.wait_idx) < T.wait_target) {
+          while (!((SFCDD_LEAN & 16) ? 0 : dead) && ld_relaxed(A.ctr + T.wait_idx) < T.wait_target) {
             __nanosleep(ns);
             ns = ns < 256 ? 2 * ns : 256;
             watchdog();
@@ -1054,9 +1063,12 @@ __global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? 72 : 96
       if (tr) tr[2] = gtimer();
     }
     __syncwarp();
-    mbar_wait_guard(bar, phase);
+    if (SFCDD_LEAN & 1)
+      mbar_wait(bar, phase);
+    else
+      mbar_wait_guard(bar, phase);
     phase ^= 1u;
-    if (A.mode & 32) {  // diagnostic mode: leave once a stuck wait was recorded
+    if (!(SFCDD_LEAN & 1) && (A.mode & 32)) {  // diagnostic mode: leave once a stuck wait was recorded
       dead = __shfl_sync(FULL, dead, 0);
       if (dead) {
         if (lane == 0) {
@@ -1067,21 +1079,60 @@ __global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? 72 : 96
       }
     }
     if (tr && lane == 0) tr[3] = gtimer();
-    if (T.kind == TK_FRAG_FWD || T.kind == TK_FRAG_BWD) {
+#if !(SFCDD_LEAN & 32)  // (the if-chain measured 3 % faster than the switch below on C2: code layout)
+    if ((SFCDD_LEAN & 4) && T.kind == TK_FRAG_FWD) {
+      run_frag(h, true, S, A, F, lane, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);
+    } else if ((SFCDD_LEAN & 4) && T.kind == TK_FRAG_BWD) {
+      run_frag(h, false, S, A, F, lane, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);
+    } else if (T.kind == TK_FRAG_FWD || T.kind == TK_FRAG_BWD) {
       run_frag(h, T.kind == TK_FRAG_FWD, S, A, F, lane, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);
     } else if (SPLIT && T.kind == TK_ASM_FWD) {
       run_asm(h, A, F, lane);
     } else if (SPLIT && T.kind == TK_XB_BWD) {
       run_xb(h, A, F, lane);
-    } else if (T.kind == TK_ROW_FWD && h[RW_INBLOB]) {
+    } else if (T.kind == TK_ROW_FWD && (!DIRECT || h[RW_INBLOB])) {
       run_row_blob<SPLIT>(h, S, A, F, lane, bar, phase);
-    } else if (T.kind == TK_COL_BWD && h[CL_INBLOB]) {
+    } else if (T.kind == TK_COL_BWD && (!DIRECT || h[CL_INBLOB])) {
       run_col_blob<SPLIT>(h, S, A, F, lane, bar, phase);
     } else if constexpr (DIRECT) {
       phase = run_dense<SPLIT>(T.kind == TK_ROW_FWD, h, S, A, F, A.blobs + T.blob_off, lane, bar, phase);
     } else {
       __trap();  // a DIRECT block in a plan built without them
     }
+#else
+    switch (T.kind) {
+      case TK_FRAG_FWD:
+        run_frag(h, true, S, A, F, lane, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);
+        break;
+      case TK_FRAG_BWD:
+        run_frag(h, false, S, A, F, lane, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);
+        break;
+      case TK_ROW_FWD:
+        if (!DIRECT || h[RW_INBLOB]) {
+          run_row_blob<SPLIT>(h, S, A, F, lane, bar, phase);
+          break;
+        }
+        [[fallthrough]];
+      default:
+        if constexpr (SPLIT) {
+          if (T.kind == TK_ASM_FWD) {
+            run_asm(h, A, F, lane);
+            break;
+          }
+          if (T.kind == TK_XB_BWD) {
+            run_xb(h, A, F, lane);
+            break;
+          }
+        }
+        if (T.kind == TK_COL_BWD && (!DIRECT || h[CL_INBLOB])) {
+          run_col_blob<SPLIT>(h, S, A, F, lane, bar, phase);
+          break;
+        }
+        if constexpr (DIRECT)  // ROW or COL block streamed from HBM
+          phase = run_dense<SPLIT>(T.kind == TK_ROW_FWD, h, S, A, F, A.blobs + T.blob_off, lane, bar, phase);
+        break;
+    }
+#endif
     __syncwarp();
     if (lane == 0) {
       // release: cumulative over the warp's writes (ordered before it by __syncwarp)

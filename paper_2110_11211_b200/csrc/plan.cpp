@@ -616,6 +616,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         const int32_t L = s + m - k0;
         int32_t c = std::min<int32_t>(opt.col_max, s - k0);
         while (c > 1 && blob_size(CL_WORDS + c + (inl ? m : 0), (int64_t)L * c) > opt.blob_max) --c;
+        if (std::getenv("SFCDD_EVEN_COLS") && c > 1 && (c & 1) && k0 + c < s) --c;
         return c;
       };
       std::vector<std::pair<int32_t, int32_t>> csplit;
