@@ -456,10 +456,15 @@ __device__ __forceinline__ void run_frag(const int32_t* h, bool fwd, double* S, 
       if (lv < 6) stamp(3 + 2 * lv);
     }
     for (int c = lane; c < ncol; c += 32) __stcg(xy + cols[c], S[hi16(colpos[c])]);
-    if (h[H_TOP_UPD] >= 0) {
-      const int4 R = recs[h[H_TOP]];
-      const double* u = S + R.y + rec_s(R);
-      for (int a = lane; a < rec_m(R); a += 32) __stcg(A.upd + h[H_TOP_UPD] + a, u[a]);
+    {  // update vectors of the tops (one per packed sibling subtree)
+      const int32_t* tops = h + h[H_TOPS];
+      for (int tp = 0; tp < h[H_NTOP]; ++tp) {
+        const int slot = tops[2 * tp + 1];
+        if (slot < 0) continue;
+        const int4 R = recs[tops[2 * tp]];
+        const double* u = S + R.y + rec_s(R);
+        for (int a = lane; a < rec_m(R); a += 32) __stcg(A.upd + slot + a, u[a]);
+      }
     }
     stamp(14);
     if (pt && lane == 0) pt[15] = nlev;

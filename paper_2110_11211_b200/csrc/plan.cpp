@@ -25,7 +25,8 @@ struct Group {
   int32_t factor = 0;
   bool big = false;
   std::vector<int32_t> sns;  // supernode ids, ascending (= postorder)
-  int32_t top = -1;
+  int32_t top = -1;           // BIG: the supernode; FRAG: the first top
+  std::vector<int32_t> tops;  // FRAG: the roots of the group's subtrees (siblings: one parent supernode)
   int32_t parent = -1;  // parent group
   std::vector<int32_t> kids;
   std::vector<int32_t> ftask, btask;  // indices into the unordered task list
@@ -171,6 +172,8 @@ PlanOptions::PlanOptions() {
   if (const char* e = std::getenv("SFCDD_DIRECT_ROWS")) direct_min_rows = std::atoi(e);
   if (const char* e = std::getenv("SFCDD_DIRECT_COLS")) direct_min_cols = std::atoi(e);
   if (const char* e = std::getenv("SFCDD_SPLIT_MIN")) split_min_factors = std::atoi(e);
+  if (const char* e = std::getenv("SFCDD_PACK")) pack_siblings = std::atoi(e) != 0;
+  if (const char* e = std::getenv("SFCDD_PACK_MAX")) pack_max = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("SFCDD_WPB")) wpb = std::atoi(e);
   tuned = std::getenv("SFCDD_BLOB_MAX") || std::getenv("SFCDD_WPB");
 }
@@ -268,16 +271,63 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
       return blob_size(H_WORDS + 2 + c.meta_ints + m_top + c.ext_u, c.vals);
     };
     auto frag_scratch = [&](const Cluster& c, int64_t m_top) { return c.frontal + m_top + c.ext_u; };
-    auto close = [&](int32_t root, bool big) {
+    auto close_roots = [&](const std::vector<int32_t>& roots, bool big) {
       Group g;
       g.factor = (int32_t)fi;
-      g.sns = std::move(members[root]);
+      for (int32_t r : roots) {
+        g.sns.insert(g.sns.end(), members[r].begin(), members[r].end());
+        members[r].clear();
+        open[r] = 0;
+      }
       std::sort(g.sns.begin(), g.sns.end());
-      g.top = root;
+      g.tops = roots;
+      std::sort(g.tops.begin(), g.tops.end());
+      g.top = g.tops[0];
       g.big = big;
       for (int32_t k : g.sns) group_of[fi][k] = (int32_t)groups.size();
       groups.push_back(std::move(g));
-      open[root] = 0;
+    };
+    auto close = [&](int32_t root, bool big) { close_roots({root}, big); };
+    // Sibling packing: the closed subtrees below one parent supernode (3-D
+    // subdomains: dozens of tiny leaf subtrees hang off every wide front) share
+    // fragments -- first-fit decreasing into bins that respect the blob and
+    // scratch budgets (upper bounds: nothing is shared between the subtrees)
+    auto pack_siblings = [&](std::vector<int32_t>& roots) {
+      if (roots.empty()) return;
+      if (!opt.pack_siblings || roots.size() == 1) {
+        for (int32_t r : roots) close(r, false);
+        roots.clear();
+        return;
+      }
+      struct Bin {
+        int64_t ints = 0, vals = 0, scratch = 0;
+        std::vector<int32_t> roots;
+      };
+      auto r_ints = [&](int32_t r) { return cl[r].meta_ints + F.sn[r].m + cl[r].ext_u + 2; };
+      auto r_scr = [&](int32_t r) { return cl[r].frontal + F.sn[r].m + cl[r].ext_u; };
+      std::stable_sort(roots.begin(), roots.end(), [&](int32_t a, int32_t b) {
+        return 4 * r_ints(a) + 8 * cl[a].vals > 4 * r_ints(b) + 8 * cl[b].vals;
+      });
+      std::vector<Bin> bins;
+      for (int32_t r : roots) {
+        Bin* dst = nullptr;
+        for (Bin& b : bins)
+          if (blob_size(H_WORDS + 2 + b.ints + r_ints(r), b.vals + cl[r].vals) <= opt.blob_max &&
+              b.scratch + r_scr(r) <= opt.scratch_max && (int32_t)b.roots.size() < opt.pack_max) {
+            dst = &b;
+            break;
+          }
+        if (!dst) {
+          bins.emplace_back();
+          dst = &bins.back();
+        }
+        dst->ints += r_ints(r);
+        dst->vals += cl[r].vals;
+        dst->scratch += r_scr(r);
+        dst->roots.push_back(r);
+      }
+      for (Bin& b : bins) close_roots(b.roots, false);
+      roots.clear();
     };
     for (int64_t k = 0; k < ns; ++k) {
       const Supernode& S = F.sn[k];
@@ -290,9 +340,11 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
       c.ext_u = child_m(k);
       const bool big = S.s > SMALL_MAX_S || frag_bytes(c, S.m) > opt.blob_max ||
                        frag_scratch(c, S.m) > opt.scratch_max;
+      std::vector<int32_t> shut;  // children closed below k
       if (big) {
         for (int32_t q = F.child_ptr[k]; q < F.child_ptr[k + 1]; ++q)
-          if (open[F.child_list[q]]) close(F.child_list[q], false);
+          if (open[F.child_list[q]]) shut.push_back(F.child_list[q]);
+        pack_siblings(shut);
         members[k] = {(int32_t)k};
         close((int32_t)k, true);
         continue;
@@ -317,9 +369,10 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
           mc.clear();
           open[ch] = 0;
         } else {
-          close(ch, false);
+          shut.push_back(ch);
         }
       }
+      pack_siblings(shut);
       cl[k] = c;
       open[k] = 1;
     }
@@ -704,7 +757,6 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
     std::vector<ValDesc> fvd;
     int64_t fvals = 0;
     ints[H_NSN] = nsn;
-    ints[H_TOP_UPD] = upd_slot[gr.factor][gr.top];
     loc.assign(F.sn.size(), -1);
     for (int32_t t = 0; t < nsn; ++t) loc[gr.sns[t]] = t;
     std::vector<int32_t> lev(nsn, 0);
@@ -739,10 +791,19 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
       cpos[i] = pos;
       pos += sn_of(i).s;
     }
-    std::map<int32_t, int32_t> extx;  // permuted row -> staging position (rows of the top)
-    for (int32_t a = 0; a < Top.m; ++a) extx[F.rows[Top.rows_off + a]] = pos + a;
+    std::map<int32_t, int32_t> extx;  // row -> staging position (rows of the tops: one parent front)
+    std::vector<int32_t> extx_rows;
     const int32_t extx_base = pos;
-    pos += Top.m;
+    for (int32_t tp : gr.tops) {
+      const Supernode& T = F.sn[tp];
+      for (int32_t a = 0; a < T.m; ++a) {
+        const int32_t r = F.rows[T.rows_off + a];
+        if (extx.emplace(r, pos).second) {
+          extx_rows.push_back(r);
+          ++pos;
+        }
+      }
+    }
     std::map<int32_t, int32_t> extu_pos;  // external child -> staging position
     std::vector<int32_t> extu;            // global update index per staged double
     const int32_t extu_base = pos;
@@ -759,7 +820,12 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
     }
     const int32_t scratch_used = pos;
     ints[H_NLEV] = nlev;
-    ints[H_TOP] = lid[loc[gr.top]];
+    ints[H_NTOP] = (int32_t)gr.tops.size();
+    ints[H_TOPS] = (int32_t)ints.size();
+    for (int32_t tp : gr.tops) {
+      ints.push_back(lid[loc[tp]]);
+      ints.push_back(upd_slot[gr.factor][tp]);
+    }
     ints[H_COLS] = (int32_t)ints.size();
     for (int32_t i = 0; i < nsn; ++i)
       for (int32_t c = 0; c < sn_of(i).s; ++c) ints.push_back(F.perm[sn_of(i).col0 + c]);
@@ -767,10 +833,10 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
     ints[H_COLPOS] = (int32_t)ints.size();
     for (int32_t i = 0; i < nsn; ++i)
       for (int32_t c = 0; c < sn_of(i).s; ++c) put_pair(ints, scr[i] + c, cpos[i] + c);
-    ints[H_NEXTX] = Top.m;
+    ints[H_NEXTX] = (int32_t)extx_rows.size();
     ints[H_EXTX_BASE] = extx_base;
     ints[H_EXTX] = (int32_t)ints.size();
-    for (int32_t a = 0; a < Top.m; ++a) ints.push_back(F.perm[F.rows[Top.rows_off + a]]);
+    for (int32_t r : extx_rows) ints.push_back(F.perm[r]);
     ints[H_NEXTU] = (int32_t)extu.size();
     ints[H_EXTU_BASE] = extu_base;
     ints[H_EXTU] = (int32_t)ints.size();
@@ -1260,7 +1326,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
       for (const TaskDev& T : P.tasks) {
         if (T.kind != TK_FRAG_FWD) continue;
         const int32_t* h = reinterpret_cast<const int32_t*>(P.blobs.data() + T.blob_off);
-        const int32_t* rec = h + h[H_REC] + 4 * h[H_TOP];
+        const int32_t* rec = h + h[H_REC] + 4 * h[h[H_TOPS]];
         const double sc = h[H_NCOL], mt = (double)((unsigned)rec[0] >> 16);
         const double dv = sc * (sc + 1) / 2 + sc * mt;
         dense += dv;

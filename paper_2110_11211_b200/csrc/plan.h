@@ -4,9 +4,10 @@
 // values) is moved HBM -> slot by one cp.async.bulk.
 //
 // Work units ("groups"):
-//  * FRAG: a connected subtree of small supernodes.  One forward task and one
-//    backward task share the blob; the warp runs the subtree level by level
-//    entirely in its slot.
+//  * FRAG: a connected subtree of small supernodes, or several sibling
+//    subtrees (roots with the same parent supernode) packed together.  One
+//    forward task and one backward task share the blob; the warp runs the
+//    subtrees level by level entirely in its slot.
 //  * BIG: one supernode J too large for a slot.  Forward = ROW tasks (blocks
 //    of rows of M = [L_JJ^-1 ; L_BJ L_JJ^-1], each re-assembling f_J from the
 //    children's update vectors), backward = COL tasks (blocks of columns of M).
@@ -85,8 +86,8 @@ enum FragHdr {
   H_NLEV,
   H_SCRATCH,    // doubles of scratch used
   H_VAL_OFF,    // byte offset of the value area within the blob
-  H_TOP,        // local id of the fragment's top supernode
-  H_TOP_UPD,    // global update slot of the top supernode (-1 none)
+  H_NTOP,       // number of top supernodes (roots of the fragment's subtrees: siblings below one parent)
+  H_TOPS,       // int offset of their pairs {local id, global update slot (-1 none)}
   H_NCOL,       // number of fragment columns
   H_COLS,       // int offset: ro[ncol]
   H_COLPOS,     // int offset: (fpos | cpos << 16)[ncol]
@@ -237,6 +238,8 @@ struct PlanOptions {
                                    // (SFCDD_DIRECT_ROWS; 0: never, 1 << 20: always; -1: 8 in plans that hold a
                                    // supernode too wide for any BLOB block, else 0 -- measured)
   int32_t direct_min_cols = -1;    // ... fewer full-height columns: DIRECT COL blocks (SFCDD_DIRECT_COLS; -1: 4 / 0)
+  bool pack_siblings = true;       // FRAG groups may hold several sibling subtrees (SFCDD_PACK=0: one subtree each)
+  int32_t pack_max = 64;           // ... at most this many (SFCDD_PACK_MAX)
   int32_t split_min_factors = 256; // ASM / XB only in plans of >= this many factors: with few
                                    // subdomains the top of the trees is latency bound and the
                                    // extra dependency hop costs more than it saves (SFCDD_SPLIT_MIN)

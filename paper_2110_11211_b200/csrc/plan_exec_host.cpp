@@ -189,9 +189,11 @@ void plan_exec_host(const DevicePlan& P, const double* rhs, double* xy) {
             });
         }
         for (int32_t c = 0; c < ncol; ++c) x[cols[c]] = S[hi16(colpos[c])];
-        if (h[H_TOP_UPD] >= 0) {
-          const int32_t* R = recs + R_WORDS * h[H_TOP];
-          for (int32_t a = 0; a < rm(R); ++a) upd[h[H_TOP_UPD] + a] = S[R[R_SCR] + rs(R) + a];
+        for (int32_t tp = 0; tp < h[H_NTOP]; ++tp) {
+          const int32_t* tops = h + h[H_TOPS] + 2 * tp;
+          if (tops[1] < 0) continue;
+          const int32_t* R = recs + R_WORDS * tops[0];
+          for (int32_t a = 0; a < rm(R); ++a) upd[tops[1] + a] = S[R[R_SCR] + rs(R) + a];
         }
       } else {
         for (int32_t c = 0; c < ncol; ++c) S[lo16(colpos[c])] = x[cols[c]];
