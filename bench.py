@@ -58,6 +58,22 @@ METRIC = "PCG DOF-iterations/s (SFC two-level Schwarz, Poisson)"
 UNIT = "DOF-it/s"
 
 
+def superlu_cap(config, p):
+    """Sum over the subdomains of nnz(L) of the reference's own factorization
+    (SuperLU, MMD on A^T + A), cached by tools/superlu_nnz.py from the oracle:
+    the algorithmic bytes never credit the builder's extra fill.  C5: the mean
+    of sampled subdomains times P."""
+    f = ROOT / "profiles" / "superlu_nnz.json"
+    if not f.exists():
+        return None
+    e = json.loads(f.read_text()).get(config)
+    if not e:
+        return None
+    if e.get("sum_nnz_L"):
+        return int(e["sum_nnz_L"])
+    return int(round(e["mean_nnz_L"] * p)) if e.get("mean_nnz_L") else None
+
+
 def measured_peak_gbs():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -387,8 +403,10 @@ def run_sharded(args, cfg):
     dist.destroy_process_group()
 
 
-def run_gpu(args, cfg):
+def run_gpu(args, cfg, config=None, emit=True, cpu_baseline=True):
     import torch
+
+    config = config or args.config
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -410,7 +428,7 @@ def run_gpu(args, cfg):
     op = sf.setup(Ah, part, sf.build_coarse(part, Ah, q), sf.SchwarzConfig("balanced", "omega", gamma, q))
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t0
-    if args.config == "c4":  # BASELINE configs[3]: fault-tolerance mode
+    if config == "c4":  # BASELINE configs[3]: fault-tolerance mode
         op.set_fault(5, np.random.default_rng(42).choice(p, size=int(round(0.1 * p)), replace=False))
     stats = op.stats()
     log(f"setup {setup_s:.2f}s stats={stats}")
@@ -493,25 +511,38 @@ def run_gpu(args, cfg):
     peak, peak_kind = measured_peak_gbs()
     cpu = None
     nnz_alg = stats["factor_nnz_l"]
-    if not args.no_cpu_baseline and world == 1 and args.config == "c5":
+    cap = superlu_cap(config, p)  # cached for every config: never credit extra fill
+    nnz_src = "builder nnz(L)"
+    if cap is not None and cap < nnz_alg:
+        nnz_alg, nnz_src = cap, "SuperLU-MMD nnz(L) of the oracle (profiles/superlu_nnz.json)"
+    do_cpu = cpu_baseline and not args.no_cpu_baseline and world == 1
+    if do_cpu and config == "c5":
         cpu = cpu_extrapolated_c5(levels, p, gamma, q)
-    elif not args.no_cpu_baseline and world == 1:
+    elif do_cpu:
         cb = cpu_oracle_sample(levels, p, gamma, q, args.cpu_iters)
-        nnz_alg = min(nnz_alg, cb["nnz_superlu"])
+        if cb["nnz_superlu"] < nnz_alg:
+            nnz_alg, nnz_src = cb["nnz_superlu"], "SuperLU-MMD nnz(L) of the oracle (this run)"
         cpu = {"value": cb["value"], "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": f"{cb['iterations']} PCG iterations of the oracle port on {desc.split(':')[0]} "
-                         f"(scipy SuperLU solves, 1 of {os.cpu_count()} host threads; setup "
-                         f"{cb['setup_seconds']:.1f}s untimed)"}
+               "sample": f"ORACLE PORT (oracle/sfcdd_oracle.py: the reference's scipy SuperLU solves and numpy "
+                         f"kernels, pinned bit-exactly to the reference; not the reference package itself): "
+                         f"{cb['iterations']} PCG iterations on {desc.split(':')[0]}, 1 of {os.cpu_count()} host "
+                         f"threads (the reference's thread pool does not parallelise SuperLU solves), setup "
+                         f"{cb['setup_seconds']:.1f}s untimed"}
     dag_bytes = 16.0 * nnz_alg + 16.0 * (1 + 2 * gamma) * n
     achieved = dag_bytes / (dag_ms * 1e-3) / 1e9
-    traffic = None
+    its_per_solve = total_its / args.steps
+    # whole PCG iteration: B_iter = 8 V N (V = 15 vector passes) + 16 sum nnz_alg(L_i) + 32 nnz(L0)
+    iter_ms = ms / args.steps / its_per_solve
+    iter_bytes = 8.0 * 15 * n + 16.0 * nnz_alg + 32.0 * stats["coarse_nnz"]
+    traffic, traffic_src = None, None
     tp = ROOT / "profiles" / "dag_traffic.json"
     if tp.exists():
         try:
-            traffic = json.loads(tp.read_text()).get(args.config)
+            tj = json.loads(tp.read_text())
+            traffic = tj.get(config)
+            traffic_src = tj.get("_source") if traffic is not None else None
         except Exception:
             traffic = None
-    its_per_solve = total_its / args.steps
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -528,20 +559,26 @@ def run_gpu(args, cfg):
                    "factor_nnz_stored": stats["factor_nnz"],
                    "factor_nnz_l": stats["factor_nnz_l"], "dag_tasks": stats["num_tasks"]},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "kernel": "k_dag (local solves)",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "traffic_source": traffic_src, "kernel": "k_dag (local solves)",
                      "kernel_ms": dag_ms, "peak_kind": peak_kind,
-                     "algorithmic_bytes_per_launch": dag_bytes},
-        "breakdown_ms": {"pcg_iteration": ms / args.steps / its_per_solve, "apply": apply_ms,
+                     "algorithmic_bytes_per_launch": dag_bytes, "nnz_alg": nnz_alg, "nnz_alg_source": nnz_src},
+        "breakdown_ms": {"pcg_iteration": iter_ms, "apply": apply_ms,
                          "local_solves": dag_ms, "matvec": mv_ms},
+        "iteration_roofline": {"bound": "hbm", "bytes": iter_bytes, "achieved": iter_bytes / (iter_ms * 1e-3) / 1e9,
+                               "peak": peak, "unit": "GB/s", "frac": iter_bytes / (iter_ms * 1e-3) / 1e9 / peak,
+                               "formula": "8*15*N + 16*sum nnz_alg(L_i) + 32*nnz(L0) per PCG iteration (SURVEY 8(d))"},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 2 * 8 * n,
                 "d2h_bytes_per_step": 8 * n + 8 * (int(its_per_solve) + 1)},
         "gpu_launches": launches_per_solve * args.steps,
         "clocks": clk.summary(),
     }
-    print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+    if emit:
+        print(json.dumps(line), flush=True)
+    return line
 
 
 def log(msg):
@@ -562,6 +599,9 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=30, help="PCG iterations in the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="use the multi-GPU sharded path even at N=1")
+    ap.add_argument("--also", default=None,
+                    help="comma-separated extra configs measured in the same run and reported under \"also\" "
+                         "(default: c3,c4 when the headline config c2 runs on one GPU; \"none\" disables)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     _, world, _ = dist_env()
@@ -584,7 +624,32 @@ def main():
     elif world > 1 or args.sharded:
         run_sharded(args, cfg)
     else:
-        run_gpu(args, cfg)
+        also = args.also if args.also is not None else ("c3,c4" if args.config == "c2" and world == 1 else "none")
+        names = [a for a in also.split(",") if a and a != "none"]
+        if not names:
+            run_gpu(args, cfg)
+            return
+        t_start = time.perf_counter()
+        line = run_gpu(args, cfg, emit=False)
+        extra = []
+        for nm in names:  # the other single-GPU BASELINE configs, same timing rules, fewer steps
+            if time.perf_counter() - t_start > 240:
+                extra.append({"config": nm, "skipped": "time budget of the default run"})
+                continue
+            try:
+                sub = argparse.Namespace(**vars(args))
+                sub.steps = min(args.steps, 2)
+                l2 = run_gpu(sub, CONFIGS[nm], config=nm, emit=False, cpu_baseline=False)
+                extra.append({"config": nm, "workload": l2["config"]["workload"], "value": l2["value"], "unit": UNIT,
+                              "steps": l2["steps"], "ms_per_step": l2["ms_per_step"],
+                              "iterations": l2["config"]["iterations"], "e2e": l2["e2e"]["value"],
+                              "roofline_frac": l2["roofline"]["frac"], "kernel_ms": l2["roofline"]["kernel_ms"],
+                              "iteration_roofline_frac": l2["iteration_roofline"]["frac"],
+                              "setup_seconds": l2["config"]["setup_seconds"], "clocks": l2["clocks"]})
+            except Exception as e:  # the headline line must survive
+                extra.append({"config": nm, "error": repr(e)[:300]})
+        line["also"] = extra
+        print(json.dumps(line), flush=True)
 
 
 if __name__ == "__main__":

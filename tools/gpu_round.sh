@@ -14,6 +14,12 @@ for w in $WHAT; do
     bench) timeout 600 python bench.py > $OUT/bench_c2.json 2> $OUT/bench_c2.err ;;
     c3) timeout 900 python bench.py --config c3 --steps 3 --warmup 3 --no-cpu-baseline > $OUT/bench_c3.json 2> $OUT/bench_c3.err ;;
     c4) timeout 1500 python bench.py --config c4 --steps 3 --warmup 3 --no-cpu-baseline > $OUT/bench_c4.json 2> $OUT/bench_c4.err ;;
+    c5) timeout 1500 python bench.py --config c5 --steps 2 --warmup 3 > $OUT/bench_c5.json 2> $OUT/bench_c5.err ;;
+    ncu5)
+      timeout 600 python tools/profile_apply.py c5 3 > $OUT/plain_c5.log 2>&1 &&
+      timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_dag -s 3 -c 1 \
+          -o $OUT/dag_c5 python tools/profile_apply.py c5 3 > $OUT/ncu_full_c5.log 2>&1
+      echo "ncu exit $?" >> $OUT/ncu_full_c5.log ;;
     ref) timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_reference_c2.json 2> $OUT/bench_reference_c2.err ;;
     ncu)
       timeout 300 python tools/profile_pcg.py c2 6 > $OUT/plain.log 2>&1 &&
