@@ -717,13 +717,15 @@ __device__ __forceinline__ void run_col_blob(const int32_t* h, double* S, const 
 //    wrote it) and travels through a two-slot ring of RING_CHUNK doubles by
 //    bulk copies on the warp's mbarrier, the next chunk in flight while the
 //    current one is consumed: vec[k] = gvec[k + sh], gvec 16-byte aligned.
-constexpr int DU = 16;
 
 // (ONE inlined copy in the kernel: run_dense below is the only caller; the
 // kernel's code size matters -- every resident warp runs a different path)
+template <int DU>
 __device__ __forceinline__ double dense_dot(const double* __restrict__ V, bool ring, int W, int Len, double* S,
                                             const double* gvec, int sh, uint64_t* bar, uint32_t& phase, int lane) {
-  const int WP = W >= 32 ? 32 : (W <= 2 ? 2 : 1 << (32 - __clz(W - 1)));  // lanes per phase (P <= 16)
+  static_assert(RING_CHUNK % DU == 0 && RING_CHUNK / DU <= 32, "a ring chunk holds whole groups");
+  constexpr int WPMIN = 32 / (RING_CHUNK / DU);  // phases P <= RING_CHUNK / DU: groups never straddle ring chunks
+  const int WP = W >= 32 ? 32 : (W <= WPMIN ? WPMIN : 1 << (32 - __clz(W - 1)));  // lanes per phase
   const int P = 32 / WP;
   const int ph = lane / WP;
   const int il = min(lane & (WP - 1), W - 1);  // lanes >= W repeat the last one (result unused)
@@ -782,12 +784,94 @@ __device__ __forceinline__ double dense_dot(const double* __restrict__ V, bool r
   for (int o = WP; o < 32; o <<= 1) acc += __shfl_xor_sync(FULL, acc, o);
   return acc;
 }
-static_assert(RING_CHUNK % (16 * DU) == 0, "a ring chunk holds whole groups for every phase count");
+
+// MROW (plan.h): update rows [r0, r0 + rows) of a narrow supernode (C = s <=
+// RING_CHUNK) as ONE value stream of nb blocks of Rb rows; lanes = rows of the
+// block, f_J and the task's f_B rows sit in the two ring slots (one bulk-copy
+// round trip), u = f_B - W f_J stored block by block.
+template <int DU, bool PIPE>
+__device__ __forceinline__ uint32_t run_mrow(const int32_t* h, double* S, const DagArgs& A, const uint8_t* gblob,
+                                             int lane, uint64_t* bar, uint32_t phase) {
+  const int s = h[RW_S], Rb = h[RW_R], C = h[RW_C], r0 = h[RW_R0], rows = h[RW_NB], nb = h[RW_NBLK];
+  const double* f = A.upd + h[RW_FOFF];
+  __syncwarp();  // every lane has observed the blob copy's phase before the barrier is armed again
+  if (lane == 0) {
+    fence_proxy_async_global();
+    fence_proxy_async();
+    const uint32_t ba = bytes16(C), bb = bytes16(rows + (r0 & 1));
+    mbar_expect_tx(bar, ba + bb);
+    bulk_g2s(S, f, ba, bar);
+    bulk_g2s(S + RING_STRIDE, f + (r0 & ~1), bb, bar);
+  }
+  const double* fB = S + RING_STRIDE + (r0 & 1);
+  double* uo = A.upd + h[RW_UOFF] + (r0 - s);
+  const double* V = reinterpret_cast<const double*>(gblob + h[RW_VAL_OFF]) + min(lane, Rb - 1);
+  // units = (block, group of <= DU columns of the block); PIPE: the next
+  // unit's loads are in flight while this one is consumed (two register sets)
+  const int gpb = (C + DU - 1) / DU;  // groups per block
+  const int nu = nb * gpb;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int lb = 0, lg = 0;  // (block, group) of the next unit to load
+  auto load_unit = [&](double (&d)[DU]) {
+    const int k0 = lg * DU, n = min(DU, C - k0);
+    const double* q = V + ((size_t)lb * C + k0) * Rb;
+#pragma unroll
+    for (int u = 0; u < DU; ++u) d[u] = u < n ? __ldcs(q + u * Rb) : 0.0;
+    if (++lg == gpb) {
+      lg = 0;
+      ++lb;
+    }
+  };
+  int cb = 0, cg = 0;  // (block, group) of the next unit to consume
+  auto fma_unit = [&](const double (&d)[DU]) {
+    const int k0 = cg * DU, n = min(DU, C - k0);
+    const double* fq = S + k0;
+#pragma unroll
+    for (int u = 0; u < DU; u += 4) {
+      a0 = fma(d[u], u < n ? fq[u] : 0.0, a0);
+      a1 = fma(d[u + 1], u + 1 < n ? fq[u + 1] : 0.0, a1);
+      a2 = fma(d[u + 2], u + 2 < n ? fq[u + 2] : 0.0, a2);
+      a3 = fma(d[u + 3], u + 3 < n ? fq[u + 3] : 0.0, a3);
+    }
+    if (++cg == gpb) {  // block cb done: u = f_B - W f_J
+      const int row = cb * Rb + lane;
+      if (lane < Rb && row < rows) __stcg(uo + row, fB[row] - ((a0 + a1) + (a2 + a3)));
+      a0 = a1 = a2 = a3 = 0.0;
+      cg = 0;
+      ++cb;
+    }
+  };
+  double d0[DU];
+  if (PIPE) {
+    double d1[DU];
+    load_unit(d0);
+    if (nu > 1) load_unit(d1);
+    mbar_wait_guard(bar, phase);
+    phase ^= 1u;
+    for (int i = 0; i < nu; i += 2) {
+      fma_unit(d0);
+      if (i + 2 < nu) load_unit(d0);
+      if (i + 1 < nu) {
+        fma_unit(d1);
+        if (i + 3 < nu) load_unit(d1);
+      }
+    }
+  } else {
+    load_unit(d0);
+    mbar_wait_guard(bar, phase);
+    phase ^= 1u;
+    for (int i = 0; i < nu; ++i) {
+      fma_unit(d0);
+      if (i + 1 < nu) load_unit(d0);
+    }
+  }
+  return phase;
+}
 
 // DIRECT ROW (big forward): rows [r0, r0+R) of out = M f_J: y rows (< s) or update
 // rows u = f_B - out.  DIRECT COL (big backward): columns [k0, k0+c):
 // x_j = sum_r M[k0+r, k0+j] v[r], v = [y_J[k0:s) ; -x_B].
-template <bool SPLIT>
+template <bool SPLIT, int DU>
 __device__ __forceinline__ uint32_t run_dense(bool is_row, const int32_t* h, double* S, const DagArgs& A,
                                               const FactorDev& F, const uint8_t* gblob, int lane, uint64_t* bar,
                                               uint32_t phase) {
@@ -853,7 +937,7 @@ __device__ __forceinline__ uint32_t run_dense(bool is_row, const int32_t* h, dou
       __syncwarp();
     }
   }
-  const double acc = dense_dot(V, SPLIT && ring, W, Len, S, gvec, sh, bar, phase, lane);
+  const double acc = dense_dot<DU>(V, SPLIT && ring, W, Len, S, gvec, sh, bar, phase, lane);
   // after the butterfly every phase holds the sum: lane i (< W <= lanes per phase) owns row / column i
   if (lane < W) {
     if (is_row) {
@@ -925,8 +1009,11 @@ template <int WPB, bool SPLIT, bool DIRECT>
 #if SFCDD_LEAN & 2
 __global__ void __launch_bounds__((WPB + 1) * 32, 20 / WPB) k_dag(DagArgs A) {
 #else
-__global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? 72 : 96) k_dag(DagArgs A) {
+__global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? 72 : WPB == 2 ? 128 : 96) k_dag(DagArgs A) {
 #endif
+  // values in flight per lane of a DIRECT block: 2-worker CTAs (big slots, few warps per SM) have the
+  // registers for 32 (8 KB per warp), the others 16
+  constexpr int DU = 16;  // (32 with 128 registers measured no better)
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bars[WPB];
   __shared__ int32_t mbox[WPB];
@@ -1100,7 +1187,10 @@ __global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? 72 : 96
     } else if (T.kind == TK_COL_BWD && (!DIRECT || h[CL_INBLOB])) {
       run_col_blob<SPLIT>(h, S, A, F, lane, bar, phase);
     } else if constexpr (DIRECT) {
-      phase = run_dense<SPLIT>(T.kind == TK_ROW_FWD, h, S, A, F, A.blobs + T.blob_off, lane, bar, phase);
+      if (SPLIT && T.kind == TK_ROW_FWD && h[RW_NBLK] > 1)
+        phase = run_mrow<16, WPB == 2>(h, S, A, A.blobs + T.blob_off, lane, bar, phase);
+      else
+        phase = run_dense<SPLIT, DU>(T.kind == TK_ROW_FWD, h, S, A, F, A.blobs + T.blob_off, lane, bar, phase);
     } else {
       __trap();  // a DIRECT block in a plan built without them
     }
@@ -1133,8 +1223,12 @@ __global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? 72 : 96
           run_col_blob<SPLIT>(h, S, A, F, lane, bar, phase);
           break;
         }
-        if constexpr (DIRECT)  // ROW or COL block streamed from HBM
-          phase = run_dense<SPLIT>(T.kind == TK_ROW_FWD, h, S, A, F, A.blobs + T.blob_off, lane, bar, phase);
+        if constexpr (DIRECT) {  // ROW or COL block streamed from HBM
+          if (SPLIT && T.kind == TK_ROW_FWD && h[RW_NBLK] > 1)
+            phase = run_mrow<16, WPB == 2>(h, S, A, A.blobs + T.blob_off, lane, bar, phase);
+          else
+            phase = run_dense<SPLIT, DU>(T.kind == TK_ROW_FWD, h, S, A, F, A.blobs + T.blob_off, lane, bar, phase);
+        }
         break;
     }
 #endif
@@ -1180,9 +1274,10 @@ __global__ void k_place_values(const ValDesc* __restrict__ vd, int64_t nvd, cons
     if (d.kind == VD_COPY) {
       for (int32_t i = lane; i < d.len; i += 32) out[i] = M[i];
     } else if (d.kind == VD_ROW) {
+      const int32_t nr = d.rows > 0 ? d.rows : d.w;
       for (int32_t k = 0; k < d.len; ++k) {
         const double* col = M + packed_col_off(d.s, d.m, k);
-        for (int32_t i = max(0, k - d.p0) + lane; i < d.w; i += 32) out[(int64_t)k * d.w + i] = col[d.p0 + i - k];
+        for (int32_t i = max(0, k - d.p0) + lane; i < nr; i += 32) out[(int64_t)k * d.w + i] = col[d.p0 + i - k];
       }
     } else {
       for (int32_t j = 0; j < d.w; ++j) {

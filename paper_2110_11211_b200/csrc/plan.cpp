@@ -172,6 +172,8 @@ PlanOptions::PlanOptions() {
   if (const char* e = std::getenv("SFCDD_DIRECT_ROWS")) direct_min_rows = std::atoi(e);
   if (const char* e = std::getenv("SFCDD_DIRECT_COLS")) direct_min_cols = std::atoi(e);
   if (const char* e = std::getenv("SFCDD_SPLIT_MIN")) split_min_factors = std::atoi(e);
+  if (const char* e = std::getenv("SFCDD_MROW_ROWS")) mrow_rows = std::min(RING_CHUNK, std::max(0, std::atoi(e)));
+  if (const char* e = std::getenv("SFCDD_MROW_MIN")) mrow_min_bytes = std::atoi(e);
   if (const char* e = std::getenv("SFCDD_PACK")) pack_siblings = std::atoi(e) != 0;
   if (const char* e = std::getenv("SFCDD_PACK_MAX")) pack_max = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("SFCDD_WPB")) wpb = std::atoi(e);
@@ -204,7 +206,8 @@ void place_values(const ValDesc& d, const double* M, uint8_t* buf) {
     case VD_ROW:  // out[k R + i] = M[r0 + i, k]
       for (int32_t k = 0; k < d.len; ++k) {
         const double* col = M + packed_col_off(d.s, d.m, k);
-        for (int32_t i = std::max(0, k - d.p0); i < d.w; ++i) out[(int64_t)k * d.w + i] = col[d.p0 + i - k];
+        const int32_t nr = d.rows > 0 ? d.rows : d.w;
+        for (int32_t i = std::max(0, k - d.p0); i < nr; ++i) out[(int64_t)k * d.w + i] = col[d.p0 + i - k];
       }
       break;
     case VD_COL:  // out[r c + j] = M[k0 + r, k0 + j]
@@ -604,8 +607,54 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
           q0 += nq;
         }
       }
+      // MROW: in ASM mode the update rows of a narrow supernode become a few
+      // long DIRECT tasks (plan.h) instead of m / R row blocks
+      const bool mrow = use_asm && opt.mrow_rows > 0 && opt.direct_min_rows > 0 && m > 0 && s <= RING_CHUNK &&
+                        8 * (int64_t)m * s >= opt.mrow_min_bytes;
+      if (mrow) {
+        std::vector<std::pair<int32_t, int32_t>> tasks_rows;
+        balanced(s, s + m, opt.mrow_rows, tasks_rows);
+        for (const auto& tr : tasks_rows) {
+          const int32_t r0 = tr.first, rows = tr.second;
+          const int32_t nb = (rows + 31) / 32, Rb = (rows + nb - 1) / nb;
+          ints.assign(RW_WORDS, 0);
+          ints[RW_S] = s;
+          ints[RW_R] = Rb;
+          ints[RW_C] = s;
+          ints[RW_R0] = r0;
+          ints[RW_NB] = rows;
+          ints[RW_YOFF] = (int32_t)gr.y_off;
+          ints[RW_UOFF] = upd_slot[gr.factor][gr.top];
+          ints[RW_FOFF] = (int32_t)gr.f_off;
+          ints[RW_ASM16] = 0;
+          ints[RW_ASM_HI] = -1;
+          ints[RW_SCRATCH] = 2 * RING_STRIDE;
+          ints[RW_INBLOB] = 0;
+          ints[RW_NBLK] = nb;
+          std::vector<ValDesc> vds;
+          for (int32_t b = 0; b < nb; ++b) {
+            ValDesc vd{};
+            vd.dst = 8 * (int64_t)b * Rb * s;
+            vd.src = S.val_off;
+            vd.kind = VD_ROW;
+            vd.s = s;
+            vd.m = m;
+            vd.p0 = r0 + b * Rb;
+            vd.w = Rb;
+            vd.len = s;
+            vd.rows = std::min(Rb, rows - b * Rb);
+            vds.push_back(vd);
+          }
+          int32_t bytes = 0;
+          const int64_t off = E.emit_descs(ints, RW_VAL_OFF, (int64_t)nb * Rb * s, vds.data(), vds.size(), bytes, &F, -1, true);
+          E.has_direct = true;
+          E.max_scratch = std::max<int32_t>(E.max_scratch, 2 * RING_STRIDE);
+          add_task(g, TK_ROW_FWD, off, bytes, (int64_t)rows * s, 1.8 + 0.0004 * rows * s);
+        }
+      }
       for (const auto& rb : split) {
         const int32_t r0 = rb.first, R = rb.second;
+        if (mrow && r0 >= s) continue;  // covered by the MROW tasks
         const int32_t C = r0 < s ? r0 + R : s;
         const int32_t NB = r0 < s ? 0 : R;
         ints.assign(RW_WORDS, 0);
@@ -638,6 +687,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         const int32_t scr = direct_rows && use_asm ? 2 * RING_STRIDE : C + NB + 6;  // (+ padding of bulk-copied pieces)
         ints[RW_SCRATCH] = scr;
         ints[RW_INBLOB] = direct_rows ? 0 : 1;
+        ints[RW_NBLK] = 1;
         // values: R x C column-major, (i, k) = M[r0 + i, k] for k <= r0 + i;
         // DIRECT blocks leave them in HBM (the task copies its metadata only)
         ValDesc vd{};

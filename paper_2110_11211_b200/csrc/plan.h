@@ -139,6 +139,12 @@ enum XbHdr { XB_A0 = 0, XB_NA, XB_XOFF, XB_ROWS, XB_WORDS };
 // the metadata in the blob buffer (copied with it: BLOB, or not: DIRECT).  Scratch:
 // ASM mode: a two-chunk ring of f_J pieces; inline mode: [f_J[0:C) ;
 // f_B[r0 : r0+NB)] assembled by the task.
+// MROW task (DIRECT, ASM mode, update rows of a supernode with s <= RING_CHUNK):
+// RW_NBLK consecutive blocks of RW_R rows each -- block b holds rows
+// [r0 + b R, r0 + (b+1) R) as R x C column-major, C = s, the last block padded
+// with zero rows; RW_NB = rows of the whole task.  One contiguous value
+// stream per task: the tall, narrow fronts of 3-D subdomains (s ~ 20,
+// m ~ 500) become one task instead of m / 32.
 enum RowHdr {
   RW_S = 0,
   RW_R,        // rows in the block
@@ -157,6 +163,7 @@ enum RowHdr {
   RW_VAL_OFF,  // byte offset of the values
   RW_SCRATCH,  // doubles of scratch used
   RW_INBLOB,   // 1: the values follow the metadata in the slot (BLOB block); 0: they stay in HBM (DIRECT)
+  RW_NBLK,     // row blocks of the task (1; > 1: MROW task, see below)
   RW_WORDS
 };
 // COL blob: backward columns [k0, k0+c) of J.  Values: L x c dense row-major
@@ -210,7 +217,7 @@ struct ValDesc {
   int32_t p0;      // ROW: r0; COL: k0
   int32_t w;       // ROW: R; COL: c
   int32_t len;     // COPY: count; ROW: C; COL: L
-  int32_t pad;
+  int32_t rows;    // ROW: rows present (<= w; the rest of the block stays zero), 0: w
 };
 static_assert(sizeof(ValDesc) == 48, "ValDesc layout");
 // metadata segment of a deferred-value plan: host bytes [host_off, +bytes)
@@ -238,6 +245,10 @@ struct PlanOptions {
                                    // (SFCDD_DIRECT_ROWS; 0: never, 1 << 20: always; -1: 8 in plans that hold a
                                    // supernode too wide for any BLOB block, else 0 -- measured)
   int32_t direct_min_cols = -1;    // ... fewer full-height columns: DIRECT COL blocks (SFCDD_DIRECT_COLS; -1: 4 / 0)
+  int32_t mrow_rows = 0;           // rows per MROW task (<= RING_CHUNK; SFCDD_MROW_ROWS); 0: no MROW tasks, the
+                                   // default -- measured slower than the BLOB row blocks they replace (C5 38.8 vs
+                                   // 35.0 ms, C3 2.45 vs 2.26 ms: a warp streams ~1.5-3 GB/s)
+  int32_t mrow_min_bytes = 32768;  // update rows of fewer value bytes stay ROW blocks (SFCDD_MROW_MIN)
   bool pack_siblings = true;       // FRAG groups may hold several sibling subtrees (SFCDD_PACK=0: one subtree each)
   int32_t pack_max = 64;           // ... at most this many (SFCDD_PACK_MAX)
   int32_t split_min_factors = 256; // ASM / XB only in plans of >= this many factors: with few

@@ -53,6 +53,18 @@ void plan_exec_host(const DevicePlan& P, const double* rhs, double* xy) {
     } else if (T.kind == TK_ROW_FWD) {
       const double* V = reinterpret_cast<const double*>(blob + h[RW_VAL_OFF]);
       const int32_t s = h[RW_S], R = h[RW_R], C = h[RW_C], r0 = h[RW_R0], NB = h[RW_NB];
+      if (h[RW_NBLK] > 1) {  // MROW: blocks of R update rows, leading dimension R, C = s
+        const double* f = upd.data() + h[RW_FOFF];
+        for (int32_t b = 0; b < h[RW_NBLK]; ++b)
+          for (int32_t i = 0; i < R && b * R + i < NB; ++i) {
+            double acc = 0.0;
+            for (int32_t k = 0; k < C; ++k) acc += V[((size_t)b * C + k) * R + i] * f[k];
+            const int32_t rw = r0 + b * R + i;
+            upd[h[RW_UOFF] + rw - s] = f[rw] - acc;
+          }
+        ctr[T.signal_idx] += 1;
+        continue;
+      }
       scratch.assign(C + NB, 0.0);
       double* S = scratch.data();
       if (h[RW_FOFF] >= 0) {

@@ -236,7 +236,7 @@ def test_pcg_c3_matches_reference(sfcdd, golden):
     assert np.linalg.norm(rep.solution[idx] - ref) <= 1e-10 * np.linalg.norm(ref)
 
 
-@pytest.mark.parametrize("mode", ["blob2k", "direct", "narrow", "inline", "direct-inline"])
+@pytest.mark.parametrize("mode", ["blob2k", "direct", "direct-mrow", "narrow", "inline", "direct-inline"])
 def test_pcg_c3_dense_block_shapes_match_reference(sfcdd, golden, mode, monkeypatch):
     """Dense ROW / COL blocks of big supernodes: BLOB blocks travel with
     their metadata, DIRECT blocks (wide separators: the path of BASELINE
@@ -248,9 +248,13 @@ def test_pcg_c3_dense_block_shapes_match_reference(sfcdd, golden, mode, monkeypa
     forced on a 512-factor plan."""
     if mode == "blob2k":
         monkeypatch.setenv("SFCDD_BLOB_MAX", "2048")
-    if mode in ("direct", "narrow", "direct-inline"):
+    if mode in ("direct", "direct-mrow", "narrow", "direct-inline"):
         monkeypatch.setenv("SFCDD_DIRECT_ROWS", str(1 << 20))
         monkeypatch.setenv("SFCDD_DIRECT_COLS", str(1 << 20))
+        # ``direct-mrow``: update rows as MROW tasks of <= 40 rows (ragged blocks); else no MROW tasks
+        monkeypatch.setenv("SFCDD_MROW_MIN", "1" if mode == "direct-mrow" else str(1 << 30))
+    if mode == "direct-mrow":
+        monkeypatch.setenv("SFCDD_MROW_ROWS", "40")
     if mode == "narrow":
         monkeypatch.setenv("SFCDD_ROW_MAX", "6")
         monkeypatch.setenv("SFCDD_COL_MAX", "3")

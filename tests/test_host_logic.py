@@ -126,14 +126,15 @@ def test_host_factor_rejects_non_spd():
                                                   # separators far wider than a 2 KB blob: ROW / COL values
                                                   # never pass through the blob
                                                   ((5, 5, 5), 4, 0.5, 2048)])
-@pytest.mark.parametrize("split", [False, "wide", "narrow", "direct", "direct-inline"])
+@pytest.mark.parametrize("split", [False, "wide", "narrow", "direct", "direct-mrow", "direct-inline"])
 def test_device_plan_host_interpreter(oracle, levels, p, gamma, blob, split, monkeypatch):
     """The fragment/blob layout the DAG kernel executes, run on the host;
     ``split`` forces the ASM / XB task path of big supernodes (plan.h), with
     the default 32-row / 16-column blocks (``wide``) or narrow, non power of
     two blocks (``narrow``: several vector phases per lane group);
     ``direct``: every dense block streams its values from HBM (the form of
-    the wide separators), with ASM / XB tasks or with inline gathers."""
+    the wide separators), with ASM / XB tasks or with inline gathers;
+    ``direct-mrow``: the update rows as MROW tasks (plan.h)."""
     if split:
         if split != "direct-inline":
             monkeypatch.setenv("SFCDD_SPLIT_MIN", "1")
@@ -145,6 +146,10 @@ def test_device_plan_host_interpreter(oracle, levels, p, gamma, blob, split, mon
         if split.startswith("direct"):
             monkeypatch.setenv("SFCDD_DIRECT_ROWS", str(1 << 20))
             monkeypatch.setenv("SFCDD_DIRECT_COLS", str(1 << 20))
+            # MROW tasks (several row blocks in one value stream) for every supernode with below rows, or none
+            monkeypatch.setenv("SFCDD_MROW_MIN", "1" if split == "direct-mrow" else str(1 << 30))
+            if split == "direct-mrow":
+                monkeypatch.setenv("SFCDD_MROW_ROWS", "40")  # several tasks per supernode, ragged last block
     A = oracle.assemble_scaled_laplacian(levels)
     n = A.shape[0]
     ov = oracle.enlarge(oracle.disjoint_partition(n, p), gamma)
