@@ -65,6 +65,7 @@ struct DagArgs {
                   // {1, task, wait_idx, value, target, kind} here and every warp leaves at its next wait
                   // instead of trapping; the host reads it back after the launch
   unsigned long long watchdog_ns;
+  int32_t pf_dist;  // > 0: the claimer of task t pulls the descriptor and blob of task t + pf_dist into L2
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -428,7 +429,6 @@ __device__ __forceinline__ void run_frag(const int32_t* h, bool fwd, double* S, 
     stamp(1);
     for (int lv = 0; lv < nlev; ++lv) {
       const int32_t* L = levtab + L_WORDS * lv;
-      if (lv == nlev - 1) ahead();
       if (L[L_RUN1] > L[L_RUN0]) {  // multifrontal assembly, gather form
         gather_runs(runs, gp, L[L_RUN0], L[L_RUN1], S, lane);
         __syncwarp();
@@ -455,6 +455,7 @@ __device__ __forceinline__ void run_frag(const int32_t* h, bool fwd, double* S, 
       __syncwarp();
       if (lv < 6) stamp(3 + 2 * lv);
     }
+    ahead();  // (the levels are done: only the result stores remain)
     for (int c = lane; c < ncol; c += 32) __stcg(xy + cols[c], S[hi16(colpos[c])]);
     {  // update vectors of the tops (one per packed sibling subtree)
       const int32_t* tops = h + h[H_TOPS];
@@ -480,7 +481,6 @@ __device__ __forceinline__ void run_frag(const int32_t* h, bool fwd, double* S, 
     stamp(1);
     for (int lv = nlev - 1; lv >= 0; --lv) {
       const int32_t* L = levtab + L_WORDS * lv;
-      if (lv == 0) ahead();
       if (L[L_BP1] > L[L_BP0]) {  // v_B = -x(rows)
         for (int p = L[L_BP0] + lane; p < L[L_BP1]; p += 32) S[lo16(bp[p])] = -S[hi16(bp[p])];
         __syncwarp();
@@ -499,6 +499,7 @@ __device__ __forceinline__ void run_frag(const int32_t* h, bool fwd, double* S, 
       __syncwarp();
       if (ls < 4) stamp(3 + 2 * ls);
     }
+    ahead();
     for (int c = lane; c < ncol; c += 32) __stcg(xy + cols[c], S[hi16(colpos[c])]);
     stamp(14);
     if (pt && lane == 0) pt[15] = nlev;
@@ -1044,9 +1045,6 @@ __global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? 72 : WP
   // is always claimable)
   const int q = (int)((blockIdx.x * WPB + warp) % (unsigned)A.nq);
   int32_t* qh = A.qhead + 32 * q;
-  // hook at a task's tail (claiming the next task there was measured slower:
-  // holding a claimed task for even ~1 us delays the critical path)
-  auto ahead = [&]() {};
   // static mode (mode bit 16, experimental): worker w runs tasks w, w + W,
   // w + 2W, ... of the queue order (W = resident workers).  Deadlock-free for
   // the same reason as claiming (each worker's list follows one topological
@@ -1054,6 +1052,16 @@ __global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? 72 : WP
   // claim atomic, and the next descriptor is loaded (one word per lane)
   // while the current task runs.
   const bool stat = (A.mode & 16) != 0;
+  // hook at a FRAG task's tail, after its last level: the claim atomic of the
+  // NEXT task is issued before the result stores and the completion post, so
+  // its L2 round trip (~0.8 us between a worker's tasks) overlaps them.  The
+  // claimed task is held for the stores only (claiming a whole level earlier
+  // was measured slower: a held task delays its dependents); deadlock-free as
+  // before -- this task is past its waits and completes unconditionally.
+  int tnext = -1;
+  auto ahead = [&]() {
+    if ((A.mode & 64) && !stat && lane == 0) tnext = q + A.nq * atomicAdd(qh, 1);
+  };
   const int nw = (int)gridDim.x * WPB;
   int ts = (int)blockIdx.x * WPB + warp;
   constexpr int TW = (int)(sizeof(TaskDev) / 4);
@@ -1065,7 +1073,10 @@ __global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? 72 : WP
     if (stat) {
       t = ts;
     } else {
-      if (lane == 0) t = q + A.nq * atomicAdd(qh, 1);
+      if (lane == 0) {
+        t = tnext >= 0 ? tnext : q + A.nq * atomicAdd(qh, 1);
+        tnext = -1;
+      }
       t = __shfl_sync(FULL, t, 0);
     }
     if (t >= A.ntask) {
@@ -1091,6 +1102,16 @@ __global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? 72 : WP
       pw = (lane < TW && ts < A.ntask) ? __ldg(reinterpret_cast<const int32_t*>(A.tasks + ts) + lane) : 0;
     } else {
       T = A.tasks[t];
+    }
+    // L2 prefetch of a task about one task duration ahead in the queue order
+    // (whoever claims it then finds its descriptor and blob in L2, not DRAM):
+    // lane 1 loads that descriptor now and issues the blob prefetch once this
+    // task's own blob has arrived -- nothing on this task's chain waits for it
+    int64_t pf_off = 0;
+    int32_t pf_bytes = 0;
+    if (A.pf_dist > 0 && lane == 1 && t + A.pf_dist < A.ntask) {
+      pf_off = __ldg(&A.tasks[t + A.pf_dist].blob_off);
+      pf_bytes = __ldg(&A.tasks[t + A.pf_dist].copy_bytes);
     }
     // issued now, consumed after the blob / dependency waits (off the claim chain)
     const FactorDev F = A.factors[T.factor];
@@ -1171,6 +1192,8 @@ __global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? 72 : WP
       }
     }
     if (tr && lane == 0) tr[3] = gtimer();
+    if (pf_bytes > 0)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.blobs + pf_off), "r"(pf_bytes) : "memory");
 #if !(SFCDD_LEAN & 32)  // (the if-chain measured 3 % faster than the switch below on C2: code layout)
     if ((SFCDD_LEAN & 4) && T.kind == TK_FRAG_FWD) {
       run_frag(h, true, S, A, F, lane, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);
@@ -1332,6 +1355,7 @@ DagSolver::DagSolver(const DevicePlan& plan, int device, int64_t extra_xy) : dev
   if (const char* e = std::getenv("SFCDD_DAG_MODE")) mode_ = std::atoi(e);
   if (const char* e = std::getenv("SFCDD_SIG_NS")) sig_ns_ = std::atoi(e);
   if (const char* e = std::getenv("SFCDD_SIG_WAIT_NS")) sig_wait_ns_ = std::atoi(e);
+  if (const char* e = std::getenv("SFCDD_PF_DIST")) pf_dist_ = std::max(0, std::atoi(e));
   smem_ = wpb_ * slot_bytes_;
   SFCDD_REQUIRE(smem_ <= 227 * 1024, SFCDD_EINTERNAL, "DAG shared-memory footprint exceeds 227 KB");
   auto up = [&](void** dst, const void* src, size_t bytes) {
@@ -1444,6 +1468,7 @@ void DagSolver::solve(const double* rhs, cudaStream_t st, const int32_t* skip) {
   a.sig_wait_ns = (uint32_t)sig_wait_ns_;
   a.diag = qhead_ + 32 * (int64_t)nq_;
   a.watchdog_ns = 1000000ull * (unsigned long long)watchdog_ms_;
+  a.pf_dist = pf_dist_;
   void* params[] = {&a};
   if (mode_ & 16)  // static worker lists need every CTA resident: cooperative launch guarantees it (or fails)
     CUDA_CHECK(cudaLaunchCooperativeKernel(kern_, dim3(grid_), dim3((wpb_ + 1) * 32), params, smem_, st));

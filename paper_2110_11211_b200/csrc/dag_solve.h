@@ -40,6 +40,8 @@ class DagSolver {
   const void* kern_ = nullptr;
   int64_t xy_doubles_ = 0, ctr_words_ = 0, bytes_ = 0;
   int32_t watchdog_ms_ = 20000;  // dependency-wait watchdog (SFCDD_WATCHDOG_MS)
+  int32_t pf_dist_ = 1536;       // L2 prefetch distance in queue positions (SFCDD_PF_DIST, 0 = off): about one
+                                 // task duration of claims ahead (C2 k_dag -1.3 %, C3 -3.3 %, profiles/r02/README.md)
   uint8_t* blobs_ = nullptr;
   TaskDev* tasks_ = nullptr;
   FactorDev* factors_ = nullptr;

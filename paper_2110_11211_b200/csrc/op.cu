@@ -587,7 +587,7 @@ __global__ void k_tile_tvec(const double* __restrict__ gv, const double* __restr
 
 // p = z + beta p_old with z = (w - R0^T y0b) + R0^T y0, Ap, p.Ap (k_pm_w on tiles)
 template <int D, int PER>
-__global__ void k_tile_pm_w(const double* __restrict__ w, const double* __restrict__ y0,
+__global__ void __launch_bounds__(VEC_THREADS, PER <= 4 ? 7 : 1) k_tile_pm_w(const double* __restrict__ w, const double* __restrict__ y0,
                             const double* __restrict__ y0b, const int32_t* __restrict__ agg,
                             const double* __restrict__ pold, Stencil S, Tiles T, double* __restrict__ pnew,
                             double* __restrict__ ap, double* __restrict__ part, DevState* st) {
@@ -859,7 +859,7 @@ __global__ void k_pm_w(const double* __restrict__ w, const double* __restrict__ 
 }
 
 // x += alpha p ; r -= alpha Ap ; ||r|| -> history ; R0 r partials
-__global__ void k_update(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+__global__ void __launch_bounds__(VEC_THREADS, 7) k_update(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
                          const double* __restrict__ ap, Chunks C, double* __restrict__ part_rr,
                          double* __restrict__ part_c, DevState* st, double* hist) {
   if (skip(st)) return;

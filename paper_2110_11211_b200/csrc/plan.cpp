@@ -37,6 +37,9 @@ struct Group {
   int32_t height = 0;
 };
 
+// alignment padding and the run-table sentinel of a FRAG blob (ints)
+constexpr int64_t FRAG_PAD = 8;
+
 // running size of an open FRAG cluster (upper bounds)
 struct Cluster {
   int64_t meta_ints = 0;
@@ -44,6 +47,7 @@ struct Cluster {
   int64_t frontal = 0;    // sum (2s+m): frontal slots + column values
   int64_t ext_u = 0;      // doubles of external child updates
   int64_t nsn = 0;
+  int64_t height = 1;     // tree levels of the cluster (one level-table row each)
 };
 
 inline int64_t align16(int64_t x) { return (x + 15) & ~int64_t(15); }
@@ -163,7 +167,7 @@ PlanOptions::PlanOptions() {
   if (const char* e = std::getenv("SFCDD_BLOB_MAX")) blob_max = std::atoi(e);
   if (const char* e = std::getenv("SFCDD_SCRATCH_MAX")) scratch_max = std::atoi(e);
   if (const char* e = std::getenv("SFCDD_WORKERS")) workers = std::atoi(e);
-  if (const char* e = std::getenv("SFCDD_ROW_MAX")) row_max = std::min(32, std::max(1, std::atoi(e)));
+  if (const char* e = std::getenv("SFCDD_ROW_MAX")) row_max = std::min(128, std::max(1, std::atoi(e)));
   if (const char* e = std::getenv("SFCDD_COL_MAX")) col_max = std::min(32, std::max(1, std::atoi(e)));
   if (const char* e = std::getenv("SFCDD_SLACK_US")) slack_us = std::atof(e);
   if (const char* e = std::getenv("SFCDD_ASM_MAX")) asm_max = std::max(32, std::atoi(e));
@@ -271,7 +275,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
     std::vector<std::vector<int32_t>> members(ns);
     group_of[fi].assign(ns, -1);
     auto frag_bytes = [&](const Cluster& c, int64_t m_top) {
-      return blob_size(H_WORDS + 2 + c.meta_ints + m_top + c.ext_u, c.vals);
+      return blob_size(H_WORDS + 2 + FRAG_PAD + c.meta_ints + L_WORDS * c.height + m_top + c.ext_u, c.vals);
     };
     auto frag_scratch = [&](const Cluster& c, int64_t m_top) { return c.frontal + m_top + c.ext_u; };
     auto close_roots = [&](const std::vector<int32_t>& roots, bool big) {
@@ -306,7 +310,9 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         int64_t ints = 0, vals = 0, scratch = 0;
         std::vector<int32_t> roots;
       };
-      auto r_ints = [&](int32_t r) { return cl[r].meta_ints + F.sn[r].m + cl[r].ext_u + 2; };
+      auto r_ints = [&](int32_t r) {  // (one level table per root: an upper bound, the levels are shared)
+        return cl[r].meta_ints + L_WORDS * cl[r].height + F.sn[r].m + cl[r].ext_u + 2;
+      };
       auto r_scr = [&](int32_t r) { return cl[r].frontal + F.sn[r].m + cl[r].ext_u; };
       std::stable_sort(roots.begin(), roots.end(), [&](int32_t a, int32_t b) {
         return 4 * r_ints(a) + 8 * cl[a].vals > 4 * r_ints(b) + 8 * cl[b].vals;
@@ -315,7 +321,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
       for (int32_t r : roots) {
         Bin* dst = nullptr;
         for (Bin& b : bins)
-          if (blob_size(H_WORDS + 2 + b.ints + r_ints(r), b.vals + cl[r].vals) <= opt.blob_max &&
+          if (blob_size(H_WORDS + 2 + FRAG_PAD + b.ints + r_ints(r), b.vals + cl[r].vals) <= opt.blob_max &&
               b.scratch + r_scr(r) <= opt.scratch_max && (int32_t)b.roots.size() < opt.pack_max) {
             dst = &b;
             break;
@@ -336,8 +342,11 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
       const Supernode& S = F.sn[k];
       Cluster c;
       c.nsn = 1;
-      c.meta_ints = R_WORDS + L_WORDS + 2 * S.s + child_m(k) + (S.s + S.m) + S.m +
-                    2 * ((S.s + S.m + 31) / 32 + S.s + 1);
+      // record, cols + colpos, gather pairs, runs (distinct front positions
+      // the children touch), v_B pairs, forward + backward items (packed items
+      // are shared between supernodes: at most one each)
+      c.meta_ints = R_WORDS + 2 * S.s + child_m(k) + std::min<int64_t>(S.s + S.m, child_m(k)) + S.m +
+                    2 * ((S.s + S.m + 31) / 32 + (S.s + 31) / 32);
       c.vals = packed_size(S.s, S.m);
       c.frontal = 2 * S.s + S.m;
       c.ext_u = child_m(k);
@@ -365,6 +374,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         t.vals += d.vals;
         t.frontal += d.frontal;
         t.ext_u += d.ext_u - F.sn[ch].m;
+        t.height = std::max(t.height, d.height + 1);
         if (frag_bytes(t, S.m) <= opt.blob_max && frag_scratch(t, S.m) <= opt.scratch_max) {
           c = t;
           auto& mc = members[ch];
@@ -507,8 +517,8 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
       auto row_split = [&](bool inl, std::vector<std::pair<int32_t, int32_t>>& out) {
         out.clear();
         if (direct_rows) {
-          balanced(0, s, opt.row_max, out);
-          balanced(s, s + m, opt.row_max, out);
+          balanced(0, s, std::min(opt.row_max, 32), out);  // DIRECT: one lane per row
+          balanced(s, s + m, std::min(opt.row_max, 32), out);
           if (inl)  // the task's own assembly CSR must fit the blob, its front piece the scratch
             for (const auto& rb : out) {
               const int32_t r0 = rb.first, R = rb.second;
@@ -519,7 +529,9 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
             }
           return true;
         }
-        static const int32_t cand[] = {32, 16, 8, 4, 2, 1};
+        // (any row count runs: lanes = rows, blocks of > 32 rows in passes; the
+        // finer steps fill the blob where a power of two would leave it half empty)
+        static const int32_t cand[] = {128, 112, 96, 80, 64, 56, 48, 40, 32, 28, 24, 20, 16, 14, 12, 10, 8, 6, 4, 3, 2, 1};
         for (int32_t r0 = 0; r0 < s + m;) {
           const int32_t lim = r0 < s ? s : s + m;
           int32_t R = 0;

@@ -236,7 +236,8 @@ struct PlanOptions {
   int32_t big_scratch_max = 8192;  // doubles of scratch a BIG task may use
   int32_t workers = 0;             // warps assumed by the queue-order simulation (0: from the slot size; SFCDD_WORKERS)
   int32_t sms = 148;               // SMs of the target device (set by the caller)
-  int32_t row_max = 32;            // rows per ROW task (SFCDD_ROW_MAX; latency vs task count), <= 32
+  int32_t row_max = 128;           // rows per BLOB ROW task (SFCDD_ROW_MAX; latency vs task count), <= 128;
+                                   // DIRECT ROW blocks hold <= 32 rows (one lane per row)
   int32_t col_max = 16;            // columns per COL task (SFCDD_COL_MAX), <= 32
   int32_t asm_max = 256;           // front positions per ASM task (SFCDD_ASM_MAX)
   double asm_redundancy = 4.0;     // BLOB supernodes: ASM when the ROW tasks would gather the front >= this often (SFCDD_ASM_RED)
