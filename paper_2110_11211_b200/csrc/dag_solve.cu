@@ -1118,7 +1118,9 @@ __global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? 72 : WP
     // slot addresses computed from the shared base so the compiler keeps the
     // shared state space (LDS, not generic loads) for every blob/scratch access
     const int32_t* h = reinterpret_cast<const int32_t*>(smem + (size_t)warp * A.slot_bytes);
-    double* S = reinterpret_cast<double*>(smem + (size_t)warp * A.slot_bytes + A.blob_max);
+    // the scratch follows the task's own blob (128-byte aligned): blob and
+    // scratch share the slot, so small-scratch tasks carry larger blobs
+    double* S = reinterpret_cast<double*>(smem + (size_t)warp * A.slot_bytes + ((T.copy_bytes + 127) & ~127));
     unsigned long long* tr = A.trace ? A.trace + 5 * (size_t)t : nullptr;
     if (lane == 0) {
       if (tr) {
@@ -1337,7 +1339,7 @@ DagSolver::DagSolver(const DevicePlan& plan, int device, int64_t extra_xy) : dev
   ntask_ = (int32_t)plan.tasks.size();
   host_tasks = plan.tasks;
   blob_max_ = round128(plan.blob_max);
-  slot_bytes_ = blob_max_ + round128(8 * (int64_t)std::max(plan.max_scratch, 16));
+  slot_bytes_ = round128(std::max<int64_t>(plan.slot_need, 256));
   // worker warps per CTA: the plan's choice (plan.h choose_blob_shape, SFCDD_WPB)
   wpb_ = plan.wpb;
   SFCDD_REQUIRE(wpb_ == 2 || wpb_ == 4 || wpb_ == 8, SFCDD_EVALUE, "worker warps per CTA must be 2, 4 or 8");

@@ -68,6 +68,10 @@ struct FactorEmit {
   std::vector<TaskDev> tasks;
   std::vector<double> tw;
   int32_t max_scratch = 0, max_copy = 0;
+  int64_t max_slot = 0;  // max over tasks of align128(blob bytes) + 8 * scratch doubles
+  void need_slot(int32_t bytes, int64_t scratch_doubles) {
+    max_slot = std::max<int64_t>(max_slot, ((int64_t)bytes + 127) / 128 * 128 + 8 * scratch_doubles);
+  }
   bool has_direct = false;
 
   int64_t put_meta(const std::vector<int32_t>& ints, int64_t meta_bytes) {
@@ -181,6 +185,7 @@ PlanOptions::PlanOptions() {
   if (const char* e = std::getenv("SFCDD_PACK")) pack_siblings = std::atoi(e) != 0;
   if (const char* e = std::getenv("SFCDD_PACK_MAX")) pack_max = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("SFCDD_WPB")) wpb = std::atoi(e);
+  if (const char* e = std::getenv("SFCDD_SLOT_MAX")) slot_max = std::max(-1, std::atoi(e));
   tuned = std::getenv("SFCDD_BLOB_MAX") || std::getenv("SFCDD_WPB");
 }
 
@@ -199,6 +204,10 @@ void choose_blob_shape(const std::vector<const HostFactor*>& factors, PlanOption
     opt.blob_max = 16 * 1024;
     opt.wpb = 2;
   }
+  // one budget for blob + scratch (the scratch follows the task's own blob):
+  // the largest slot that keeps 5 CTAs per SM resident (228 KB of shared
+  // memory, 1 KB reserved and < 256 B static per CTA)
+  if (opt.slot_max == 0) opt.slot_max = (int32_t)(((233472 / 5 - 1024 - 256) / opt.wpb) / 128 * 128);
 }
 
 void place_values(const ValDesc& d, const double* M, uint8_t* buf) {
@@ -247,6 +256,19 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
   SFCDD_REQUIRE(opt.wpb == 2 || opt.wpb == 4 || opt.wpb == 8, SFCDD_EVALUE, "SFCDD_WPB must be 2, 4 or 8");
   DevicePlan P;
   P.blob_max = opt.blob_max;
+  // Slot budget (opt.slot_max > 0): a task's scratch starts right after its
+  // own blob (dag_solve.cu), so blob and scratch share one budget -- a task
+  // with little scratch may carry a blob larger than blob_max.  Otherwise the
+  // two areas have separate budgets (explicit blob_max / scratch_max).
+  const bool slot_budget = opt.slot_max > 0;
+  auto fits_frag = [&](int64_t bytes, int64_t scratch) {
+    if (!slot_budget) return bytes <= opt.blob_max && scratch <= opt.scratch_max;
+    return (bytes + 127) / 128 * 128 + 8 * scratch <= opt.slot_max && scratch < 65536;
+  };
+  auto blob_cap = [&](int64_t scratch) -> int64_t {  // largest blob next to `scratch` doubles
+    if (!slot_budget) return opt.blob_max;
+    return std::max<int64_t>(2048, (opt.slot_max - 8 * scratch) / 128 * 128);
+  };
   P.wpb = opt.wpb;
   std::vector<Group> groups;
   std::vector<std::vector<int32_t>> group_of(factors.size());
@@ -321,8 +343,9 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
       for (int32_t r : roots) {
         Bin* dst = nullptr;
         for (Bin& b : bins)
-          if (blob_size(H_WORDS + 2 + FRAG_PAD + b.ints + r_ints(r), b.vals + cl[r].vals) <= opt.blob_max &&
-              b.scratch + r_scr(r) <= opt.scratch_max && (int32_t)b.roots.size() < opt.pack_max) {
+          if (fits_frag(blob_size(H_WORDS + 2 + FRAG_PAD + b.ints + r_ints(r), b.vals + cl[r].vals),
+                        b.scratch + r_scr(r)) &&
+              (int32_t)b.roots.size() < opt.pack_max) {
             dst = &b;
             break;
           }
@@ -350,8 +373,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
       c.vals = packed_size(S.s, S.m);
       c.frontal = 2 * S.s + S.m;
       c.ext_u = child_m(k);
-      const bool big = S.s > SMALL_MAX_S || frag_bytes(c, S.m) > opt.blob_max ||
-                       frag_scratch(c, S.m) > opt.scratch_max;
+      const bool big = S.s > SMALL_MAX_S || !fits_frag(frag_bytes(c, S.m), frag_scratch(c, S.m));
       std::vector<int32_t> shut;  // children closed below k
       if (big) {
         for (int32_t q = F.child_ptr[k]; q < F.child_ptr[k + 1]; ++q)
@@ -375,7 +397,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         t.frontal += d.frontal;
         t.ext_u += d.ext_u - F.sn[ch].m;
         t.height = std::max(t.height, d.height + 1);
-        if (frag_bytes(t, S.m) <= opt.blob_max && frag_scratch(t, S.m) <= opt.scratch_max) {
+        if (fits_frag(frag_bytes(t, S.m), frag_scratch(t, S.m))) {
           c = t;
           auto& mc = members[ch];
           members[k].insert(members[k].end(), mc.begin(), mc.end());
@@ -540,7 +562,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
             const int32_t Re = std::min(cnd, lim - r0);
             const int32_t C = r0 < s ? r0 + Re : s, NB = r0 < s ? 0 : Re;
             const int64_t meta = inl ? RW_WORDS + C + (C + NB + 1) + row_nnz(r0, C, NB) : RW_WORDS;
-            if (blob_size(meta, (int64_t)Re * C) <= opt.blob_max && C + NB + 2 <= opt.big_scratch_max) {
+            if (blob_size(meta, (int64_t)Re * C) <= blob_cap(C + NB + 6) && C + NB + 2 <= opt.big_scratch_max) {
               R = Re;
               break;
             }
@@ -615,6 +637,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
           int32_t bytes = 0;
           const int64_t off = E.emit(ints, -1, 0, nullptr, bytes);  // metadata only
           ints.clear();
+          E.need_slot(bytes, 0);
           add_task(g, TK_ASM_FWD, off, bytes, 0, 1.2 + 0.004 * (nq + (double)e));
           q0 += nq;
         }
@@ -661,6 +684,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
           const int64_t off = E.emit_descs(ints, RW_VAL_OFF, (int64_t)nb * Rb * s, vds.data(), vds.size(), bytes, &F, -1, true);
           E.has_direct = true;
           E.max_scratch = std::max<int32_t>(E.max_scratch, 2 * RING_STRIDE);
+          E.need_slot(bytes, 2 * RING_STRIDE);
           add_task(g, TK_ROW_FWD, off, bytes, (int64_t)rows * s, 1.8 + 0.0004 * rows * s);
         }
       }
@@ -713,7 +737,8 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         const int32_t asm_word = asm16 >= 0 ? RW_ASM16 : -1;
         int32_t bytes = 0;
         const int64_t off = E.emit(ints, RW_VAL_OFF, (int64_t)R * C, &vd, bytes, F, asm_word, direct_rows);
-        SFCDD_REQUIRE(bytes <= opt.blob_max, SFCDD_EINTERNAL, "ROW blob exceeds the slot");
+        SFCDD_REQUIRE(bytes <= blob_cap(scr), SFCDD_EINTERNAL, "ROW blob exceeds the slot");
+        E.need_slot(bytes, scr);
         E.has_direct = E.has_direct || direct_rows;
         E.max_scratch = std::max<int32_t>(E.max_scratch, scr);
         add_task(g, TK_ROW_FWD, off, bytes, (int64_t)R * C, (use_asm ? 1.8 : 2.36) + 0.0013 * R * C);
@@ -730,7 +755,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
       auto col_width = [&](int32_t k0, bool inl) {
         const int32_t L = s + m - k0;
         int32_t c = std::min<int32_t>(opt.col_max, s - k0);
-        while (c > 1 && blob_size(CL_WORDS + c + (inl ? m : 0), (int64_t)L * c) > opt.blob_max) --c;
+        while (c > 1 && blob_size(CL_WORDS + c + (inl ? m : 0), (int64_t)L * c) > blob_cap(L + 2)) --c;
         if (std::getenv("SFCDD_EVEN_COLS") && c > 1 && (c & 1) && k0 + c < s) --c;
         return c;
       };
@@ -770,6 +795,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
           int32_t bytes = 0;
           const int64_t off = E.emit(ints, -1, 0, nullptr, bytes);  // metadata only
           ints.clear();
+          E.need_slot(bytes, 0);
           add_task(g, TK_XB_BWD, off, bytes, 0, 1.2 + 0.003 * na);
           a0 += na;
         }
@@ -805,8 +831,9 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         vd.len = L;
         int32_t bytes = 0;
         const int64_t off = E.emit(ints, CL_VAL_OFF, (int64_t)L * c, &vd, bytes, F, -1, direct_cols);
-        SFCDD_REQUIRE(bytes <= opt.blob_max, SFCDD_EINTERNAL,
+        SFCDD_REQUIRE(bytes <= blob_cap(scr), SFCDD_EINTERNAL,
                       "big supernode column does not fit a task blob (s+m = " + std::to_string(s + m) + ")");
+        E.need_slot(bytes, scr);
         E.has_direct = E.has_direct || direct_cols;
         E.max_scratch = std::max<int32_t>(E.max_scratch, scr);
         add_task(g, TK_COL_BWD, off, bytes, nv, (use_xb ? 1.8 : 2.24) + 0.0013 * nv);
@@ -1093,10 +1120,11 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
     ints.insert(ints.end(), items.begin(), items.end());
     ints[H_SCRATCH] = scratch_used;
     ints[H_ZERO] = nsn > 0 ? cpos[0] : 0;  // frontal slots [0, cpos[0])
-    SFCDD_REQUIRE(scratch_used <= opt.scratch_max, SFCDD_EINTERNAL, "fragment scratch exceeds budget");
+    SFCDD_REQUIRE(slot_budget || scratch_used <= opt.scratch_max, SFCDD_EINTERNAL, "fragment scratch exceeds budget");
     int32_t bytes = 0;
     const int64_t off = E.emit_frag(ints, H_VAL_OFF, fvals, fvd, bytes, F);
-    SFCDD_REQUIRE(bytes <= opt.blob_max, SFCDD_EINTERNAL, "fragment blob exceeds the slot budget");
+    SFCDD_REQUIRE(fits_frag(bytes, scratch_used), SFCDD_EINTERNAL, "fragment blob exceeds the slot budget");
+    E.need_slot(bytes, scratch_used);
     E.max_scratch = std::max(E.max_scratch, scratch_used);
     // task time model (us), fitted to traced C2 launches (tools/trace_dag.py)
     add_task(g, TK_FRAG_FWD, off, bytes, nvals, 2.13 + 0.0041 * nvals + 0.57 * nlev);
@@ -1162,6 +1190,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
     }
     cursor += E.size;
     P.max_scratch = std::max(P.max_scratch, E.max_scratch);
+    P.slot_need = std::max(P.slot_need, E.max_slot);
     P.max_copy = std::max(P.max_copy, E.max_copy);
     P.has_direct = P.has_direct || E.has_direct;
   }
@@ -1275,7 +1304,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
     // CTAs, <= 20 worker warps/SM by registers (dag_solve.cu)
     int64_t workers = opt.workers;
     if (workers <= 0) {
-      const int64_t slot = (opt.blob_max + 127) / 128 * 128 + (8 * std::max(P.max_scratch, 16) + 127) / 128 * 128;
+      const int64_t slot = std::max<int64_t>(P.slot_need, 256);
       const int64_t ctas = std::max<int64_t>(1, (227 * 1024) / (opt.wpb * slot));
       workers = (int64_t)opt.sms * std::min<int64_t>(20, opt.wpb * ctas);
     }

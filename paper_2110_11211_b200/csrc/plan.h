@@ -257,6 +257,10 @@ struct PlanOptions {
                                    // extra dependency hop costs more than it saves (SFCDD_SPLIT_MIN)
   double slack_us = 4.0;           // queue-order simulation: dependents become ready this late (SFCDD_SLACK_US)
   int32_t wpb = 4;                 // worker warps per DAG CTA: 2, 4 or 8 (SFCDD_WPB)
+  int32_t slot_max = 0;            // > 0: ONE byte budget for a task's blob + scratch (the scratch follows the
+                                   // task's own blob in the slot); 0: set by choose_blob_shape to the largest
+                                   // slot that keeps 5 CTAs per SM; -1: separate blob_max / scratch_max budgets
+                                   // (SFCDD_SLOT_MAX)
   bool tuned = false;              // blob_max / wpb fixed by the environment (no automatic choice)
   bool defer_values = false;       // build the plan from symbolic factors: blobs hold metadata only
                                    // (DevicePlan::segs), values are placed later by the descriptors
@@ -290,6 +294,7 @@ struct DevicePlan {
   bool has_direct = false;  // some ROW / COL task streams its values from HBM (selects the kernel variant)
   int32_t wpb = 4;          // worker warps per DAG CTA the plan was simulated for
   int32_t max_scratch = 0;  // doubles, over all tasks
+  int64_t slot_need = 0;    // bytes of shared memory a worker needs: max over tasks of align128(blob) + scratch
   int32_t max_copy = 0;     // bytes
   int32_t blob_max = 0;
   double sim_us = 0.0;  // makespan of the simulated schedule (model time)
