@@ -35,6 +35,10 @@
 #define SFCDD_LEAN 0  // experiment switches (tools/build_variants.sh): 1 no watchdog / diagnostics, 2 launch-bounds
 #endif                // register cap, 4 specialised FRAG calls, 8 no syncwarp before the ROW front copy
 
+#ifndef SFCDD_REGS4
+#define SFCDD_REGS4 72  // registers per thread of the 4-worker kernel: 5 CTAs of 160 threads per SM
+#endif
+
 namespace sfcdd {
 
 namespace {
@@ -1010,7 +1014,7 @@ template <int WPB, bool SPLIT, bool DIRECT>
 #if SFCDD_LEAN & 2
 __global__ void __launch_bounds__((WPB + 1) * 32, 20 / WPB) k_dag(DagArgs A) {
 #else
-__global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? 72 : WPB == 2 ? 128 : 96) k_dag(DagArgs A) {
+__global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? SFCDD_REGS4 : WPB == 2 ? 128 : 96) k_dag(DagArgs A) {
 #endif
   // values in flight per lane of a DIRECT block: 2-worker CTAs (big slots, few warps per SM) have the
   // registers for 32 (8 KB per warp), the others 16
