@@ -1116,6 +1116,9 @@ static void coarse_solve(sfcdd_op* op, const double* part, const int32_t* ptr, b
 static int64_t coarse_solve_launches(const sfcdd_op* op, bool direct) {
   return op->ainv ? 1 : (direct ? 0 : 1) + 1 + 1;  // GEMV | [segment sums] + DAG + output
 }
+// the tile-slot sums of R0 Â w ride in the second coarse GEMV (dense inverse, few aggregates)
+static bool slot_sums_fused(const sfcdd_op* op) { return op->ainv != nullptr && op->n0 <= 2048; }
+
 static int64_t apply_launches(const sfcdd_op* op, bool pcg, bool partials_ready) {
   const int v = op->variant;
   const bool direct = op->nch == op->n0;
@@ -1123,7 +1126,9 @@ static int64_t apply_launches(const sfcdd_op* op, bool pcg, bool partials_ready)
   if (v != SFCDD_VARIANT_ONE_LEVEL) k += (partials_ready ? 0 : 1) + coarse_solve_launches(op, direct);
   if (v == SFCDD_VARIANT_BALANCED) k += 1;  // t
   k += 1 + 1;                               // DAG + combine
-  if (mode_of(v) == 2) k += op->tile_agg ? 2 + coarse_solve_launches(op, true) : 1 + coarse_solve_launches(op, direct);
+  if (mode_of(v) == 2)
+    k += op->tile_agg ? (slot_sums_fused(op) ? 1 : 2) + coarse_solve_launches(op, true)
+                      : 1 + coarse_solve_launches(op, direct);
   if (!(pcg && mode_of(v) == 2)) k += 1;    // finalize
   return k;
 }
@@ -1169,10 +1174,17 @@ static void apply_device(sfcdd_op* op, const double* g, double* h, cudaStream_t 
     PcgFin fin{op->part_a, op->part_c, op->y0, op->nch, fused ? dst : nullptr, op->agg_ptr, direct};
     if (op->tile_agg) {  // c = R0 Â w per aggregate from the tile slots
       TILE_LAUNCH(k_tile_agg_matvec, op, st, op->w, op->d_agg_start, op->agg, S, op->tiles, op->part_t, sk);
-      k_slot_sums<<<nblocks(op->n0, VEC_THREADS), VEC_THREADS, 0, st>>>(op->part_t, op->tiles.sptr, op->n0,
-                                                                       op->cvec, sk);
-      kmark(st, "matvec_chunk");
-      coarse_solve(op, op->cvec, op->agg_ptr, true, op->y0b, sk, fin, st);
+      if (slot_sums_fused(op)) {
+        // small dense coarse problems: every GEMV CTA sums the slots itself (same order
+        // as k_slot_sums: bitwise equal), one launch less on the iteration's critical path
+        kmark(st, "matvec_chunk");
+        coarse_solve(op, op->part_t, op->tiles.sptr, false, op->y0b, sk, fin, st);
+      } else {
+        k_slot_sums<<<nblocks(op->n0, VEC_THREADS), VEC_THREADS, 0, st>>>(op->part_t, op->tiles.sptr, op->n0,
+                                                                         op->cvec, sk);
+        kmark(st, "matvec_chunk");
+        coarse_solve(op, op->cvec, op->agg_ptr, true, op->y0b, sk, fin, st);
+      }
     } else {
       k_matvec_chunk<<<op->nch, VEC_THREADS, 0, st>>>(op->w, S, C, op->part_b, sk);
       kmark(st, "matvec_chunk");

@@ -200,7 +200,9 @@ void choose_blob_shape(const std::vector<const HostFactor*>& factors, PlanOption
     }
   if (std::getenv("SFCDD_PLAN_DEBUG"))
     std::fprintf(stderr, "[plan] values in supernodes above one blob: %.1f%%\n", tot > 0.0 ? 100.0 * big / tot : 0.0);
-  if (tot > 0.0 && big > 0.42 * tot) {  // measured: C2 34 % -> 8 KB wins by 13 %; C4 47 %, C3 79 % -> 16 KB wins by 4 %, 17 %
+  // measured with the shared blob + scratch slot budget (profiles/r02/s5): C2 34 % -> 8 KB / 4 workers wins by
+  // 7 %, C4 47 % -> by 5 %; C3 79 % needs 16 KB (a row of its widest BLOB supernode does not fit 8 KB)
+  if (tot > 0.0 && big > 0.60 * tot) {
     opt.blob_max = 16 * 1024;
     opt.wpb = 2;
   }
