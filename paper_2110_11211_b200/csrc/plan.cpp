@@ -269,7 +269,12 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
   };
   auto blob_cap = [&](int64_t scratch) -> int64_t {  // largest blob next to `scratch` doubles
     if (!slot_budget) return opt.blob_max;
-    return std::max<int64_t>(2048, (opt.slot_max - 8 * scratch) / 128 * 128);
+    // (a task whose scratch leaves less than half a blob falls back to the
+    // separate budgets: the slot then grows to blob_max + its scratch, as
+    // without the slot budget -- few-subdomain plans with wide separators,
+    // whose COL tasks gather a whole front column into the scratch)
+    const int64_t room = (opt.slot_max - 8 * scratch) / 128 * 128;
+    return room >= opt.blob_max / 2 ? room : opt.blob_max;
   };
   P.wpb = opt.wpb;
   std::vector<Group> groups;
@@ -547,7 +552,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
             for (const auto& rb : out) {
               const int32_t r0 = rb.first, R = rb.second;
               const int32_t C = r0 < s ? r0 + R : s, NB = r0 < s ? 0 : R;
-              if (blob_size(RW_WORDS + C + (C + NB + 1) + row_nnz(r0, C, NB), 0) > opt.blob_max ||
+              if (blob_size(RW_WORDS + C + (C + NB + 1) + row_nnz(r0, C, NB), 0) > blob_cap(C + NB + 6) ||
                   C + NB + 2 > opt.big_scratch_max)
                 return false;
             }
@@ -739,7 +744,10 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         const int32_t asm_word = asm16 >= 0 ? RW_ASM16 : -1;
         int32_t bytes = 0;
         const int64_t off = E.emit(ints, RW_VAL_OFF, (int64_t)R * C, &vd, bytes, F, asm_word, direct_rows);
-        SFCDD_REQUIRE(bytes <= blob_cap(scr), SFCDD_EINTERNAL, "ROW blob exceeds the slot");
+        SFCDD_REQUIRE(bytes <= blob_cap(scr), SFCDD_EINTERNAL,
+                      "ROW blob exceeds the slot (bytes " + std::to_string(bytes) + ", scratch " + std::to_string(scr) +
+                          ", s " + std::to_string(s) + ", R " + std::to_string(R) + ", C " + std::to_string(C) +
+                          (use_asm ? ", asm" : global_asm ? ", record" : ", inline") + (direct_rows ? ", direct)" : ", blob)"));
         E.need_slot(bytes, scr);
         E.has_direct = E.has_direct || direct_rows;
         E.max_scratch = std::max<int32_t>(E.max_scratch, scr);
@@ -766,7 +774,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
       if (direct_cols) {
         balanced(0, s, opt.col_max, csplit);
         const bool inline_fits =
-            blob_size(CL_WORDS + opt.col_max + m, 0) <= opt.blob_max && s + m + 2 <= opt.big_scratch_max;
+            blob_size(CL_WORDS + opt.col_max + m, 0) <= blob_cap(s + m + 2) && s + m + 2 <= opt.big_scratch_max;
         ring_col = split_ok || !inline_fits;  // v is contiguous in upd: y_J then -x_B
         use_xb = m > 0 && ring_col;
       } else {
@@ -774,7 +782,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         for (int32_t k0 = 0; k0 < s; k0 += col_width(k0, false)) ++ncol_tasks;
         // XB also when a column block with its inline row list cannot fit a blob
         const bool inline_fits =
-            blob_size(CL_WORDS + 1 + m, (int64_t)(s + m)) <= opt.blob_max && s + m + 2 <= opt.big_scratch_max;
+            blob_size(CL_WORDS + 1 + m, (int64_t)(s + m)) <= blob_cap(s + m + 2) && s + m + 2 <= opt.big_scratch_max;
         use_xb = m > 0 && ((split_ok && ncol_tasks >= opt.xb_min_tasks) || !inline_fits);
         ring_col = use_xb || (m == 0 && !inline_fits);
         for (int32_t k0 = 0; k0 < s;) {

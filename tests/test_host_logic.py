@@ -164,6 +164,25 @@ def test_device_plan_host_interpreter(oracle, levels, p, gamma, blob, split, mon
         off += r.length
 
 
+@pytest.mark.parametrize("levels,p,gamma", [((5, 5, 5), 2, 0.5), ((8, 8), 2, 0.5)])
+def test_default_plan_few_wide_subdomains(oracle, levels, p, gamma):
+    """Default blob shape and slot budget (one budget for blob + scratch) on
+    few, large subdomains: separators ~ 1000 wide whose ROW / COL tasks carry
+    inline gather lists and a whole front column of scratch (the C5-sized
+    proxy of tools/plan_stats.py c5p at a size that runs in seconds)."""
+    A = oracle.assemble_scaled_laplacian(levels)
+    n = A.shape[0]
+    ov = oracle.enlarge(oracle.disjoint_partition(n, p), gamma)
+    rhs = np.random.default_rng(5).standard_normal(n)
+    xy, nfrag = host_plan_solve(A, ov, rhs)
+    off = 0
+    for r in ov:
+        idx = r.indices()
+        xr = spla.spsolve(A[idx][:, idx].tocsc(), rhs[idx])
+        assert np.linalg.norm(xy[off:off + r.length] - xr) <= 1e-11 * np.linalg.norm(xr)  # two exact factorizations
+        off += r.length
+
+
 # ---- partition mirror: known answers of the reference tests (test_partition.py:24-116)
 def test_partition_known_answers():
     assert [r.length for r in pt.disjoint_partition(9, 2)] == [5, 4]
