@@ -564,7 +564,7 @@ __device__ __noinline__ void run_xb(const int32_t* h, const DagArgs& A, const Fa
 // ================================================= BLOB ROW (big forward)
 // values in the slot: rows [r0, r0+R) of out = M f_J; lanes = (row, k-phase)
 // when R < 32; the assembled front f = [f_J ; f_B] is read contiguously (ASM tasks)
-template <bool SPLIT>
+template <bool SPLIT, bool WIDE>
 __device__ __forceinline__ void run_row_blob(const int32_t* h, double* S, const DagArgs& A, const FactorDev& F,
                                              int lane, uint64_t* bar, uint32_t& phase) {
   const int s = h[RW_S], R = h[RW_R], C = h[RW_C], r0 = h[RW_R0], NB = h[RW_NB];
@@ -629,17 +629,29 @@ __device__ __forceinline__ void run_row_blob(const int32_t* h, double* S, const 
   double* uo = A.upd + h[RW_UOFF];
   for (int rb = 0; rb < R; rb += RP) {
     const int i = rb + il;
-    double a0 = 0.0, a1 = 0.0;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     if (i < R) {
+      // WIDE (16 KB blobs, 2-worker CTAs: long rows): four independent (value, f)
+      // load pairs in flight per step -- the loop is bound by the shared-memory
+      // latency of a step, not by its FMAs (C3 k_dag -3 %).  The 8 KB kernel keeps
+      // two: the larger code costs it more than the loop gains (C2 +2.5 %)
       const double* v = V + i;
       int k = ph;
-      for (; k + P < C; k += 2 * P) {
+      for (; WIDE && k + 3 * P < C; k += 4 * P) {
+        const double m0 = v[k * R], m1 = v[(k + P) * R], m2 = v[(k + 2 * P) * R], m3 = v[(k + 3 * P) * R];
+        const double f0 = S[k], f1 = S[k + P], f2 = S[k + 2 * P], f3 = S[k + 3 * P];
+        a0 = fma(m0, f0, a0);
+        a1 = fma(m1, f1, a1);
+        a2 = fma(m2, f2, a2);
+        a3 = fma(m3, f3, a3);
+      }
+      for (; !WIDE && k + P < C; k += 2 * P) {
         a0 = fma(v[k * R], S[k], a0);
         a1 = fma(v[(k + P) * R], S[k + P], a1);
       }
-      if (k < C) a0 = fma(v[k * R], S[k], a0);
+      for (; k < C; k += P) a0 = fma(v[k * R], S[k], a0);
     }
-    double acc = a0 + a1;
+    double acc = (a0 + a1) + (a2 + a3);
     for (int o = RP; o < 32; o <<= 1) acc += __shfl_xor_sync(FULL, acc, o);
     if (ph == 0 && i < R) {
       const int row = r0 + i;
@@ -653,7 +665,7 @@ __device__ __forceinline__ void run_row_blob(const int32_t* h, double* S, const 
 
 // ================================================ BLOB COL (big backward)
 // columns [k0, k0+c): x_j = sum_r M[k0+r, k0+j] v[r]; lanes = (column, row-phase)
-template <bool SPLIT>
+template <bool SPLIT, bool WIDE>
 __device__ __forceinline__ void run_col_blob(const int32_t* h, double* S, const DagArgs& A, const FactorDev& F,
                                              int lane, uint64_t* bar, uint32_t& phase) {
   const int s = h[CL_S], m = h[CL_M], k0 = h[CL_K0], c = h[CL_C];
@@ -689,17 +701,25 @@ __device__ __forceinline__ void run_col_blob(const int32_t* h, double* S, const 
   const int j = lane & (CP - 1), ph = lane / CP;
   for (int jb = 0; jb < c; jb += CP) {
     const int jj = jb + j;
-    double a0 = 0.0, a1 = 0.0;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     if (jj < c) {
       const double* v = V + jj;
       int r = ph;
-      for (; r + P < L; r += 2 * P) {
+      for (; WIDE && r + 3 * P < L; r += 4 * P) {
+        const double m0 = v[r * c], m1 = v[(r + P) * c], m2 = v[(r + 2 * P) * c], m3 = v[(r + 3 * P) * c];
+        const double f0 = Sv[r], f1 = Sv[r + P], f2 = Sv[r + 2 * P], f3 = Sv[r + 3 * P];
+        a0 = fma(m0, f0, a0);
+        a1 = fma(m1, f1, a1);
+        a2 = fma(m2, f2, a2);
+        a3 = fma(m3, f3, a3);
+      }
+      for (; !WIDE && r + P < L; r += 2 * P) {
         a0 = fma(v[r * c], Sv[r], a0);
         a1 = fma(v[(r + P) * c], Sv[r + P], a1);
       }
-      if (r < L) a0 = fma(v[r * c], Sv[r], a0);
+      for (; r < L; r += P) a0 = fma(v[r * c], Sv[r], a0);
     }
-    double acc = a0 + a1;
+    double acc = (a0 + a1) + (a2 + a3);
     for (int o = CP; o < 32; o <<= 1) acc += __shfl_xor_sync(FULL, acc, o);
     if (ph == 0 && jj < c) __stcg(xy + cols[jj], acc);
   }
@@ -1212,9 +1232,9 @@ __global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? SFCDD_R
     } else if (SPLIT && T.kind == TK_XB_BWD) {
       run_xb(h, A, F, lane);
     } else if (T.kind == TK_ROW_FWD && (!DIRECT || h[RW_INBLOB])) {
-      run_row_blob<SPLIT>(h, S, A, F, lane, bar, phase);
+      run_row_blob<SPLIT, WPB == 2>(h, S, A, F, lane, bar, phase);
     } else if (T.kind == TK_COL_BWD && (!DIRECT || h[CL_INBLOB])) {
-      run_col_blob<SPLIT>(h, S, A, F, lane, bar, phase);
+      run_col_blob<SPLIT, WPB == 2>(h, S, A, F, lane, bar, phase);
     } else if constexpr (DIRECT) {
       if (SPLIT && T.kind == TK_ROW_FWD && h[RW_NBLK] > 1)
         phase = run_mrow<16, WPB == 2>(h, S, A, A.blobs + T.blob_off, lane, bar, phase);
@@ -1233,7 +1253,7 @@ __global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? SFCDD_R
         break;
       case TK_ROW_FWD:
         if (!DIRECT || h[RW_INBLOB]) {
-          run_row_blob<SPLIT>(h, S, A, F, lane, bar, phase);
+          run_row_blob<SPLIT, WPB == 2>(h, S, A, F, lane, bar, phase);
           break;
         }
         [[fallthrough]];
@@ -1249,7 +1269,7 @@ __global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? SFCDD_R
           }
         }
         if (T.kind == TK_COL_BWD && (!DIRECT || h[CL_INBLOB])) {
-          run_col_blob<SPLIT>(h, S, A, F, lane, bar, phase);
+          run_col_blob<SPLIT, WPB == 2>(h, S, A, F, lane, bar, phase);
           break;
         }
         if constexpr (DIRECT) {  // ROW or COL block streamed from HBM
