@@ -574,6 +574,12 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
               break;
             }
           }
+          // not even one row next to its scratch: the separate budgets (the slot grows past slot_max)
+          if (R == 0 && slot_budget) {
+            const int32_t C = r0 < s ? r0 + 1 : s, NB = r0 < s ? 0 : 1;
+            const int64_t meta = inl ? RW_WORDS + C + (C + NB + 1) + row_nnz(r0, C, NB) : RW_WORDS;
+            if (blob_size(meta, (int64_t)C) <= opt.blob_max && C + NB + 2 <= opt.big_scratch_max) R = 1;
+          }
           if (R == 0) return false;
           out.emplace_back(r0, R);
           r0 += R;
@@ -744,7 +750,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         const int32_t asm_word = asm16 >= 0 ? RW_ASM16 : -1;
         int32_t bytes = 0;
         const int64_t off = E.emit(ints, RW_VAL_OFF, (int64_t)R * C, &vd, bytes, F, asm_word, direct_rows);
-        SFCDD_REQUIRE(bytes <= blob_cap(scr), SFCDD_EINTERNAL,
+        SFCDD_REQUIRE(bytes <= std::max<int64_t>(blob_cap(scr), opt.blob_max), SFCDD_EINTERNAL,
                       "ROW blob exceeds the slot (bytes " + std::to_string(bytes) + ", scratch " + std::to_string(scr) +
                           ", s " + std::to_string(s) + ", R " + std::to_string(R) + ", C " + std::to_string(C) +
                           (use_asm ? ", asm" : global_asm ? ", record" : ", inline") + (direct_rows ? ", direct)" : ", blob)"));
@@ -766,6 +772,8 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         const int32_t L = s + m - k0;
         int32_t c = std::min<int32_t>(opt.col_max, s - k0);
         while (c > 1 && blob_size(CL_WORDS + c + (inl ? m : 0), (int64_t)L * c) > blob_cap(L + 2)) --c;
+        // (c == 1 may exceed the slot cap and still fit blob_max: the slot then grows past slot_max,
+        // the separate-budget behaviour for a column whose gathered vector fills most of a slot)
         if (std::getenv("SFCDD_EVEN_COLS") && c > 1 && (c & 1) && k0 + c < s) --c;
         return c;
       };
@@ -841,7 +849,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
         vd.len = L;
         int32_t bytes = 0;
         const int64_t off = E.emit(ints, CL_VAL_OFF, (int64_t)L * c, &vd, bytes, F, -1, direct_cols);
-        SFCDD_REQUIRE(bytes <= blob_cap(scr), SFCDD_EINTERNAL,
+        SFCDD_REQUIRE(bytes <= std::max<int64_t>(blob_cap(scr), opt.blob_max), SFCDD_EINTERNAL,
                       "big supernode column does not fit a task blob (s+m = " + std::to_string(s + m) + ")");
         E.need_slot(bytes, scr);
         E.has_direct = E.has_direct || direct_cols;

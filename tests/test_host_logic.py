@@ -183,6 +183,28 @@ def test_default_plan_few_wide_subdomains(oracle, levels, p, gamma):
         off += r.length
 
 
+@pytest.mark.parametrize("levels,blob,slot", [((7, 7), 2048, 2816), ((8, 8), 4096, 5632)])
+def test_slot_budget_column_wider_than_the_slot_cap(oracle, levels, blob, slot, monkeypatch):
+    """Slot budget (one budget for blob + scratch): a COL / ROW task whose
+    gathered vector leaves less room than ONE column / row of values (but more
+    than half a blob, so the cap applies) falls back to the separate budgets
+    instead of failing with 'column does not fit a task blob' -- the C5-shaped
+    GPU test's failure mode (s + m = 1625 under 16 KB blobs), scaled to
+    2 / 4 KB blobs with the same slot : blob ratio."""
+    monkeypatch.setenv("SFCDD_SLOT_MAX", str(slot))
+    A = oracle.assemble_scaled_laplacian(levels)
+    n = A.shape[0]
+    ov = oracle.enlarge(oracle.disjoint_partition(n, 2), 0.5)
+    rhs = np.random.default_rng(1).standard_normal(n)
+    xy, _ = host_plan_solve(A, ov, rhs, blob_max=blob)
+    off = 0
+    for r in ov:
+        idx = r.indices()
+        xr = spla.spsolve(A[idx][:, idx].tocsc(), rhs[idx])
+        assert np.linalg.norm(xy[off:off + r.length] - xr) <= 1e-11 * np.linalg.norm(xr)
+        off += r.length
+
+
 # ---- partition mirror: known answers of the reference tests (test_partition.py:24-116)
 def test_partition_known_answers():
     assert [r.length for r in pt.disjoint_partition(9, 2)] == [5, 4]
