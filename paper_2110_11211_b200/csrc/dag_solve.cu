@@ -232,9 +232,10 @@ __device__ __forceinline__ int hi16(int32_t v) { return (int)((uint32_t)v >> 16)
 
 // Gather n values with all of a lane's global loads in flight before any
 // store (8 per lane per round): one memory latency instead of one per element.
-template <typename Load, typename Store>
+// (RB = 16 in the 128-register 2-worker kernel -- one round for the ~360 values a 3-D fragment
+// gathers -- measured slower: C3 k_dag 1.79 -> 1.90 ms, C5 27.7 -> 30.5 ms)
+template <int RB = 8, typename Load, typename Store>
 __device__ __forceinline__ void warp_gather(int n, int lane, Load ld, Store st) {
-  constexpr int RB = 8;
   for (int base = 0; base < n; base += RB * 32) {
     double v[RB];
 #pragma unroll
@@ -398,7 +399,7 @@ __device__ __forceinline__ void bwd_lanes(const int4* recs, const double* vals, 
   if (act && (local & (P - 1)) == 0) S[R.w + k] = acc;
 }
 
-template <typename Ahead>
+template <int RB, typename Ahead>
 __device__ __forceinline__ void run_frag(const int32_t* h, bool fwd, double* S, const DagArgs& A, const FactorDev& F,
                                          int lane, unsigned long long* pt, Ahead ahead) {
   auto stamp = [&](int i) {
@@ -424,7 +425,7 @@ __device__ __forceinline__ void run_frag(const int32_t* h, bool fwd, double* S, 
     {  // one batched gather: right-hand side at the columns + external child updates
       const int32_t* eu = h + h[H_EXTU];
       const int nu = h[H_NEXTU], ub = h[H_EXTU_BASE];
-      warp_gather(
+      warp_gather<RB>(
           ncol + nu, lane,
           [&](int c) { return c < ncol ? __ldg(A.rhs + gidx(F, cols[c])) : __ldcg(A.upd + eu[c - ncol]); },
           [&](int c, double v) { S[c < ncol ? lo16(colpos[c]) : ub + (c - ncol)] = v; });
@@ -478,7 +479,7 @@ __device__ __forceinline__ void run_frag(const int32_t* h, bool fwd, double* S, 
     {  // one batched gather: y at the columns + x of the external ancestor rows
       const int32_t* ex = h + h[H_EXTX];
       const int nx = h[H_NEXTX], xb = h[H_EXTX_BASE];
-      warp_gather(ncol + nx, lane, [&](int c) { return __ldcg(xy + (c < ncol ? cols[c] : ex[c - ncol])); },
+      warp_gather<RB>(ncol + nx, lane, [&](int c) { return __ldcg(xy + (c < ncol ? cols[c] : ex[c - ncol])); },
                   [&](int c, double v) { S[c < ncol ? lo16(colpos[c]) : xb + (c - ncol)] = v; });
     }
     __syncwarp();
@@ -566,7 +567,8 @@ __device__ __noinline__ void run_xb(const int32_t* h, const DagArgs& A, const Fa
 // when R < 32; the assembled front f = [f_J ; f_B] is read contiguously (ASM tasks)
 template <bool SPLIT, bool WIDE>
 __device__ __forceinline__ void run_row_blob(const int32_t* h, double* S, const DagArgs& A, const FactorDev& F,
-                                             int lane, uint64_t* bar, uint32_t& phase) {
+                                             int lane, uint64_t* bar, uint32_t& phase, unsigned long long* pt) {
+  if (pt && lane == 0) pt[0] = clock64();  // trace stamps: start, front in the slot, products done, stored
   const int s = h[RW_S], R = h[RW_R], C = h[RW_C], r0 = h[RW_R0], NB = h[RW_NB];
   const double* V = reinterpret_cast<const double*>(reinterpret_cast<const uint8_t*>(h) + h[RW_VAL_OFF]);
   int boff = C;  // S index of the first update-row value f_B[r0 - s + i]
@@ -605,23 +607,44 @@ __device__ __forceinline__ void run_row_blob(const int32_t* h, double* S, const 
   } else {
     // f = base + child updates in fixed order (base 0 for update rows); the
     // metadata is in the slot, so every load below is one global round trip
+    // U front positions per lane, their right-hand side and first three update
+    // loads all in flight (nearly every position has <= 3 contributions): one
+    // global round trip per batch instead of one per pair of contributions
+    // (traced on C3: the gather was half of a ROW task); same summation order
     const int32_t* cols = h + h[RW_COLS];
     const int32_t* ptr = h + h[RW_PTR];
     const int32_t* src = h + h[RW_SRC];
-    for (int q = lane; q < C + NB; q += 32) {
-      const int e0 = ptr[q], e1 = ptr[q + 1];
-      double acc = q < C ? __ldg(A.rhs + gidx(F, cols[q])) : 0.0;
-      int e = e0;
-      for (; e + 2 <= e1; e += 2) {
-        const double u0 = __ldcg(A.upd + src[e]), u1 = __ldcg(A.upd + src[e + 1]);
-        acc += u0;
-        acc += u1;
+    constexpr int U = WIDE ? 4 : 2;
+    for (int base = 0; base < C + NB; base += 32 * U) {
+      int e0[U], cn[U];
+      double acc[U], v0[U], v1[U], v2[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int q = base + lane + 32 * u;
+        const bool ok = q < C + NB;
+        e0[u] = ok ? ptr[q] : 0;
+        cn[u] = ok ? ptr[q + 1] - e0[u] : 0;
+        acc[u] = (ok && q < C) ? __ldg(A.rhs + gidx(F, cols[q])) : 0.0;
+        v0[u] = cn[u] > 0 ? __ldcg(A.upd + src[e0[u]]) : 0.0;
+        v1[u] = cn[u] > 1 ? __ldcg(A.upd + src[e0[u] + 1]) : 0.0;
+        v2[u] = cn[u] > 2 ? __ldcg(A.upd + src[e0[u] + 2]) : 0.0;
       }
-      if (e < e1) acc += __ldcg(A.upd + src[e]);
-      S[q] = acc;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int q = base + lane + 32 * u;
+        if (q >= C + NB) continue;
+        double a = acc[u];
+        if (cn[u] > 0) a += v0[u];
+        if (cn[u] > 1) a += v1[u];
+        if (cn[u] > 2) a += v2[u];
+        for (int e = e0[u] + 3; e < e0[u] + cn[u]; ++e) a += __ldcg(A.upd + src[e]);
+        S[q] = a;
+      }
     }
   }
   __syncwarp();
+  if (pt && lane == 0) pt[1] = clock64();
+  // (per-pass lane phases for a ragged last pass -- 40 rows as 32 + 8 x 4 phases -- measured slower: C3 +1.3 %)
   const int RP = R >= 32 ? 32 : (R <= 1 ? 1 : 1 << (32 - __clz(R - 1)));  // lanes per phase
   const int P = 32 / RP;
   const int il = lane & (RP - 1), ph = lane / RP;
@@ -660,6 +683,10 @@ __device__ __forceinline__ void run_row_blob(const int32_t* h, double* S, const 
       else
         __stcg(uo + (row - s), S[boff + i] - acc);
     }
+  }
+  if (pt && lane == 0) {
+    pt[2] = clock64();
+    pt[15] = 100 + R;  // (marks a ROW record for tools/analyze_trace.py)
   }
 }
 
@@ -810,6 +837,92 @@ __device__ __forceinline__ double dense_dot(const double* __restrict__ V, bool r
   return acc;
 }
 
+// The same dot product with the VALUES travelling through a ring of VST
+// shared-memory stages filled by bulk copies (one mbarrier per stage): up to
+// VST * 4 KB of a task's value stream in flight instead of the DU loads per
+// lane of dense_dot (4 KB per warp, one memory latency per group), and no
+// registers held by loads in flight.  Used where the slot has room for >= 2
+// stages behind the task's scratch (wide slots of the 2-worker kernel); the
+// stage area is free shared memory of the slot, the planner reserves nothing.
+// A stage holds kc = min(RING_CHUNK, 512 / WP) vector entries (kc W values,
+// <= 4 KB; kc divides RING_CHUNK, so a stage never straddles a vector chunk).
+constexpr int VST = 4;             // value stages per worker (mbarriers)
+constexpr int VSTAGE_DOUBLES = 512;
+
+__device__ __forceinline__ double dense_dot_tma(const double* __restrict__ V, bool ring, int W, int Len, double* S,
+                                                const double* gvec, int sh, uint64_t* bar, uint32_t& phase,
+                                                uint64_t* vbar, uint32_t& vph, double* stage, int nst, int lane) {
+  const int WP = W >= 32 ? 32 : (W <= 1 ? 1 : 1 << (32 - __clz(W - 1)));  // lanes per phase
+  const int P = 32 / WP;
+  const int ph = lane / WP;
+  const int il = min(lane & (WP - 1), W - 1);  // lanes >= W repeat the last one (result unused)
+  const int kc = min(RING_CHUNK, VSTAGE_DOUBLES / WP);
+  const int nch = (Len + kc - 1) / kc;
+  const uint64_t pol = policy_evict_first();
+  // every lane has observed the barrier phase of the task's blob copy before
+  // the barrier is armed again, and is done with the slot's previous contents
+  __syncwarp();
+  auto issue = [&](int c, int st) {  // lane 0: values of vector entries [c kc, (c + 1) kc) -> stage st
+    const int k0 = c * kc, nk = min(kc, Len - k0);
+    const uint32_t nb = (uint32_t)((8 * nk * W + 15) & ~15);
+    mbar_expect_tx(vbar + st, nb);
+    bulk_g2s_hint(stage + st * VSTAGE_DOUBLES, V + (size_t)k0 * W, nb, vbar + st, pol);
+  };
+  if (lane == 0) {
+    fence_proxy_async();  // earlier generic accesses of the ring slots / stages -> async writes
+    if (ring) {
+      fence_proxy_async_global();  // the producers' generic-proxy writes -> this bulk read
+      const uint32_t nb = bytes16(min(RING_CHUNK, Len) + sh);
+      mbar_expect_tx(bar, nb);
+      bulk_g2s(S, gvec, nb, bar);
+    }
+    for (int c = 0; c < nst && c < nch; ++c) issue(c, c);
+  }
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int st = 0;
+  for (int c = 0; c < nch; ++c) {
+    const int k0 = c * kc, nk = min(kc, Len - k0);
+    const int rc = k0 / RING_CHUNK;
+    if (ring && k0 == rc * RING_CHUNK) {
+      mbar_wait_guard(bar, phase);
+      phase ^= 1u;
+      // every lane has consumed vector chunk rc - 1 (its slot may be refilled)
+      // and has observed chunk rc's phase (the barrier may be armed again)
+      __syncwarp();
+      if (lane == 0 && RING_CHUNK * (rc + 1) < Len) {
+        fence_proxy_async();
+        const uint32_t nb = bytes16(min(RING_CHUNK, Len - RING_CHUNK * (rc + 1)) + sh);
+        mbar_expect_tx(bar, nb);
+        bulk_g2s(S + ((rc + 1) & 1) * RING_STRIDE, gvec + RING_CHUNK * (rc + 1), nb, bar);
+      }
+    }
+    const double* vec = ring ? S + (rc & 1) * RING_STRIDE + sh + (k0 - rc * RING_CHUNK) : S + k0;
+    mbar_wait_guard(vbar + st, (vph >> st) & 1u);
+    vph ^= 1u << st;
+    const double* v = stage + st * VSTAGE_DOUBLES + il;
+    int k = ph;
+    for (; k + 3 * P < nk; k += 4 * P) {
+      const double m0 = v[k * W], m1 = v[(k + P) * W], m2 = v[(k + 2 * P) * W], m3 = v[(k + 3 * P) * W];
+      const double f0 = vec[k], f1 = vec[k + P], f2 = vec[k + 2 * P], f3 = vec[k + 3 * P];
+      a0 = fma(m0, f0, a0);
+      a1 = fma(m1, f1, a1);
+      a2 = fma(m2, f2, a2);
+      a3 = fma(m3, f3, a3);
+    }
+    for (; k < nk; k += P) a0 = fma(v[k * W], vec[k], a0);
+    // every lane is done with stage st and has observed its phase: refill it
+    __syncwarp();
+    if (lane == 0 && c + nst < nch) {
+      fence_proxy_async();
+      issue(c + nst, st);
+    }
+    st = st + 1 == nst ? 0 : st + 1;
+  }
+  double acc = (a0 + a1) + (a2 + a3);
+  for (int o = WP; o < 32; o <<= 1) acc += __shfl_xor_sync(FULL, acc, o);
+  return acc;
+}
+
 // MROW (plan.h): update rows [r0, r0 + rows) of a narrow supernode (C = s <=
 // RING_CHUNK) as ONE value stream of nb blocks of Rb rows; lanes = rows of the
 // block, f_J and the task's f_B rows sit in the two ring slots (one bulk-copy
@@ -899,7 +1012,7 @@ __device__ __forceinline__ uint32_t run_mrow(const int32_t* h, double* S, const 
 template <bool SPLIT, int DU>
 __device__ __forceinline__ uint32_t run_dense(bool is_row, const int32_t* h, double* S, const DagArgs& A,
                                               const FactorDev& F, const uint8_t* gblob, int lane, uint64_t* bar,
-                                              uint32_t phase) {
+                                              uint32_t phase, uint64_t* vbar, uint32_t& vph, const uint8_t* slot_end) {
   double* xy = A.xy + F.xy_off;
   const double* V;
   const double* gvec = nullptr;
@@ -962,7 +1075,14 @@ __device__ __forceinline__ uint32_t run_dense(bool is_row, const int32_t* h, dou
       __syncwarp();
     }
   }
-  const double acc = dense_dot<DU>(V, SPLIT && ring, W, Len, S, gvec, sh, bar, phase, lane);
+  // value stages behind the task's scratch, if the slot has room for two or more (and the block is
+  // worth a pipeline: at least two stages of values)
+  double* stage = reinterpret_cast<double*>(
+      (reinterpret_cast<uintptr_t>(S + (is_row ? h[RW_SCRATCH] : h[CL_SCRATCH])) + 127) & ~(uintptr_t)127);
+  const int nst = min(VST, (int)((slot_end - reinterpret_cast<const uint8_t*>(stage)) / (8 * VSTAGE_DOUBLES)));
+  const bool staged = !(A.mode & 128) && nst >= 2 && (int64_t)W * Len >= 2 * VSTAGE_DOUBLES;
+  const double acc = staged ? dense_dot_tma(V, SPLIT && ring, W, Len, S, gvec, sh, bar, phase, vbar, vph, stage, nst, lane)
+                            : dense_dot<DU>(V, SPLIT && ring, W, Len, S, gvec, sh, bar, phase, lane);
   // after the butterfly every phase holds the sum: lane i (< W <= lanes per phase) owns row / column i
   if (lane < W) {
     if (is_row) {
@@ -1041,6 +1161,7 @@ __global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? SFCDD_R
   constexpr int DU = 16;  // (32 with 128 registers measured no better)
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bars[WPB];
+  __shared__ __align__(8) uint64_t vbars[DIRECT ? WPB * VST : 1];  // value-stage barriers of the DIRECT blocks
   __shared__ int32_t mbox[WPB];
   __shared__ int32_t nexit;
   __shared__ __align__(8) uint64_t sigbar;
@@ -1060,10 +1181,13 @@ __global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? SFCDD_R
   uint64_t* bar = &bars[warp];
   if (lane == 0) {
     mbar_init(bar, 1);
+    if (DIRECT)
+      for (int i = 0; i < VST; ++i) mbar_init(&vbars[warp * VST + i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
   uint32_t phase = 0;
+  uint32_t vph = 0;  // parity of each value-stage barrier's next phase (bit i: stage i)
   // queue of this warp (interleaved split of the global order: spreads the
   // claim atomics over nq lines; deadlock-free, the smallest unfinished task
   // is always claimable)
@@ -1222,38 +1346,40 @@ __global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? SFCDD_R
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.blobs + pf_off), "r"(pf_bytes) : "memory");
 #if !(SFCDD_LEAN & 32)  // (the if-chain measured 3 % faster than the switch below on C2: code layout)
     if ((SFCDD_LEAN & 4) && T.kind == TK_FRAG_FWD) {
-      run_frag(h, true, S, A, F, lane, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);
+      run_frag<8>(h, true, S, A, F, lane, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);
     } else if ((SFCDD_LEAN & 4) && T.kind == TK_FRAG_BWD) {
-      run_frag(h, false, S, A, F, lane, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);
+      run_frag<8>(h, false, S, A, F, lane, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);
     } else if (T.kind == TK_FRAG_FWD || T.kind == TK_FRAG_BWD) {
-      run_frag(h, T.kind == TK_FRAG_FWD, S, A, F, lane, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);
+      run_frag<8>(h, T.kind == TK_FRAG_FWD, S, A, F, lane, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);
     } else if (SPLIT && T.kind == TK_ASM_FWD) {
       run_asm(h, A, F, lane);
     } else if (SPLIT && T.kind == TK_XB_BWD) {
       run_xb(h, A, F, lane);
     } else if (T.kind == TK_ROW_FWD && (!DIRECT || h[RW_INBLOB])) {
-      run_row_blob<SPLIT, WPB == 2>(h, S, A, F, lane, bar, phase);
+      run_row_blob<SPLIT, WPB == 2>(h, S, A, F, lane, bar, phase, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr);
     } else if (T.kind == TK_COL_BWD && (!DIRECT || h[CL_INBLOB])) {
       run_col_blob<SPLIT, WPB == 2>(h, S, A, F, lane, bar, phase);
     } else if constexpr (DIRECT) {
       if (SPLIT && T.kind == TK_ROW_FWD && h[RW_NBLK] > 1)
         phase = run_mrow<16, WPB == 2>(h, S, A, A.blobs + T.blob_off, lane, bar, phase);
       else
-        phase = run_dense<SPLIT, DU>(T.kind == TK_ROW_FWD, h, S, A, F, A.blobs + T.blob_off, lane, bar, phase);
+        phase = run_dense<SPLIT, DU>(T.kind == TK_ROW_FWD, h, S, A, F, A.blobs + T.blob_off, lane, bar, phase,
+                                     &vbars[DIRECT ? warp * VST : 0], vph,
+                                     smem + (size_t)(warp + 1) * A.slot_bytes);
     } else {
       __trap();  // a DIRECT block in a plan built without them
     }
 #else
     switch (T.kind) {
       case TK_FRAG_FWD:
-        run_frag(h, true, S, A, F, lane, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);
+        run_frag<8>(h, true, S, A, F, lane, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);
         break;
       case TK_FRAG_BWD:
-        run_frag(h, false, S, A, F, lane, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);
+        run_frag<8>(h, false, S, A, F, lane, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);
         break;
       case TK_ROW_FWD:
         if (!DIRECT || h[RW_INBLOB]) {
-          run_row_blob<SPLIT, WPB == 2>(h, S, A, F, lane, bar, phase);
+          run_row_blob<SPLIT, WPB == 2>(h, S, A, F, lane, bar, phase, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr);
           break;
         }
         [[fallthrough]];
@@ -1276,7 +1402,9 @@ __global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? SFCDD_R
           if (SPLIT && T.kind == TK_ROW_FWD && h[RW_NBLK] > 1)
             phase = run_mrow<16, WPB == 2>(h, S, A, A.blobs + T.blob_off, lane, bar, phase);
           else
-            phase = run_dense<SPLIT, DU>(T.kind == TK_ROW_FWD, h, S, A, F, A.blobs + T.blob_off, lane, bar, phase);
+            phase = run_dense<SPLIT, DU>(T.kind == TK_ROW_FWD, h, S, A, F, A.blobs + T.blob_off, lane, bar, phase,
+                                     &vbars[DIRECT ? warp * VST : 0], vph,
+                                     smem + (size_t)(warp + 1) * A.slot_bytes);
         }
         break;
     }
@@ -1385,7 +1513,7 @@ DagSolver::DagSolver(const DevicePlan& plan, int device, int64_t extra_xy) : dev
   smem_ = wpb_ * slot_bytes_;
   SFCDD_REQUIRE(smem_ <= 227 * 1024, SFCDD_EINTERNAL, "DAG shared-memory footprint exceeds 227 KB");
   auto up = [&](void** dst, const void* src, size_t bytes) {
-    CUDA_CHECK(cudaMalloc(dst, std::max<size_t>(bytes, 16)));
+    CUDA_CHECK(cudaMalloc(dst, std::max<size_t>(bytes, 16) + 16));  // (+16: 16-byte rounded tails of bulk copies)
     if (bytes) CUDA_CHECK(cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice));
     bytes_ += std::max<size_t>(bytes, 16);
   };
@@ -1394,7 +1522,7 @@ DagSolver::DagSolver(const DevicePlan& plan, int device, int64_t extra_xy) : dev
     up((void**)&blobs_, plan.blobs.data(), plan.blobs.size());
   } else {
     // metadata now (staged image + segment scatter), values later (place_values)
-    CUDA_CHECK(cudaMalloc(&blobs_, std::max<int64_t>(plan.blob_bytes, 16)));
+    CUDA_CHECK(cudaMalloc(&blobs_, std::max<int64_t>(plan.blob_bytes, 16) + 16));  // (+16: a value stage's 16-byte rounded tail)
     bytes_ += std::max<int64_t>(plan.blob_bytes, 16);
     CUDA_CHECK(cudaMemset(blobs_, 0, std::max<int64_t>(plan.blob_bytes, 16)));
     uint8_t* img = nullptr;

@@ -2124,7 +2124,8 @@ extern "C" int sfcdd_op_trace(sfcdd_op* op, const double* g_dev, uint64_t* out_h
     for (int j = 12; j < 24; ++j) out_host[24 * t + j] = 0;
     // FRAG forward phase stamps (clock64): [0] start [1] prologue done
     // [2+2l, 3+2l] level l assembly / rows done (l < 4) [10] end [11] nlev
-    if (T.kind == TK_FRAG_FWD || T.kind == TK_FRAG_BWD)
+    // (BLOB ROW tasks: [0] start [1] front in the slot [2] products + stores issued [11] 100 + rows)
+    if (T.kind == TK_FRAG_FWD || T.kind == TK_FRAG_BWD || T.kind == TK_ROW_FWD)
       for (int j = 0; j < 12; ++j) out_host[24 * t + 12 + j] = h[5 * nt + 16 * t + (j < 10 ? j : j + 4)];
   }
   SFCDD_API_END

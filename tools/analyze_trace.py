@@ -54,3 +54,11 @@ if wid.max() > 0:
     print("per-worker gap between tasks: mean %.2f us, median %.2f us, p90 %.2f us" % (gap.mean()/1e3, np.median(gap)/1e3, np.percentile(gap, 90)/1e3))
     busy = (tend - t0).sum(); span = (tend.max() - t0.min()) * (wid.max() + 1)
     print("worker time in tasks %.1f%%, in gaps %.1f%%" % (100*busy/span, 100*gap.sum()/span))
+
+# BLOB ROW phase stamps (clock64): [0] start [1] front vector in the slot [2] products + stores issued
+m = (T[:, 5] == 2) & (T[:, 12] > 0) & (T[:, 14] > 0)
+if m.any():
+    Pp = T[m][:, 12:24]
+    tot_ns = (T[m][:, 4] - T[m][:, 3])
+    print(f"row (blob): {m.sum()} tasks, data->end {tot_ns.mean()/1e3:.2f} us; front gather {np.mean(Pp[:,1]-Pp[:,0]):.0f} cycles, "
+          f"products + stores {np.mean(Pp[:,2]-Pp[:,1]):.0f} cycles, mean rows {np.mean(Pp[:,11]-100):.1f}")

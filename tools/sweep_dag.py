@@ -19,8 +19,8 @@ import paper_2110_11211_b200 as sf  # noqa: E402
 from paper_2110_11211_b200 import _lib  # noqa: E402
 
 CFG = {"c1": ((7, 7), 16, 0.5, 4), "c2": ((10, 10), 64, 0.5, 16), "c3": ((7, 7, 7), 512, 0.5, 8),
-       "c4": ((12, 12), 256, 0.5, 16)}
-KEYS = {"WPB": "SFCDD_WPB", "BLOB": "SFCDD_BLOB_MAX", "SCR": "SFCDD_SCRATCH_MAX", "MODE": "SFCDD_DAG_MODE", "Q": "SFCDD_QUEUES", "W": "SFCDD_WORKERS", "ROW": "SFCDD_ROW_MAX", "COL": "SFCDD_COL_MAX", "ORD": "SFCDD_ORDER", "LEAF": "SFCDD_ND_LEAF", "SIG": "SFCDD_SIG_NS", "CTAS": "SFCDD_CTAS_PER_SM", "RS": "SFCDD_RELAX_SMALL", "RSF": "SFCDD_RELAX_SMALL_FRAC", "RF": "SFCDD_RELAX_FRAC", "SLACK": "SFCDD_SLACK_US", "AR": "SFCDD_ASM_RED", "XM": "SFCDD_XB_MIN", "PF": "SFCDD_PF_DIST", "SLOT": "SFCDD_SLOT_MAX", "SPLIT": "SFCDD_SPLIT_MIN"}
+       "c4": ((12, 12), 256, 0.5, 16), "c5": ((8, 8, 8), 512, 0.5, 64)}
+KEYS = {"WPB": "SFCDD_WPB", "BLOB": "SFCDD_BLOB_MAX", "SCR": "SFCDD_SCRATCH_MAX", "MODE": "SFCDD_DAG_MODE", "Q": "SFCDD_QUEUES", "W": "SFCDD_WORKERS", "ROW": "SFCDD_ROW_MAX", "COL": "SFCDD_COL_MAX", "ORD": "SFCDD_ORDER", "LEAF": "SFCDD_ND_LEAF", "SIG": "SFCDD_SIG_NS", "CTAS": "SFCDD_CTAS_PER_SM", "RS": "SFCDD_RELAX_SMALL", "RSF": "SFCDD_RELAX_SMALL_FRAC", "RF": "SFCDD_RELAX_FRAC", "SLACK": "SFCDD_SLACK_US", "AR": "SFCDD_ASM_RED", "XM": "SFCDD_XB_MIN", "PF": "SFCDD_PF_DIST", "SLOT": "SFCDD_SLOT_MAX", "DR": "SFCDD_DIRECT_ROWS", "DC": "SFCDD_DIRECT_COLS", "SPLIT": "SFCDD_SPLIT_MIN"}
 name = sys.argv[1]
 levels, p, gamma, q = CFG[name]
 A = sf.assemble_laplacian(levels)
