@@ -1510,6 +1510,9 @@ DagSolver::DagSolver(const DevicePlan& plan, int device, int64_t extra_xy) : dev
   if (const char* e = std::getenv("SFCDD_SIG_NS")) sig_ns_ = std::atoi(e);
   if (const char* e = std::getenv("SFCDD_SIG_WAIT_NS")) sig_wait_ns_ = std::atoi(e);
   if (const char* e = std::getenv("SFCDD_PF_DIST")) pf_dist_ = std::max(0, std::atoi(e));
+  for (const FactorDev& F : plan.factors) rhs_doubles_ = std::max<int64_t>(rhs_doubles_, F.gmod);
+  if (const char* e = std::getenv("SFCDD_L2_PERSIST")) l2_persist_ = std::atoi(e);
+  if (l2_persist_) CUDA_CHECK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 48u << 20));
   smem_ = wpb_ * slot_bytes_;
   SFCDD_REQUIRE(smem_ <= 227 * 1024, SFCDD_EINTERNAL, "DAG shared-memory footprint exceeds 227 KB");
   auto up = [&](void** dst, const void* src, size_t bytes) {
@@ -1624,10 +1627,25 @@ void DagSolver::solve(const double* rhs, cudaStream_t st, const int32_t* skip) {
   a.watchdog_ns = 1000000ull * (unsigned long long)watchdog_ms_;
   a.pf_dist = pf_dist_;
   void* params[] = {&a};
+  if (l2_persist_) {  // experiment: keep the gathered vector resident in L2 while the blobs stream through
+    cudaStreamAttrValue av{};
+    av.accessPolicyWindow.base_ptr = l2_persist_ == 2 ? (void*)xy_ : (void*)rhs;
+    av.accessPolicyWindow.num_bytes =
+        (size_t)std::min<int64_t>(8 * (l2_persist_ == 2 ? xy_doubles_ : rhs_doubles_), 32ll << 20);
+    av.accessPolicyWindow.hitRatio = 1.0f;
+    av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    CUDA_CHECK(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &av));
+  }
   if (mode_ & 16)  // static worker lists need every CTA resident: cooperative launch guarantees it (or fails)
     CUDA_CHECK(cudaLaunchCooperativeKernel(kern_, dim3(grid_), dim3((wpb_ + 1) * 32), params, smem_, st));
   else
     CUDA_CHECK(cudaLaunchKernel(kern_, dim3(grid_), dim3((wpb_ + 1) * 32), params, smem_, st));
+  if (l2_persist_) {
+    cudaStreamAttrValue av{};
+    av.accessPolicyWindow.num_bytes = 0;
+    CUDA_CHECK(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &av));
+  }
   if (mode_ & 32) {  // diagnostic mode (not capturable): report a stuck dependency wait
     int32_t d[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     CUDA_CHECK(cudaMemcpyAsync(d, a.diag, sizeof(d), cudaMemcpyDeviceToHost, st));
