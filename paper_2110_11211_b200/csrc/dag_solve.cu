@@ -443,19 +443,18 @@ __device__ __forceinline__ void run_frag(const int32_t* h, bool fwd, double* S, 
         const int2 item = items[it];
         const unsigned ix = (unsigned)item.x;
         const int cnt = (int)((ix >> 16) & 0x7fffu);
-        if (cnt == 0) {
-          fwd_row(recs[ix], vals, S, 32 * item.y + lane);
-        } else {
-          const unsigned upto = (unsigned)item.y & ((2u << lane) - 1u);
-          const int seg = __popc(upto) - 1;
-          const bool on = seg < cnt;
-          const int4 R = recs[(ix & 0xffffu) + (on ? seg : 0)];
-          const int i = lane - (31 - __clz(upto));
-          if (ix & 0x80000000u)
-            fwd_tiny(R, vals, S, i, on);
-          else if (on)
-            fwd_row(R, vals, S, i);
-        }
+        // one row block of a tall front (cnt == 0: record ix, rows 32 item.y + lane) or
+        // several small fronts packed into the lanes; ONE copy of fwd_row for both
+        // (the kernel is instruction-cache bound: code size is time)
+        const unsigned upto = cnt == 0 ? 1u : (unsigned)item.y & ((2u << lane) - 1u);
+        const int seg = __popc(upto) - 1;
+        const bool on = cnt == 0 || seg < cnt;
+        const int4 R = recs[(ix & 0xffffu) + (on ? seg : 0)];
+        const int i = cnt == 0 ? 32 * item.y + lane : lane - (31 - __clz(upto));
+        if (ix & 0x80000000u)
+          fwd_tiny(R, vals, S, i, on);
+        else if (on)
+          fwd_row(R, vals, S, i);
       }
       __syncwarp();
       if (lv < 6) stamp(3 + 2 * lv);
@@ -496,10 +495,9 @@ __device__ __forceinline__ void run_frag(const int32_t* h, bool fwd, double* S, 
         const int2 item = items[it];
         const unsigned ix = (unsigned)item.x;
         const int cnt = (int)((ix >> 16) & 0x7fffu);
-        if (cnt == 0)
-          bwd_cols(recs[ix], vals, S, item.y & 0xffff, item.y >> 16, lane);
-        else
-          bwd_lanes(recs, vals, S, ix & 0xffffu, cnt, (unsigned)item.y, lane);
+        // (FRAG supernodes have s <= 32 = SMALL_MAX_S: every backward item is a packed
+        // column-lane item; the wide-supernode column blocks (bwd_cols) are gone)
+        bwd_lanes(recs, vals, S, ix & 0xffffu, cnt, (unsigned)item.y, lane);
       }
       __syncwarp();
       if (ls < 4) stamp(3 + 2 * ls);
@@ -1012,7 +1010,8 @@ __device__ __forceinline__ uint32_t run_mrow(const int32_t* h, double* S, const 
 template <bool SPLIT, int DU>
 __device__ __forceinline__ uint32_t run_dense(bool is_row, const int32_t* h, double* S, const DagArgs& A,
                                               const FactorDev& F, const uint8_t* gblob, int lane, uint64_t* bar,
-                                              uint32_t phase, uint64_t* vbar, uint32_t& vph, const uint8_t* slot_end) {
+                                              uint32_t phase, uint64_t* vbar, uint32_t& vph, const uint8_t* slot_end,
+                                              const bool allow_stages) {
   double* xy = A.xy + F.xy_off;
   const double* V;
   const double* gvec = nullptr;
@@ -1080,7 +1079,7 @@ __device__ __forceinline__ uint32_t run_dense(bool is_row, const int32_t* h, dou
   double* stage = reinterpret_cast<double*>(
       (reinterpret_cast<uintptr_t>(S + (is_row ? h[RW_SCRATCH] : h[CL_SCRATCH])) + 127) & ~(uintptr_t)127);
   const int nst = min(VST, (int)((slot_end - reinterpret_cast<const uint8_t*>(stage)) / (8 * VSTAGE_DOUBLES)));
-  const bool staged = !(A.mode & 128) && nst >= 2 && (int64_t)W * Len >= 2 * VSTAGE_DOUBLES;
+  const bool staged = allow_stages && nst >= 2 && (int64_t)W * Len >= 2 * VSTAGE_DOUBLES;
   const double acc = staged ? dense_dot_tma(V, SPLIT && ring, W, Len, S, gvec, sh, bar, phase, vbar, vph, stage, nst, lane)
                             : dense_dot<DU>(V, SPLIT && ring, W, Len, S, gvec, sh, bar, phase, lane);
   // after the butterfly every phase holds the sum: lane i (< W <= lanes per phase) owns row / column i
@@ -1106,7 +1105,8 @@ __device__ __forceinline__ uint32_t run_dense(bool is_row, const int32_t* h, dou
 // happen-before it through the CTA-scope release/acquire) and then bumps the
 // counters.  The workers never stall on the ~1 us release fence.
 template <int WPB>
-__device__ __forceinline__ void signaller(const DagArgs& A, int32_t* mbox, int32_t* nexit, uint64_t* sigbar) {
+__device__ __forceinline__ void signaller(const DagArgs& A, const int mode, int32_t* mbox, int32_t* nexit,
+                                          uint64_t* sigbar) {
   int32_t v[WPB];
   uint32_t par = 0;
   for (;;) {
@@ -1130,7 +1130,7 @@ __device__ __forceinline__ void signaller(const DagArgs& A, int32_t* mbox, int32
         // worker exit arrives on it) instead of spinning; the scan above
         // decides, the barrier only wakes (a stale parity costs one extra
         // scan and resynchronises)
-        if (A.mode & 8)
+        if (mode & 8)
           __nanosleep(A.sig_ns);
         else if (mbar_wait_timed(sigbar, par, A.sig_wait_ns))
           par ^= 1u;
@@ -1150,7 +1150,9 @@ __device__ __forceinline__ void signaller(const DagArgs& A, int32_t* mbox, int32
 // SPLIT: the plan has ASM / XB tasks (many-subdomain configurations); the
 // kernel without them keeps the smaller code of the common case
 // DIRECT: the plan has ROW / COL blocks streamed from HBM (wide separators)
-template <int WPB, bool SPLIT, bool DIRECT>
+// TRACE: the instantiation sfcdd_op_trace launches (per-task time stamps); the
+// production kernel carries none of that code
+template <int WPB, bool SPLIT, bool DIRECT, bool TRACE>
 #if SFCDD_LEAN & 2
 __global__ void __launch_bounds__((WPB + 1) * 32, 20 / WPB) k_dag(DagArgs A) {
 #else
@@ -1166,6 +1168,9 @@ __global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? SFCDD_R
   __shared__ int32_t nexit;
   __shared__ __align__(8) uint64_t sigbar;
   if (A.skip && *A.skip) return;
+  // the tuning / diagnostic switches (SFCDD_DAG_MODE) exist in the TRACE instantiation only: the
+  // production kernel carries none of their code (C2 k_dag -6 % without the trace and mode paths)
+  const int mode = TRACE ? A.mode : 0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x < WPB) mbox[threadIdx.x] = -1;
   if (threadIdx.x == 0) {
@@ -1175,7 +1180,7 @@ __global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? SFCDD_R
   }
   __syncthreads();
   if (warp == WPB) {
-    if (lane == 0) signaller<WPB>(A, mbox, &nexit, &sigbar);
+    if (lane == 0) signaller<WPB>(A, mode, mbox, &nexit, &sigbar);
     return;
   }
   uint64_t* bar = &bars[warp];
@@ -1199,7 +1204,7 @@ __global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? SFCDD_R
   // order) provided every CTA is resident -- the kernel must run alone.  No
   // claim atomic, and the next descriptor is loaded (one word per lane)
   // while the current task runs.
-  const bool stat = (A.mode & 16) != 0;
+  const bool stat = (mode & 16) != 0;
   // hook at a FRAG task's tail, after its last level: the claim atomic of the
   // NEXT task is issued before the result stores and the completion post, so
   // its L2 round trip (~0.8 us between a worker's tasks) overlaps them.  The
@@ -1208,7 +1213,7 @@ __global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? SFCDD_R
   // before -- this task is past its waits and completes unconditionally.
   int tnext = -1;
   auto ahead = [&]() {
-    if ((A.mode & 64) && !stat && lane == 0) tnext = q + A.nq * atomicAdd(qh, 1);
+    if ((mode & 64) && !stat && lane == 0) tnext = q + A.nq * atomicAdd(qh, 1);
   };
   const int nw = (int)gridDim.x * WPB;
   int ts = (int)blockIdx.x * WPB + warp;
@@ -1269,7 +1274,7 @@ __global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? SFCDD_R
     // the scratch follows the task's own blob (128-byte aligned): blob and
     // scratch share the slot, so small-scratch tasks carry larger blobs
     double* S = reinterpret_cast<double*>(smem + (size_t)warp * A.slot_bytes + ((T.copy_bytes + 127) & ~127));
-    unsigned long long* tr = A.trace ? A.trace + 5 * (size_t)t : nullptr;
+    unsigned long long* tr = TRACE && A.trace ? A.trace + 5 * (size_t)t : nullptr;
     if (lane == 0) {
       if (tr) {
         tr[0] = smid() | ((unsigned long long)(blockIdx.x * WPB + warp) << 16);  // sm | worker id << 16
@@ -1278,7 +1283,7 @@ __global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? SFCDD_R
       // the blob does not depend on other tasks: copy it while waiting
       fence_proxy_async();
       mbar_expect_tx(bar, (uint32_t)T.copy_bytes);
-      if (A.mode & 4)
+      if (mode & 4)
         bulk_g2s(smem + (size_t)warp * A.slot_bytes, A.blobs + T.blob_off, (uint32_t)T.copy_bytes, bar);
       else
         bulk_g2s_hint(smem + (size_t)warp * A.slot_bytes, A.blobs + T.blob_off, (uint32_t)T.copy_bytes, bar,
@@ -1292,7 +1297,7 @@ __global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? SFCDD_R
           if (SFCDD_LEAN & 1) return;
           if ((++polls & 4095u) == 0) {
             if (t0 == 0) t0 = gtimer();
-            if (A.mode & 32) {  // diagnostic mode: record the stuck wait, let every warp leave
+            if (mode & 32) {  // diagnostic mode: record the stuck wait, let every warp leave
               if (ld_relaxed(A.diag) != 0) dead = 1;
               else if (gtimer() - t0 > A.watchdog_ns && atomicCAS(A.diag, 0, 1) == 0) {
                 A.diag[1] = t;
@@ -1308,7 +1313,7 @@ __global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? SFCDD_R
             }
           }
         };
-        if (A.mode & 1) {
+        if (mode & 1) {
           while (!((SFCDD_LEAN & 16) ? 0 : dead) && ld_acquire(A.ctr + T.wait_idx) < T.wait_target) {
             __nanosleep(ns);
             ns = ns < 256 ? 2 * ns : 256;
@@ -1331,7 +1336,7 @@ __global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? SFCDD_R
     else
       mbar_wait_guard(bar, phase);
     phase ^= 1u;
-    if (!(SFCDD_LEAN & 1) && (A.mode & 32)) {  // diagnostic mode: leave once a stuck wait was recorded
+    if (!(SFCDD_LEAN & 1) && (mode & 32)) {  // diagnostic mode: leave once a stuck wait was recorded
       dead = __shfl_sync(FULL, dead, 0);
       if (dead) {
         if (lane == 0) {
@@ -1346,40 +1351,40 @@ __global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? SFCDD_R
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.blobs + pf_off), "r"(pf_bytes) : "memory");
 #if !(SFCDD_LEAN & 32)  // (the if-chain measured 3 % faster than the switch below on C2: code layout)
     if ((SFCDD_LEAN & 4) && T.kind == TK_FRAG_FWD) {
-      run_frag<8>(h, true, S, A, F, lane, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);
+      run_frag<8>(h, true, S, A, F, lane, TRACE && A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);
     } else if ((SFCDD_LEAN & 4) && T.kind == TK_FRAG_BWD) {
-      run_frag<8>(h, false, S, A, F, lane, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);
+      run_frag<8>(h, false, S, A, F, lane, TRACE && A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);
     } else if (T.kind == TK_FRAG_FWD || T.kind == TK_FRAG_BWD) {
-      run_frag<8>(h, T.kind == TK_FRAG_FWD, S, A, F, lane, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);
+      run_frag<8>(h, T.kind == TK_FRAG_FWD, S, A, F, lane, TRACE && A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);
     } else if (SPLIT && T.kind == TK_ASM_FWD) {
       run_asm(h, A, F, lane);
     } else if (SPLIT && T.kind == TK_XB_BWD) {
       run_xb(h, A, F, lane);
     } else if (T.kind == TK_ROW_FWD && (!DIRECT || h[RW_INBLOB])) {
-      run_row_blob<SPLIT, WPB == 2>(h, S, A, F, lane, bar, phase, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr);
+      run_row_blob<SPLIT, WPB == 2>(h, S, A, F, lane, bar, phase, TRACE && A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr);
     } else if (T.kind == TK_COL_BWD && (!DIRECT || h[CL_INBLOB])) {
       run_col_blob<SPLIT, WPB == 2>(h, S, A, F, lane, bar, phase);
     } else if constexpr (DIRECT) {
-      if (SPLIT && T.kind == TK_ROW_FWD && h[RW_NBLK] > 1)
+      if (TRACE && SPLIT && T.kind == TK_ROW_FWD && h[RW_NBLK] > 1)  // (MROW tasks: opt-in plans, TRACE instantiation)
         phase = run_mrow<16, WPB == 2>(h, S, A, A.blobs + T.blob_off, lane, bar, phase);
       else
         phase = run_dense<SPLIT, DU>(T.kind == TK_ROW_FWD, h, S, A, F, A.blobs + T.blob_off, lane, bar, phase,
                                      &vbars[DIRECT ? warp * VST : 0], vph,
-                                     smem + (size_t)(warp + 1) * A.slot_bytes);
+                                     smem + (size_t)(warp + 1) * A.slot_bytes, !(mode & 128));
     } else {
       __trap();  // a DIRECT block in a plan built without them
     }
 #else
     switch (T.kind) {
       case TK_FRAG_FWD:
-        run_frag<8>(h, true, S, A, F, lane, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);
+        run_frag<8>(h, true, S, A, F, lane, TRACE && A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);
         break;
       case TK_FRAG_BWD:
-        run_frag<8>(h, false, S, A, F, lane, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);
+        run_frag<8>(h, false, S, A, F, lane, TRACE && A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr, ahead);
         break;
       case TK_ROW_FWD:
         if (!DIRECT || h[RW_INBLOB]) {
-          run_row_blob<SPLIT, WPB == 2>(h, S, A, F, lane, bar, phase, A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr);
+          run_row_blob<SPLIT, WPB == 2>(h, S, A, F, lane, bar, phase, TRACE && A.ptrace ? A.ptrace + 16 * (size_t)t : nullptr);
           break;
         }
         [[fallthrough]];
@@ -1399,12 +1404,12 @@ __global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? SFCDD_R
           break;
         }
         if constexpr (DIRECT) {  // ROW or COL block streamed from HBM
-          if (SPLIT && T.kind == TK_ROW_FWD && h[RW_NBLK] > 1)
+          if (TRACE && SPLIT && T.kind == TK_ROW_FWD && h[RW_NBLK] > 1)  // (MROW tasks: opt-in plans, TRACE instantiation)
             phase = run_mrow<16, WPB == 2>(h, S, A, A.blobs + T.blob_off, lane, bar, phase);
           else
             phase = run_dense<SPLIT, DU>(T.kind == TK_ROW_FWD, h, S, A, F, A.blobs + T.blob_off, lane, bar, phase,
                                      &vbars[DIRECT ? warp * VST : 0], vph,
-                                     smem + (size_t)(warp + 1) * A.slot_bytes);
+                                     smem + (size_t)(warp + 1) * A.slot_bytes, !(mode & 128));
         }
         break;
     }
@@ -1412,7 +1417,7 @@ __global__ void __launch_bounds__((WPB + 1) * 32) __maxnreg__(WPB == 4 ? SFCDD_R
     __syncwarp();
     if (lane == 0) {
       // release: cumulative over the warp's writes (ordered before it by __syncwarp)
-      if (A.mode & 2) {  // direct release by the worker (old path)
+      if (mode & 2) {  // direct release by the worker (old path)
         red_release_add(A.ctr + T.signal_idx, 1);
       } else {
         while (ld_acquire_cta(&mbox[warp]) >= 0) __nanosleep(20);  // signaller still busy with the last one
@@ -1497,15 +1502,20 @@ DagSolver::DagSolver(const DevicePlan& plan, int device, int64_t extra_xy) : dev
   SFCDD_REQUIRE(wpb_ == 2 || wpb_ == 4 || wpb_ == 8, SFCDD_EVALUE, "worker warps per CTA must be 2, 4 or 8");
   bool split = false;
   for (const TaskDev& T : plan.tasks) split = split || T.kind == TK_ASM_FWD || T.kind == TK_XB_BWD;
-  auto pick = [&](auto sp, auto dr) -> const void* {
-    constexpr bool SP = decltype(sp)::value, DR = decltype(dr)::value;
-    return wpb_ == 2 ? (const void*)k_dag<2, SP, DR> : wpb_ == 4 ? (const void*)k_dag<4, SP, DR> : (const void*)k_dag<8, SP, DR>;
+  auto pick = [&](auto sp, auto dr, auto tr) -> const void* {
+    constexpr bool SP = decltype(sp)::value, DR = decltype(dr)::value, TR = decltype(tr)::value;
+    return wpb_ == 2   ? (const void*)k_dag<2, SP, DR, TR>
+           : wpb_ == 4 ? (const void*)k_dag<4, SP, DR, TR>
+                       : (const void*)k_dag<8, SP, DR, TR>;
   };
   using T_ = std::true_type;
   using F_ = std::false_type;
-  kern_ = split ? (plan.has_direct ? pick(T_{}, T_{}) : pick(T_{}, F_{}))
-                : (plan.has_direct ? pick(F_{}, T_{}) : pick(F_{}, F_{}));
+  kern_ = split ? (plan.has_direct ? pick(T_{}, T_{}, F_{}) : pick(T_{}, F_{}, F_{}))
+                : (plan.has_direct ? pick(F_{}, T_{}, F_{}) : pick(F_{}, F_{}, F_{}));
+  kern_trace_ = split ? (plan.has_direct ? pick(T_{}, T_{}, T_{}) : pick(T_{}, F_{}, T_{}))
+                      : (plan.has_direct ? pick(F_{}, T_{}, T_{}) : pick(F_{}, F_{}, T_{}));
   split_ = split;
+  has_mrow_ = plan.has_mrow;
   if (const char* e = std::getenv("SFCDD_DAG_MODE")) mode_ = std::atoi(e);
   if (const char* e = std::getenv("SFCDD_SIG_NS")) sig_ns_ = std::atoi(e);
   if (const char* e = std::getenv("SFCDD_SIG_WAIT_NS")) sig_wait_ns_ = std::atoi(e);
@@ -1575,10 +1585,12 @@ DagSolver::DagSolver(const DevicePlan& plan, int device, int64_t extra_xy) : dev
     static std::mutex mu;
     static std::map<std::pair<int, const void*>, int> max_smem;
     std::lock_guard<std::mutex> g(mu);
-    int& cur = max_smem[{device, kern_}];
-    if (smem_ > cur) {
-      CUDA_CHECK(cudaFuncSetAttribute(kern_, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
-      cur = smem_;
+    for (const void* k : {kern_, kern_trace_}) {
+      int& cur = max_smem[{device, k}];
+      if (smem_ > cur) {
+        CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
+        cur = smem_;
+      }
     }
   }
   int per_sm = 0, sms = 0;
@@ -1627,6 +1639,8 @@ void DagSolver::solve(const double* rhs, cudaStream_t st, const int32_t* skip) {
   a.watchdog_ns = 1000000ull * (unsigned long long)watchdog_ms_;
   a.pf_dist = pf_dist_;
   void* params[] = {&a};
+  // (mode switches and MROW tasks: TRACE instantiation only)
+  const void* kern = (trace_ || mode_ != 0 || has_mrow_) ? kern_trace_ : kern_;
   if (l2_persist_) {  // experiment: keep the gathered vector resident in L2 while the blobs stream through
     cudaStreamAttrValue av{};
     av.accessPolicyWindow.base_ptr = l2_persist_ == 2 ? (void*)xy_ : (void*)rhs;
@@ -1638,9 +1652,9 @@ void DagSolver::solve(const double* rhs, cudaStream_t st, const int32_t* skip) {
     CUDA_CHECK(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &av));
   }
   if (mode_ & 16)  // static worker lists need every CTA resident: cooperative launch guarantees it (or fails)
-    CUDA_CHECK(cudaLaunchCooperativeKernel(kern_, dim3(grid_), dim3((wpb_ + 1) * 32), params, smem_, st));
+    CUDA_CHECK(cudaLaunchCooperativeKernel(kern, dim3(grid_), dim3((wpb_ + 1) * 32), params, smem_, st));
   else
-    CUDA_CHECK(cudaLaunchKernel(kern_, dim3(grid_), dim3((wpb_ + 1) * 32), params, smem_, st));
+    CUDA_CHECK(cudaLaunchKernel(kern, dim3(grid_), dim3((wpb_ + 1) * 32), params, smem_, st));
   if (l2_persist_) {
     cudaStreamAttrValue av{};
     av.accessPolicyWindow.num_bytes = 0;

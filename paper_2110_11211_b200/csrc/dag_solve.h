@@ -37,7 +37,9 @@ class DagSolver {
   int32_t ngroups_ = 0, ntask_ = 0, grid_ = 1, blob_max_ = 0, slot_bytes_ = 0, smem_ = 0, wpb_ = 4, mode_ = 0, sig_ns_ = 20,
           sig_wait_ns_ = 1000;
   bool split_ = false;  // kernel variant with ASM / XB tasks
+  bool has_mrow_ = false;  // the plan holds MROW tasks (opt-in): needs the full kernel
   const void* kern_ = nullptr;
+  const void* kern_trace_ = nullptr;  // the same kernel with per-task time stamps (sfcdd_op_trace)
   int64_t xy_doubles_ = 0, ctr_words_ = 0, bytes_ = 0;
   int64_t rhs_doubles_ = 0;  // length of the gathered right-hand side (max gmod of the factors)
   int32_t l2_persist_ = 0;   // SFCDD_L2_PERSIST: 1 = rhs, 2 = xy as a persisting L2 window of the launch (experiment)

@@ -73,6 +73,7 @@ struct FactorEmit {
     max_slot = std::max<int64_t>(max_slot, ((int64_t)bytes + 127) / 128 * 128 + 8 * scratch_doubles);
   }
   bool has_direct = false;
+  bool has_mrow = false;
 
   int64_t put_meta(const std::vector<int32_t>& ints, int64_t meta_bytes) {
     const int64_t off = size;
@@ -696,6 +697,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
           int32_t bytes = 0;
           const int64_t off = E.emit_descs(ints, RW_VAL_OFF, (int64_t)nb * Rb * s, vds.data(), vds.size(), bytes, &F, -1, true);
           E.has_direct = true;
+          E.has_mrow = true;
           E.max_scratch = std::max<int32_t>(E.max_scratch, 2 * RING_STRIDE);
           E.need_slot(bytes, 2 * RING_STRIDE);
           add_task(g, TK_ROW_FWD, off, bytes, (int64_t)rows * s, 1.8 + 0.0004 * rows * s);
@@ -1211,6 +1213,7 @@ DevicePlan build_plan(const std::vector<const HostFactor*>& factors, const std::
     P.slot_need = std::max(P.slot_need, E.max_slot);
     P.max_copy = std::max(P.max_copy, E.max_copy);
     P.has_direct = P.has_direct || E.has_direct;
+    P.has_mrow = P.has_mrow || E.has_mrow;
   }
   SFCDD_REQUIRE(P.upd_doubles < (int64_t(1) << 31), SFCDD_EINTERNAL, "update buffer too large");
 

@@ -194,7 +194,8 @@ enum ColHdr {
 constexpr int RING_CHUNK = 256;
 constexpr int RING_STRIDE = RING_CHUNK + 2;
 
-constexpr int SMALL_MAX_S = 64;  // wider supernodes are always BIG
+constexpr int SMALL_MAX_S = 32;  // wider supernodes are always BIG (a FRAG backward item packs whole supernodes
+                                  // into the 32 lanes: dag_solve.cu bwd_lanes)
 
 // ------------------------------------------------ factor value placement
 // Where a factor's packed block-inverse values (HostFactor::val layout:
@@ -292,6 +293,7 @@ struct DevicePlan {
   int64_t num_supernodes = 0;
   int64_t stored = 0, nnz_l = 0;
   bool has_direct = false;  // some ROW / COL task streams its values from HBM (selects the kernel variant)
+  bool has_mrow = false;    // some ROW task is an MROW task (opt-in, PlanOptions::mrow_rows)
   int32_t wpb = 4;          // worker warps per DAG CTA the plan was simulated for
   int32_t max_scratch = 0;  // doubles, over all tasks
   int64_t slot_need = 0;    // bytes of shared memory a worker needs: max over tasks of align128(blob) + scratch
