@@ -269,6 +269,7 @@ __device__ __forceinline__ void run_apply(const int32_t* runs, const int32_t* gp
   double acc = d + v0;
   acc = n > 1 ? acc + v1 : acc;
   acc = n > 2 ? acc + v2 : acc;
+  #pragma unroll 1
   for (int p = p0 + 3; p < p1; ++p) acc += S[hi16(gp[p])];
   S[dst] = acc;
 }
@@ -277,6 +278,7 @@ __device__ __forceinline__ void run_apply(const int32_t* runs, const int32_t* gp
 __device__ __forceinline__ void gather_runs(const int32_t* runs, const int32_t* gp, int r0, int r1, double* S,
                                             int lane) {
   // (one copy of run_apply: two runs per lane in flight measured no faster than the smaller code)
+  #pragma unroll 1
   for (int r = r0 + lane; r < r1; r += 32) run_apply(runs, gp, r, S);
 }
 
@@ -305,6 +307,7 @@ __device__ __forceinline__ void fwd_row(const int4 R, const double* vals, double
     idx = i3 + step - 3;
     step -= 4;
   }
+  #pragma unroll 1
   for (; k <= kmax; ++k) {
     a0 = fma(M[idx], f[k], a0);
     idx += step;
@@ -392,6 +395,7 @@ __device__ __forceinline__ void bwd_lanes(const int4* recs, const double* vals, 
   }
   double acc = a0 + a1;
   const int pmax = (int)__reduce_max_sync(FULL, act ? (unsigned)P : 1u);
+  #pragma unroll 1
   for (int d = 1; d < pmax; d <<= 1) {
     const double o = __shfl_xor_sync(FULL, acc, d);
     if (d < P) acc += o;
@@ -420,6 +424,7 @@ __device__ __forceinline__ void run_frag(const int32_t* h, bool fwd, double* S, 
   if (fwd) {
     stamp(0);
     const int nzero = h[H_ZERO];
+    #pragma unroll 1
     for (int i = lane; i < nzero; i += 32) S[i] = 0.0;
     __syncwarp();
     {  // one batched gather: right-hand side at the columns + external child updates
@@ -432,6 +437,7 @@ __device__ __forceinline__ void run_frag(const int32_t* h, bool fwd, double* S, 
     }
     __syncwarp();
     stamp(1);
+    #pragma unroll 1
     for (int lv = 0; lv < nlev; ++lv) {
       const int32_t* L = levtab + L_WORDS * lv;
       if (L[L_RUN1] > L[L_RUN0]) {  // multifrontal assembly, gather form
@@ -439,6 +445,7 @@ __device__ __forceinline__ void run_frag(const int32_t* h, bool fwd, double* S, 
         __syncwarp();
       }
       if (lv < 6) stamp(2 + 2 * lv);
+      #pragma unroll 1
       for (int it = L[L_FI0]; it < L[L_FI1]; ++it) {  // rows of the level's supernodes
         const int2 item = items[it];
         const unsigned ix = (unsigned)item.x;
@@ -460,14 +467,17 @@ __device__ __forceinline__ void run_frag(const int32_t* h, bool fwd, double* S, 
       if (lv < 6) stamp(3 + 2 * lv);
     }
     ahead();  // (the levels are done: only the result stores remain)
+    #pragma unroll 1
     for (int c = lane; c < ncol; c += 32) __stcg(xy + cols[c], S[hi16(colpos[c])]);
     {  // update vectors of the tops (one per packed sibling subtree)
       const int32_t* tops = h + h[H_TOPS];
+      #pragma unroll 1
       for (int tp = 0; tp < h[H_NTOP]; ++tp) {
         const int slot = tops[2 * tp + 1];
         if (slot < 0) continue;
         const int4 R = recs[tops[2 * tp]];
         const double* u = S + R.y + rec_s(R);
+        #pragma unroll 1
         for (int a = lane; a < rec_m(R); a += 32) __stcg(A.upd + slot + a, u[a]);
       }
     }
@@ -483,14 +493,17 @@ __device__ __forceinline__ void run_frag(const int32_t* h, bool fwd, double* S, 
     }
     __syncwarp();
     stamp(1);
+    #pragma unroll 1
     for (int lv = nlev - 1; lv >= 0; --lv) {
       const int32_t* L = levtab + L_WORDS * lv;
       if (L[L_BP1] > L[L_BP0]) {  // v_B = -x(rows)
+        #pragma unroll 1
         for (int p = L[L_BP0] + lane; p < L[L_BP1]; p += 32) S[lo16(bp[p])] = -S[hi16(bp[p])];
         __syncwarp();
       }
       const int ls = nlev - 1 - lv;
       if (ls < 4) stamp(2 + 2 * ls);
+      #pragma unroll 1
       for (int it = L[L_BI0]; it < L[L_BI1]; ++it) {  // columns / packed small supernodes
         const int2 item = items[it];
         const unsigned ix = (unsigned)item.x;
@@ -503,6 +516,7 @@ __device__ __forceinline__ void run_frag(const int32_t* h, bool fwd, double* S, 
       if (ls < 4) stamp(3 + 2 * ls);
     }
     ahead();
+    #pragma unroll 1
     for (int c = lane; c < ncol; c += 32) __stcg(xy + cols[c], S[hi16(colpos[c])]);
     stamp(14);
     if (pt && lane == 0) pt[15] = nlev;
@@ -635,6 +649,7 @@ __device__ __forceinline__ void run_row_blob(const int32_t* h, double* S, const 
         if (cn[u] > 0) a += v0[u];
         if (cn[u] > 1) a += v1[u];
         if (cn[u] > 2) a += v2[u];
+        #pragma unroll 1
         for (int e = e0[u] + 3; e < e0[u] + cn[u]; ++e) a += __ldcg(A.upd + src[e]);
         S[q] = a;
       }
@@ -648,6 +663,7 @@ __device__ __forceinline__ void run_row_blob(const int32_t* h, double* S, const 
   const int il = lane & (RP - 1), ph = lane / RP;
   double* yo = A.upd + h[RW_YOFF];
   double* uo = A.upd + h[RW_UOFF];
+  #pragma unroll 1
   for (int rb = 0; rb < R; rb += RP) {
     const int i = rb + il;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
@@ -670,6 +686,7 @@ __device__ __forceinline__ void run_row_blob(const int32_t* h, double* S, const 
         a0 = fma(v[k * R], S[k], a0);
         a1 = fma(v[(k + P) * R], S[k + P], a1);
       }
+      #pragma unroll 1
       for (; k < C; k += P) a0 = fma(v[k * R], S[k], a0);
     }
     double acc = (a0 + a1) + (a2 + a3);
@@ -724,6 +741,7 @@ __device__ __forceinline__ void run_col_blob(const int32_t* h, double* S, const 
   const int CP = c >= 32 ? 32 : (c <= 1 ? 1 : 1 << (32 - __clz(c - 1)));  // lanes per phase
   const int P = 32 / CP;
   const int j = lane & (CP - 1), ph = lane / CP;
+  #pragma unroll 1
   for (int jb = 0; jb < c; jb += CP) {
     const int jj = jb + j;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
@@ -742,6 +760,7 @@ __device__ __forceinline__ void run_col_blob(const int32_t* h, double* S, const 
         a0 = fma(v[r * c], Sv[r], a0);
         a1 = fma(v[(r + P) * c], Sv[r + P], a1);
       }
+      #pragma unroll 1
       for (; r < L; r += P) a0 = fma(v[r * c], Sv[r], a0);
     }
     double acc = (a0 + a1) + (a2 + a3);
