@@ -240,6 +240,7 @@ __device__ __forceinline__ int hi16(int32_t v) { return (int)((uint32_t)v >> 16)
 // gathers -- measured slower: C3 k_dag 1.79 -> 1.90 ms, C5 27.7 -> 30.5 ms)
 template <int RB = 8, typename Load, typename Store>
 __device__ __forceinline__ void warp_gather(int n, int lane, Load ld, Store st) {
+  #pragma unroll 1
   for (int base = 0; base < n; base += RB * 32) {
     double v[RB];
 #pragma unroll
@@ -298,6 +299,7 @@ __device__ __forceinline__ void fwd_row(const int4 R, const double* vals, double
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
   int idx = i, step = s + m - 1;
   int k = 0;
+  #pragma unroll 1
   for (; k + 3 <= kmax; k += 4) {
     const int i1 = idx + step, i2 = i1 + step - 1, i3 = i2 + step - 2;
     a0 = fma(M[idx], f[k], a0);
@@ -355,6 +357,7 @@ __device__ __forceinline__ void bwd_cols(const int4 R, const double* vals, doubl
     const double* vk = v + k;
     const int len = s + m - k;
     int t = ph;
+    #pragma unroll 1
     for (; t + P < len; t += 2 * P) {
       a0 = fma(col[t], vk[t], a0);
       a1 = fma(col[t + P], vk[t + P], a1);
@@ -362,6 +365,7 @@ __device__ __forceinline__ void bwd_cols(const int4 R, const double* vals, doubl
     if (t < len) a0 = fma(col[t], vk[t], a0);
   }
   double acc = a0 + a1;
+  #pragma unroll 1
   for (int o = CP; o < 32; o <<= 1) acc += __shfl_xor_sync(FULL, acc, o);
   if (ph == 0 && j < c) S[R.w + k] = acc;
 }
@@ -387,6 +391,7 @@ __device__ __forceinline__ void bwd_lanes(const int4* recs, const double* vals, 
     const double* v = S + R.y + k;
     const int len = s + m - k;
     int t = local & (P - 1);
+    #pragma unroll 1
     for (; t + P < len; t += 2 * P) {
       a0 = fma(col[t], v[t], a0);
       a1 = fma(col[t + P], v[t + P], a1);
@@ -534,6 +539,7 @@ __device__ __noinline__ void run_asm(const int32_t* h, const DagArgs& A, const F
   const int32_t* src = h + h[AS_SRC];
   double* f = A.upd + h[AS_FOFF] + q0;
   constexpr int U = 2;
+  #pragma unroll 1
   for (int base = 0; base < nq; base += 32 * U) {
     double acc[U], v0[U], v1[U], v2[U];
     int e0[U], e1[U];
@@ -558,6 +564,7 @@ __device__ __noinline__ void run_asm(const int32_t* h, const DagArgs& A, const F
       if (n > 0) a += v0[u];
       if (n > 1) a += v1[u];
       if (n > 2) a += v2[u];
+      #pragma unroll 1
       for (int e = e0[u] + 3; e < e1[u]; ++e) a += __ldcg(A.upd + src[e]);
       __stcg(f + i, a);
     }
@@ -609,10 +616,12 @@ __device__ __forceinline__ void run_row_blob(const int32_t* h, double* S, const 
     const int32_t* cols = am + 2;
     const int32_t* ptr = cols + s;
     const int32_t* src = ptr + s + __ldg(am + 1) + 1;
+    #pragma unroll 1
     for (int q = lane; q < C + NB; q += 32) {
       const int p = q < C ? q : r0 + (q - C);
       const int e0 = __ldg(ptr + p), e1 = __ldg(ptr + p + 1);
       double acc = q < C ? __ldg(A.rhs + gidx(F, __ldg(cols + q))) : 0.0;
+      #pragma unroll 1
       for (int e = e0; e < e1; ++e) acc += __ldcg(A.upd + __ldg(src + e));
       S[q] = acc;
     }
@@ -627,6 +636,7 @@ __device__ __forceinline__ void run_row_blob(const int32_t* h, double* S, const 
     const int32_t* ptr = h + h[RW_PTR];
     const int32_t* src = h + h[RW_SRC];
     constexpr int U = WIDE ? 4 : 2;
+    #pragma unroll 1
     for (int base = 0; base < C + NB; base += 32 * U) {
       int e0[U], cn[U];
       double acc[U], v0[U], v1[U], v2[U];
@@ -674,6 +684,7 @@ __device__ __forceinline__ void run_row_blob(const int32_t* h, double* S, const 
       // two: the larger code costs it more than the loop gains (C2 +2.5 %)
       const double* v = V + i;
       int k = ph;
+      #pragma unroll 1
       for (; WIDE && k + 3 * P < C; k += 4 * P) {
         const double m0 = v[k * R], m1 = v[(k + P) * R], m2 = v[(k + 2 * P) * R], m3 = v[(k + 3 * P) * R];
         const double f0 = S[k], f1 = S[k + P], f2 = S[k + 2 * P], f3 = S[k + 3 * P];
@@ -682,6 +693,7 @@ __device__ __forceinline__ void run_row_blob(const int32_t* h, double* S, const 
         a2 = fma(m2, f2, a2);
         a3 = fma(m3, f3, a3);
       }
+      #pragma unroll 1
       for (; !WIDE && k + P < C; k += 2 * P) {
         a0 = fma(v[k * R], S[k], a0);
         a1 = fma(v[(k + P) * R], S[k + P], a1);
@@ -690,6 +702,7 @@ __device__ __forceinline__ void run_row_blob(const int32_t* h, double* S, const 
       for (; k < C; k += P) a0 = fma(v[k * R], S[k], a0);
     }
     double acc = (a0 + a1) + (a2 + a3);
+    #pragma unroll 1
     for (int o = RP; o < 32; o <<= 1) acc += __shfl_xor_sync(FULL, acc, o);
     if (ph == 0 && i < R) {
       const int row = r0 + i;
@@ -748,6 +761,7 @@ __device__ __forceinline__ void run_col_blob(const int32_t* h, double* S, const 
     if (jj < c) {
       const double* v = V + jj;
       int r = ph;
+      #pragma unroll 1
       for (; WIDE && r + 3 * P < L; r += 4 * P) {
         const double m0 = v[r * c], m1 = v[(r + P) * c], m2 = v[(r + 2 * P) * c], m3 = v[(r + 3 * P) * c];
         const double f0 = Sv[r], f1 = Sv[r + P], f2 = Sv[r + 2 * P], f3 = Sv[r + 3 * P];
@@ -756,6 +770,7 @@ __device__ __forceinline__ void run_col_blob(const int32_t* h, double* S, const 
         a2 = fma(m2, f2, a2);
         a3 = fma(m3, f3, a3);
       }
+      #pragma unroll 1
       for (; !WIDE && r + P < L; r += 2 * P) {
         a0 = fma(v[r * c], Sv[r], a0);
         a1 = fma(v[(r + P) * c], Sv[r + P], a1);
@@ -764,6 +779,7 @@ __device__ __forceinline__ void run_col_blob(const int32_t* h, double* S, const 
       for (; r < L; r += P) a0 = fma(v[r * c], Sv[r], a0);
     }
     double acc = (a0 + a1) + (a2 + a3);
+    #pragma unroll 1
     for (int o = CP; o < 32; o <<= 1) acc += __shfl_xor_sync(FULL, acc, o);
     if (ph == 0 && jj < c) __stcg(xy + cols[jj], acc);
   }
@@ -819,6 +835,7 @@ __device__ __forceinline__ double dense_dot(const double* __restrict__ V, bool r
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
   const int GPC = ring ? RING_CHUNK / (P * DU) : ng;  // groups per ring chunk (>= 1)
   const double* fq = S + ph;  // vec entry of this lane's next value (no ring)
+  #pragma unroll 1
   for (int g = 0; g < ng; ++g) {
     // DU independent loads per lane in flight (the only latency the loop pays)
     const int left = nj - g * DU;  // entries of this lane still to do
@@ -850,6 +867,7 @@ __device__ __forceinline__ double dense_dot(const double* __restrict__ V, bool r
     fq += P * DU;
   }
   double acc = (a0 + a1) + (a2 + a3);
+  #pragma unroll 1
   for (int o = WP; o < 32; o <<= 1) acc += __shfl_xor_sync(FULL, acc, o);
   return acc;
 }
@@ -893,10 +911,12 @@ __device__ __forceinline__ double dense_dot_tma(const double* __restrict__ V, bo
       mbar_expect_tx(bar, nb);
       bulk_g2s(S, gvec, nb, bar);
     }
+    #pragma unroll 1
     for (int c = 0; c < nst && c < nch; ++c) issue(c, c);
   }
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
   int st = 0;
+  #pragma unroll 1
   for (int c = 0; c < nch; ++c) {
     const int k0 = c * kc, nk = min(kc, Len - k0);
     const int rc = k0 / RING_CHUNK;
@@ -918,6 +938,7 @@ __device__ __forceinline__ double dense_dot_tma(const double* __restrict__ V, bo
     vph ^= 1u << st;
     const double* v = stage + st * VSTAGE_DOUBLES + il;
     int k = ph;
+    #pragma unroll 1
     for (; k + 3 * P < nk; k += 4 * P) {
       const double m0 = v[k * W], m1 = v[(k + P) * W], m2 = v[(k + 2 * P) * W], m3 = v[(k + 3 * P) * W];
       const double f0 = vec[k], f1 = vec[k + P], f2 = vec[k + 2 * P], f3 = vec[k + 3 * P];
@@ -926,6 +947,7 @@ __device__ __forceinline__ double dense_dot_tma(const double* __restrict__ V, bo
       a2 = fma(m2, f2, a2);
       a3 = fma(m3, f3, a3);
     }
+    #pragma unroll 1
     for (; k < nk; k += P) a0 = fma(v[k * W], vec[k], a0);
     // every lane is done with stage st and has observed its phase: refill it
     __syncwarp();
@@ -936,6 +958,7 @@ __device__ __forceinline__ double dense_dot_tma(const double* __restrict__ V, bo
     st = st + 1 == nst ? 0 : st + 1;
   }
   double acc = (a0 + a1) + (a2 + a3);
+  #pragma unroll 1
   for (int o = WP; o < 32; o <<= 1) acc += __shfl_xor_sync(FULL, acc, o);
   return acc;
 }
@@ -1057,11 +1080,13 @@ __device__ __forceinline__ uint32_t run_dense(bool is_row, const int32_t* h, dou
       const int32_t* cols = ga ? am + 2 : h + h[RW_COLS];
       const int32_t* ptr = ga ? cols + s : h + h[RW_PTR];
       const int32_t* src = ga ? ptr + s + __ldg(am + 1) + 1 : h + h[RW_SRC];
+      #pragma unroll 1
       for (int q = lane; q < C + NB; q += 32) {
         const int p = ga && q >= C ? r0 + (q - C) : q;
         const int e0 = ptr[p], e1 = ptr[p + 1];
         double a = q < C ? __ldg(A.rhs + gidx(F, cols[q])) : 0.0;
         int e = e0;
+        #pragma unroll 1
         for (; e + 2 <= e1; e += 2) {
           const double u0 = __ldcg(A.upd + src[e]), u1 = __ldcg(A.upd + src[e + 1]);
           a += u0;
