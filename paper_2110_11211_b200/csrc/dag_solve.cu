@@ -1563,6 +1563,9 @@ DagSolver::DagSolver(const DevicePlan& plan, int device, int64_t extra_xy) : dev
   if (const char* e = std::getenv("SFCDD_DAG_MODE")) mode_ = std::atoi(e);
   if (const char* e = std::getenv("SFCDD_SIG_NS")) sig_ns_ = std::atoi(e);
   if (const char* e = std::getenv("SFCDD_SIG_WAIT_NS")) sig_wait_ns_ = std::atoi(e);
+  // L2 prefetch-ahead where the blobs of one launch are many times the L2 (measured with the
+  // final kernel: C3 4.7 GB -0.8 %, C4 15 GB -3 %, C5 92 GB -1.8 %; C2 0.9 GB +1.1 %: off)
+  pf_dist_ = plan.blob_bytes > (2ll << 30) ? 1536 : 0;
   if (const char* e = std::getenv("SFCDD_PF_DIST")) pf_dist_ = std::max(0, std::atoi(e));
   for (const FactorDev& F : plan.factors) rhs_doubles_ = std::max<int64_t>(rhs_doubles_, F.gmod);
   if (const char* e = std::getenv("SFCDD_L2_PERSIST")) l2_persist_ = std::atoi(e);

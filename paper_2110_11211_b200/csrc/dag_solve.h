@@ -44,8 +44,8 @@ class DagSolver {
   int64_t rhs_doubles_ = 0;  // length of the gathered right-hand side (max gmod of the factors)
   int32_t l2_persist_ = 0;   // SFCDD_L2_PERSIST: 1 = rhs, 2 = xy as a persisting L2 window of the launch (experiment)
   int32_t watchdog_ms_ = 20000;  // dependency-wait watchdog (SFCDD_WATCHDOG_MS)
-  int32_t pf_dist_ = 1536;       // L2 prefetch distance in queue positions (SFCDD_PF_DIST, 0 = off): about one
-                                 // task duration of claims ahead (C2 k_dag -1.3 %, C3 -3.3 %, profiles/r02/README.md)
+  int32_t pf_dist_ = 0;          // L2 prefetch distance in queue positions (SFCDD_PF_DIST; set per plan in the
+                                 // constructor: about one task duration of claims ahead, or 0)
   uint8_t* blobs_ = nullptr;
   TaskDev* tasks_ = nullptr;
   FactorDev* factors_ = nullptr;
