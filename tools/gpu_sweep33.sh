@@ -1,0 +1,3 @@
+T=${1:-sw33}; mkdir -p gpurun_out/$T
+timeout 900 python tools/sweep_dag.py c2 "MODE=0" "MODE=0" > gpurun_out/$T/sweep_c2.jsonl 2> gpurun_out/$T/sweep_c2.err
+timeout 1200 python tools/sweep_dag.py c4 "MODE=0" > gpurun_out/$T/sweep_c4.jsonl 2> gpurun_out/$T/sweep_c4.err
